@@ -1,0 +1,136 @@
+/*
+ * gcabem_b200 — C ABI of the B200 (sm_100a) BEM setup hot path.
+ *
+ * Drop-in boundary for the reference package `gcabem` (pure Python + numba,
+ * /root/reference/pkg/src/gcabem). Each entry point names the reference
+ * interface it replaces. Plain pointers and sizes only; every call returns a
+ * status (0 = ok) and never throws; gcabem_last_error() holds the message of
+ * the calling thread's last failure. All entry points are thread-safe; work
+ * on one mesh/plan handle is ordered on that handle's CUDA stream.
+ *
+ * Conventions
+ *   equation: 0 = laplace, 1 = helmholtz          (kernels.py:23-43 KernelSpec)
+ *   layer:    0 = single, 1 = double
+ *   case:     0 = disjoint, 1 = vertex, 2 = edge, 3 = identical (quadrature.py:50)
+ *   complex values are interleaved (re, im) float64 pairs (numpy complex128).
+ *   Triangle charts follow mesh.py:3-10: Phi(s,t) = v0 + s(v1-v0) + t(v2-v1).
+ */
+#ifndef GCABEM_B200_H
+#define GCABEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GCABEM_OK 0
+#define GCABEM_ERR_ARG 1      /* invalid argument (ValueError on the Python side) */
+#define GCABEM_ERR_CUDA 2     /* CUDA runtime failure (BackendError) */
+#define GCABEM_ERR_NODEV 3    /* no CUDA device visible (BackendError) */
+
+typedef struct gcabem_mesh_s *gcabem_mesh_t;
+typedef struct gcabem_plan_s *gcabem_plan_t;
+
+/* ---- library / device ------------------------------------------------- */
+int gcabem_version(void);
+const char *gcabem_last_error(void);
+int gcabem_device_count(int *count);
+/* name (>= 256 bytes), SM count, SM clock kHz */
+int gcabem_device_info(int device, char *name, int *sm_count, int *clock_khz);
+
+/* Pinned host memory for payload buffers (cudaHostAlloc / cudaFreeHost). */
+int gcabem_host_alloc(int64_t nbytes, void **ptr);
+int gcabem_host_free(void *ptr);
+
+/* ---- raw pair quadrature ------------------------------------------------
+ * Replaces pairquad.pair_values (reference pairquad.py:95-112; numba ABI
+ * pairquad.py:18-24,31). Host arrays: ox..e2y, ny are (n,3) C-order float64,
+ * gx, gy (n,), ny may be NULL (zeros), xs/ys (nq,2), w (nq,). out is
+ * complex128 (n,) interleaved. Coincident points give non-finite values
+ * silently, as in the reference (pairquad.py:98-99). */
+int gcabem_pair_values(int device, int equation, int layer, double kappa, int64_t n,
+                       const double *ox, const double *e1x, const double *e2x,
+                       const double *gx, const double *oy, const double *e1y,
+                       const double *e2y, const double *gy, const double *ny,
+                       int64_t nq, const double *xs, const double *ys, const double *w,
+                       double *out);
+
+/* ---- device mesh replica --------------------------------------------------
+ * Uploads mesh.SurfaceMesh (mesh.py:39-78): vertices (nv,3) f64, triangles
+ * (nt,3) i64, normals (nt,3), gramians (nt,). Builds the per-triangle chart
+ * table (mesh.chart_arrays, mesh.py:207-222, identity permutation). */
+int gcabem_mesh_create(int device, int64_t nv, const double *vertices, int64_t nt,
+                       const int64_t *triangles, const double *normals,
+                       const double *gramians, gcabem_mesh_t *out);
+int gcabem_mesh_destroy(gcabem_mesh_t mesh);
+
+/* Index-based batch. Replaces scheduler.batch_quadrature (scheduler.py:235-261):
+ * charts gathered on device from (tri, perm); perm_x/perm_y (n,3) uint8 may
+ * be NULL (identity). Rule (xs,ys,w) as in gcabem_pair_values. */
+int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double kappa,
+                            int64_t n, const int64_t *tri_x, const int64_t *tri_y,
+                            const uint8_t *perm_x, const uint8_t *perm_y, int64_t nq,
+                            const double *xs, const double *ys, const double *w,
+                            double *out);
+
+/* ---- assembly plan --------------------------------------------------------
+ * The device side of scheduler.run_assembly (scheduler.py:442-505): executes
+ * every disjoint work list (execute_list :368 -> batch_quadrature :235 ->
+ * distribute_disjoint :334) and then every singular list (distribute_singular
+ * :362, the overwrite protocol) into one device-resident payload buffer that
+ * holds all block-tree leaves (make_payloads :411) back to back, complex128.
+ *
+ * blocks: nblocks x 6 int64 {payload_base, ld, nrows, ncols, rows_at, cols_at}
+ *   — a WorkBlock (scheduler.py:87-103): entry (i,j) goes to
+ *   payload[payload_base + i*ld + j], row panel panels[rows_at+i], column
+ *   panel panels[cols_at+j]. The rule is the disjoint rule of order
+ *   disjoint_n given in factored form: gauss_pts/gauss_wts (disjoint_n,)
+ *   = quadrature.gauss_legendre (:82). Orders 1..12.
+ * items: nitems x 4 int64 {case, tri_x, tri_y, payload_index} — WorkItem
+ *   (scheduler.py:106-117) with payload_index = leaf base + offset;
+ *   perms: nitems x 6 uint8 (perm_x, perm_y) from classify_pair (:197).
+ *   Items must be grouped by case (any order inside a case).
+ * singular rules: for case c in 1..3, sq[c-1] points, rows of 5 float64
+ *   (sx, sy... see below) in srule[c-1]: {x_s, x_t, y_s, y_t, w}
+ *   (quadrature.build_rule, :170). */
+int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa,
+                       int disjoint_n, const double *gauss_pts, const double *gauss_wts,
+                       int64_t payload_len, int64_t nblocks, const int64_t *blocks,
+                       int64_t npanels, const int64_t *panels, int64_t nitems,
+                       const int64_t *items, const uint8_t *perms, const int64_t *sq,
+                       const double *const *srule, gcabem_plan_t *out);
+/* Launch all kernels on the plan stream (async). The payload is zeroed first
+ * (make_payloads semantics), then disjoint, then singular overwrites. */
+int gcabem_plan_execute(gcabem_plan_t plan);
+/* Copy the payload (payload_len complex128) to host memory (pinned for full
+ * PCIe rate) and wait. */
+int gcabem_plan_download(gcabem_plan_t plan, double *host);
+int gcabem_plan_synchronize(gcabem_plan_t plan);
+/* CUDA-event durations of the last execute, ms: [disjoint, singular, total]. */
+int gcabem_plan_timing(gcabem_plan_t plan, float *ms3);
+/* Device pointer of the payload (for device-resident consumers). */
+int gcabem_plan_payload(gcabem_plan_t plan, void **dev_ptr);
+int gcabem_plan_destroy(gcabem_plan_t plan);
+
+/* ---- GCA Green matrices ---------------------------------------------------
+ * Replaces gca.build_green_matrix (gca.py:136-179), batched over clusters.
+ * Cluster c owns panels[panel_at[c] .. panel_at[c+1]) and nsrc sources at
+ * src + c*nsrc*8, each {px,py,pz, nx,ny,nz, weight, role} (role 0 monopole,
+ * 1 dipole; GreenSourceSet gca.py:47-52). Output for cluster c starts at
+ * entry out_at[c] (entries, row-major |t| x nsrc), real float64 for laplace,
+ * complex128 for helmholtz: A[i,j] = w_j * gram_i * sum_q wq k_j(X_iq).
+ * duffy (order^2 x 3 rows {s, t, wq}) = quadrature.duffy_panel_rule(order). */
+int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_t nclusters,
+                          const int64_t *panel_at, const int64_t *panels, int64_t nsrc,
+                          const double *src, int64_t nduffy, const double *duffy,
+                          const int64_t *out_at, int64_t out_len, double *out_host);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+/* Dependent-DFMA throughput probe: achieved FP64 TFLOP/s (FMA = 2 flops). */
+int gcabem_fp64_probe(int device, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

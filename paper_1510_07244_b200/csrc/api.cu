@@ -1,0 +1,543 @@
+// C ABI of gcabem_b200 (declared in include/gcabem_b200.h). Host-side
+// ownership, uploads, task decomposition and error mapping; no compute here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gcabem_b200.h"
+#include "gcabem_common.cuh"
+
+using namespace gcabem;
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int code, const std::string &msg) {
+    g_error = msg;
+    return code;
+}
+
+#define GC_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_error(GCABEM_ERR_CUDA, std::string(#call) + ": " +                 \
+                                                  cudaGetErrorString(e_));                \
+    } while (0)
+
+#define GC_ARG(cond, msg)                                             \
+    do {                                                              \
+        if (!(cond)) return set_error(GCABEM_ERR_ARG, (msg));         \
+    } while (0)
+
+// RAII device buffer
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {
+        release();
+        n = count;
+        if (count == 0) return cudaSuccess;
+        return cudaMalloc(&p, sizeof(T) * count);
+    }
+    cudaError_t upload(const T *host, size_t count, cudaStream_t s) {
+        cudaError_t e = alloc(count);
+        if (e != cudaSuccess || count == 0) return e;
+        return cudaMemcpyAsync(p, host, sizeof(T) * count, cudaMemcpyHostToDevice, s);
+    }
+};
+
+std::mutex g_rule_mutex;
+std::set<std::pair<int, int>> g_rules_loaded;  // (device, order)
+
+// Constant-memory disjoint rule of `order` on `device` (idempotent: the
+// tables are functions of the Gauss rule only).
+int ensure_disjoint_rule(int device, int order, const double *g, const double *gw) {
+    std::lock_guard<std::mutex> lock(g_rule_mutex);
+    if (g_rules_loaded.count({device, order})) return GCABEM_OK;
+    GC_CUDA(upload_disjoint_rule(order, g, gw));
+    GC_CUDA(cudaDeviceSynchronize());
+    g_rules_loaded.insert({device, order});
+    return GCABEM_OK;
+}
+
+int check_kind(int equation, int layer, double kappa) {
+    GC_ARG(equation == 0 || equation == 1, "unknown equation");
+    GC_ARG(layer == 0 || layer == 1, "unknown layer");
+    GC_ARG(!(equation == 1 && kappa < 0.0), "kappa must be >= 0");
+    return GCABEM_OK;
+}
+
+// Pack an (n,5) generic rule {xs, xt, ys, yt, w} from (q,2),(q,2),(q,) arrays.
+std::vector<double> pack_rule(int64_t q, const double *xs, const double *ys, const double *w) {
+    std::vector<double> r(5 * q);
+    for (int64_t k = 0; k < q; ++k) {
+        r[5 * k] = xs[2 * k];
+        r[5 * k + 1] = xs[2 * k + 1];
+        r[5 * k + 2] = ys[2 * k];
+        r[5 * k + 3] = ys[2 * k + 1];
+        r[5 * k + 4] = w[k];
+    }
+    return r;
+}
+
+}  // namespace
+
+struct gcabem_mesh_s {
+    int device = 0;
+    int64_t nv = 0, nt = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf<double> V;
+    DevBuf<int32_t> T;
+    DevBuf<Chart> charts;
+};
+
+struct gcabem_plan_s {
+    gcabem_mesh_t mesh = nullptr;
+    int kind = 0, order = 0;
+    double kappa = 0.0;
+    int64_t payload_len = 0;
+    DevBuf<double2> payload;
+    DevBuf<BlockDesc> blocks;
+    DevBuf<int2> tasks;
+    int64_t ntasks = 0;
+    DevBuf<int32_t> panels;
+    DevBuf<SingItem> items;
+    int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])
+    DevBuf<double> srule[3];
+    int64_t sq[3] = {0, 0, 0};
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool executed = false;
+};
+
+extern "C" {
+
+int gcabem_version(void) { return 100; }
+
+const char *gcabem_last_error(void) { return g_error.c_str(); }
+
+int gcabem_device_count(int *count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return set_error(GCABEM_ERR_NODEV, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    }
+    *count = n;
+    return GCABEM_OK;
+}
+
+int gcabem_device_info(int device, char *name, int *sm_count, int *clock_khz) {
+    cudaDeviceProp prop;
+    GC_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (name) {
+        std::strncpy(name, prop.name, 255);
+        name[255] = 0;
+    }
+    if (sm_count) *sm_count = prop.multiProcessorCount;
+    if (clock_khz) {
+        int clk = 0;
+        cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+        *clock_khz = clk;
+    }
+    return GCABEM_OK;
+}
+
+int gcabem_host_alloc(int64_t nbytes, void **ptr) {
+    GC_ARG(nbytes >= 0 && ptr, "bad host_alloc arguments");
+    *ptr = nullptr;
+    if (nbytes == 0) return GCABEM_OK;
+    GC_CUDA(cudaHostAlloc(ptr, (size_t)nbytes, cudaHostAllocPortable));
+    return GCABEM_OK;
+}
+
+int gcabem_host_free(void *ptr) {
+    if (ptr) GC_CUDA(cudaFreeHost(ptr));
+    return GCABEM_OK;
+}
+
+int gcabem_pair_values(int device, int equation, int layer, double kappa, int64_t n,
+                       const double *ox, const double *e1x, const double *e2x,
+                       const double *gx, const double *oy, const double *e1y,
+                       const double *e2y, const double *gy, const double *ny, int64_t nq,
+                       const double *xs, const double *ys, const double *w, double *out) {
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    GC_ARG(n >= 0 && nq >= 0, "negative size");
+    if (n == 0) return GCABEM_OK;
+    GC_CUDA(cudaSetDevice(device));
+    std::vector<double> packed(24 * (size_t)n, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        double *p = packed.data() + 24 * i;
+        for (int c = 0; c < 3; ++c) {
+            p[c] = ox[3 * i + c];
+            p[3 + c] = e1x[3 * i + c];
+            p[6 + c] = e2x[3 * i + c];
+            p[9 + c] = oy[3 * i + c];
+            p[12 + c] = e1y[3 * i + c];
+            p[15 + c] = e2y[3 * i + c];
+            p[18 + c] = ny ? ny[3 * i + c] : 0.0;
+        }
+        p[21] = gx[i];
+        p[22] = gy[i];
+    }
+    std::vector<double> rule = pack_rule(nq, xs, ys, w);
+    cudaStream_t s;
+    GC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DevBuf<double> dp, dr;
+    DevBuf<double2> dout;
+    cudaError_t e = dp.upload(packed.data(), packed.size(), s);
+    if (e == cudaSuccess) e = dr.upload(rule.data(), rule.size(), s);
+    if (e == cudaSuccess) e = dout.alloc(n);
+    if (e == cudaSuccess)
+        e = launch_raw(kind_of(equation, layer), dp.p, n, dr.p, nq, dout.p, kappa, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    GC_CUDA(e);
+    return GCABEM_OK;
+}
+
+int gcabem_mesh_create(int device, int64_t nv, const double *vertices, int64_t nt,
+                       const int64_t *triangles, const double *normals, const double *gramians,
+                       gcabem_mesh_t *out) {
+    GC_ARG(out && nv > 0 && nt > 0, "empty mesh");
+    GC_ARG(nv < (int64_t(1) << 31) && nt < (int64_t(1) << 31), "mesh too large for int32 indices");
+    *out = nullptr;
+    GC_CUDA(cudaSetDevice(device));
+    std::vector<int32_t> T(3 * nt);
+    std::vector<Chart> charts(nt);
+    for (int64_t t = 0; t < nt; ++t) {
+        const int64_t i0 = triangles[3 * t], i1 = triangles[3 * t + 1], i2 = triangles[3 * t + 2];
+        GC_ARG(i0 >= 0 && i0 < nv && i1 >= 0 && i1 < nv && i2 >= 0 && i2 < nv,
+               "triangle index out of range");
+        T[3 * t] = (int32_t)i0;
+        T[3 * t + 1] = (int32_t)i1;
+        T[3 * t + 2] = (int32_t)i2;
+        Chart &c = charts[t];
+        for (int k = 0; k < 3; ++k) {
+            c.o[k] = vertices[3 * i0 + k];
+            c.e1[k] = vertices[3 * i1 + k] - vertices[3 * i0 + k];
+            c.e2[k] = vertices[3 * i2 + k] - vertices[3 * i1 + k];
+            c.n[k] = normals[3 * t + k];
+            c.pad[k] = 0.0;
+        }
+        c.gram = gramians[t];
+    }
+    auto *m = new gcabem_mesh_s();
+    m->device = device;
+    m->nv = nv;
+    m->nt = nt;
+    cudaError_t e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = m->V.upload(vertices, 3 * nv, m->stream);
+    if (e == cudaSuccess) e = m->T.upload(T.data(), T.size(), m->stream);
+    if (e == cudaSuccess) e = m->charts.upload(charts.data(), charts.size(), m->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
+    if (e != cudaSuccess) {
+        gcabem_mesh_destroy(m);
+        GC_CUDA(e);
+    }
+    *out = m;
+    return GCABEM_OK;
+}
+
+int gcabem_mesh_destroy(gcabem_mesh_t mesh) {
+    if (!mesh) return GCABEM_OK;
+    cudaSetDevice(mesh->device);
+    if (mesh->stream) cudaStreamSynchronize(mesh->stream);
+    mesh->V.release();
+    mesh->T.release();
+    mesh->charts.release();
+    if (mesh->stream) cudaStreamDestroy(mesh->stream);
+    delete mesh;
+    return GCABEM_OK;
+}
+
+int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double kappa,
+                            int64_t n, const int64_t *tri_x, const int64_t *tri_y,
+                            const uint8_t *perm_x, const uint8_t *perm_y, int64_t nq,
+                            const double *xs, const double *ys, const double *w, double *out) {
+    GC_ARG(mesh, "null mesh");
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    if (n == 0) return GCABEM_OK;
+    GC_CUDA(cudaSetDevice(mesh->device));
+    std::vector<SingItem> items(n);
+    for (int64_t i = 0; i < n; ++i) {
+        GC_ARG(tri_x[i] >= 0 && tri_x[i] < mesh->nt && tri_y[i] >= 0 && tri_y[i] < mesh->nt,
+               "triangle index out of range");
+        SingItem &it = items[i];
+        std::memset(&it, 0, sizeof it);
+        it.out = i;
+        it.tri_x = (int32_t)tri_x[i];
+        it.tri_y = (int32_t)tri_y[i];
+        for (int k = 0; k < 3; ++k) {
+            it.px[k] = perm_x ? perm_x[3 * i + k] : (uint8_t)k;
+            it.py[k] = perm_y ? perm_y[3 * i + k] : (uint8_t)k;
+            GC_ARG(it.px[k] < 3 && it.py[k] < 3, "bad permutation");
+        }
+    }
+    std::vector<double> rule = pack_rule(nq, xs, ys, w);
+    DevBuf<SingItem> di;
+    DevBuf<double> dr;
+    DevBuf<double2> dout;
+    cudaStream_t s = mesh->stream;
+    GC_CUDA(di.upload(items.data(), n, s));
+    GC_CUDA(dr.upload(rule.data(), rule.size(), s));
+    GC_CUDA(dout.alloc(n));
+    GC_CUDA(launch_generic(kind_of(equation, layer), mesh->V.p, mesh->T.p, mesh->charts.p, di.p,
+                           n, dr.p, nq, dout.p, kappa, s));
+    GC_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+    return GCABEM_OK;
+}
+
+int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa, int disjoint_n,
+                       const double *gauss_pts, const double *gauss_wts, int64_t payload_len,
+                       int64_t nblocks, const int64_t *blocks, int64_t npanels,
+                       const int64_t *panels, int64_t nitems, const int64_t *items,
+                       const uint8_t *perms, const int64_t *sq, const double *const *srule,
+                       gcabem_plan_t *out) {
+    GC_ARG(mesh && out, "null argument");
+    *out = nullptr;
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    GC_ARG(disjoint_n >= 1 && disjoint_n <= MAX_ORDER, "disjoint order outside [1, 12]");
+    GC_ARG(payload_len >= 0 && nblocks >= 0 && npanels >= 0 && nitems >= 0, "negative size");
+    GC_CUDA(cudaSetDevice(mesh->device));
+    if (int rc = ensure_disjoint_rule(mesh->device, disjoint_n, gauss_pts, gauss_wts)) return rc;
+
+    // WorkBlocks -> descriptors + fixed-size tasks (DISJOINT_TPB pairs each)
+    std::vector<BlockDesc> bd(nblocks);
+    std::vector<int2> tasks;
+    for (int64_t b = 0; b < nblocks; ++b) {
+        const int64_t *r = blocks + 6 * b;
+        const int64_t base = r[0], ld = r[1], nr = r[2], nc = r[3], ra = r[4], ca = r[5];
+        GC_ARG(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31), "block too large");
+        GC_ARG(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels,
+               "block panel range out of bounds");
+        GC_ARG(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= payload_len),
+               "block payload range out of bounds");
+        GC_ARG(nblocks < (int64_t(1) << 31), "too many blocks");
+        bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
+        for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
+            tasks.push_back(make_int2((int)b, (int)k0));
+    }
+    std::vector<int32_t> pan(npanels);
+    for (int64_t k = 0; k < npanels; ++k) {
+        GC_ARG(panels[k] >= 0 && panels[k] < mesh->nt, "panel index out of range");
+        pan[k] = (int32_t)panels[k];
+    }
+    // singular items grouped by case 1..3
+    std::vector<SingItem> si(nitems);
+    int64_t counts[4] = {0, 0, 0, 0};
+    for (int64_t k = 0; k < nitems; ++k) {
+        const int64_t c = items[4 * k];
+        GC_ARG(c >= 1 && c <= 3, "singular item case must be vertex/edge/identical");
+        GC_ARG(k == 0 || c >= items[4 * (k - 1)], "singular items must be grouped by case");
+        counts[c]++;
+        SingItem &it = si[k];
+        std::memset(&it, 0, sizeof it);
+        it.out = items[4 * k + 3];
+        GC_ARG(it.out >= 0 && it.out < payload_len, "singular item outside the payload");
+        GC_ARG(items[4 * k + 1] >= 0 && items[4 * k + 1] < mesh->nt && items[4 * k + 2] >= 0 &&
+                   items[4 * k + 2] < mesh->nt,
+               "triangle index out of range");
+        it.tri_x = (int32_t)items[4 * k + 1];
+        it.tri_y = (int32_t)items[4 * k + 2];
+        for (int j = 0; j < 3; ++j) {
+            it.px[j] = perms[6 * k + j];
+            it.py[j] = perms[6 * k + 3 + j];
+            GC_ARG(it.px[j] < 3 && it.py[j] < 3, "bad permutation");
+        }
+    }
+    auto *p = new gcabem_plan_s();
+    p->mesh = mesh;
+    p->kind = kind_of(equation, layer);
+    p->order = disjoint_n;
+    p->kappa = kappa;
+    p->payload_len = payload_len;
+    p->ntasks = (int64_t)tasks.size();
+    p->case_at[0] = 0;
+    for (int c = 1; c <= 3; ++c) p->case_at[c] = p->case_at[c - 1] + counts[c];
+    cudaStream_t s = mesh->stream;
+    cudaError_t e = p->payload.alloc(payload_len);
+    if (e == cudaSuccess) e = p->blocks.upload(bd.data(), bd.size(), s);
+    if (e == cudaSuccess) e = p->tasks.upload(tasks.data(), tasks.size(), s);
+    if (e == cudaSuccess) e = p->panels.upload(pan.data(), pan.size(), s);
+    if (e == cudaSuccess) e = p->items.upload(si.data(), si.size(), s);
+    for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
+        p->sq[c] = sq ? sq[c] : 0;
+        if (p->sq[c] > 0 && counts[c + 1] > 0) e = p->srule[c].upload(srule[c], 5 * p->sq[c], s);
+    }
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    if (e != cudaSuccess) {
+        gcabem_plan_destroy(p);
+        GC_CUDA(e);
+    }
+    for (int c = 0; c < 3; ++c)
+        if (counts[c + 1] > 0 && p->sq[c] <= 0) {
+            gcabem_plan_destroy(p);
+            return set_error(GCABEM_ERR_ARG, "singular items without a rule");
+        }
+    *out = p;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_execute(gcabem_plan_t p) {
+    GC_ARG(p, "null plan");
+    gcabem_mesh_t m = p->mesh;
+    GC_CUDA(cudaSetDevice(m->device));
+    cudaStream_t s = m->stream;
+    if (p->payload_len > 0)
+        GC_CUDA(cudaMemsetAsync(p->payload.p, 0, sizeof(double2) * p->payload_len, s));
+    GC_CUDA(cudaEventRecord(p->ev[0], s));
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, p->blocks.p, p->tasks.p, p->ntasks,
+                            p->panels.p, p->payload.p, p->kappa, s));
+    GC_CUDA(cudaEventRecord(p->ev[1], s));
+    for (int c = 0; c < 3; ++c) {
+        const int64_t n = p->case_at[c + 1] - p->case_at[c];
+        if (n == 0) continue;
+        GC_CUDA(launch_generic(p->kind, m->V.p, m->T.p, m->charts.p, p->items.p + p->case_at[c], n,
+                               p->srule[c].p, p->sq[c], p->payload.p, p->kappa, s));
+    }
+    GC_CUDA(cudaEventRecord(p->ev[2], s));
+    p->executed = true;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_download(gcabem_plan_t p, double *host) {
+    GC_ARG(p && (host || p->payload_len == 0), "null argument");
+    GC_CUDA(cudaSetDevice(p->mesh->device));
+    if (p->payload_len > 0)
+        GC_CUDA(cudaMemcpyAsync(host, p->payload.p, sizeof(double2) * p->payload_len,
+                                cudaMemcpyDeviceToHost, p->mesh->stream));
+    GC_CUDA(cudaStreamSynchronize(p->mesh->stream));
+    return GCABEM_OK;
+}
+
+int gcabem_plan_synchronize(gcabem_plan_t p) {
+    GC_ARG(p, "null plan");
+    GC_CUDA(cudaSetDevice(p->mesh->device));
+    GC_CUDA(cudaStreamSynchronize(p->mesh->stream));
+    return GCABEM_OK;
+}
+
+int gcabem_plan_timing(gcabem_plan_t p, float *ms3) {
+    GC_ARG(p && ms3, "null argument");
+    GC_ARG(p->executed, "plan not executed");
+    GC_CUDA(cudaSetDevice(p->mesh->device));
+    GC_CUDA(cudaEventSynchronize(p->ev[2]));
+    GC_CUDA(cudaEventElapsedTime(&ms3[0], p->ev[0], p->ev[1]));
+    GC_CUDA(cudaEventElapsedTime(&ms3[1], p->ev[1], p->ev[2]));
+    GC_CUDA(cudaEventElapsedTime(&ms3[2], p->ev[0], p->ev[2]));
+    return GCABEM_OK;
+}
+
+int gcabem_plan_payload(gcabem_plan_t p, void **dev_ptr) {
+    GC_ARG(p && dev_ptr, "null argument");
+    *dev_ptr = p->payload.p;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_destroy(gcabem_plan_t p) {
+    if (!p) return GCABEM_OK;
+    cudaSetDevice(p->mesh->device);
+    cudaStreamSynchronize(p->mesh->stream);
+    for (auto &e : p->ev)
+        if (e) cudaEventDestroy(e);
+    delete p;
+    return GCABEM_OK;
+}
+
+int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_t nclusters,
+                          const int64_t *panel_at, const int64_t *panels, int64_t nsrc,
+                          const double *src, int64_t nduffy, const double *duffy,
+                          const int64_t *out_at, int64_t out_len, double *out_host) {
+    GC_ARG(mesh, "null mesh");
+    if (int rc = check_kind(equation, 0, kappa)) return rc;
+    GC_ARG(nclusters >= 0 && nsrc > 0 && nduffy > 0, "bad sizes");
+    if (nclusters == 0) return GCABEM_OK;
+    GC_ARG(nclusters < (int64_t(1) << 31), "too many clusters");
+    GC_CUDA(cudaSetDevice(mesh->device));
+    const int64_t npan = panel_at[nclusters];
+    std::vector<int32_t> pan(npan);
+    for (int64_t k = 0; k < npan; ++k) {
+        GC_ARG(panels[k] >= 0 && panels[k] < mesh->nt, "panel index out of range");
+        pan[k] = (int32_t)panels[k];
+    }
+    std::vector<int2> tasks;
+    for (int64_t c = 0; c < nclusters; ++c) {
+        const int64_t ne = (panel_at[c + 1] - panel_at[c]) * nsrc;
+        GC_ARG(ne >= 0 && ne < (int64_t(1) << 31), "cluster too large");
+        GC_ARG(out_at[c] >= 0 && out_at[c] + ne <= out_len, "output range out of bounds");
+        for (int64_t e0 = 0; e0 < ne; e0 += GREEN_TPB) tasks.push_back(make_int2((int)c, (int)e0));
+    }
+    const int64_t width = equation == 0 ? 1 : 2;
+    cudaStream_t s = mesh->stream;
+    DevBuf<int64_t> dpa, doa;
+    DevBuf<int32_t> dpan;
+    DevBuf<double> dsrc, dduf, dout;
+    DevBuf<int2> dtask;
+    GC_CUDA(dpa.upload(panel_at, nclusters + 1, s));
+    GC_CUDA(doa.upload(out_at, nclusters, s));
+    GC_CUDA(dpan.upload(pan.data(), pan.size(), s));
+    GC_CUDA(dsrc.upload(src, (size_t)(nclusters * nsrc * 8), s));
+    GC_CUDA(dduf.upload(duffy, (size_t)(3 * nduffy), s));
+    GC_CUDA(dtask.upload(tasks.data(), tasks.size(), s));
+    GC_CUDA(dout.alloc((size_t)(out_len * width)));
+    GC_CUDA(launch_green(equation, mesh->charts.p, dtask.p, (int64_t)tasks.size(), dpa.p, dpan.p,
+                         doa.p, (int)nsrc, dsrc.p, dduf.p, (int)nduffy, dout.p, kappa, s));
+    GC_CUDA(cudaMemcpyAsync(out_host, dout.p, sizeof(double) * out_len * width,
+                            cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+    return GCABEM_OK;
+}
+
+int gcabem_fp64_probe(int device, double *tflops) {
+    GC_ARG(tflops, "null argument");
+    GC_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    GC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DevBuf<double> sink;
+    GC_CUDA(sink.alloc(1));
+    cudaEvent_t a, b;
+    GC_CUDA(cudaEventCreate(&a));
+    GC_CUDA(cudaEventCreate(&b));
+    const int iters = 1 << 14, blocks = sms * 8;
+    GC_CUDA(launch_fp64_probe(sink.p, iters, blocks, 0));  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        GC_CUDA(cudaEventRecord(a, 0));
+        GC_CUDA(launch_fp64_probe(sink.p, iters, blocks, 0));
+        GC_CUDA(cudaEventRecord(b, 0));
+        GC_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        GC_CUDA(cudaEventElapsedTime(&ms, a, b));
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 2.0 * 8.0 * iters * (double)blocks * 256.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return GCABEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Shared device-side definitions of the gcabem_b200 library (sm_100a).
+//
+// Data layout in HBM:
+//   Chart[nt]      128 B per triangle = one L2 line: origin, edge1, edge2,
+//                  unit normal, Gramian (mesh.chart_arrays, reference
+//                  mesh.py:207-222, identity permutation; normals/gramians
+//                  from make_surface_mesh mesh.py:111-116).
+//   BlockDesc[]    one per WorkBlock (scheduler.py:87-103).
+//   payload        double2[payload_len]: all block-tree leaves back to back
+//                  in preorder, row-major (make_payloads scheduler.py:411-422).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gcabem {
+
+struct __align__(16) Chart {
+    double o[3], e1[3], e2[3], n[3], gram, pad[3];
+};
+static_assert(sizeof(Chart) == 128, "Chart must be one 128 B line");
+
+struct BlockDesc {
+    int64_t base;     // payload index of entry (0,0)
+    int64_t rows_at;  // offset of the row panels in the panel array
+    int64_t cols_at;  // offset of the column panels
+    int32_t ld;       // payload row stride (leaf ncols)
+    int32_t nr, nc;
+    int32_t pad;
+};
+
+struct SingItem {
+    int64_t out;          // payload index (leaf base + WorkItem.offset)
+    int32_t tri_x, tri_y;
+    uint8_t px[3], py[3]; // classify_pair permutations
+    uint8_t pad[2];
+};
+static_assert(sizeof(SingItem) == 24, "SingItem layout");
+
+enum Kind { L_SLP = 0, L_DLP = 1, H_SLP = 2, H_DLP = 3 };
+constexpr int MAX_ORDER = 12;
+constexpr int DISJOINT_TPB = 128;   // pairs (threads) per disjoint task
+constexpr int GENERIC_TPB = 128;
+constexpr int GREEN_TPB = 128;
+constexpr int RULE_CHUNK = 256;     // rule points staged in shared memory at once
+
+inline int kind_of(int equation, int layer) { return equation * 2 + layer; }
+
+// ---- launchers (kernels.cu) ------------------------------------------------
+cudaError_t upload_disjoint_rule(int order, const double *gauss_pts, const double *gauss_wts);
+cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const BlockDesc *blocks,
+                            const int2 *tasks, int64_t ntasks, const int32_t *panels,
+                            double2 *payload, double kappa, cudaStream_t s);
+// Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
+// index-based batch. Charts gathered with permutations from V/T.
+cudaError_t launch_generic(int kind, const double *V, const int32_t *T, const Chart *charts,
+                           const SingItem *items, int64_t n, const double *rule, int64_t q,
+                           double2 *payload, double kappa, cudaStream_t s);
+// Raw charts (gcabem_pair_values): per pair 22 doubles
+// {ox,e1x,e2x, oy,e1y,e2y, ny} (21) + gx, gy packed as 24 doubles.
+cudaError_t launch_raw(int kind, const double *pairs, int64_t n, const double *rule, int64_t q,
+                       double2 *out, double kappa, cudaStream_t s);
+cudaError_t launch_green(int equation, const Chart *charts, const int2 *tasks, int64_t ntasks,
+                         const int64_t *panel_at, const int32_t *panels, const int64_t *out_at,
+                         int nsrc, const double *src, const double *duffy, int nq, double *out,
+                         double kappa, cudaStream_t s);
+cudaError_t launch_fp64_probe(double *sink, int iters, int blocks, cudaStream_t s);
+
+}  // namespace gcabem

@@ -1,0 +1,335 @@
+"""Green cross approximation: per-cluster interpolation operators.
+
+Drop-in for gcabem.gca (pkg/src/gcabem/gca.py). Per cluster t, monopole and
+dipole sources sit on a tensor Gauss grid over the boundary of the
+(1 + delta)-enlarged box; the Green matrix A_t (panel integrals of those
+source fields) is compressed by partially pivoted ACA; row pivots become
+the interpolation points and V = A_t[:, ct] A_t[tt, ct]^-1.
+
+Split (north_star): the Green matrices of ALL clusters are evaluated in
+batched sm_100a launches (csrc/kernels.cu green_kernel, C ABI
+gcabem_green_matrices); the pivoting (ACA) and the small V solve stay on the
+CPU, overlapped with the next batch of Green matrices on the device.
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .cluster import BlockTree, ClusterTree
+from .device import device_mesh
+from .kernels import KernelSpec
+from .mesh import SurfaceMesh
+from .pairquad import default_device
+from .quadrature import duffy_panel_rule, gauss_legendre
+
+ROLE_MONOPOLE = 0
+ROLE_DIPOLE = 1
+
+DEFAULT_DELTA = 1.0
+DEFAULT_FACE_POINTS = 6
+DEFAULT_EPSILON = 1e-4
+
+_PIVOT_COND_LIMIT = 1e14
+_GREEN_BATCH_BYTES = 1 << 30   # device output per batched launch
+
+
+class GcaError(RuntimeError):
+    """Green cross approximation construction failure (gca.py:43)."""
+
+
+@dataclass(frozen=True)
+class GreenSourceSet:
+    points: np.ndarray   # (P, 3)
+    weights: np.ndarray  # (P,)
+    normals: np.ndarray  # (P, 3)
+    roles: np.ndarray    # (P,) uint8
+
+    def packed(self) -> np.ndarray:
+        """(P, 8) device rows {p, n, w, role}."""
+        return np.column_stack([self.points, self.normals, self.weights,
+                                self.roles.astype(np.float64)])
+
+
+@dataclass(frozen=True)
+class ACAResult:
+    row_pivots: np.ndarray
+    col_pivots: np.ndarray
+    rank: int
+    residual_estimate: float
+
+
+@dataclass(frozen=True)
+class InterpolationOperator:
+    cluster: int
+    pivots_local: np.ndarray
+    pivots_global: np.ndarray
+    V: np.ndarray
+
+    @property
+    def rank(self) -> int:
+        return int(self.V.shape[1])
+
+
+@dataclass(frozen=True)
+class GcaParams:
+    delta: float = DEFAULT_DELTA
+    m: int = DEFAULT_FACE_POINTS
+    epsilon: float = DEFAULT_EPSILON
+    rule_order: int = 3
+
+
+def green_sources(box_lo, box_hi, delta: float, m: int,
+                  scene_diameter: float = 0.0) -> GreenSourceSet:
+    """m x m Gauss points per face of the box grown by delta * (largest
+    half-extent), each point twice (monopole, dipole); face order axis 0,1,2,
+    negative side first (gca.py:83-133)."""
+    if delta <= 0.0:
+        raise ValueError("delta must be > 0")
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    lo = np.asarray(box_lo, dtype=np.float64)
+    hi = np.asarray(box_hi, dtype=np.float64)
+    center = 0.5 * (lo + hi)
+    hmax = 0.5 * max(float(np.max(hi - lo)), 1e-8 * scene_diameter)
+    if hmax <= 0.0:
+        raise ValueError("degenerate box with no scene diameter to fall back on")
+    half = 0.5 * (hi - lo) + delta * hmax
+    g = gauss_legendre(m)
+    wuv = (np.repeat(g.weights, m) * np.tile(g.weights, m))
+    P, W, N = [], [], []
+    for axis in range(3):
+        a1, a2 = (axis + 1) % 3, (axis + 2) % 3
+        u = -half[a1] + 2.0 * half[a1] * g.points
+        v = -half[a2] + 2.0 * half[a2] * g.points
+        face_w = wuv * (4.0 * half[a1] * half[a2])
+        for sign in (-1.0, 1.0):
+            pts = np.empty((m * m, 3))
+            pts[:, axis] = center[axis] + sign * half[axis]
+            pts[:, a1] = center[a1] + np.repeat(u, m)
+            pts[:, a2] = center[a2] + np.tile(v, m)
+            nrm = np.zeros((m * m, 3))
+            nrm[:, axis] = sign
+            P.append(np.repeat(pts, 2, axis=0))
+            W.append(np.repeat(face_w, 2))
+            N.append(np.repeat(nrm, 2, axis=0))
+    roles = np.tile(np.array([ROLE_MONOPOLE, ROLE_DIPOLE], dtype=np.uint8), 6 * m * m)
+    return GreenSourceSet(np.concatenate(P), np.concatenate(W), np.concatenate(N), roles)
+
+
+def build_green_matrices(mesh: SurfaceMesh, panel_lists, source_sets, spec: KernelSpec,
+                         order: int = 3, device: int | None = None) -> list:
+    """Green matrices of many clusters in one device launch (gca.py:136-179).
+
+    A[i, j] = w_j * integral over panel i of source field j: monopole
+    columns use the single layer of spec.equation, dipole columns its
+    derivative along the source normal (d = x - source). float64 for
+    Laplace, complex128 for Helmholtz.
+    """
+    device = default_device() if device is None else device
+    ncl = len(panel_lists)
+    if ncl == 0:
+        return []
+    nsrc = len(source_sets[0].weights)
+    if any(len(s.weights) != nsrc for s in source_sets):
+        raise ValueError("all source sets of one batch must have the same size")
+    dm = device_mesh(mesh, device)
+    sizes = np.array([len(p) for p in panel_lists], dtype=np.int64)
+    panel_at = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    panels = np.concatenate([np.asarray(p, dtype=np.int64) for p in panel_lists]) \
+        if sizes.sum() else np.empty(0, np.int64)
+    out_at = (panel_at[:-1] * nsrc).astype(np.int64)
+    out_len = int(panel_at[-1] * nsrc)
+    src = np.ascontiguousarray(np.stack([s.packed() for s in source_sets]))
+    pts, wq = duffy_panel_rule(order)
+    duffy = np.ascontiguousarray(np.column_stack([pts, wq]))
+    complex_out = spec.is_complex
+    flat = np.empty(out_len * (2 if complex_out else 1), dtype=np.float64)
+    eq = 0 if spec.equation == "laplace" else 1
+    nat.check(nat.lib().gcabem_green_matrices(
+        dm.handle, eq, float(spec.kappa), ncl, nat.ptr(panel_at), nat.ptr(panels), nsrc,
+        nat.ptr(src), duffy.shape[0], nat.ptr(duffy), nat.ptr(out_at), out_len,
+        nat.ptr(flat)))
+    vals = flat.view(np.complex128) if complex_out else flat
+    out = []
+    for c in range(ncl):
+        A = vals[out_at[c]:out_at[c] + sizes[c] * nsrc].reshape(sizes[c], nsrc)
+        if not np.all(np.isfinite(A)):
+            raise GcaError("source coincides with a panel quadrature point")
+        out.append(A)
+    return out
+
+
+def build_green_matrix(mesh: SurfaceMesh, panels, sources: GreenSourceSet, spec: KernelSpec,
+                       order: int = 3) -> np.ndarray:
+    """One cluster's Green matrix (gca.py:136), on the device."""
+    return build_green_matrices(mesh, [np.asarray(panels, dtype=np.int64)], [sources],
+                                spec, order)[0]
+
+
+def aca(matrix: np.ndarray, epsilon: float, max_rank: int | None = None) -> ACAResult:
+    """Partially pivoted ACA (gca.py:182-245): next row = largest residual
+    column entry among unused rows, next column = largest residual row entry
+    (ties to the lowest index); stop when |u||v| <= eps * sqrt(estimate)."""
+    if epsilon <= 0.0:
+        raise ValueError("epsilon must be > 0")
+    A = np.asarray(matrix)
+    nr, nc = A.shape
+    cap = min(nr, nc) if max_rank is None else min(max_rank, nr, nc)
+    dtype = np.result_type(A.dtype, np.float64)
+    U: list = []
+    W: list = []
+    rows: list = []
+    cols: list = []
+    taken = np.zeros(nr, dtype=bool)
+    est2 = 0.0
+    resid = 0.0
+    cand = 0
+    while len(rows) < cap:
+        if cand >= nr or taken[cand]:
+            free = np.flatnonzero(~taken)
+            if free.size == 0:
+                break
+            cand = int(free[0])
+        i = cand
+        r = A[i, :].astype(dtype, copy=True)
+        for u, w in zip(U, W):
+            r -= u[i] * w
+        j = int(np.argmax(np.abs(r)))
+        taken[i] = True
+        if r[j] == 0.0:
+            cand = nr
+            continue
+        w = r / r[j]
+        c = A[:, j].astype(dtype, copy=True)
+        for u, ww in zip(U, W):
+            c -= ww[j] * u
+        U.append(c)
+        W.append(w)
+        rows.append(i)
+        cols.append(j)
+        nu = float(np.linalg.norm(c))
+        nw = float(np.linalg.norm(w))
+        mix = 0.0
+        for u, ww in zip(U[:-1], W[:-1]):
+            mix += (np.vdot(u, c) * np.vdot(ww, w)).real
+        est2 = max(est2 + nu * nu * nw * nw + 2.0 * mix, 0.0)
+        resid = nu * nw
+        if resid <= epsilon * np.sqrt(est2):
+            break
+        mag = np.abs(c)
+        mag[taken] = 0.0
+        cand = int(np.argmax(mag))
+        if mag[cand] == 0.0:
+            cand = nr
+    return ACAResult(np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64),
+                     len(rows), resid)
+
+
+def _solve_with_refinement(A_cols: np.ndarray, pivot_block: np.ndarray) -> np.ndarray:
+    """V = A_cols inv(pivot_block) plus two refinement sweeps (gca.py:248-256)."""
+    V = np.linalg.solve(pivot_block.T, A_cols.T).T
+    for _ in range(2):
+        R = A_cols - V @ pivot_block
+        if np.max(np.abs(R)) <= 1e-15 * max(np.max(np.abs(A_cols)), 1.0):
+            break
+        V = V + np.linalg.solve(pivot_block.T, R.T).T
+    return V
+
+
+def _operator_from_green(cluster_index: int, panels: np.ndarray, A: np.ndarray,
+                         epsilon: float) -> InterpolationOperator:
+    """ACA + pivot solve with one tighter retry (gca.py:268-282)."""
+    eps = epsilon
+    for _ in range(2):
+        res = aca(A, eps)
+        if res.rank == 0:
+            raise GcaError(f"cluster {cluster_index}: zero Green matrix")
+        block = A[np.ix_(res.row_pivots, res.col_pivots)]
+        if np.linalg.cond(block) <= _PIVOT_COND_LIMIT:
+            V = _solve_with_refinement(A[:, res.col_pivots], block)
+            return InterpolationOperator(cluster_index, res.row_pivots,
+                                         panels[res.row_pivots], V)
+        eps *= 0.1
+    raise GcaError(f"cluster {cluster_index}: singular ACA pivot block "
+                   f"(condition above {_PIVOT_COND_LIMIT:.0e})")
+
+
+def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, box_lo, box_hi,
+                                 spec: KernelSpec, params: GcaParams,
+                                 scene_diameter: float = 0.0) -> InterpolationOperator:
+    """One cluster: sources, device Green matrix, host ACA (gca.py:259-282)."""
+    panels = np.asarray(panels, dtype=np.int64)
+    src = green_sources(box_lo, box_hi, params.delta, params.m, scene_diameter)
+    A = build_green_matrix(mesh, panels, src, spec, params.rule_order)
+    return _operator_from_green(cluster_index, panels, A, params.epsilon)
+
+
+def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device) -> dict:
+    """Batched device Green matrices, host ACA of batch k overlapped with the
+    device evaluation of batch k+1 (ctypes releases the GIL)."""
+    ids = sorted(ids)
+    nsrc = 12 * params.m * params.m
+    width = 16 if spec.is_complex else 8
+    batches, cur, cur_bytes = [], [], 0
+    for cid in ids:
+        nb = tree.nodes[cid].size * nsrc * width
+        if cur and cur_bytes + nb > _GREEN_BATCH_BYTES:
+            batches.append(cur)
+            cur, cur_bytes = [], 0
+        cur.append(cid)
+        cur_bytes += nb
+    if cur:
+        batches.append(cur)
+
+    def run(batch):
+        pl = [tree.panels(tree.nodes[c]) for c in batch]
+        ss = [green_sources(tree.nodes[c].lo, tree.nodes[c].hi, params.delta, params.m, scene)
+              for c in batch]
+        return pl, build_green_matrices(mesh, pl, ss, spec, params.rule_order, device)
+
+    ops: dict = {}
+    result: dict = {}
+
+    def worker(k):
+        try:
+            result[k] = run(batches[k])
+        except BaseException as exc:  # surfaced on the host thread
+            result[k] = exc
+
+    th = None
+    if batches:
+        th = threading.Thread(target=worker, args=(0,))
+        th.start()
+    for k in range(len(batches)):
+        th.join()
+        got = result.pop(k)
+        if isinstance(got, BaseException):
+            raise got
+        if k + 1 < len(batches):
+            th = threading.Thread(target=worker, args=(k + 1,))
+            th.start()
+        pl, As = got
+        for cid, panels, A in zip(batches[k], pl, As):
+            ops[cid] = _operator_from_green(cid, panels, A, params.epsilon)
+    return ops
+
+
+def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
+                                  params: GcaParams, device: int | None = None):
+    """Operators for every cluster in an admissible block (gca.py:285-310);
+    (row_ops, col_ops) — the same dict for a shared cluster tree."""
+    device = default_device() if device is None else device
+    scene = mesh.diameter()
+    row_ids = {b.row for b in block_tree.leaves if b.kind == "admissible"}
+    col_ids = {b.col for b in block_tree.leaves if b.kind == "admissible"}
+    if block_tree.row_tree is block_tree.col_tree:
+        ops = _ops_for_tree(mesh, block_tree.row_tree, row_ids | col_ids, spec, params, scene,
+                            device)
+        return ops, ops
+    return (_ops_for_tree(mesh, block_tree.row_tree, row_ids, spec, params, scene, device),
+            _ops_for_tree(mesh, block_tree.col_tree, col_ids, spec, params, scene, device))
+

@@ -1,0 +1,90 @@
+"""Compressed operator container (drop-in for gcabem.h2, pkg/src/gcabem/h2.py).
+
+GCAMatrix.payloads maps block-leaf index -> complex128 C-ordered array,
+dense (|t|, |s|) or coupling (rank_t, rank_s), exactly as the reference
+(h2.py:28-46). On this implementation every payload is a VIEW into one
+contiguous buffer (leaves in block-tree preorder, row-major), the host
+image of the device payload the kernels write; ``buffer`` exposes it.
+"""
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .cluster import BlockTree
+
+DENSE_EXPANSION_CAP = 4096
+
+
+@dataclass
+class GCAMatrix:
+    block_tree: BlockTree
+    row_ops: dict
+    col_ops: dict
+    payloads: dict
+    buffer: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (len(self.block_tree.row_tree.permutation),
+                len(self.block_tree.col_tree.permutation))
+
+    def checksum(self) -> str:
+        """sha256 over all leaf payloads in block-tree preorder (h2.py:40-46)."""
+        h = hashlib.sha256()
+        for leaf in self.block_tree.leaves:
+            h.update(np.ascontiguousarray(self.payloads[leaf.index]).tobytes())
+        return h.hexdigest()
+
+
+def _coupling_block(M: GCAMatrix, leaf) -> np.ndarray:
+    return M.row_ops[leaf.row].V @ M.payloads[leaf.index] @ M.col_ops[leaf.col].V.T
+
+
+def matvec(M: GCAMatrix, x: np.ndarray) -> np.ndarray:
+    """y = M x, leaves accumulated in preorder (h2.py:49-71). The column-side
+    operator is conj(V_s), so its conjugate transpose is the plain V_s^T."""
+    rows, cols = M.shape
+    x = np.asarray(x)
+    if x.shape != (cols,):
+        raise ValueError(f"dimension mismatch: operator {M.shape}, vector {x.shape}")
+    rt, ct = M.block_tree.row_tree, M.block_tree.col_tree
+    xp = np.asarray(x, dtype=np.complex128)[ct.permutation]
+    yp = np.zeros(rows, dtype=np.complex128)
+    for leaf in M.block_tree.leaves:
+        t, s = rt.nodes[leaf.row], ct.nodes[leaf.col]
+        xs = xp[s.start:s.start + s.size]
+        P = M.payloads[leaf.index]
+        if leaf.kind == "dense":
+            yp[t.start:t.start + t.size] += P @ xs
+        else:
+            yp[t.start:t.start + t.size] += M.row_ops[leaf.row].V @ (P @ (M.col_ops[leaf.col].V.T @ xs))
+    y = np.empty(rows, dtype=np.complex128)
+    y[rt.permutation] = yp
+    return y
+
+
+def to_dense(M: GCAMatrix, cap: int = DENSE_EXPANSION_CAP) -> np.ndarray:
+    """Expand every leaf into the global matrix (verification; h2.py:74-93)."""
+    rows, cols = M.shape
+    if rows > cap or cols > cap:
+        raise ValueError(f"matrix {rows}x{cols} exceeds the expansion cap {cap}")
+    rt, ct = M.block_tree.row_tree, M.block_tree.col_tree
+    G = np.zeros((rows, cols), dtype=np.complex128)
+    for leaf in M.block_tree.leaves:
+        t, s = rt.nodes[leaf.row], ct.nodes[leaf.col]
+        blk = M.payloads[leaf.index] if leaf.kind == "dense" else _coupling_block(M, leaf)
+        G[np.ix_(rt.permutation[t.start:t.start + t.size],
+                 ct.permutation[s.start:s.start + s.size])] = blk
+    return G
+
+
+def storage_bytes(M: GCAMatrix) -> dict:
+    """Byte footprint by component (h2.py:96-105)."""
+    near = sum(M.payloads[l.index].nbytes for l in M.block_tree.leaves if l.kind == "dense")
+    coup = sum(M.payloads[l.index].nbytes for l in M.block_tree.leaves if l.kind == "admissible")
+    ops = {id(op): op for op in list(M.row_ops.values()) + list(M.col_ops.values())}
+    bases = sum(op.V.nbytes + op.pivots_global.nbytes for op in ops.values())
+    return {"near": near, "coupling": coup, "bases": bases, "total": near + coup + bases}

@@ -1,0 +1,416 @@
+"""Case-homogeneous work packages executed on B200s (drop-in for gcabem.scheduler).
+
+Reference: pkg/src/gcabem/scheduler.py (paper Alg. 1-4). The host builds
+exactly the reference's packages — disjoint lists of WorkBlocks under the
+byte budget, corrective singular lists from the shared-vertex scan of
+flagged blocks — and the device executes them: one fused launch runs every
+disjoint list straight into a device-resident payload buffer (all leaves
+back to back), then one launch per singular case overwrites the corrected
+entries (the overwrite protocol, scheduler.py:9-12, :488-494: stream order
+gives the happens-before). One D2H returns the payload into pinned host
+memory; GCAMatrix.payloads are views into it.
+
+The reference's worker threads and queues (:264-408) have no counterpart:
+the device is the worker pool. With several devices, leaves are statically
+partitioned (no exchange step exists). There is no CPU backend: a missing
+library or device raises BackendError.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import _native as nat
+from ._native import BackendError
+from .cluster import BlockTree
+from .device import DeviceMesh, device_mesh
+from .h2 import GCAMatrix
+from .kernels import KernelSpec
+from .mesh import SurfaceMesh
+from .packaging import (BYTES_PER_PAIR, PAIR_RECORD_BYTES, SINGULAR_CASES, VALUE_BYTES,
+                        AssemblyPackages, SchedulerConfigError, make_packages, shard_leaves)
+from .quadrature import QuadRule4D, build_rule, classify_pair, gauss_legendre
+
+DEFAULT_MAXSIZE = 8 * 2 ** 20
+_CASE_OF_SHARED = {1: "vertex", 2: "edge", 3: "identical"}
+
+__all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "AssemblyStats",
+           "split_block", "ListBuilder", "batch_quadrature", "execute_list", "run_assembly",
+           "make_payloads", "BackendError", "SchedulerConfigError", "CUDA_BACKEND",
+           "BATCH_BACKEND", "SCALAR_BACKEND", "DEFAULT_MAXSIZE", "BYTES_PER_PAIR",
+           "PAIR_RECORD_BYTES", "VALUE_BYTES", "SINGULAR_CASES", "AssemblyPlan"]
+
+
+@dataclass(frozen=True)
+class Backend:
+    """Execution target. kind "cuda" is the only kind: the sm_100a kernels on
+    `devices` (reference Backend scheduler.py:51-66 had host kinds only)."""
+    name: str
+    kind: str = "cuda"
+    affinity: str = ""
+    devices: tuple = (0,)
+
+    def __post_init__(self):
+        if self.kind != "cuda":
+            raise SchedulerConfigError(
+                f"unknown backend kind {self.kind!r} (this build executes on CUDA only)")
+        if not self.affinity:
+            object.__setattr__(self, "affinity", self.name)
+        if not self.devices:
+            raise SchedulerConfigError("backend needs at least one device")
+
+
+CUDA_BACKEND = Backend("cuda")
+# Reference names kept so reference-style configs resolve; both run on CUDA.
+SCALAR_BACKEND = Backend("scalar")
+BATCH_BACKEND = Backend("batch")
+
+
+@dataclass(frozen=True)
+class SchedulerParams:
+    """scheduler.py:69-84. workers_per_backend is accepted for API
+    compatibility; 0 still means inline (synchronous) execution order."""
+    maxsize_bytes: int = DEFAULT_MAXSIZE
+    workers_per_backend: int = 2
+    backends: tuple = (CUDA_BACKEND,)
+    affinity: dict = field(default_factory=lambda: {
+        "disjoint": "cuda", "vertex": "cuda", "edge": "cuda", "identical": "cuda"})
+
+    def backend_for(self, case: str) -> Backend:
+        wanted = self.affinity.get(case)
+        for b in self.backends:
+            if b.name == wanted:
+                return b
+        return self.backends[0]
+
+
+@dataclass
+class WorkBlock:
+    """Disjoint-list item (scheduler.py:87-103)."""
+    leaf_id: int
+    row_panels: np.ndarray
+    col_panels: np.ndarray
+    row_slots: np.ndarray
+    col_slots: np.ndarray
+    flagged: bool
+
+    @property
+    def num_pairs(self) -> int:
+        return len(self.row_panels) * len(self.col_panels)
+
+    @property
+    def nbytes(self) -> int:
+        return self.num_pairs * BYTES_PER_PAIR
+
+
+@dataclass(frozen=True)
+class WorkItem:
+    """Singular corrective item (scheduler.py:106-117)."""
+    case: str
+    tri_x: int
+    tri_y: int
+    leaf_id: int
+    offset: int
+
+    @property
+    def nbytes(self) -> int:
+        return BYTES_PER_PAIR
+
+
+@dataclass
+class WorkList:
+    case: str
+    items: list
+    nbytes: int = 0
+    state: str = "filling"
+    seq: int = -1
+    attempts: int = 0
+    backend: str = ""
+    t_enqueue: float = 0.0
+    t_dequeue: float = 0.0
+    t_done: float = 0.0
+
+    @property
+    def num_pairs(self) -> int:
+        if self.case == "disjoint":
+            return sum(b.num_pairs for b in self.items)
+        return len(self.items)
+
+
+@dataclass
+class AssemblyStats:
+    lists_executed: int = 0
+    pairs_executed: int = 0
+    block_pairs: int = 0
+    corrective_items: int = 0
+    events: list = field(default_factory=list)
+    device_ms: dict = field(default_factory=dict)
+
+    def event_rows(self):
+        return list(self.events)
+
+
+def split_block(block: WorkBlock, maxsize: int) -> list:
+    """Halve the longer index dimension until each part fits (scheduler.py:153-175)."""
+    if block.nbytes <= maxsize:
+        return [block]
+    if block.num_pairs <= 1:
+        raise SchedulerConfigError(
+            f"maxsize {maxsize} smaller than one pair record ({BYTES_PER_PAIR} B)")
+    if len(block.row_panels) >= len(block.col_panels):
+        h = len(block.row_panels) // 2
+        halves = [replace(block, row_panels=block.row_panels[s], row_slots=block.row_slots[s])
+                  for s in (slice(None, h), slice(h, None))]
+    else:
+        h = len(block.col_panels) // 2
+        halves = [replace(block, col_panels=block.col_panels[s], col_slots=block.col_slots[s])
+                  for s in (slice(None, h), slice(h, None))]
+    return [p for half in halves for p in split_block(half, maxsize)]
+
+
+class ListBuilder:
+    """Byte-budgeted list accumulation (scheduler.py:178-208)."""
+
+    def __init__(self, case: str, maxsize: int, sink):
+        if maxsize < BYTES_PER_PAIR:
+            raise SchedulerConfigError(
+                f"maxsize {maxsize} smaller than one pair record ({BYTES_PER_PAIR} B)")
+        self.case, self.maxsize, self.sink = case, maxsize, sink
+        self.current = WorkList(case, [])
+
+    def add_block(self, block: WorkBlock) -> None:
+        for part in split_block(block, self.maxsize):
+            self._add(part, part.nbytes)
+
+    def add_item(self, item: WorkItem) -> None:
+        self._add(item, item.nbytes)
+
+    def _add(self, item, nbytes: int) -> None:
+        if self.current.nbytes + nbytes > self.maxsize and self.current.items:
+            self.flush()
+        self.current.items.append(item)
+        self.current.nbytes += nbytes
+
+    def flush(self) -> None:
+        if self.current.items:
+            done, self.current = self.current, WorkList(self.case, [])
+            done.state = "ready"
+            self.sink(done)
+
+
+def make_payloads(block_tree: BlockTree, row_ops, col_ops) -> dict:
+    """Zeroed payloads per leaf (scheduler.py:411-422)."""
+    out = {}
+    for leaf in block_tree.leaves:
+        if leaf.kind == "dense":
+            shape = (block_tree.row_tree.nodes[leaf.row].size,
+                     block_tree.col_tree.nodes[leaf.col].size)
+        else:
+            shape = (row_ops[leaf.row].rank, col_ops[leaf.col].rank)
+        out[leaf.index] = np.zeros(shape, dtype=np.complex128)
+    return out
+
+
+def batch_quadrature(backend: Backend, case: str, mesh: SurfaceMesh, spec: KernelSpec,
+                     rule: QuadRule4D, tri_x, tri_y, perms_x=None, perms_y=None) -> np.ndarray:
+    """One case-homogeneous batch of pair integrals on the device
+    (scheduler.py:235-261): charts gathered on device from (tri, perm)."""
+    dm = device_mesh(mesh, backend.devices[0])
+    tx, ty = nat.i64(tri_x), nat.i64(tri_y)
+    n = tx.shape[0]
+    out = np.empty(n, dtype=np.complex128)
+    if n == 0:
+        return out
+    px = None if perms_x is None else nat.u8(perms_x)
+    py = None if perms_y is None else nat.u8(perms_y)
+    eq, layer = spec.code
+    xs, ys, w = nat.f64(rule.x_points), nat.f64(rule.y_points), nat.f64(rule.weights)
+    nat.check(nat.lib().gcabem_batch_quadrature(
+        dm.handle, eq, layer, float(spec.kappa), n, nat.ptr(tx), nat.ptr(ty), nat.ptr(px),
+        nat.ptr(py), w.shape[0], nat.ptr(xs), nat.ptr(ys), nat.ptr(w), nat.ptr(out)))
+    return out
+
+
+def execute_list(lst: WorkList, backend: Backend, mesh: SurfaceMesh, spec: KernelSpec,
+                 orders, payloads: dict, on_corrective=None) -> None:
+    """Run ONE list on the device and distribute (scheduler.py:368-395, :334-365).
+    run_assembly does not go through here (it fuses all lists); this is the
+    per-list API for callers that drive lists themselves."""
+    lst.t_dequeue = time.monotonic()
+    lst.attempts += 1
+    if lst.items:
+        if lst.case == "disjoint":
+            tx = np.concatenate([np.repeat(b.row_panels, len(b.col_panels)) for b in lst.items])
+            ty = np.concatenate([np.tile(b.col_panels, len(b.row_panels)) for b in lst.items])
+            vals = batch_quadrature(backend, "disjoint", mesh, spec,
+                                    build_rule("disjoint", orders[0]), tx, ty)
+            pos = 0
+            tri = mesh.triangles
+            for blk in lst.items:
+                nr, nc = len(blk.row_panels), len(blk.col_panels)
+                P = payloads[blk.leaf_id]
+                P[np.ix_(blk.row_slots, blk.col_slots)] = vals[pos:pos + nr * nc].reshape(nr, nc)
+                pos += nr * nc
+                if not blk.flagged:
+                    continue
+                ta, tb = tri[blk.row_panels], tri[blk.col_panels]
+                shared = sum((ta[:, a][:, None] == tb[:, b][None, :]).astype(np.int8)
+                             for a in range(3) for b in range(3))
+                for a, b in np.argwhere(shared > 0):
+                    item = WorkItem(_CASE_OF_SHARED[int(shared[a, b])], int(blk.row_panels[a]),
+                                    int(blk.col_panels[b]), blk.leaf_id,
+                                    int(blk.row_slots[a]) * P.shape[1] + int(blk.col_slots[b]))
+                    if on_corrective is not None:
+                        on_corrective(item)
+        else:
+            cls = [classify_pair(mesh, it.tri_x, it.tri_y) for it in lst.items]
+            vals = batch_quadrature(
+                backend, lst.case, mesh, spec, build_rule(lst.case, orders[1]),
+                [it.tri_x for it in lst.items], [it.tri_y for it in lst.items],
+                np.array([c.perm_x for c in cls]), np.array([c.perm_y for c in cls]))
+            for it, v in zip(lst.items, vals):
+                payloads[it.leaf_id].flat[it.offset] = v
+    lst.state = "done"
+    lst.t_done = time.monotonic()
+
+
+# ---------------------------------------------------------------------------
+# fused device execution
+
+class AssemblyPlan:
+    """Device plan of one operator on one device: packages uploaded once,
+    executable repeatedly (C ABI gcabem_plan_*). Payload stays in HBM until
+    download()."""
+
+    def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
+                 leaf_range=None):
+        lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
+        self.leaf_range = (lo, hi)
+        self.payload_offset = int(pk.leaf_base[lo])
+        self.payload_len = int(pk.leaf_base[hi] - pk.leaf_base[lo])
+        blocks = pk.device_blocks(lo, hi)
+        items, perms = pk.device_items(lo, hi)
+        self.disjoint_pairs = int(np.sum(blocks[:, 2] * blocks[:, 3])) if blocks.size else 0
+        self.singular_counts = [int(np.count_nonzero(items[:, 0] == c)) for c in (1, 2, 3)]
+        dn, sn = orders
+        g = gauss_legendre(dn)
+        gp, gw = nat.f64(g.points), nat.f64(g.weights)
+        rules = [build_rule(c, sn).packed() for c in SINGULAR_CASES]
+        self.singular_q = [r.shape[0] for r in rules]
+        sq = np.array(self.singular_q, dtype=np.int64)
+        rptr = (ctypes.c_void_p * 3)(*[r.ctypes.data for r in rules])
+        eq, layer = spec.code
+        self.spec, self.orders, self.device = spec, tuple(orders), dm.device
+        self._dm = dm
+        self.h2d_bytes = int(blocks.nbytes + pk.panels.nbytes + items.nbytes + perms.nbytes
+                             + sum(r.nbytes for r in rules))
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().gcabem_plan_create(
+            dm.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw),
+            self.payload_len, blocks.shape[0], nat.ptr(blocks), pk.panels.size,
+            nat.ptr(pk.panels), items.shape[0], nat.ptr(items), nat.ptr(perms), nat.ptr(sq),
+            ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
+        self.handle = h.value
+        self._keep = rules
+
+    def execute(self) -> None:
+        nat.check(nat.lib().gcabem_plan_execute(self.handle))
+
+    def synchronize(self) -> None:
+        nat.check(nat.lib().gcabem_plan_synchronize(self.handle))
+
+    def download(self, out: np.ndarray) -> None:
+        """Copy the payload into `out` (complex128, payload_len, ideally pinned)."""
+        if out.dtype != np.complex128 or out.size != self.payload_len or \
+                not out.flags.c_contiguous:
+            raise ValueError("download target must be contiguous complex128 of payload_len")
+        nat.check(nat.lib().gcabem_plan_download(self.handle, nat.ptr(out)))
+
+    def timing_ms(self) -> dict:
+        ms = (ctypes.c_float * 3)()
+        nat.check(nat.lib().gcabem_plan_timing(self.handle, ms))
+        return {"disjoint": ms[0], "singular": ms[1], "total": ms[2]}
+
+    def flops(self) -> dict:
+        """Algorithmic FP64 flops of one execute (SURVEY §8(d) convention)."""
+        from .roofline import pair_flops
+        dq = self.orders[0] ** 4
+        dis = pair_flops(self.spec, "disjoint", dq) * self.disjoint_pairs
+        sing = sum(pair_flops(self.spec, "singular", q) * n
+                   for q, n in zip(self.singular_q, self.singular_counts))
+        return {"disjoint": dis, "singular": sing}
+
+    def close(self) -> None:
+        h, self.handle = getattr(self, "handle", None), None
+        if h and nat._lib is not None:
+            nat._lib.gcabem_plan_destroy(h)
+
+    def __del__(self):
+        self.close()
+
+
+def _events(pk: AssemblyPackages, backend: str, t0: float, t1: float) -> list:
+    """One row per executed list (scheduler.py:303-315), in inline order."""
+    rows = []
+    npairs = pk.blk_nr * pk.blk_nc
+    per_list = np.bincount(pk.blk_list, weights=npairs, minlength=pk.n_disjoint_lists)
+    nblk = np.bincount(pk.blk_list, minlength=pk.n_disjoint_lists)
+    for k in range(pk.n_disjoint_lists):
+        p = int(per_list[k])
+        rows.append({"case": "disjoint", "items": int(nblk[k]), "pairs": p,
+                     "bytes": p * BYTES_PER_PAIR, "backend": backend, "enqueue": t0,
+                     "dequeue": t0, "done": t1})
+    for case, ranges in pk.singular_lists().items():
+        for a, b in ranges:
+            rows.append({"case": case, "items": b - a, "pairs": b - a,
+                         "bytes": (b - a) * BYTES_PER_PAIR, "backend": backend,
+                         "enqueue": t0, "dequeue": t0, "done": t1})
+    return rows
+
+
+def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
+                 row_ops: dict, col_ops: dict, params: SchedulerParams | None = None,
+                 orders: tuple = (3, 5), stats: AssemblyStats | None = None) -> GCAMatrix:
+    """Assemble the compressed operator (scheduler.py:442-505) on the device(s)."""
+    params = params or SchedulerParams()
+    stats = stats if stats is not None else AssemblyStats()
+    if not params.backends:
+        raise SchedulerConfigError("at least one backend required")
+    backend = params.backend_for("disjoint")
+    t0 = time.monotonic()
+    pk = make_packages(mesh.triangles, block_tree, row_ops, col_ops, params.maxsize_bytes)
+    payload = nat.pinned_empty(pk.payload_len, np.complex128)
+    devices = list(backend.devices)
+    shards = shard_leaves(pk, len(devices), orders[0] ** 4,
+                          [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES])
+    plans = []
+    try:
+        for dev, rng in zip(devices, shards):
+            plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng))
+        for p in plans:
+            p.execute()
+        for p in plans:
+            if p.payload_len:
+                p.download(payload[p.payload_offset:p.payload_offset + p.payload_len])
+            else:
+                p.synchronize()
+        stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans}
+    finally:
+        for p in plans:
+            p.close()
+    t1 = time.monotonic()
+    stats.block_pairs += pk.block_pairs()
+    stats.corrective_items += pk.num_items
+    ev = _events(pk, backend.name, t0, t1)
+    stats.events.extend(ev)
+    stats.lists_executed += len(ev)
+    stats.pairs_executed += sum(r["pairs"] for r in ev)
+    payloads = {}
+    for k in range(pk.leaf_ids.size):
+        a, b = int(pk.leaf_base[k]), int(pk.leaf_base[k + 1])
+        payloads[int(pk.leaf_ids[k])] = payload[a:b].reshape(tuple(pk.leaf_shape[k]))
+    return GCAMatrix(block_tree, row_ops, col_ops, payloads, buffer=payload)
+

@@ -1,0 +1,271 @@
+"""GPU parity: the sm_100a path through the C ABI against the oracle/golden.
+
+Tolerance (north_star): entries within 1e-12 relative in FP64; reference
+roundoff entries (|ref| < 1e-9 * leaf max, e.g. DLP identical pairs) within
+1e-12 of the leaf-block max. Integer packaging is
+bit-exact (tests/test_host.py).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import (SPECS, golden_ops, oracle_assemble, p2_check, packages_for,
+                     sphere_setup)
+from paper_1510_07244_b200 import (cluster, gca, kernels, mesh, packaging, pairquad,
+                                   quadrature, scheduler, solver)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel_err(got, ref):
+    mag = np.abs(ref)
+    scale = np.where(mag < 1e-9 * mag.max(), mag.max(), mag)
+    return float(np.max(np.abs(got - ref) / scale))
+
+
+def spec_of(name):
+    eq, layer, kappa = SPECS[name]
+    return kernels.KernelSpec(eq, layer, kappa)
+
+
+@pytest.fixture(scope="module")
+def pv(gload):
+    return gload("pair_values_L3.npz")
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_pair_values_raw_charts(pv, name):
+    """pairquad.pair_values (pairquad.py:95) on caller charts vs the reference."""
+    spec = spec_of(name)
+    for rn in (3, 5):
+        r = quadrature.build_rule("disjoint", rn)
+        a = [pv[f"raw_{k}"] for k in ("ox", "e1x", "e2x", "gx", "oy", "e1y", "e2y", "gy")]
+        got = pairquad.pair_values(spec, *a, pv["raw_ny"] if spec.needs_normal else None,
+                                   r.x_points, r.y_points, r.weights)
+        assert rel_err(got, pv[f"raw_{rn}_{name}"]) <= TOL
+
+
+@pytest.mark.parametrize("case", ["disjoint", "vertex", "edge", "identical"])
+@pytest.mark.parametrize("name", list(SPECS))
+def test_batch_quadrature_golden(pv, case, name):
+    """scheduler.batch_quadrature (scheduler.py:235) on device vs reference outputs."""
+    m = mesh.build_sphere_mesh(3)
+    spec = spec_of(name)
+    orders = (1, 2, 3, 4, 5, 7) if case == "disjoint" else (2, 3, 5, 7)
+    px = pv[f"{case}_perm_x"] if case != "disjoint" else None
+    py = pv[f"{case}_perm_y"] if case != "disjoint" else None
+    for n in orders:
+        got = scheduler.batch_quadrature(scheduler.CUDA_BACKEND, case, m, spec,
+                                         quadrature.build_rule(case, n), pv[f"{case}_tri_x"],
+                                         pv[f"{case}_tri_y"], px, py)
+        assert rel_err(got, pv[f"{case}_{n}_{name}"]) <= TOL, (case, n)
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+@pytest.mark.parametrize("orders", [(3, 5), (2, 3), (4, 5), (7, 7)])
+def test_run_assembly_L3(gload, name, orders):
+    """Full fused device assembly vs oracle over the same (bit-exact) packages."""
+    eq, layer, kappa = SPECS[name]
+    m, bt, ops, pk = packages_for(3, eq, gload("gca_L3.npz"))
+    M = scheduler.run_assembly(m, bt, kernels.KernelSpec(eq, layer, kappa), ops, ops,
+                               scheduler.SchedulerParams(), orders)
+    ref = oracle_assemble(m, pk, eq, layer, kappa, orders)
+    ok, worst, nfb = p2_check(pk, M.buffer, ref, TOL)
+    assert ok, (worst, nfb)
+    for leaf in bt.leaves:  # payload views, shapes as make_payloads
+        assert M.payloads[leaf.index].base is not None
+    assert set(M.payloads) == {l.index for l in bt.leaves}
+
+
+def test_c1_near_field_L4():
+    """BASELINE config 1: L4 sphere, Laplace SLP, near field only, orders 3/5."""
+    m, bt, ops, pk = packages_for(4, "laplace", near_only=True)
+    stats = scheduler.AssemblyStats()
+    M = scheduler.run_assembly(m, bt, kernels.KernelSpec("laplace", "single"), {}, {},
+                               scheduler.SchedulerParams(), (3, 5), stats)
+    ref = oracle_assemble(m, pk, "laplace", "single", 0.0, (3, 5))
+    ok, worst, _ = p2_check(pk, M.buffer, ref, TOL)
+    assert ok, worst
+    assert stats.corrective_items == 26576
+    assert stats.block_pairs == 653312
+
+
+def test_small_maxsize_split_blocks(gload):
+    """4 KiB lists force split_block on every leaf; results must not change."""
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), "helmholtz")
+    spec = kernels.KernelSpec("helmholtz", "double", 4.0)
+    a = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
+    b = scheduler.run_assembly(m, bt, spec, ops, ops,
+                               scheduler.SchedulerParams(maxsize_bytes=4096), (3, 5))
+    assert np.array_equal(a.buffer, b.buffer)  # device arithmetic is order-free per entry
+
+
+def test_multi_device_shards_equal_single(gload):
+    """Leaf-range sharding (one plan per shard) gives the same payload."""
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), "laplace")
+    spec = kernels.KernelSpec("laplace", "double")
+    one = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
+    be = scheduler.Backend("cuda", devices=(0, 0, 0))
+    three = scheduler.run_assembly(m, bt, spec, ops, ops,
+                                   scheduler.SchedulerParams(backends=(be,)), (3, 5))
+    assert np.array_equal(one.buffer, three.buffer)
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+def test_green_matrix_vs_reference(gload, eq, kappa):
+    g = gload("gca_L3.npz")
+    m, t, _ = sphere_setup(3)
+    node = t.nodes[int(g["green_cluster"][0])]
+    src = gca.green_sources(node.lo, node.hi, 1.0, 6, m.diameter())
+    for order in (3, 4):
+        A = gca.build_green_matrix(m, t.panels(node), src, kernels.KernelSpec(eq, "single", kappa),
+                                   order)
+        ref = g[f"green_{eq}_{order}"]
+        assert A.dtype == ref.dtype
+        assert float(np.max(np.abs(A - ref) / np.abs(ref))) <= TOL
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+def test_gca_operators_pivots(gload, eq, kappa):
+    """Device Green matrices + host ACA reproduce the reference pivots."""
+    g = gload("gca_L3.npz")
+    m, t, bt = sphere_setup(3)
+    ops, col = gca.build_interpolation_operators(m, bt, kernels.KernelSpec(eq, "single", kappa),
+                                                 gca.GcaParams())
+    assert ops is col
+    cids = g[f"ops_{eq}_cids"]
+    assert np.array_equal(sorted(ops), cids)
+    piv = np.concatenate([ops[int(c)].pivots_global for c in cids])
+    assert np.array_equal(piv, g[f"ops_{eq}_pivots"])
+    V3 = ops[int(cids[0])].V
+    assert np.max(np.abs(V3 - g[f"ops_{eq}_V3"])) <= 1e-8 * np.max(np.abs(g[f"ops_{eq}_V3"]))
+
+
+def test_assemble_operator_pipeline():
+    """solver.assemble_operator end to end (trees, device GCA, device assembly)."""
+    m = mesh.build_sphere_mesh(3)
+    cfg = solver.PipelineConfig()
+    op = solver.assemble_operator(m, kernels.KernelSpec("laplace", "single"), cfg)
+    bt = op.matrix.block_tree
+    pk = packaging.make_packages(m.triangles, bt, op.matrix.row_ops, op.matrix.col_ops,
+                                 cfg.scheduler.maxsize_bytes)
+    ref = oracle_assemble(m, pk, "laplace", "single", 0.0, cfg.orders)
+    ok, worst, _ = p2_check(pk, op.matrix.buffer, ref, TOL)
+    assert ok, worst
+    dlp = solver.assemble_operator(m, kernels.KernelSpec("laplace", "double"), cfg,
+                                   trees=bt, ops=(op.matrix.row_ops, op.matrix.col_ops))
+    assert dlp.matrix.buffer.shape == op.matrix.buffer.shape
+
+
+@pytest.mark.parametrize("case,frozen", [("identical", 1.003065884979),
+                                         ("edge", 0.483538914315),
+                                         ("vertex", 0.225006419777)])
+def test_singular_rules_converge_to_analytic(case, frozen):
+    """Reference KAT (tests/oracles.py:71-78, test_quadrature.py:145-161)
+    through integrate_pair on the device."""
+    def planar(v0, v1, v2):
+        v0, v1, v2 = (np.array([p[0], p[1], 0.0]) for p in (v0, v1, v2))
+        return mesh.AffineChart(v0, v1 - v0, v2 - v1,
+                                float(np.linalg.norm(np.cross(v1 - v0, v2 - v1))))
+    charts = {"identical": (planar((0, 0), (1, 0), (0, 1)), planar((0, 0), (1, 0), (0, 1))),
+              "edge": (planar((1, 0), (0, 1), (0, 0)), planar((1, 0), (0, 1), (1, 1))),
+              "vertex": (planar((1, 0), (0, 1), (0, 0)), planar((1, 0), (2, 0), (1.5, 1)))}
+    cx, cy = charts[case]
+    spec = kernels.KernelSpec("laplace", "single")
+    target = frozen * kernels.INV_4PI
+    val = quadrature.integrate_pair(cx, cy, spec, quadrature.build_rule(case, 8)).real
+    assert abs(val - target) / target <= 1e-4
+    ref12 = quadrature.integrate_pair(cx, cy, spec, quadrature.build_rule(case, 12)).real
+    diffs = [abs(quadrature.integrate_pair(cx, cy, spec, quadrature.build_rule(case, n)).real
+                 - ref12) for n in range(3, 12)]
+    assert all(a > b for a, b in zip(diffs, diffs[1:]))
+
+
+def test_coincident_points_non_finite():
+    """Disjoint rule over an identical pair: non-finite, silently (pairquad.py:98)."""
+    m = mesh.build_sphere_mesh(1)
+    spec = kernels.KernelSpec("laplace", "single")
+    got = scheduler.batch_quadrature(scheduler.CUDA_BACKEND, "disjoint", m, spec,
+                                     quadrature.build_rule("disjoint", 3), [2], [2])
+    assert not np.isfinite(got[0])
+
+
+def test_empty_and_single_inputs():
+    m = mesh.build_sphere_mesh(1)
+    spec = kernels.KernelSpec("helmholtz", "double", 2.0)
+    r = quadrature.build_rule("disjoint", 3)
+    assert scheduler.batch_quadrature(scheduler.CUDA_BACKEND, "disjoint", m, spec, r,
+                                      [], []).shape == (0,)
+    e = np.empty((0, 3))
+    assert pairquad.pair_values(spec, e, e, e, np.empty(0), e, e, e, np.empty(0), e,
+                                r.x_points, r.y_points, r.weights).shape == (0,)
+    one = scheduler.batch_quadrature(scheduler.CUDA_BACKEND, "disjoint", m, spec, r, [0], [20])
+    ref = oracle.batch_quadrature("helmholtz", "double", 2.0, m.vertices, m.triangles,
+                                  m.normals, m.gramians, [0], [20], None, None, *oracle.rule(
+                                      "disjoint", 3))
+    assert rel_err(one, ref) <= TOL
+
+
+def test_bad_arguments_raise():
+    m = mesh.build_sphere_mesh(1)
+    spec = kernels.KernelSpec("laplace", "single")
+    with pytest.raises(ValueError):
+        scheduler.batch_quadrature(scheduler.CUDA_BACKEND, "disjoint", m, spec,
+                                   quadrature.build_rule("disjoint", 3), [0], [m.num_triangles])
+
+
+def test_slp_block_symmetry_L5():
+    """Size-independent property at L5: the disjoint-rule SLP is symmetric, so
+    dense leaves (t,s) and (s,t) are transposes on uncorrected entries."""
+    m, t, bt = sphere_setup(5)
+    near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    M = scheduler.run_assembly(m, near, kernels.KernelSpec("laplace", "single"), {}, {},
+                               scheduler.SchedulerParams(), (4, 5))
+    leaf = {(l.row, l.col): l.index for l in near.leaves}
+    worst = 0.0
+    for (r, c), idx in leaf.items():
+        if r < c and (c, r) in leaf:
+            A, B = M.payloads[idx], M.payloads[leaf[(c, r)]].T
+            ta, tb = m.triangles[t.panels(t.nodes[r])], m.triangles[t.panels(t.nodes[c])]
+            touch = (ta[:, None, :, None] == tb[None, :, None, :]).any(axis=(2, 3))
+            worst = max(worst, float(np.max(np.abs(A - B)[~touch] / np.abs(A)[~touch])))
+    assert worst <= 1e-13
+
+
+def test_sampled_parity_C2_level6():
+    """BASELINE config 2 scale (L6, 32768 triangles, orders 4/5, Laplace DLP,
+    near field): device payload vs oracle on a deterministic sample of
+    entries (every disjoint pair of 300 blocks + 3000 singular items)."""
+    m, t, bt = sphere_setup(6)
+    near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    pk = packaging.make_packages(m.triangles, near, {}, {}, 8 << 20)
+    M = scheduler.run_assembly(m, near, kernels.KernelSpec("laplace", "double"), {}, {},
+                               scheduler.SchedulerParams(), (4, 5))
+    rng = np.random.default_rng(6)
+    blocks = pk.device_blocks()
+    sel = rng.choice(len(blocks), 300, replace=False)
+    items, perms = pk.device_items()
+    corrected = set(items[:, 3].tolist())
+    xs, ys, w = oracle.rule("disjoint", 4)
+    for b in sel:
+        base, ld, nr, nc, ra, ca = blocks[b]
+        i, j = np.divmod(np.arange(nr * nc), nc)
+        idx = base + i * ld + j
+        keep = np.array([k not in corrected for k in idx])
+        ref = oracle.batch_quadrature("laplace", "double", 0.0, m.vertices, m.triangles,
+                                      m.normals, m.gramians, pk.panels[ra + i][keep],
+                                      pk.panels[ca + j][keep], None, None, xs, ys, w)
+        assert rel_err(M.buffer[idx[keep]], ref) <= TOL
+    s = rng.choice(len(items), 3000, replace=False)
+    for code, case in ((1, "vertex"), (2, "edge"), (3, "identical")):
+        ss = s[items[s, 0] == code]
+        ref = oracle.batch_quadrature("laplace", "double", 0.0, m.vertices, m.triangles,
+                                      m.normals, m.gramians, items[ss, 1], items[ss, 2],
+                                      perms[ss, :3].astype(np.int64),
+                                      perms[ss, 3:].astype(np.int64), *oracle.rule(case, 5))
+        got = M.buffer[items[ss, 3]]
+        big = np.max(np.abs(M.buffer))
+        assert float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-9 * big))) <= TOL

@@ -1,0 +1,174 @@
+"""Host-side (CPU) parts of the drop-in, bit-exact against the reference."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import golden_ops, sphere_setup
+from paper_1510_07244_b200 import cluster, gca, kernels, mesh, packaging, quadrature, scheduler
+
+
+def sha(*a):
+    h = hashlib.sha256()
+    for x in a:
+        h.update(np.ascontiguousarray(x).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("level", range(6))
+def test_sphere_bitwise(golden, level):
+    m = mesh.build_sphere_mesh(level)
+    r = golden["sphere"][str(level)]
+    assert (m.num_vertices, m.num_triangles) == (r["nv"], r["nt"])
+    for name in ("vertices", "triangles", "normals", "gramians"):
+        assert sha(getattr(m, name)) == r[name], name
+
+
+def test_gauss_and_rules_bitwise(golden):
+    for n, h in golden["gauss"].items():
+        g = quadrature.gauss_legendre(int(n))
+        assert sha(g.points, g.weights) == h
+    for key, h in golden["rules"].items():
+        case, n = key.split("/")
+        r = quadrature.build_rule(case, int(n))
+        assert sha(r.x_points, r.y_points, r.weights) == h, key
+    for n, h in golden["duffy"].items():
+        assert sha(*quadrature.duffy_panel_rule(int(n))) == h
+
+
+def test_rule_cache_and_bounds():
+    quadrature.clear_rule_cache()
+    a = quadrature.build_rule("edge", 4)
+    assert quadrature.build_rule("edge", 4) is a
+    assert quadrature.rule_cache_stats() == {"builds": 1, "lookups": 2}
+    with pytest.raises(ValueError):
+        quadrature.build_rule("disjoint", 13)
+    with pytest.raises(ValueError):
+        quadrature.build_rule("nearby", 3)
+    for case in quadrature.CASES:
+        assert abs(quadrature.build_rule(case, 5).weights.sum() - 0.25) <= 1e-13
+
+
+def test_classification_all_pairs_L2(gload):
+    cls = gload("classify_L2.npz")["cls"]
+    m = mesh.build_sphere_mesh(2)
+    nt = m.num_triangles
+    a, b = np.meshgrid(np.arange(nt), np.arange(nt), indexing="ij")
+    case, px, py = quadrature.classify_pairs(m.triangles, a.ravel(), b.ravel())
+    got = np.concatenate([case[:, None], px, py], axis=1).reshape(nt, nt, 7)
+    assert np.array_equal(got.astype(np.int8), cls)
+    c = quadrature.classify_pair(m, 3, 3)
+    assert c.case == "identical" and c.perm_x == (0, 1, 2)
+
+
+def test_classify_rejects_three_shared():
+    V = np.array([[0, 0, 0.0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    T = np.array([[0, 1, 2], [0, 2, 1], [0, 1, 3], [1, 2, 3]])
+    m = mesh.make_surface_mesh(V, T, validate=False)
+    with pytest.raises(mesh.MeshError):
+        quadrature.classify_pair(m, 0, 1)
+
+
+@pytest.mark.parametrize("level", [3, 4])
+def test_trees_bitwise(gload, level):
+    g = gload("trees.npz")
+    m, t, bt = sphere_setup(level)
+    assert np.array_equal(t.permutation, g[f"L{level}_perm"])
+    assert np.array_equal([n.start for n in t.nodes], g[f"L{level}_start"])
+    assert np.array_equal([n.size for n in t.nodes], g[f"L{level}_size"])
+    assert np.array_equal(np.array([n.lo for n in t.nodes]), g[f"L{level}_lo"])
+    kind = {"admissible": 0, "dense": 1, "split": 2}
+    got = np.array([(b.row, b.col, kind[b.kind], len(b.children)) for b in bt.nodes])
+    assert np.array_equal(got, g[f"L{level}_blocks"])
+    assert np.array_equal([b.index for b in bt.leaves], g[f"L{level}_leaves"])
+
+
+CODE = {"disjoint": 0, "vertex": 1, "edge": 2, "identical": 3}
+
+
+@pytest.mark.parametrize("tag,maxsize", [("8M", 8 * 2 ** 20), ("4K", 4096)])
+def test_package_assignment_bitwise(gload, tag, maxsize):
+    """Disjoint list boundaries, split blocks, singular items and singular list
+    boundaries equal the reference's inline run (scheduler.py:442-505)."""
+    g = gload("assembly.npz")
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), "laplace")
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, maxsize)
+    seq = packaging.inline_lists(pk)
+    assert np.array_equal([CODE[c] for c, _ in seq], g[f"lists_{tag}_case"])
+    assert np.array_equal([len(x) for _, x in seq], g[f"lists_{tag}_len"])
+    rec = []
+    for c, x in seq:
+        for k in x:
+            if c == "disjoint":
+                lf = pk.blk_leaf[k]
+                rec.append([pk.leaf_ids[lf], pk.blk_nr[k], pk.blk_nc[k], pk.blk_r0[k],
+                            pk.blk_c0[k], int(pk.leaf_flagged[lf])])
+            else:
+                rec.append([pk.item_tri_x[k], pk.item_tri_y[k], pk.leaf_ids[pk.item_leaf[k]],
+                            pk.item_offset[k], 0, 0])
+    assert np.array_equal(np.array(rec), g[f"lists_{tag}_items"])
+
+
+def test_split_and_listbuilder_api():
+    blk = scheduler.WorkBlock(0, np.arange(10), np.arange(7), np.arange(10), np.arange(7), False)
+    parts = scheduler.split_block(blk, 32 * 16)
+    assert sum(p.num_pairs for p in parts) == 70
+    assert all(p.nbytes <= 32 * 16 for p in parts)
+    assert [(len(p.row_panels), len(p.col_panels)) for p in parts] == \
+        [(r[1], r[3]) for r in packaging._split(10, 7, 32 * 16)]
+    out = []
+    lb = scheduler.ListBuilder("disjoint", 32 * 40, out.append)
+    for p in parts:
+        lb._add(p, p.nbytes)
+    lb.flush()
+    lid, n = packaging._greedy_lists(np.array([p.nbytes for p in parts]), 32 * 40)
+    assert n == len(out)
+    with pytest.raises(scheduler.SchedulerConfigError):
+        scheduler.ListBuilder("disjoint", 16, out.append)
+    with pytest.raises(scheduler.SchedulerConfigError):
+        scheduler.Backend("x", "batch")
+
+
+def test_green_sources_bitwise(gload):
+    g = gload("gca_L3.npz")
+    m, t, _ = sphere_setup(3)
+    node = t.nodes[int(g["green_cluster"][0])]
+    s = gca.green_sources(node.lo, node.hi, 1.0, 6, m.diameter())
+    for name in ("points", "weights", "normals", "roles"):
+        assert np.array_equal(getattr(s, name), g[f"src_{name}"]), name
+
+
+@pytest.mark.parametrize("eq", ["laplace", "helmholtz"])
+def test_aca_pivots_on_reference_green(gload, eq):
+    g = gload("gca_L3.npz")
+    res = gca.aca(g[f"green_{eq}_3"], 1e-4)
+    assert np.array_equal(res.row_pivots, g[f"aca_{eq}_rows"])
+    assert np.array_equal(res.col_pivots, g[f"aca_{eq}_cols"])
+
+
+def test_kernel_values_bitwise(gload):
+    g = gload("kernel_values.npz")
+    specs = {"L-SLP": kernels.KernelSpec("laplace", "single"),
+             "L-DLP": kernels.KernelSpec("laplace", "double"),
+             "H-SLP": kernels.KernelSpec("helmholtz", "single", 4.0),
+             "H-DLP": kernels.KernelSpec("helmholtz", "double", 4.0)}
+    for name, spec in specs.items():
+        got = kernels.eval_batch(spec, g["xs"], g["ys"], g["ns"] if spec.needs_normal else None)
+        assert np.array_equal(got, g[name]), name
+    with pytest.raises(ValueError):
+        kernels.KernelSpec("helmholtz", "single", -1.0)
+    with pytest.raises(ValueError):
+        kernels.eval(specs["L-SLP"], np.ones(3), np.ones(3))
+
+
+def test_shard_leaves_partition():
+    m, t, bt = sphere_setup(4)
+    near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    pk = packaging.make_packages(m.triangles, near, {}, {}, 8 << 20)
+    for n in (1, 2, 3, 8):
+        sh = packaging.shard_leaves(pk, n, 81, [1250, 3125, 3750])
+        assert sh[0][0] == 0 and sh[-1][1] == pk.leaf_ids.size
+        assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+        assert sum(len(pk.device_items(lo, hi)[0]) for lo, hi in sh) == pk.num_items
+        assert sum(len(pk.device_blocks(lo, hi)) for lo, hi in sh) == pk.num_blocks
