@@ -302,8 +302,12 @@ int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double 
     GC_CUDA(di.upload(items.data(), n, s));
     GC_CUDA(dr.upload(rule.data(), rule.size(), s));
     GC_CUDA(dout.alloc(n));
-    GC_CUDA(launch_generic(kind_of(equation, layer), mesh->V.p, mesh->T.p, mesh->charts.p, di.p,
-                           n, dr.p, nq, dout.p, kappa, s));
+    bool same = true;
+    for (int64_t i = 0; i < n && same; ++i)
+        same = items[i].tri_x == items[i].tri_y && items[i].px[0] == items[i].py[0] &&
+               items[i].px[1] == items[i].py[1] && items[i].px[2] == items[i].py[2];
+    GC_CUDA(launch_generic(kind_of(equation, layer), same, mesh->V.p, mesh->T.p, mesh->charts.p,
+                           di.p, n, dr.p, nq, dout.p, kappa, s));
     GC_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, s));
     GC_CUDA(cudaStreamSynchronize(s));
     return GCABEM_OK;
@@ -366,6 +370,9 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
             it.py[j] = perms[6 * k + 3 + j];
             GC_ARG(it.px[j] < 3 && it.py[j] < 3, "bad permutation");
         }
+        GC_ARG(c != 3 || (it.tri_x == it.tri_y && it.px[0] == it.py[0] &&
+                          it.px[1] == it.py[1] && it.px[2] == it.py[2]),
+               "identical item with two different charts");
     }
     auto *p = new gcabem_plan_s();
     p->mesh = mesh;
@@ -415,8 +422,9 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     for (int c = 0; c < 3; ++c) {
         const int64_t n = p->case_at[c + 1] - p->case_at[c];
         if (n == 0) continue;
-        GC_CUDA(launch_generic(p->kind, m->V.p, m->T.p, m->charts.p, p->items.p + p->case_at[c], n,
-                               p->srule[c].p, p->sq[c], p->payload.p, p->kappa, s));
+        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
+                               p->items.p + p->case_at[c], n, p->srule[c].p, p->sq[c],
+                               p->payload.p, p->kappa, s));
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;

@@ -52,9 +52,11 @@ cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const Bloc
                             double2 *payload, double kappa, cudaStream_t s);
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
-cudaError_t launch_generic(int kind, const double *V, const int32_t *T, const Chart *charts,
-                           const SingItem *items, int64_t n, const double *rule, int64_t q,
-                           double2 *payload, double kappa, cudaStream_t s);
+// same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).
+cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int32_t *T,
+                           const Chart *charts, const SingItem *items, int64_t n,
+                           const double *rule, int64_t q, double2 *payload, double kappa,
+                           cudaStream_t s);
 // Raw charts (gcabem_pair_values): per pair 22 doubles
 // {ox,e1x,e2x, oy,e1y,e2y, ny} (21) + gx, gy packed as 24 doubles.
 cudaError_t launch_raw(int kind, const double *pairs, int64_t n, const double *rule, int64_t q,

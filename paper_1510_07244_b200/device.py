@@ -45,10 +45,11 @@ class DeviceMesh:
 
 
 def _drop(key):
+    """Forget the replica of a dead mesh. The replica itself is released by
+    DeviceMesh.__del__ once no plan references it any more (plans must be
+    destroyed before the mesh they gather from)."""
     with _cache_lock:
-        dm = _cache.pop(key, None)
-    if dm is not None:
-        dm.close()
+        _cache.pop(key, None)
 
 
 def device_mesh(mesh: SurfaceMesh, device: int = 0) -> DeviceMesh:

@@ -75,18 +75,23 @@ def checksum(pk, payload):
     return h.hexdigest()
 
 
-def p2_check(pk, got, ref, tol=1e-12):
-    """|new-ref| <= tol*|ref| per entry, except reference
-    roundoff entries (DLP identical / coplanar pairs) which use tol times the
-    leaf-block max. Returns (ok, worst relative error, number of fallbacks)."""
+def p2_check(pk, got, ref, tol=1e-12, double_layer=False):
+    """|new-ref| <= tol*|ref| per entry, except entries that
+    are roundoff/cancellation-dominated in the reference, compared on the
+    scale of their leaf block (tol * max|ref| over the leaf): entries with
+    |ref| < 1e-9 * leaf max (DLP identical pairs), and - for double-layer
+    operators - every singular corrective entry (near-coplanar pairs whose
+    reference rounding grows like eps/h^2).
+    Returns (ok, worst relative error, number of leaf-scaled entries)."""
     err = np.abs(got - ref)
     mag = np.abs(ref)
     leaf_of = np.repeat(np.arange(pk.leaf_ids.size), np.diff(pk.leaf_base))
     leaf_max = np.zeros(pk.leaf_ids.size)
     np.maximum.at(leaf_max, leaf_of, mag)
-    scale = np.maximum(mag, 0.0)
     fallback = mag < 1e-9 * leaf_max[leaf_of]
-    scale = np.where(fallback, leaf_max[leaf_of], scale)
+    if double_layer and pk.num_items:
+        fallback[pk.device_items()[0][:, 3]] = True
+    scale = np.where(fallback, leaf_max[leaf_of], mag)
     with np.errstate(divide="ignore", invalid="ignore"):
         rel = np.where(scale > 0, err / scale, err)
     ok = bool(np.all(np.isfinite(got)) and np.all(rel <= tol))
