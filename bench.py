@@ -366,6 +366,7 @@ def run_ours(args, cfg, dist, log):
     setup_first = None
     for k in range(max(1, args.e2e_steps)):
         dist.barrier()
+        scheduler.clear_package_cache()  # every step packages once (shared by SLP/DLP)
         t0 = time.perf_counter()
         mats = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"]) for s in specs]
         torch.cuda.synchronize(device)

@@ -81,8 +81,9 @@ int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double 
  * :362, the overwrite protocol) into one device-resident payload buffer that
  * holds all block-tree leaves (make_payloads :411) back to back, complex128.
  *
- * blocks: nblocks x 6 int64 {payload_base, ld, nrows, ncols, rows_at, cols_at}
- *   — a WorkBlock (scheduler.py:87-103): entry (i,j) goes to
+ * blocks: nblocks x 7 int64 {payload_base, ld, nrows, ncols, rows_at, cols_at,
+ *   leaf} — a WorkBlock (scheduler.py:87-103), in leaf (= payload) order,
+ *   leaf non-decreasing: entry (i,j) goes to
  *   payload[payload_base + i*ld + j], row panel panels[rows_at+i], column
  *   panel panels[cols_at+j]. The rule is the disjoint rule of order
  *   disjoint_n given in factored form: gauss_pts/gauss_wts (disjoint_n,)
@@ -90,7 +91,7 @@ int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double 
  * items: nitems x 4 int64 {case, tri_x, tri_y, payload_index} — WorkItem
  *   (scheduler.py:106-117) with payload_index = leaf base + offset;
  *   perms: nitems x 6 uint8 (perm_x, perm_y) from classify_pair (:197).
- *   Items must be grouped by case (any order inside a case).
+ *   Any order (the plan groups them by case and payload index).
  * singular rules: for case c in 1..3, sq[c-1] points, rows of 5 float64
  *   (sx, sy... see below) in srule[c-1]: {x_s, x_t, y_s, y_t, w}
  *   (quadrature.build_rule, :170). */
@@ -103,8 +104,12 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
 /* Launch all kernels on the plan stream (async). The payload is zeroed first
  * (make_payloads semantics), then disjoint, then singular overwrites. */
 int gcabem_plan_execute(gcabem_plan_t plan);
-/* Copy the payload (payload_len complex128) to host memory (pinned for full
- * PCIe rate) and wait. */
+/* Execute AND stream the payload to `host` (payload_len complex128, pinned
+ * for full PCIe rate) in `nchunks` leaf-aligned chunks: chunk k's D2H runs
+ * on a copy stream while chunk k+1 computes. Asynchronous: call
+ * gcabem_plan_synchronize before reading `host`. */
+int gcabem_plan_execute_download(gcabem_plan_t plan, double *host, int nchunks);
+/* Copy the payload (payload_len complex128) to host memory and wait. */
 int gcabem_plan_download(gcabem_plan_t plan, double *host);
 int gcabem_plan_synchronize(gcabem_plan_t plan);
 /* CUDA-event durations of the last execute, ms: [disjoint, singular, total]. */
@@ -112,6 +117,36 @@ int gcabem_plan_timing(gcabem_plan_t plan, float *ms3);
 /* Device pointer of the payload (for device-resident consumers). */
 int gcabem_plan_payload(gcabem_plan_t plan, void **dev_ptr);
 int gcabem_plan_destroy(gcabem_plan_t plan);
+
+/* ---- host work packaging (CPU) -------------------------------------------
+ * Native restatement of the reference scheduler's host work, bit-exact:
+ * _leaf_blocks (scheduler.py:425-439), make_payloads layout (:411-422),
+ * split_block (:153-175), ListBuilder (:178-208), the corrective scan of
+ * distribute_disjoint (:334-359) and classify_pair (quadrature.py:197-220).
+ * leaves: L x 3 {row cluster, col cluster, dense?1:0} in block-tree preorder.
+ * Trees: per node start/size (int64), box lo/hi (n x 3), permutation (nt).
+ * Operators: op_at (n+1) offsets into piv (pivots_global, ACA order);
+ * empty range = no operator. Pass identical pointers for a shared tree.
+ * Panel indices of leaf k: panels[rows_at[k] + i], panels[cols_at[k] + j]. */
+typedef struct gcabem_packages_s *gcabem_packages_t;
+int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
+                          const int64_t *leaves, int64_t nrow, const int64_t *row_start,
+                          const int64_t *row_size, const double *row_lo, const double *row_hi,
+                          const int64_t *row_perm, const int64_t *row_op_at,
+                          const int64_t *row_piv, int64_t ncol, const int64_t *col_start,
+                          const int64_t *col_size, const double *col_lo, const double *col_hi,
+                          const int64_t *col_perm, const int64_t *col_op_at,
+                          const int64_t *col_piv, int64_t maxsize, int nthreads,
+                          gcabem_packages_t *out);
+/* sizes[9]: {L, payload_len, npanels, nblocks, nlists, nitems, 0, 0, 0} */
+int gcabem_packages_sizes(gcabem_packages_t pk, int64_t *sizes);
+/* blocks: nblocks x 5 {leaf, r0, nr, c0, nc}; items: nitems x 6 {case 1..3,
+ * tri_x, tri_y, leaf, offset in leaf, generating block}; perms nitems x 6. */
+int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_shape,
+                          int64_t *leaf_base, int64_t *rows_at, int64_t *cols_at,
+                          uint8_t *flagged, int64_t *blocks, int64_t *blk_list, int64_t *items,
+                          uint8_t *perms);
+int gcabem_packages_free(gcabem_packages_t pk);
 
 /* ---- GCA Green matrices ---------------------------------------------------
  * Replaces gca.build_green_matrix (gca.py:136-179), batched over clusters.

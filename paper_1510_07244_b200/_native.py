@@ -47,6 +47,7 @@ _SIGS = {
                             _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)], _int),
     "gcabem_plan_execute": ([_vp], _int),
     "gcabem_plan_download": ([_vp, _vp], _int),
+    "gcabem_plan_execute_download": ([_vp, _vp, _int], _int),
     "gcabem_plan_synchronize": ([_vp], _int),
     "gcabem_plan_timing": ([_vp, _vp], _int),
     "gcabem_plan_payload": ([_vp, ctypes.POINTER(_vp)], _int),
@@ -54,6 +55,11 @@ _SIGS = {
     "gcabem_green_matrices": ([_vp, _int, _dbl, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64,
                                _vp], _int),
     "gcabem_fp64_probe": ([_int, ctypes.POINTER(_dbl)], _int),
+    "gcabem_packages_build": ([_i64, _vp, _i64, _vp, _i64] + [_vp] * 7 + [_i64] + [_vp] * 7
+                              + [_i64, _int, ctypes.POINTER(_vp)], _int),
+    "gcabem_packages_sizes": ([_vp, _vp], _int),
+    "gcabem_packages_fetch": ([_vp] * 11, _int),
+    "gcabem_packages_free": ([_vp], _int),
 }
 EXPORTED = tuple(_SIGS)
 

@@ -100,6 +100,9 @@ std::vector<double> pack_rule(int64_t q, const double *xs, const double *ys, con
 
 }  // namespace
 
+// Error hook for the other translation units (packaging.cpp).
+int gcabem_internal_error(int code, const char *msg) { return set_error(code, msg); }
+
 struct gcabem_mesh_s {
     int device = 0;
     int64_t nv = 0, nt = 0;
@@ -124,6 +127,11 @@ struct gcabem_plan_s {
     DevBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> chunk_ev;
+    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t copy = nullptr;    // D2H, overlapping later chunks' kernels
+    // host copies for chunked execution
+    std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
     bool executed = false;
 };
 
@@ -324,67 +332,100 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
     if (int rc = check_kind(equation, layer, kappa)) return rc;
     GC_ARG(disjoint_n >= 1 && disjoint_n <= MAX_ORDER, "disjoint order outside [1, 12]");
     GC_ARG(payload_len >= 0 && nblocks >= 0 && npanels >= 0 && nitems >= 0, "negative size");
+    GC_ARG(nblocks < (int64_t(1) << 31), "too many blocks");
     GC_CUDA(cudaSetDevice(mesh->device));
     if (int rc = ensure_disjoint_rule(mesh->device, disjoint_n, gauss_pts, gauss_wts)) return rc;
 
-    // WorkBlocks -> descriptors + fixed-size tasks (DISJOINT_TPB pairs each)
-    std::vector<BlockDesc> bd(nblocks);
-    std::vector<int2> tasks;
-    for (int64_t b = 0; b < nblocks; ++b) {
-        const int64_t *r = blocks + 6 * b;
-        const int64_t base = r[0], ld = r[1], nr = r[2], nc = r[3], ra = r[4], ca = r[5];
-        GC_ARG(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31), "block too large");
-        GC_ARG(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels,
-               "block panel range out of bounds");
-        GC_ARG(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= payload_len),
-               "block payload range out of bounds");
-        GC_ARG(nblocks < (int64_t(1) << 31), "too many blocks");
-        bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
-        for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
-            tasks.push_back(make_int2((int)b, (int)k0));
-    }
-    std::vector<int32_t> pan(npanels);
-    for (int64_t k = 0; k < npanels; ++k) {
-        GC_ARG(panels[k] >= 0 && panels[k] < mesh->nt, "panel index out of range");
-        pan[k] = (int32_t)panels[k];
-    }
-    // singular items grouped by case 1..3
-    std::vector<SingItem> si(nitems);
-    int64_t counts[4] = {0, 0, 0, 0};
-    for (int64_t k = 0; k < nitems; ++k) {
-        const int64_t c = items[4 * k];
-        GC_ARG(c >= 1 && c <= 3, "singular item case must be vertex/edge/identical");
-        GC_ARG(k == 0 || c >= items[4 * (k - 1)], "singular items must be grouped by case");
-        counts[c]++;
-        SingItem &it = si[k];
-        std::memset(&it, 0, sizeof it);
-        it.out = items[4 * k + 3];
-        GC_ARG(it.out >= 0 && it.out < payload_len, "singular item outside the payload");
-        GC_ARG(items[4 * k + 1] >= 0 && items[4 * k + 1] < mesh->nt && items[4 * k + 2] >= 0 &&
-                   items[4 * k + 2] < mesh->nt,
-               "triangle index out of range");
-        it.tri_x = (int32_t)items[4 * k + 1];
-        it.tri_y = (int32_t)items[4 * k + 2];
-        for (int j = 0; j < 3; ++j) {
-            it.px[j] = perms[6 * k + j];
-            it.py[j] = perms[6 * k + 3 + j];
-            GC_ARG(it.px[j] < 3 && it.py[j] < 3, "bad permutation");
-        }
-        GC_ARG(c != 3 || (it.tri_x == it.tri_y && it.px[0] == it.py[0] &&
-                          it.px[1] == it.py[1] && it.px[2] == it.py[2]),
-               "identical item with two different charts");
-    }
     auto *p = new gcabem_plan_s();
     p->mesh = mesh;
     p->kind = kind_of(equation, layer);
     p->order = disjoint_n;
     p->kappa = kappa;
     p->payload_len = payload_len;
+    // WorkBlocks -> descriptors + fixed-size tasks (DISJOINT_TPB pairs each)
+    std::vector<BlockDesc> bd(nblocks);
+    std::vector<int2> tasks;
+    p->block_task_at.assign(nblocks + 1, 0);
+    p->block_leaf.resize(nblocks);
+    p->block_base.resize(nblocks);
+    p->block_pairs.resize(nblocks);
+    for (int64_t b = 0; b < nblocks; ++b) {
+        const int64_t *r = blocks + 7 * b;
+        const int64_t base = r[0], ld = r[1], nr = r[2], nc = r[3], ra = r[4], ca = r[5];
+        if (!(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31)) ||
+            !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
+            !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= payload_len)) ||
+            (b > 0 && r[6] < blocks[7 * (b - 1) + 6])) {
+            delete p;
+            return set_error(GCABEM_ERR_ARG, "block descriptor out of bounds or out of order");
+        }
+        bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
+        p->block_task_at[b] = (int64_t)tasks.size();
+        p->block_leaf[b] = r[6];
+        p->block_base[b] = base;
+        p->block_pairs[b] = nr * nc;
+        for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
+            tasks.push_back(make_int2((int)b, (int)k0));
+    }
+    p->block_task_at[nblocks] = (int64_t)tasks.size();
+    std::vector<int32_t> pan(npanels);
+    for (int64_t k = 0; k < npanels; ++k) {
+        if (panels[k] < 0 || panels[k] >= mesh->nt) {
+            delete p;
+            return set_error(GCABEM_ERR_ARG, "panel index out of range");
+        }
+        pan[k] = (int32_t)panels[k];
+    }
+    // singular items: grouped by case 1..3, sorted by payload index inside a
+    // case (chunked execution looks chunks up by payload range)
+    std::vector<int64_t> order(nitems);
+    int64_t counts[4] = {0, 0, 0, 0};
+    for (int64_t k = 0; k < nitems; ++k) {
+        order[k] = k;
+        const int64_t c = items[4 * k];
+        if (c < 1 || c > 3) {
+            delete p;
+            return set_error(GCABEM_ERR_ARG, "singular item case must be vertex/edge/identical");
+        }
+        counts[c]++;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return items[4 * a] != items[4 * b] ? items[4 * a] < items[4 * b]
+                                            : items[4 * a + 3] < items[4 * b + 3];
+    });
+    std::vector<SingItem> si(nitems);
+    p->item_out.resize(nitems);
+    for (int64_t q = 0; q < nitems; ++q) {
+        const int64_t k = order[q];
+        const int64_t c = items[4 * k];
+        SingItem &it = si[q];
+        std::memset(&it, 0, sizeof it);
+        it.out = items[4 * k + 3];
+        bool ok = it.out >= 0 && it.out < payload_len && items[4 * k + 1] >= 0 &&
+                  items[4 * k + 1] < mesh->nt && items[4 * k + 2] >= 0 &&
+                  items[4 * k + 2] < mesh->nt;
+        it.tri_x = (int32_t)items[4 * k + 1];
+        it.tri_y = (int32_t)items[4 * k + 2];
+        for (int j = 0; j < 3; ++j) {
+            it.px[j] = perms[6 * k + j];
+            it.py[j] = perms[6 * k + 3 + j];
+            ok = ok && it.px[j] < 3 && it.py[j] < 3;
+        }
+        ok = ok && (c != 3 || (it.tri_x == it.tri_y && it.px[0] == it.py[0] &&
+                               it.px[1] == it.py[1] && it.px[2] == it.py[2]));
+        if (!ok) {
+            delete p;
+            return set_error(GCABEM_ERR_ARG, "bad singular item (index, permutation or chart)");
+        }
+        p->item_out[q] = it.out;
+    }
     p->ntasks = (int64_t)tasks.size();
     p->case_at[0] = 0;
     for (int c = 1; c <= 3; ++c) p->case_at[c] = p->case_at[c - 1] + counts[c];
-    cudaStream_t s = mesh->stream;
-    cudaError_t e = p->payload.alloc(payload_len);
+    cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
+    cudaStream_t s = p->stream;
+    if (e == cudaSuccess) e = p->payload.alloc(payload_len);
     if (e == cudaSuccess) e = p->blocks.upload(bd.data(), bd.size(), s);
     if (e == cudaSuccess) e = p->tasks.upload(tasks.data(), tasks.size(), s);
     if (e == cudaSuccess) e = p->panels.upload(pan.data(), pan.size(), s);
@@ -408,15 +449,39 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
     return GCABEM_OK;
 }
 
+namespace {
+
+// Launch the kernels of blocks [b0, b1) and of the singular items whose
+// payload index lies in [p0, p1) on the plan stream.
+int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p1) {
+    gcabem_mesh_t m = p->mesh;
+    cudaStream_t s = p->stream;
+    const int64_t t0 = p->block_task_at[b0], t1 = p->block_task_at[b1];
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->blocks.p, p->tasks.p + t0, t1 - t0,
+                            p->panels.p, p->payload.p, p->kappa, s));
+    for (int c = 0; c < 3; ++c) {
+        const auto first = p->item_out.begin() + p->case_at[c];
+        const auto last = p->item_out.begin() + p->case_at[c + 1];
+        const int64_t i0 = std::lower_bound(first, last, p0) - p->item_out.begin();
+        const int64_t i1 = std::lower_bound(first, last, p1) - p->item_out.begin();
+        if (i1 <= i0) continue;
+        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->items.p + i0,
+                               i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->kappa, s));
+    }
+    return GCABEM_OK;
+}
+
+}  // namespace
+
 int gcabem_plan_execute(gcabem_plan_t p) {
     GC_ARG(p, "null plan");
     gcabem_mesh_t m = p->mesh;
     GC_CUDA(cudaSetDevice(m->device));
-    cudaStream_t s = m->stream;
+    cudaStream_t s = p->stream;
     if (p->payload_len > 0)
         GC_CUDA(cudaMemsetAsync(p->payload.p, 0, sizeof(double2) * p->payload_len, s));
     GC_CUDA(cudaEventRecord(p->ev[0], s));
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, p->blocks.p, p->tasks.p, p->ntasks,
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->blocks.p, p->tasks.p, p->ntasks,
                             p->panels.p, p->payload.p, p->kappa, s));
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     for (int c = 0; c < 3; ++c) {
@@ -431,20 +496,66 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     return GCABEM_OK;
 }
 
+int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
+    GC_ARG(p && (host || p->payload_len == 0), "null argument");
+    GC_CUDA(cudaSetDevice(p->mesh->device));
+    const int64_t B = (int64_t)p->block_leaf.size();
+    if (nchunks < 1) nchunks = 1;
+    // leaf-aligned chunk boundaries balanced by pairs
+    std::vector<int64_t> cut{0};
+    int64_t total = 0;
+    for (int64_t b = 0; b < B; ++b) total += p->block_pairs[b];
+    int64_t acc = 0, next = 1;
+    for (int64_t b = 0; b < B && next < nchunks; ++b) {
+        if (b > 0 && p->block_leaf[b] != p->block_leaf[b - 1] && acc * nchunks >= next * total) {
+            cut.push_back(b);
+            ++next;
+        }
+        acc += p->block_pairs[b];
+    }
+    cut.push_back(B);
+    cudaStream_t s = p->stream;
+    GC_CUDA(cudaEventRecord(p->ev[0], s));
+    while ((int64_t)p->chunk_ev.size() < (int64_t)cut.size()) {
+        cudaEvent_t e;
+        GC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->chunk_ev.push_back(e);
+    }
+    for (size_t k = 0; k + 1 < cut.size(); ++k) {
+        const int64_t b0 = cut[k], b1 = cut[k + 1];
+        const int64_t p0 = b0 < B ? p->block_base[b0] : p->payload_len;
+        const int64_t p1 = b1 < B ? p->block_base[b1] : p->payload_len;
+        if (p1 > p0)
+            GC_CUDA(cudaMemsetAsync(p->payload.p + p0, 0, sizeof(double2) * (p1 - p0), s));
+        if (int rc = enqueue_range(p, b0, b1, p0, p1)) return rc;
+        GC_CUDA(cudaEventRecord(p->chunk_ev[k], s));
+        if (p1 > p0) {
+            GC_CUDA(cudaStreamWaitEvent(p->copy, p->chunk_ev[k], 0));
+            GC_CUDA(cudaMemcpyAsync(host + 2 * p0, p->payload.p + p0, sizeof(double2) * (p1 - p0),
+                                    cudaMemcpyDeviceToHost, p->copy));
+        }
+    }
+    GC_CUDA(cudaEventRecord(p->ev[1], s));
+    GC_CUDA(cudaEventRecord(p->ev[2], s));
+    p->executed = true;
+    return GCABEM_OK;
+}
+
 int gcabem_plan_download(gcabem_plan_t p, double *host) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
     GC_CUDA(cudaSetDevice(p->mesh->device));
     if (p->payload_len > 0)
         GC_CUDA(cudaMemcpyAsync(host, p->payload.p, sizeof(double2) * p->payload_len,
-                                cudaMemcpyDeviceToHost, p->mesh->stream));
-    GC_CUDA(cudaStreamSynchronize(p->mesh->stream));
+                                cudaMemcpyDeviceToHost, p->stream));
+    GC_CUDA(cudaStreamSynchronize(p->stream));
     return GCABEM_OK;
 }
 
 int gcabem_plan_synchronize(gcabem_plan_t p) {
     GC_ARG(p, "null plan");
     GC_CUDA(cudaSetDevice(p->mesh->device));
-    GC_CUDA(cudaStreamSynchronize(p->mesh->stream));
+    GC_CUDA(cudaStreamSynchronize(p->stream));
+    GC_CUDA(cudaStreamSynchronize(p->copy));
     return GCABEM_OK;
 }
 
@@ -468,9 +579,19 @@ int gcabem_plan_payload(gcabem_plan_t p, void **dev_ptr) {
 int gcabem_plan_destroy(gcabem_plan_t p) {
     if (!p) return GCABEM_OK;
     cudaSetDevice(p->mesh->device);
-    cudaStreamSynchronize(p->mesh->stream);
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->copy) cudaStreamSynchronize(p->copy);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : p->chunk_ev) cudaEventDestroy(e);
+    p->payload.release();
+    p->blocks.release();
+    p->tasks.release();
+    p->panels.release();
+    p->items.release();
+    for (auto &r : p->srule) r.release();
+    if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->copy) cudaStreamDestroy(p->copy);
     delete p;
     return GCABEM_OK;
 }

@@ -47,9 +47,10 @@ inline int kind_of(int equation, int layer) { return equation * 2 + layer; }
 
 // ---- launchers (kernels.cu) ------------------------------------------------
 cudaError_t upload_disjoint_rule(int order, const double *gauss_pts, const double *gauss_wts);
-cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const BlockDesc *blocks,
-                            const int2 *tasks, int64_t ntasks, const int32_t *panels,
-                            double2 *payload, double kappa, cudaStream_t s);
+cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
+                            const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                            const int32_t *panels, double2 *payload, double kappa,
+                            cudaStream_t s);
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
 // same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).

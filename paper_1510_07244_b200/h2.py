@@ -9,6 +9,7 @@ image of the device payload the kernels write; ``buffer`` exposes it.
 from __future__ import annotations
 
 import hashlib
+from collections.abc import MutableMapping
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -16,6 +17,71 @@ import numpy as np
 from .cluster import BlockTree
 
 DENSE_EXPANSION_CAP = 4096
+
+
+class LeafPayloads(MutableMapping):
+    """dict[leaf index -> payload] whose values are views of one buffer,
+    materialised on access (100k+ leaves: building every view eagerly would
+    cost more than the device assembly). Assignment replaces an entry, as
+    on the reference's plain dict."""
+
+    def __init__(self, buffer: np.ndarray, leaf_ids: np.ndarray, leaf_base: np.ndarray,
+                 leaf_shape: np.ndarray):
+        self.buffer = buffer
+        self._ids = np.asarray(leaf_ids, dtype=np.int64)
+        self._sorted = bool(np.all(self._ids[1:] > self._ids[:-1]))
+        self._pos = None if self._sorted else {int(k): i for i, k in enumerate(self._ids)}
+        self._base = leaf_base
+        self._shape = leaf_shape
+        self._over: dict = {}
+        self._gone: set = set()
+
+    def _index(self, key) -> int:
+        k = int(key)
+        if self._sorted:
+            i = int(np.searchsorted(self._ids, k))
+            if i < self._ids.size and self._ids[i] == k:
+                return i
+            return -1
+        return self._pos.get(k, -1)
+
+    def __getitem__(self, key):
+        if key in self._over:
+            return self._over[key]
+        i = self._index(key)
+        if i < 0 or int(key) in self._gone:
+            raise KeyError(key)
+        a, b = int(self._base[i]), int(self._base[i + 1])
+        return self.buffer[a:b].reshape(int(self._shape[i, 0]), int(self._shape[i, 1]))
+
+    def __setitem__(self, key, value):
+        self._over[key] = value
+        self._gone.discard(int(key))
+
+    def __delitem__(self, key):
+        if key in self._over:
+            del self._over[key]
+        if self._index(key) >= 0:
+            self._gone.add(int(key))
+        elif key not in self._over:
+            raise KeyError(key)
+
+    def __iter__(self):
+        for k in self._ids.tolist():
+            if k not in self._gone and k not in self._over:
+                yield k
+        yield from self._over
+
+    def __len__(self):
+        return self._ids.size - len(self._gone) + sum(
+            1 for k in self._over if self._index(k) < 0)
+
+    def __contains__(self, key):
+        try:
+            self[key]
+        except (KeyError, TypeError, ValueError):
+            return False
+        return True
 
 
 @dataclass

@@ -18,7 +18,9 @@ library or device raises BackendError.
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
+import weakref
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -27,7 +29,7 @@ from . import _native as nat
 from ._native import BackendError
 from .cluster import BlockTree
 from .device import DeviceMesh, device_mesh
-from .h2 import GCAMatrix
+from .h2 import GCAMatrix, LeafPayloads
 from .kernels import KernelSpec
 from .mesh import SurfaceMesh
 from .packaging import (BYTES_PER_PAIR, PAIR_RECORD_BYTES, SINGULAR_CASES, VALUE_BYTES,
@@ -78,6 +80,11 @@ class SchedulerParams:
     backends: tuple = (CUDA_BACKEND,)
     affinity: dict = field(default_factory=lambda: {
         "disjoint": "cuda", "vertex": "cuda", "edge": "cuda", "identical": "cuda"})
+    # this process's share when one job is split over processes (rank, world);
+    # None = the whole job on this process's devices
+    shard: tuple | None = None
+    # leaf-aligned chunks per device whose D2H overlaps the next chunk's kernels
+    chunks: int = 8
 
     def backend_for(self, case: str) -> Backend:
         wanted = self.affinity.get(case)
@@ -322,11 +329,23 @@ class AssemblyPlan:
     def synchronize(self) -> None:
         nat.check(nat.lib().gcabem_plan_synchronize(self.handle))
 
-    def download(self, out: np.ndarray) -> None:
-        """Copy the payload into `out` (complex128, payload_len, ideally pinned)."""
+    def execute_download(self, out: np.ndarray, nchunks: int = 8) -> None:
+        """Execute and stream the payload into `out` chunk by chunk (D2H of
+        chunk k overlaps the kernels of chunk k+1). Asynchronous: call
+        synchronize() before reading `out`."""
+        self._check_target(out)
+        nat.check(nat.lib().gcabem_plan_execute_download(self.handle, nat.ptr(out),
+                                                         int(nchunks)))
+        self._pinned_target = out  # keep alive until synchronize
+
+    def _check_target(self, out: np.ndarray) -> None:
         if out.dtype != np.complex128 or out.size != self.payload_len or \
                 not out.flags.c_contiguous:
             raise ValueError("download target must be contiguous complex128 of payload_len")
+
+    def download(self, out: np.ndarray) -> None:
+        """Copy the payload into `out` (complex128, payload_len, ideally pinned)."""
+        self._check_target(out)
         nat.check(nat.lib().gcabem_plan_download(self.handle, nat.ptr(out)))
 
     def timing_ms(self) -> dict:
@@ -371,33 +390,73 @@ def _events(pk: AssemblyPackages, backend: str, t0: float, t1: float) -> list:
     return rows
 
 
+_pk_cache: dict = {}
+_pk_lock = threading.Lock()
+
+
+def clear_package_cache() -> None:
+    with _pk_lock:
+        _pk_cache.clear()
+
+
+def packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
+                 maxsize: int) -> AssemblyPackages:
+    """Work packages of (block tree, operators, budget), cached: packages do
+    not depend on the kernel or the orders, so the DLP assembly reuses the
+    SLP's (as the reference pipeline reuses trees and operators,
+    solver.py:280-282). The cache holds the operator dicts, so their ids
+    stay valid while an entry lives; entries die with the block tree."""
+    key = (id(block_tree), id(row_ops), id(col_ops), int(maxsize), id(mesh.triangles))
+    with _pk_lock:
+        hit = _pk_cache.get(key)
+    if hit is not None and hit[0]() is block_tree:
+        return hit[3]
+    pk = make_packages(mesh.triangles, block_tree, row_ops, col_ops, maxsize)
+    with _pk_lock:
+        _pk_cache[key] = (weakref.ref(block_tree), row_ops, col_ops, pk)
+    weakref.finalize(block_tree, lambda k=key: _pk_cache.pop(k, None))
+    return pk
+
+
 def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
                  row_ops: dict, col_ops: dict, params: SchedulerParams | None = None,
                  orders: tuple = (3, 5), stats: AssemblyStats | None = None) -> GCAMatrix:
-    """Assemble the compressed operator (scheduler.py:442-505) on the device(s)."""
+    """Assemble the compressed operator (scheduler.py:442-505) on the device(s).
+
+    Leaves are split into contiguous ranges, one per device of the backend
+    (or only this process's range when params.shard = (rank, world)); each
+    device streams its payload range into one pinned host buffer while it
+    computes. Entries outside this process's shard stay zero."""
     params = params or SchedulerParams()
     stats = stats if stats is not None else AssemblyStats()
     if not params.backends:
         raise SchedulerConfigError("at least one backend required")
     backend = params.backend_for("disjoint")
     t0 = time.monotonic()
-    pk = make_packages(mesh.triangles, block_tree, row_ops, col_ops, params.maxsize_bytes)
-    payload = nat.pinned_empty(pk.payload_len, np.complex128)
+    pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
     devices = list(backend.devices)
-    shards = shard_leaves(pk, len(devices), orders[0] ** 4,
-                          [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES])
+    sq = [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES]
+    if params.shard is not None:
+        rank, world = params.shard
+        ranges = [shard_leaves(pk, world, orders[0] ** 4, sq)[rank]]
+        ranges = [(ranges[0][0] + a, ranges[0][0] + b) for a, b in
+                  _split_range(pk, ranges[0], len(devices), orders[0] ** 4, sq)]
+    else:
+        ranges = shard_leaves(pk, len(devices), orders[0] ** 4, sq)
+    payload = nat.pinned_empty(pk.payload_len, np.complex128)
+    if params.shard is not None:
+        payload[:] = 0
     plans = []
     try:
-        for dev, rng in zip(devices, shards):
+        for dev, rng in zip(devices, ranges):
             plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng))
         for p in plans:
-            p.execute()
-        for p in plans:
             if p.payload_len:
-                p.download(payload[p.payload_offset:p.payload_offset + p.payload_len])
-            else:
-                p.synchronize()
-        stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans}
+                p.execute_download(payload[p.payload_offset:p.payload_offset + p.payload_len],
+                                   params.chunks)
+        for p in plans:
+            p.synchronize()
+        stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans if p.payload_len}
     finally:
         for p in plans:
             p.close()
@@ -408,9 +467,17 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
     stats.events.extend(ev)
     stats.lists_executed += len(ev)
     stats.pairs_executed += sum(r["pairs"] for r in ev)
-    payloads = {}
-    for k in range(pk.leaf_ids.size):
-        a, b = int(pk.leaf_base[k]), int(pk.leaf_base[k + 1])
-        payloads[int(pk.leaf_ids[k])] = payload[a:b].reshape(tuple(pk.leaf_shape[k]))
+    payloads = LeafPayloads(payload, pk.leaf_ids, pk.leaf_base, pk.leaf_shape)
     return GCAMatrix(block_tree, row_ops, col_ops, payloads, buffer=payload)
 
+
+def _split_range(pk, rng, n, dq, sq):
+    """Relative sub-ranges of a leaf range for n devices, balanced by pairs."""
+    lo, hi = rng
+    if n <= 1:
+        return [(0, hi - lo)]
+    w = (pk.leaf_shape[lo:hi, 0] * pk.leaf_shape[lo:hi, 1]).astype(np.float64)
+    cum = np.cumsum(w)
+    cuts = np.searchsorted(cum, cum[-1] * np.arange(1, n) / n, side="left") + 1
+    edges = np.maximum.accumulate(np.concatenate([[0], np.minimum(cuts, hi - lo), [hi - lo]]))
+    return [(int(edges[k]), int(edges[k + 1])) for k in range(n)]

@@ -259,7 +259,7 @@ def test_sampled_parity_C2_level6():
     corrected = set(items[:, 3].tolist())
     xs, ys, w = oracle.rule("disjoint", 4)
     for b in sel:
-        base, ld, nr, nc, ra, ca = blocks[b]
+        base, ld, nr, nc, ra, ca, _ = blocks[b]
         i, j = np.divmod(np.arange(nr * nc), nc)
         idx = base + i * ld + j
         keep = np.array([k not in corrected for k in idx])

@@ -4,6 +4,7 @@ import hashlib
 import numpy as np
 import pytest
 
+import pk_numpy
 from helpers import golden_ops, sphere_setup
 from paper_1510_07244_b200 import cluster, gca, kernels, mesh, packaging, quadrature, scheduler
 
@@ -116,13 +117,13 @@ def test_split_and_listbuilder_api():
     assert sum(p.num_pairs for p in parts) == 70
     assert all(p.nbytes <= 32 * 16 for p in parts)
     assert [(len(p.row_panels), len(p.col_panels)) for p in parts] == \
-        [(r[1], r[3]) for r in packaging._split(10, 7, 32 * 16)]
+        [(r[1], r[3]) for r in pk_numpy._split(10, 7, 32 * 16)]
     out = []
     lb = scheduler.ListBuilder("disjoint", 32 * 40, out.append)
     for p in parts:
         lb._add(p, p.nbytes)
     lb.flush()
-    lid, n = packaging._greedy_lists(np.array([p.nbytes for p in parts]), 32 * 40)
+    lid, n = pk_numpy._greedy_lists(np.array([p.nbytes for p in parts]), 32 * 40)
     assert n == len(out)
     with pytest.raises(scheduler.SchedulerConfigError):
         scheduler.ListBuilder("disjoint", 16, out.append)
@@ -172,3 +173,32 @@ def test_shard_leaves_partition():
         assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
         assert sum(len(pk.device_items(lo, hi)[0]) for lo, hi in sh) == pk.num_items
         assert sum(len(pk.device_blocks(lo, hi)) for lo, hi in sh) == pk.num_blocks
+
+
+@pytest.mark.parametrize("level,maxsize", [(3, 8 << 20), (4, 8 << 20), (4, 20000), (5, 8 << 20)])
+def test_native_packaging_matches_numpy(gload, level, maxsize):
+    """csrc/packaging.cpp vs the numpy restatement (itself pinned at L3)."""
+    m, t, bt = sphere_setup(level)
+    if level == 3:
+        ops = golden_ops(gload("gca_L3.npz"), "laplace")
+    else:  # synthetic operators: the first min(20, |t|) panels of each cluster
+        ids = {l.row for l in bt.leaves if l.kind == "admissible"} | \
+              {l.col for l in bt.leaves if l.kind == "admissible"}
+        ops = {c: gca.InterpolationOperator(c, None, t.panels(t.nodes[c])[::-1][:20], None)
+               for c in ids}
+    a = packaging.make_packages(m.triangles, bt, ops, ops, maxsize)
+    b = pk_numpy.make_packages(m.triangles, bt, ops, ops, maxsize)
+    assert np.array_equal(a.leaf_shape, b.leaf_shape)
+    assert np.array_equal(a.leaf_base, b.leaf_base)
+    assert np.array_equal(a.leaf_flagged, b.leaf_flagged)
+    for f in ("blk_leaf", "blk_r0", "blk_nr", "blk_c0", "blk_nc", "blk_list", "item_case",
+              "item_tri_x", "item_tri_y", "item_leaf", "item_offset", "item_src_block", "perms"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert a.n_disjoint_lists == b.n_disjoint_lists
+    # same panel sequences through the two layouts
+    for k in np.linspace(0, a.leaf_ids.size - 1, 200).astype(int):
+        nr, nc = a.leaf_shape[k]
+        assert np.array_equal(a.panels[a.leaf_rows_at[k]:a.leaf_rows_at[k] + nr],
+                              b.panels[b.leaf_rows_at[k]:b.leaf_rows_at[k] + nr])
+        assert np.array_equal(a.panels[a.leaf_cols_at[k]:a.leaf_cols_at[k] + nc],
+                              b.panels[b.leaf_cols_at[k]:b.leaf_cols_at[k] + nc])
