@@ -114,6 +114,10 @@ int gcabem_plan_download(gcabem_plan_t plan, double *host);
 int gcabem_plan_synchronize(gcabem_plan_t plan);
 /* CUDA-event durations of the last execute, ms: [disjoint, singular, total]. */
 int gcabem_plan_timing(gcabem_plan_t plan, float *ms3);
+/* Launch this plan's kernels on the caller's stream (a cudaStream_t; NULL
+ * restores the plan's own stream) so callers can order and time several
+ * plans on one timeline. */
+int gcabem_plan_set_stream(gcabem_plan_t plan, void *stream);
 /* Device pointer of the payload (for device-resident consumers). */
 int gcabem_plan_payload(gcabem_plan_t plan, void **dev_ptr);
 int gcabem_plan_destroy(gcabem_plan_t plan);

@@ -51,6 +51,7 @@ _SIGS = {
     "gcabem_plan_synchronize": ([_vp], _int),
     "gcabem_plan_timing": ([_vp, _vp], _int),
     "gcabem_plan_payload": ([_vp, ctypes.POINTER(_vp)], _int),
+    "gcabem_plan_set_stream": ([_vp, _vp], _int),
     "gcabem_plan_destroy": ([_vp], _int),
     "gcabem_green_matrices": ([_vp, _int, _dbl, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64,
                                _vp], _int),

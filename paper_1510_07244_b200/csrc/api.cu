@@ -128,7 +128,8 @@ struct gcabem_plan_s {
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> chunk_ev;
-    cudaStream_t stream = nullptr;  // kernels
+    cudaStream_t stream = nullptr;  // kernels (own_stream, or the caller's)
+    cudaStream_t own_stream = nullptr;
     cudaStream_t copy = nullptr;    // D2H, overlapping later chunks' kernels
     // host copies for chunked execution
     std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
@@ -570,6 +571,15 @@ int gcabem_plan_timing(gcabem_plan_t p, float *ms3) {
     return GCABEM_OK;
 }
 
+int gcabem_plan_set_stream(gcabem_plan_t p, void *stream) {
+    GC_ARG(p, "null plan");
+    GC_CUDA(cudaSetDevice(p->mesh->device));
+    GC_CUDA(cudaStreamSynchronize(p->stream));
+    if (p->own_stream == nullptr) p->own_stream = p->stream;
+    p->stream = stream ? (cudaStream_t)stream : p->own_stream;
+    return GCABEM_OK;
+}
+
 int gcabem_plan_payload(gcabem_plan_t p, void **dev_ptr) {
     GC_ARG(p && dev_ptr, "null argument");
     *dev_ptr = p->payload.p;
@@ -590,7 +600,8 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
     p->panels.release();
     p->items.release();
     for (auto &r : p->srule) r.release();
-    if (p->stream) cudaStreamDestroy(p->stream);
+    cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
+    if (mine) cudaStreamDestroy(mine);
     if (p->copy) cudaStreamDestroy(p->copy);
     delete p;
     return GCABEM_OK;

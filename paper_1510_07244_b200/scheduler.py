@@ -329,6 +329,10 @@ class AssemblyPlan:
     def synchronize(self) -> None:
         nat.check(nat.lib().gcabem_plan_synchronize(self.handle))
 
+    def set_stream(self, stream_handle: int | None) -> None:
+        """Run on an external cudaStream_t (e.g. torch.cuda.Stream.cuda_stream)."""
+        nat.check(nat.lib().gcabem_plan_set_stream(self.handle, stream_handle or None))
+
     def execute_download(self, out: np.ndarray, nchunks: int = 8) -> None:
         """Execute and stream the payload into `out` chunk by chunk (D2H of
         chunk k overlaps the kernels of chunk k+1). Asynchronous: call
