@@ -165,6 +165,18 @@ int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_
                           const double *src, int64_t nduffy, const double *duffy,
                           const int64_t *out_at, int64_t out_len, double *out_host);
 
+/* ---- ACA (host, threaded) ---------------------------------------------------
+ * Partially pivoted ACA of many Green matrices (gca.aca, gca.py:182-245; the
+ * CPU keeps the pivoting per north_star). Cluster c's matrix is rows
+ * [rows_at[c], rows_at[c+1]) x ncols, row-major, starting at entry
+ * rows_at[c]*ncols of A (float64, or interleaved complex128 if is_complex).
+ * Pivots of cluster c are written at out_rows/out_cols + rows_at[c], its rank
+ * to out_rank[c] and the last |u||v| to out_resid[c]. max_rank <= 0: none. */
+int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_t ncols,
+                     const double *A, double epsilon, int64_t max_rank, int nthreads,
+                     int64_t *out_rank, int64_t *out_rows, int64_t *out_cols,
+                     double *out_resid);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Dependent-DFMA throughput probe: achieved FP64 TFLOP/s (FMA = 2 flops). */
 int gcabem_fp64_probe(int device, double *tflops);

@@ -61,6 +61,8 @@ _SIGS = {
     "gcabem_packages_sizes": ([_vp, _vp], _int),
     "gcabem_packages_fetch": ([_vp] * 11, _int),
     "gcabem_packages_free": ([_vp], _int),
+    "gcabem_aca_batch": ([_int, _i64, _vp, _i64, _vp, _dbl, _i64, _int, _vp, _vp, _vp, _vp],
+                         _int),
 }
 EXPORTED = tuple(_SIGS)
 

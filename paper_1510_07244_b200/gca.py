@@ -121,7 +121,7 @@ def green_sources(box_lo, box_hi, delta: float, m: int,
 
 
 def build_green_matrices(mesh: SurfaceMesh, panel_lists, source_sets, spec: KernelSpec,
-                         order: int = 3, device: int | None = None) -> list:
+                         order: int = 3, device: int | None = None, flat: bool = False):
     """Green matrices of many clusters in one device launch (gca.py:136-179).
 
     A[i, j] = w_j * integral over panel i of source field j: monopole
@@ -147,20 +147,18 @@ def build_green_matrices(mesh: SurfaceMesh, panel_lists, source_sets, spec: Kern
     pts, wq = duffy_panel_rule(order)
     duffy = np.ascontiguousarray(np.column_stack([pts, wq]))
     complex_out = spec.is_complex
-    flat = np.empty(out_len * (2 if complex_out else 1), dtype=np.float64)
+    buf = np.empty(out_len * (2 if complex_out else 1), dtype=np.float64)
     eq = 0 if spec.equation == "laplace" else 1
     nat.check(nat.lib().gcabem_green_matrices(
         dm.handle, eq, float(spec.kappa), ncl, nat.ptr(panel_at), nat.ptr(panels), nsrc,
         nat.ptr(src), duffy.shape[0], nat.ptr(duffy), nat.ptr(out_at), out_len,
-        nat.ptr(flat)))
-    vals = flat.view(np.complex128) if complex_out else flat
-    out = []
-    for c in range(ncl):
-        A = vals[out_at[c]:out_at[c] + sizes[c] * nsrc].reshape(sizes[c], nsrc)
-        if not np.all(np.isfinite(A)):
-            raise GcaError("source coincides with a panel quadrature point")
-        out.append(A)
-    return out
+        nat.ptr(buf)))
+    vals = buf.view(np.complex128) if complex_out else buf
+    if not np.all(np.isfinite(vals)):
+        raise GcaError("source coincides with a panel quadrature point")
+    mats = [vals[out_at[c]:out_at[c] + sizes[c] * nsrc].reshape(sizes[c], nsrc)
+            for c in range(ncl)]
+    return (mats, buf, panel_at) if flat else mats
 
 
 def build_green_matrix(mesh: SurfaceMesh, panels, sources: GreenSourceSet, spec: KernelSpec,
@@ -170,63 +168,39 @@ def build_green_matrix(mesh: SurfaceMesh, panels, sources: GreenSourceSet, spec:
                                 spec, order)[0]
 
 
+def aca_batch(flat: np.ndarray, rows_at: np.ndarray, ncols: int, is_complex: bool,
+              epsilon: float, max_rank: int | None = None, nthreads: int = 0):
+    """Native threaded ACA of many matrices (C ABI gcabem_aca_batch):
+    returns [(row_pivots, col_pivots, residual)] per matrix."""
+    if epsilon <= 0.0:
+        raise ValueError("epsilon must be > 0")
+    rows_at = np.ascontiguousarray(rows_at, dtype=np.int64)
+    ncl = rows_at.size - 1
+    total = int(rows_at[-1])
+    rank = np.zeros(ncl, np.int64)
+    rows = np.zeros(max(total, 1), np.int64)
+    cols = np.zeros(max(total, 1), np.int64)
+    resid = np.zeros(ncl, np.float64)
+    flat = np.ascontiguousarray(flat, dtype=np.float64)
+    nat.check(nat.lib().gcabem_aca_batch(
+        int(is_complex), ncl, nat.ptr(rows_at), int(ncols), nat.ptr(flat), float(epsilon),
+        int(max_rank or 0), int(nthreads), nat.ptr(rank), nat.ptr(rows), nat.ptr(cols),
+        nat.ptr(resid)))
+    return [(rows[rows_at[c]:rows_at[c] + rank[c]].copy(),
+             cols[rows_at[c]:rows_at[c] + rank[c]].copy(), float(resid[c])) for c in range(ncl)]
+
+
 def aca(matrix: np.ndarray, epsilon: float, max_rank: int | None = None) -> ACAResult:
     """Partially pivoted ACA (gca.py:182-245): next row = largest residual
     column entry among unused rows, next column = largest residual row entry
-    (ties to the lowest index); stop when |u||v| <= eps * sqrt(estimate)."""
-    if epsilon <= 0.0:
-        raise ValueError("epsilon must be > 0")
+    (ties to the lowest index); stop when |u||v| <= eps * sqrt(estimate).
+    Native (csrc/aca.cpp)."""
     A = np.asarray(matrix)
-    nr, nc = A.shape
-    cap = min(nr, nc) if max_rank is None else min(max_rank, nr, nc)
-    dtype = np.result_type(A.dtype, np.float64)
-    U: list = []
-    W: list = []
-    rows: list = []
-    cols: list = []
-    taken = np.zeros(nr, dtype=bool)
-    est2 = 0.0
-    resid = 0.0
-    cand = 0
-    while len(rows) < cap:
-        if cand >= nr or taken[cand]:
-            free = np.flatnonzero(~taken)
-            if free.size == 0:
-                break
-            cand = int(free[0])
-        i = cand
-        r = A[i, :].astype(dtype, copy=True)
-        for u, w in zip(U, W):
-            r -= u[i] * w
-        j = int(np.argmax(np.abs(r)))
-        taken[i] = True
-        if r[j] == 0.0:
-            cand = nr
-            continue
-        w = r / r[j]
-        c = A[:, j].astype(dtype, copy=True)
-        for u, ww in zip(U, W):
-            c -= ww[j] * u
-        U.append(c)
-        W.append(w)
-        rows.append(i)
-        cols.append(j)
-        nu = float(np.linalg.norm(c))
-        nw = float(np.linalg.norm(w))
-        mix = 0.0
-        for u, ww in zip(U[:-1], W[:-1]):
-            mix += (np.vdot(u, c) * np.vdot(ww, w)).real
-        est2 = max(est2 + nu * nu * nw * nw + 2.0 * mix, 0.0)
-        resid = nu * nw
-        if resid <= epsilon * np.sqrt(est2):
-            break
-        mag = np.abs(c)
-        mag[taken] = 0.0
-        cand = int(np.argmax(mag))
-        if mag[cand] == 0.0:
-            cand = nr
-    return ACAResult(np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64),
-                     len(rows), resid)
+    is_complex = np.iscomplexobj(A)
+    flat = np.ascontiguousarray(A, dtype=np.complex128 if is_complex else np.float64)
+    (r, c, res), = aca_batch(flat.view(np.float64).ravel(), np.array([0, A.shape[0]]),
+                             A.shape[1], is_complex, epsilon, max_rank, nthreads=1)
+    return ACAResult(r, c, int(r.size), res)
 
 
 def _solve_with_refinement(A_cols: np.ndarray, pivot_block: np.ndarray) -> np.ndarray:
@@ -241,18 +215,22 @@ def _solve_with_refinement(A_cols: np.ndarray, pivot_block: np.ndarray) -> np.nd
 
 
 def _operator_from_green(cluster_index: int, panels: np.ndarray, A: np.ndarray,
-                         epsilon: float) -> InterpolationOperator:
-    """ACA + pivot solve with one tighter retry (gca.py:268-282)."""
+                         epsilon: float, first=None) -> InterpolationOperator:
+    """Pivot solve with one tighter ACA retry (gca.py:268-282). `first` is a
+    precomputed (rows, cols, residual) for `epsilon` (batched native ACA)."""
     eps = epsilon
-    for _ in range(2):
-        res = aca(A, eps)
-        if res.rank == 0:
+    for attempt in range(2):
+        if attempt == 0 and first is not None:
+            rows, cols = first[0], first[1]
+        else:
+            res = aca(A, eps)
+            rows, cols = res.row_pivots, res.col_pivots
+        if rows.size == 0:
             raise GcaError(f"cluster {cluster_index}: zero Green matrix")
-        block = A[np.ix_(res.row_pivots, res.col_pivots)]
+        block = A[np.ix_(rows, cols)]
         if np.linalg.cond(block) <= _PIVOT_COND_LIMIT:
-            V = _solve_with_refinement(A[:, res.col_pivots], block)
-            return InterpolationOperator(cluster_index, res.row_pivots,
-                                         panels[res.row_pivots], V)
+            V = _solve_with_refinement(A[:, cols], block)
+            return InterpolationOperator(cluster_index, rows, panels[rows], V)
         eps *= 0.1
     raise GcaError(f"cluster {cluster_index}: singular ACA pivot block "
                    f"(condition above {_PIVOT_COND_LIMIT:.0e})")
@@ -269,8 +247,9 @@ def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, 
 
 
 def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device) -> dict:
-    """Batched device Green matrices, host ACA of batch k overlapped with the
-    device evaluation of batch k+1 (ctypes releases the GIL)."""
+    """Batched device Green matrices and native threaded ACA (worker thread),
+    the pivot solves of batch k overlapped with batch k+1 (ctypes releases
+    the GIL)."""
     ids = sorted(ids)
     nsrc = 12 * params.m * params.m
     width = 16 if spec.is_complex else 8
@@ -289,7 +268,10 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device) -> 
         pl = [tree.panels(tree.nodes[c]) for c in batch]
         ss = [green_sources(tree.nodes[c].lo, tree.nodes[c].hi, params.delta, params.m, scene)
               for c in batch]
-        return pl, build_green_matrices(mesh, pl, ss, spec, params.rule_order, device)
+        mats, buf, rows_at = build_green_matrices(mesh, pl, ss, spec, params.rule_order, device,
+                                                  flat=True)
+        piv = aca_batch(buf, rows_at, nsrc, spec.is_complex, params.epsilon)
+        return pl, mats, piv
 
     ops: dict = {}
     result: dict = {}
@@ -312,9 +294,9 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device) -> 
         if k + 1 < len(batches):
             th = threading.Thread(target=worker, args=(k + 1,))
             th.start()
-        pl, As = got
-        for cid, panels, A in zip(batches[k], pl, As):
-            ops[cid] = _operator_from_green(cid, panels, A, params.epsilon)
+        pl, As, piv = got
+        for cid, panels, A, first in zip(batches[k], pl, As, piv):
+            ops[cid] = _operator_from_green(cid, panels, A, params.epsilon, first)
     return ops
 
 

@@ -202,3 +202,26 @@ def test_native_packaging_matches_numpy(gload, level, maxsize):
                               b.panels[b.leaf_rows_at[k]:b.leaf_rows_at[k] + nr])
         assert np.array_equal(a.panels[a.leaf_cols_at[k]:a.leaf_cols_at[k] + nc],
                               b.panels[b.leaf_cols_at[k]:b.leaf_cols_at[k] + nc])
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+def test_native_aca_matches_numpy_restatement(eq, kappa):
+    """csrc/aca.cpp (threaded batch) vs the numpy ACA on every admissible
+    cluster of the L4 sphere, Green matrices from the oracle (CPU)."""
+    import aca_numpy
+    import oracle
+    m, t, bt = sphere_setup(4)
+    ids = sorted({l.row for l in bt.leaves if l.kind == "admissible"})
+    mats = []
+    for cid in ids[:120]:
+        node = t.nodes[cid]
+        src = gca.green_sources(node.lo, node.hi, 1.0, 6, m.diameter())
+        mats.append(oracle.green_matrix(m.vertices, m.triangles, m.gramians, t.panels(node),
+                                        src.points, src.weights, src.normals, src.roles, eq,
+                                        kappa, 3))
+    rows_at = np.concatenate([[0], np.cumsum([a.shape[0] for a in mats])])
+    flat = np.concatenate([np.ascontiguousarray(a).view(np.float64).ravel() for a in mats])
+    got = gca.aca_batch(flat, rows_at, 432, eq == "helmholtz", 1e-4, nthreads=4)
+    for A, (r, c, _) in zip(mats, got):
+        rr, cc = aca_numpy.aca(A, 1e-4)
+        assert np.array_equal(r, rr) and np.array_equal(c, cc)
