@@ -165,6 +165,26 @@ int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_
                           const double *src, int64_t nduffy, const double *duffy,
                           const int64_t *out_at, int64_t out_len, double *out_host);
 
+/* ---- cluster / block trees (host) -------------------------------------------
+ * Bit-exact restatements of cluster.build_cluster_tree (cluster.py:87-122)
+ * and cluster.build_block_tree (:125-152), preorder node numbering. The
+ * block tree takes node diameters precomputed by the host's own norm and a
+ * norm_variant (0..3) for the distances that the caller verified reproduces
+ * np.linalg.norm bit for bit (gcabem_norm3 probes the variants). */
+typedef struct gcabem_tree_s *gcabem_tree_t;
+int gcabem_cluster_tree(int64_t nt, const double *tri_lo, const double *tri_hi,
+                        const double *mid, int64_t leaf_size, gcabem_tree_t *out);
+int gcabem_block_tree(int64_t nrow, const int64_t *row_c0, const int64_t *row_c1,
+                      const double *row_lo, const double *row_hi, const double *row_diam,
+                      int64_t ncol, const int64_t *col_c0, const int64_t *col_c1,
+                      const double *col_lo, const double *col_hi, const double *col_diam,
+                      double eta, int norm_variant, gcabem_tree_t *out);
+int gcabem_norm3(int64_t n, const double *v, int variant, double *out);
+int gcabem_tree_sizes(gcabem_tree_t t, int64_t *sizes);
+int gcabem_tree_fetch(gcabem_tree_t t, int64_t *a, int64_t *b, int64_t *c, int64_t *d,
+                      int64_t *e, int64_t *f, double *lo, double *hi);
+int gcabem_tree_free(gcabem_tree_t t);
+
 /* ---- ACA (host, threaded) ---------------------------------------------------
  * Partially pivoted ACA of many Green matrices (gca.aca, gca.py:182-245; the
  * CPU keeps the pivoting per north_star). Cluster c's matrix is rows

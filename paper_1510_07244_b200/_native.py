@@ -61,6 +61,13 @@ _SIGS = {
     "gcabem_packages_sizes": ([_vp, _vp], _int),
     "gcabem_packages_fetch": ([_vp] * 11, _int),
     "gcabem_packages_free": ([_vp], _int),
+    "gcabem_cluster_tree": ([_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(_vp)], _int),
+    "gcabem_block_tree": ([_i64] + [_vp] * 5 + [_i64] + [_vp] * 5 + [_dbl, _int,
+                                                                     ctypes.POINTER(_vp)], _int),
+    "gcabem_norm3": ([_i64, _vp, _int, _vp], _int),
+    "gcabem_tree_sizes": ([_vp, _vp], _int),
+    "gcabem_tree_fetch": ([_vp] * 9, _int),
+    "gcabem_tree_free": ([_vp], _int),
     "gcabem_aca_batch": ([_int, _i64, _vp, _i64, _vp, _dbl, _i64, _int, _vp, _vp, _vp, _vp],
                          _int),
 }

@@ -159,6 +159,10 @@ def _tree_arrays(tree: ClusterTree):
 
 
 def _leaf_arrays(bt: BlockTree):
+    native = getattr(bt, "_native_leaves", None)
+    if native is not None:
+        return native
+
     def build(b):
         L = len(b.leaves)
         arr = np.empty((L, 3), dtype=np.int64)

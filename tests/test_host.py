@@ -225,3 +225,21 @@ def test_native_aca_matches_numpy_restatement(eq, kappa):
     for A, (r, c, _) in zip(mats, got):
         rr, cc = aca_numpy.aca(A, 1e-4)
         assert np.array_equal(r, rr) and np.array_equal(c, cc)
+
+
+@pytest.mark.parametrize("level", [5, 6])
+def test_native_trees_match_python(level):
+    """csrc/trees.cpp vs the Python restatements (pinned at L3/L4 by golden)."""
+    m = mesh.build_sphere_mesh(level)
+    a = cluster.build_cluster_tree(m, 16)
+    b = cluster._build_cluster_tree_py(m, 16)
+    assert np.array_equal(a.permutation, b.permutation)
+    assert [(n.start, n.size, n.children) for n in a.nodes] == \
+        [(n.start, n.size, n.children) for n in b.nodes]
+    assert np.array_equal(np.array([n.lo for n in a.nodes]), np.array([n.lo for n in b.nodes]))
+    if level == 5:
+        ba = cluster.build_block_tree(a, a, 2.0)
+        bb = cluster._build_block_tree_py(b, b, 2.0)
+        assert len(ba.nodes) == len(bb.nodes)
+        assert list(ba.nodes) == list(bb.nodes)
+        assert list(ba.leaves) == list(bb.leaves)
