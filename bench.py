@@ -370,13 +370,17 @@ def run_ours(args, cfg, dist, log):
     for s in specs:  # warm the pinned pool and the path
         scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"])
     setup_first = None
+    e2e_phases = []
     for k in range(max(1, args.e2e_steps)):
         dist.barrier()
         scheduler.clear_package_cache()  # every step packages once (shared by SLP/DLP)
         t0 = time.perf_counter()
-        mats = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"]) for s in specs]
+        st = [scheduler.AssemblyStats() for _ in specs]
+        mats = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_)
+                for s, st_ in zip(specs, st)]
         torch.cuda.synchronize(device)
         dt = time.perf_counter() - t0
+        e2e_phases = [x.phase_s for x in st]
         e2e_t.append(dt)
         del mats
         if setup_first is None:
@@ -412,7 +416,8 @@ def run_ours(args, cfg, dist, log):
                      "peak_source": "measured DFMA probe (gcabem_fp64_probe), this device",
                      "kernel_share_of_step": share},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_dt},
+                "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_dt,
+                "phases_s": [{k: round(v, 4) for k, v in ph.items()} for ph in e2e_phases]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "h2_setup": h2_setup,

@@ -155,6 +155,7 @@ class AssemblyStats:
     corrective_items: int = 0
     events: list = field(default_factory=list)
     device_ms: dict = field(default_factory=dict)
+    phase_s: dict = field(default_factory=dict)
 
     def event_rows(self):
         return list(self.events)
@@ -294,6 +295,7 @@ class AssemblyPlan:
 
     def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
                  leaf_range=None):
+        t_prep = time.monotonic()
         lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
         self.leaf_range = (lo, hi)
         self.payload_offset = int(pk.leaf_base[lo])
@@ -315,6 +317,7 @@ class AssemblyPlan:
         self.h2d_bytes = int(blocks.nbytes + pk.panels.nbytes + items.nbytes + perms.nbytes
                              + sum(r.nbytes for r in rules))
         h = ctypes.c_void_p()
+        self.prep_s = time.monotonic() - t_prep
         nat.check(nat.lib().gcabem_plan_create(
             dm.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw),
             self.payload_len, blocks.shape[0], nat.ptr(blocks), pk.panels.size,
@@ -437,7 +440,9 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
         raise SchedulerConfigError("at least one backend required")
     backend = params.backend_for("disjoint")
     t0 = time.monotonic()
+    phase = {}
     pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
+    phase["packaging"] = time.monotonic() - t0
     devices = list(backend.devices)
     sq = [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES]
     if params.shard is not None:
@@ -447,24 +452,34 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
                   _split_range(pk, ranges[0], len(devices), orders[0] ** 4, sq)]
     else:
         ranges = shard_leaves(pk, len(devices), orders[0] ** 4, sq)
+    ta = time.monotonic()
     payload = nat.pinned_empty(pk.payload_len, np.complex128)
     if params.shard is not None:
         payload[:] = 0
+    phase["pinned_alloc"] = time.monotonic() - ta
     plans = []
     try:
+        ta = time.monotonic()
         for dev, rng in zip(devices, ranges):
             plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng))
+        phase["plan_create"] = time.monotonic() - ta
+        phase["plan_host_prep"] = sum(p.prep_s for p in plans)
+        ta = time.monotonic()
         for p in plans:
             if p.payload_len:
                 p.execute_download(payload[p.payload_offset:p.payload_offset + p.payload_len],
                                    params.chunks)
         for p in plans:
             p.synchronize()
+        phase["execute_download"] = time.monotonic() - ta
         stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans if p.payload_len}
     finally:
+        ta = time.monotonic()
         for p in plans:
             p.close()
+        phase["plan_destroy"] = time.monotonic() - ta
     t1 = time.monotonic()
+    stats.phase_s = phase
     stats.block_pairs += pk.block_pairs()
     stats.corrective_items += pk.num_items
     ev = _events(pk, backend.name, t0, t1)

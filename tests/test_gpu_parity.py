@@ -283,3 +283,43 @@ def test_sampled_parity_C2_level6():
         leaf_max = np.array([np.max(np.abs(M.buffer[pk.leaf_base[l]:pk.leaf_base[l + 1]]))
                              for l in leaf_of])
         assert float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), leaf_max))) <= TOL
+
+
+@pytest.mark.parametrize("layer", ["single", "double"])
+def test_sampled_parity_helmholtz_small_phase(layer):
+    """Fine Helmholtz mesh (L6, kappa = 2: kappa (R_x + R_y) < 1/8 for every
+    pair) exercises the factored-phase path e^{i phi0} e^{i delta} in the
+    disjoint and singular kernels; sampled entries vs the oracle."""
+    m, t, bt = sphere_setup(6)
+    near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    pk = packaging.make_packages(m.triangles, near, {}, {}, 8 << 20)
+    kappa = 2.0
+    M = scheduler.run_assembly(m, near, kernels.KernelSpec("helmholtz", layer, kappa), {}, {},
+                               scheduler.SchedulerParams(), (3, 5))
+    rng = np.random.default_rng(7)
+    blocks = pk.device_blocks()
+    items, perms = pk.device_items()
+    corrected = set(items[:, 3].tolist())
+    xs, ys, w = oracle.rule("disjoint", 3)
+    for b in rng.choice(len(blocks), 200, replace=False):
+        base, ld, nr, nc, ra, ca, _ = blocks[b]
+        i, j = np.divmod(np.arange(nr * nc), nc)
+        idx = base + i * ld + j
+        keep = np.array([k not in corrected for k in idx])
+        ref = oracle.batch_quadrature("helmholtz", layer, kappa, m.vertices, m.triangles,
+                                      m.normals, m.gramians, pk.panels[ra + i][keep],
+                                      pk.panels[ca + j][keep], None, None, xs, ys, w)
+        assert rel_err(M.buffer[idx[keep]], ref) <= TOL
+    s = rng.choice(len(items), 3000, replace=False)
+    for code, case in ((1, "vertex"), (2, "edge"), (3, "identical")):
+        ss = s[items[s, 0] == code]
+        ref = oracle.batch_quadrature("helmholtz", layer, kappa, m.vertices, m.triangles,
+                                      m.normals, m.gramians, items[ss, 1], items[ss, 2],
+                                      perms[ss, :3].astype(np.int64),
+                                      perms[ss, 3:].astype(np.int64), *oracle.rule(case, 5))
+        got = M.buffer[items[ss, 3]]
+        leaf_of = np.searchsorted(pk.leaf_base, items[ss, 3], side="right") - 1
+        leaf_max = np.array([np.max(np.abs(M.buffer[pk.leaf_base[l]:pk.leaf_base[l + 1]]))
+                             for l in leaf_of])
+        scale = np.abs(ref) if layer == "single" else np.maximum(np.abs(ref), leaf_max)
+        assert float(np.max(np.abs(got - ref) / scale)) <= TOL
