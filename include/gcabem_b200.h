@@ -31,6 +31,7 @@ extern "C" {
 
 typedef struct gcabem_mesh_s *gcabem_mesh_t;
 typedef struct gcabem_plan_s *gcabem_plan_t;
+typedef struct gcabem_layout_s *gcabem_layout_t;
 
 /* ---- library / device ------------------------------------------------- */
 int gcabem_version(void);
@@ -101,6 +102,17 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
                        int64_t npanels, const int64_t *panels, int64_t nitems,
                        const int64_t *items, const uint8_t *perms, const int64_t *sq,
                        const double *const *srule, gcabem_plan_t *out);
+/* The same in two steps: upload the packages once as a device layout, then
+ * create any number of plans (operators: SLP, DLP, orders) on it; each plan
+ * holds a reference, gcabem_layout_release drops the caller's. */
+int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblocks,
+                         const int64_t *blocks, int64_t npanels, const int64_t *panels,
+                         int64_t nitems, const int64_t *items, const uint8_t *perms,
+                         gcabem_layout_t *out);
+int gcabem_layout_release(gcabem_layout_t layout);
+int gcabem_plan_create_on(gcabem_layout_t layout, int equation, int layer, double kappa,
+                          int disjoint_n, const double *gauss_pts, const double *gauss_wts,
+                          const int64_t *sq, const double *const *srule, gcabem_plan_t *out);
 /* Launch all kernels on the plan stream (async). The payload is zeroed first
  * (make_payloads semantics), then disjoint, then singular overwrites. */
 int gcabem_plan_execute(gcabem_plan_t plan);

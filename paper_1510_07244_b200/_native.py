@@ -46,6 +46,11 @@ _SIGS = {
     "gcabem_plan_create": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
                             _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)], _int),
     "gcabem_plan_execute": ([_vp], _int),
+    "gcabem_layout_create": ([_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp,
+                              ctypes.POINTER(_vp)], _int),
+    "gcabem_layout_release": ([_vp], _int),
+    "gcabem_plan_create_on": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp,
+                               ctypes.POINTER(_vp)], _int),
     "gcabem_plan_download": ([_vp, _vp], _int),
     "gcabem_plan_execute_download": ([_vp, _vp, _int], _int),
     "gcabem_plan_synchronize": ([_vp], _int),

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -112,18 +113,29 @@ struct gcabem_mesh_s {
     DevBuf<Chart> charts;
 };
 
-struct gcabem_plan_s {
+// Device layout of one package set: uploaded once, shared by every plan
+// (operator) assembled from the same packages (e.g. SLP and DLP).
+struct gcabem_layout_s {
     gcabem_mesh_t mesh = nullptr;
-    int kind = 0, order = 0;
-    double kappa = 0.0;
     int64_t payload_len = 0;
-    DevBuf<double2> payload;
     DevBuf<BlockDesc> blocks;
     DevBuf<int2> tasks;
     int64_t ntasks = 0;
     DevBuf<int32_t> panels;
     DevBuf<SingItem> items;
     int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])
+    // host copies for chunked execution
+    std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
+    std::atomic<int> refs{1};
+};
+
+struct gcabem_plan_s {
+    gcabem_mesh_t mesh = nullptr;
+    gcabem_layout_t L = nullptr;
+    int kind = 0, order = 0;
+    double kappa = 0.0;
+    int64_t payload_len = 0;
+    DevBuf<double2> payload;
     DevBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -131,8 +143,6 @@ struct gcabem_plan_s {
     cudaStream_t stream = nullptr;  // kernels (own_stream, or the caller's)
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy = nullptr;    // D2H, overlapping later chunks' kernels
-    // host copies for chunked execution
-    std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
     bool executed = false;
 };
 
@@ -322,80 +332,79 @@ int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double 
     return GCABEM_OK;
 }
 
-int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa, int disjoint_n,
-                       const double *gauss_pts, const double *gauss_wts, int64_t payload_len,
-                       int64_t nblocks, const int64_t *blocks, int64_t npanels,
-                       const int64_t *panels, int64_t nitems, const int64_t *items,
-                       const uint8_t *perms, const int64_t *sq, const double *const *srule,
-                       gcabem_plan_t *out) {
+int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblocks,
+                         const int64_t *blocks, int64_t npanels, const int64_t *panels,
+                         int64_t nitems, const int64_t *items, const uint8_t *perms,
+                         gcabem_layout_t *out) {
     GC_ARG(mesh && out, "null argument");
     *out = nullptr;
-    if (int rc = check_kind(equation, layer, kappa)) return rc;
-    GC_ARG(disjoint_n >= 1 && disjoint_n <= MAX_ORDER, "disjoint order outside [1, 12]");
     GC_ARG(payload_len >= 0 && nblocks >= 0 && npanels >= 0 && nitems >= 0, "negative size");
     GC_ARG(nblocks < (int64_t(1) << 31), "too many blocks");
     GC_CUDA(cudaSetDevice(mesh->device));
-    if (int rc = ensure_disjoint_rule(mesh->device, disjoint_n, gauss_pts, gauss_wts)) return rc;
-
-    auto *p = new gcabem_plan_s();
-    p->mesh = mesh;
-    p->kind = kind_of(equation, layer);
-    p->order = disjoint_n;
-    p->kappa = kappa;
-    p->payload_len = payload_len;
+    auto *L = new gcabem_layout_s();
+    L->mesh = mesh;
+    L->payload_len = payload_len;
+    auto fail = [&](const char *msg) {
+        delete L;
+        return set_error(GCABEM_ERR_ARG, msg);
+    };
     // WorkBlocks -> descriptors + fixed-size tasks (DISJOINT_TPB pairs each)
     std::vector<BlockDesc> bd(nblocks);
-    std::vector<int2> tasks;
-    p->block_task_at.assign(nblocks + 1, 0);
-    p->block_leaf.resize(nblocks);
-    p->block_base.resize(nblocks);
-    p->block_pairs.resize(nblocks);
+    L->block_task_at.assign(nblocks + 1, 0);
+    L->block_leaf.resize(nblocks);
+    L->block_base.resize(nblocks);
+    L->block_pairs.resize(nblocks);
+    int64_t ntasks = 0;
     for (int64_t b = 0; b < nblocks; ++b) {
         const int64_t *r = blocks + 7 * b;
         const int64_t base = r[0], ld = r[1], nr = r[2], nc = r[3], ra = r[4], ca = r[5];
         if (!(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31)) ||
             !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
             !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= payload_len)) ||
-            (b > 0 && r[6] < blocks[7 * (b - 1) + 6])) {
-            delete p;
-            return set_error(GCABEM_ERR_ARG, "block descriptor out of bounds or out of order");
-        }
+            (b > 0 && r[6] < blocks[7 * (b - 1) + 6]))
+            return fail("block descriptor out of bounds or out of order");
         bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
-        p->block_task_at[b] = (int64_t)tasks.size();
-        p->block_leaf[b] = r[6];
-        p->block_base[b] = base;
-        p->block_pairs[b] = nr * nc;
-        for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
-            tasks.push_back(make_int2((int)b, (int)k0));
+        L->block_task_at[b] = ntasks;
+        L->block_leaf[b] = r[6];
+        L->block_base[b] = base;
+        L->block_pairs[b] = nr * nc;
+        ntasks += (nr * nc + DISJOINT_TPB - 1) / DISJOINT_TPB;
     }
-    p->block_task_at[nblocks] = (int64_t)tasks.size();
+    L->block_task_at[nblocks] = ntasks;
+    std::vector<int2> tasks(ntasks);
+    for (int64_t b = 0; b < nblocks; ++b) {
+        int64_t t = L->block_task_at[b];
+        for (int64_t k0 = 0; k0 < L->block_pairs[b]; k0 += DISJOINT_TPB)
+            tasks[t++] = make_int2((int)b, (int)k0);
+    }
     std::vector<int32_t> pan(npanels);
     for (int64_t k = 0; k < npanels; ++k) {
-        if (panels[k] < 0 || panels[k] >= mesh->nt) {
-            delete p;
-            return set_error(GCABEM_ERR_ARG, "panel index out of range");
-        }
+        if (panels[k] < 0 || panels[k] >= mesh->nt) return fail("panel index out of range");
         pan[k] = (int32_t)panels[k];
     }
     // singular items: grouped by case 1..3, sorted by payload index inside a
-    // case (chunked execution looks chunks up by payload range)
-    std::vector<int64_t> order(nitems);
+    // case (chunked execution looks chunks up by payload range); the common
+    // input (device_items order) already is, which is checked in O(n)
     int64_t counts[4] = {0, 0, 0, 0};
+    bool sorted = true;
     for (int64_t k = 0; k < nitems; ++k) {
-        order[k] = k;
         const int64_t c = items[4 * k];
-        if (c < 1 || c > 3) {
-            delete p;
-            return set_error(GCABEM_ERR_ARG, "singular item case must be vertex/edge/identical");
-        }
+        if (c < 1 || c > 3) return fail("singular item case must be vertex/edge/identical");
         counts[c]++;
+        if (k > 0) {
+            const int64_t pc = items[4 * (k - 1)];
+            sorted = sorted && (pc < c || (pc == c && items[4 * (k - 1) + 3] <= items[4 * k + 3]));
+        }
     }
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-        return items[4 * a] != items[4 * b] ? items[4 * a] < items[4 * b]
-                                            : items[4 * a + 3] < items[4 * b + 3];
-    });
+    std::vector<int64_t> order(nitems);
+    for (int64_t k = 0; k < nitems; ++k) order[k] = k;
+    if (!sorted)
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+            return items[4 * a] != items[4 * b] ? items[4 * a] < items[4 * b]
+                                                : items[4 * a + 3] < items[4 * b + 3];
+        });
     std::vector<SingItem> si(nitems);
-    p->item_out.resize(nitems);
+    L->item_out.resize(nitems);
     for (int64_t q = 0; q < nitems; ++q) {
         const int64_t k = order[q];
         const int64_t c = items[4 * k];
@@ -414,40 +423,90 @@ int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa
         }
         ok = ok && (c != 3 || (it.tri_x == it.tri_y && it.px[0] == it.py[0] &&
                                it.px[1] == it.py[1] && it.px[2] == it.py[2]));
-        if (!ok) {
-            delete p;
-            return set_error(GCABEM_ERR_ARG, "bad singular item (index, permutation or chart)");
-        }
-        p->item_out[q] = it.out;
+        if (!ok) return fail("bad singular item (index, permutation or chart)");
+        L->item_out[q] = it.out;
     }
-    p->ntasks = (int64_t)tasks.size();
-    p->case_at[0] = 0;
-    for (int c = 1; c <= 3; ++c) p->case_at[c] = p->case_at[c - 1] + counts[c];
+    L->ntasks = ntasks;
+    L->case_at[0] = 0;
+    for (int c = 1; c <= 3; ++c) L->case_at[c] = L->case_at[c - 1] + counts[c];
+    cudaStream_t s = mesh->stream;
+    cudaError_t e = L->blocks.upload(bd.data(), bd.size(), s);
+    if (e == cudaSuccess) e = L->tasks.upload(tasks.data(), tasks.size(), s);
+    if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
+    if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    if (e != cudaSuccess) {
+        delete L;
+        GC_CUDA(e);
+    }
+    *out = L;
+    return GCABEM_OK;
+}
+
+int gcabem_layout_release(gcabem_layout_t L) {
+    if (!L) return GCABEM_OK;
+    if (--L->refs > 0) return GCABEM_OK;
+    cudaSetDevice(L->mesh->device);
+    cudaStreamSynchronize(L->mesh->stream);
+    delete L;  // DevBuf destructors free the device buffers
+    return GCABEM_OK;
+}
+
+int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kappa,
+                          int disjoint_n, const double *gauss_pts, const double *gauss_wts,
+                          const int64_t *sq, const double *const *srule, gcabem_plan_t *out) {
+    GC_ARG(L && out, "null argument");
+    *out = nullptr;
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    GC_ARG(disjoint_n >= 1 && disjoint_n <= MAX_ORDER, "disjoint order outside [1, 12]");
+    gcabem_mesh_t mesh = L->mesh;
+    GC_CUDA(cudaSetDevice(mesh->device));
+    if (int rc = ensure_disjoint_rule(mesh->device, disjoint_n, gauss_pts, gauss_wts)) return rc;
+    for (int c = 0; c < 3; ++c)
+        GC_ARG(L->case_at[c + 1] == L->case_at[c] || (sq && sq[c] > 0),
+               "singular items without a rule");
+    auto *p = new gcabem_plan_s();
+    p->mesh = mesh;
+    p->L = L;
+    ++L->refs;
+    p->kind = kind_of(equation, layer);
+    p->order = disjoint_n;
+    p->kappa = kappa;
+    p->payload_len = L->payload_len;
     cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
-    cudaStream_t s = p->stream;
-    if (e == cudaSuccess) e = p->payload.alloc(payload_len);
-    if (e == cudaSuccess) e = p->blocks.upload(bd.data(), bd.size(), s);
-    if (e == cudaSuccess) e = p->tasks.upload(tasks.data(), tasks.size(), s);
-    if (e == cudaSuccess) e = p->panels.upload(pan.data(), pan.size(), s);
-    if (e == cudaSuccess) e = p->items.upload(si.data(), si.size(), s);
+    if (e == cudaSuccess) e = p->payload.alloc(p->payload_len);
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         p->sq[c] = sq ? sq[c] : 0;
-        if (p->sq[c] > 0 && counts[c + 1] > 0) e = p->srule[c].upload(srule[c], 5 * p->sq[c], s);
+        if (p->sq[c] > 0 && L->case_at[c + 1] > L->case_at[c])
+            e = p->srule[c].upload(srule[c], 5 * p->sq[c], p->stream);
     }
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
     if (e != cudaSuccess) {
         gcabem_plan_destroy(p);
         GC_CUDA(e);
     }
-    for (int c = 0; c < 3; ++c)
-        if (counts[c + 1] > 0 && p->sq[c] <= 0) {
-            gcabem_plan_destroy(p);
-            return set_error(GCABEM_ERR_ARG, "singular items without a rule");
-        }
     *out = p;
     return GCABEM_OK;
+}
+
+int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa, int disjoint_n,
+                       const double *gauss_pts, const double *gauss_wts, int64_t payload_len,
+                       int64_t nblocks, const int64_t *blocks, int64_t npanels,
+                       const int64_t *panels, int64_t nitems, const int64_t *items,
+                       const uint8_t *perms, const int64_t *sq, const double *const *srule,
+                       gcabem_plan_t *out) {
+    GC_ARG(out, "null argument");
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    gcabem_layout_t L = nullptr;
+    if (int rc = gcabem_layout_create(mesh, payload_len, nblocks, blocks, npanels, panels,
+                                      nitems, items, perms, &L))
+        return rc;
+    const int rc = gcabem_plan_create_on(L, equation, layer, kappa, disjoint_n, gauss_pts,
+                                         gauss_wts, sq, srule, out);
+    gcabem_layout_release(L);  // the plan holds its own reference
+    return rc;
 }
 
 namespace {
@@ -457,16 +516,16 @@ namespace {
 int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p1) {
     gcabem_mesh_t m = p->mesh;
     cudaStream_t s = p->stream;
-    const int64_t t0 = p->block_task_at[b0], t1 = p->block_task_at[b1];
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->blocks.p, p->tasks.p + t0, t1 - t0,
-                            p->panels.p, p->payload.p, p->kappa, s));
+    const int64_t t0 = p->L->block_task_at[b0], t1 = p->L->block_task_at[b1];
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p + t0, t1 - t0,
+                            p->L->panels.p, p->payload.p, p->kappa, s));
     for (int c = 0; c < 3; ++c) {
-        const auto first = p->item_out.begin() + p->case_at[c];
-        const auto last = p->item_out.begin() + p->case_at[c + 1];
-        const int64_t i0 = std::lower_bound(first, last, p0) - p->item_out.begin();
-        const int64_t i1 = std::lower_bound(first, last, p1) - p->item_out.begin();
+        const auto first = p->L->item_out.begin() + p->L->case_at[c];
+        const auto last = p->L->item_out.begin() + p->L->case_at[c + 1];
+        const int64_t i0 = std::lower_bound(first, last, p0) - p->L->item_out.begin();
+        const int64_t i1 = std::lower_bound(first, last, p1) - p->L->item_out.begin();
         if (i1 <= i0) continue;
-        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->items.p + i0,
+        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->L->items.p + i0,
                                i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->kappa, s));
     }
     return GCABEM_OK;
@@ -482,14 +541,14 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     if (p->payload_len > 0)
         GC_CUDA(cudaMemsetAsync(p->payload.p, 0, sizeof(double2) * p->payload_len, s));
     GC_CUDA(cudaEventRecord(p->ev[0], s));
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->blocks.p, p->tasks.p, p->ntasks,
-                            p->panels.p, p->payload.p, p->kappa, s));
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p, p->L->ntasks,
+                            p->L->panels.p, p->payload.p, p->kappa, s));
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     for (int c = 0; c < 3; ++c) {
-        const int64_t n = p->case_at[c + 1] - p->case_at[c];
+        const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
         if (n == 0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
-                               p->items.p + p->case_at[c], n, p->srule[c].p, p->sq[c],
+                               p->L->items.p + p->L->case_at[c], n, p->srule[c].p, p->sq[c],
                                p->payload.p, p->kappa, s));
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
@@ -500,19 +559,19 @@ int gcabem_plan_execute(gcabem_plan_t p) {
 int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
     GC_CUDA(cudaSetDevice(p->mesh->device));
-    const int64_t B = (int64_t)p->block_leaf.size();
+    const int64_t B = (int64_t)p->L->block_leaf.size();
     if (nchunks < 1) nchunks = 1;
     // leaf-aligned chunk boundaries balanced by pairs
     std::vector<int64_t> cut{0};
     int64_t total = 0;
-    for (int64_t b = 0; b < B; ++b) total += p->block_pairs[b];
+    for (int64_t b = 0; b < B; ++b) total += p->L->block_pairs[b];
     int64_t acc = 0, next = 1;
     for (int64_t b = 0; b < B && next < nchunks; ++b) {
-        if (b > 0 && p->block_leaf[b] != p->block_leaf[b - 1] && acc * nchunks >= next * total) {
+        if (b > 0 && p->L->block_leaf[b] != p->L->block_leaf[b - 1] && acc * nchunks >= next * total) {
             cut.push_back(b);
             ++next;
         }
-        acc += p->block_pairs[b];
+        acc += p->L->block_pairs[b];
     }
     cut.push_back(B);
     cudaStream_t s = p->stream;
@@ -524,8 +583,8 @@ int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
     }
     for (size_t k = 0; k + 1 < cut.size(); ++k) {
         const int64_t b0 = cut[k], b1 = cut[k + 1];
-        const int64_t p0 = b0 < B ? p->block_base[b0] : p->payload_len;
-        const int64_t p1 = b1 < B ? p->block_base[b1] : p->payload_len;
+        const int64_t p0 = b0 < B ? p->L->block_base[b0] : p->payload_len;
+        const int64_t p1 = b1 < B ? p->L->block_base[b1] : p->payload_len;
         if (p1 > p0)
             GC_CUDA(cudaMemsetAsync(p->payload.p + p0, 0, sizeof(double2) * (p1 - p0), s));
         if (int rc = enqueue_range(p, b0, b1, p0, p1)) return rc;
@@ -595,14 +654,11 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
         if (e) cudaEventDestroy(e);
     for (auto &e : p->chunk_ev) cudaEventDestroy(e);
     p->payload.release();
-    p->blocks.release();
-    p->tasks.release();
-    p->panels.release();
-    p->items.release();
     for (auto &r : p->srule) r.release();
     cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
     if (mine) cudaStreamDestroy(mine);
     if (p->copy) cudaStreamDestroy(p->copy);
+    gcabem_layout_release(p->L);
     delete p;
     return GCABEM_OK;
 }

@@ -288,14 +288,13 @@ def execute_list(lst: WorkList, backend: Backend, mesh: SurfaceMesh, spec: Kerne
 # ---------------------------------------------------------------------------
 # fused device execution
 
-class AssemblyPlan:
-    """Device plan of one operator on one device: packages uploaded once,
-    executable repeatedly (C ABI gcabem_plan_*). Payload stays in HBM until
-    download()."""
+class DeviceLayout:
+    """Packages of a leaf range uploaded to one device (C ABI gcabem_layout_*):
+    block descriptors, tasks, panel indices, singular items. Shared by every
+    operator assembled from the same packages; cached on the packages."""
 
-    def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
-                 leaf_range=None):
-        t_prep = time.monotonic()
+    def __init__(self, dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None):
+        t0 = time.monotonic()
         lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
         self.leaf_range = (lo, hi)
         self.payload_offset = int(pk.leaf_base[lo])
@@ -304,6 +303,50 @@ class AssemblyPlan:
         items, perms = pk.device_items(lo, hi)
         self.disjoint_pairs = int(np.sum(blocks[:, 2] * blocks[:, 3])) if blocks.size else 0
         self.singular_counts = [int(np.count_nonzero(items[:, 0] == c)) for c in (1, 2, 3)]
+        self.h2d_bytes = int(blocks.nbytes + pk.panels.nbytes + items.nbytes + perms.nbytes)
+        self.prep_s = time.monotonic() - t0
+        self.device = dm.device
+        self._dm = dm
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().gcabem_layout_create(
+            dm.handle, self.payload_len, blocks.shape[0], nat.ptr(blocks), pk.panels.size,
+            nat.ptr(pk.panels), items.shape[0], nat.ptr(items), nat.ptr(perms), ctypes.byref(h)))
+        self.handle = h.value
+
+    @staticmethod
+    def cached(dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None) -> "DeviceLayout":
+        lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
+        key = ("layout", dm.device, id(dm), lo, hi)
+        lay = pk.extra.get(key)
+        if lay is None:
+            lay = DeviceLayout(dm, pk, (lo, hi))
+            pk.extra[key] = lay
+        return lay
+
+    def close(self) -> None:
+        h, self.handle = getattr(self, "handle", None), None
+        if h and nat._lib is not None:
+            nat._lib.gcabem_layout_release(h)
+
+    def __del__(self):
+        self.close()
+
+
+class AssemblyPlan:
+    """Device plan of one operator on one device: a (shared, cached) device
+    layout of the packages plus this operator's payload, executable
+    repeatedly (C ABI gcabem_plan_*). Payload stays in HBM until download()."""
+
+    def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
+                 leaf_range=None):
+        t_prep = time.monotonic()
+        self.layout = DeviceLayout.cached(dm, pk, leaf_range)
+        lay = self.layout
+        self.leaf_range = lay.leaf_range
+        self.payload_offset = lay.payload_offset
+        self.payload_len = lay.payload_len
+        self.disjoint_pairs = lay.disjoint_pairs
+        self.singular_counts = lay.singular_counts
         dn, sn = orders
         g = gauss_legendre(dn)
         gp, gw = nat.f64(g.points), nat.f64(g.weights)
@@ -314,14 +357,11 @@ class AssemblyPlan:
         eq, layer = spec.code
         self.spec, self.orders, self.device = spec, tuple(orders), dm.device
         self._dm = dm
-        self.h2d_bytes = int(blocks.nbytes + pk.panels.nbytes + items.nbytes + perms.nbytes
-                             + sum(r.nbytes for r in rules))
-        h = ctypes.c_void_p()
+        self.h2d_bytes = lay.h2d_bytes + int(sum(r.nbytes for r in rules))
         self.prep_s = time.monotonic() - t_prep
-        nat.check(nat.lib().gcabem_plan_create(
-            dm.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw),
-            self.payload_len, blocks.shape[0], nat.ptr(blocks), pk.panels.size,
-            nat.ptr(pk.panels), items.shape[0], nat.ptr(items), nat.ptr(perms), nat.ptr(sq),
+        h = ctypes.c_void_p()
+        nat.check(nat.lib().gcabem_plan_create_on(
+            lay.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw), nat.ptr(sq),
             ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
         self.handle = h.value
         self._keep = rules
@@ -487,6 +527,7 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
     stats.lists_executed += len(ev)
     stats.pairs_executed += sum(r["pairs"] for r in ev)
     payloads = LeafPayloads(payload, pk.leaf_ids, pk.leaf_base, pk.leaf_shape)
+    phase["total"] = time.monotonic() - t0
     return GCAMatrix(block_tree, row_ops, col_ops, payloads, buffer=payload)
 
 
