@@ -209,6 +209,15 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
                      int64_t *out_rank, int64_t *out_rows, int64_t *out_cols,
                      double *out_resid);
 
+/* ---- potential evaluation --------------------------------------------------
+ * Replaces scheduler.potential_batch (scheduler.py:508-534): out (npts x nt,
+ * complex128 row-major) = plain panel integrals of the kernel field at each
+ * point, the disjoint rule of `order` (1..8) with a zero-extent x chart and
+ * gx = 2. Points on the surface give non-finite entries (the caller raises). */
+int gcabem_potential(gcabem_mesh_t mesh, int equation, int layer, double kappa, int order,
+                     const double *gauss_pts, const double *gauss_wts, int64_t npts,
+                     const double *points, double *out);
+
 /* ---- diagnostics ------------------------------------------------------------ */
 /* Dependent-DFMA throughput probe: achieved FP64 TFLOP/s (FMA = 2 flops). */
 int gcabem_fp64_probe(int device, double *tflops);

@@ -61,6 +61,7 @@ _SIGS = {
     "gcabem_green_matrices": ([_vp, _int, _dbl, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64,
                                _vp], _int),
     "gcabem_fp64_probe": ([_int, ctypes.POINTER(_dbl)], _int),
+    "gcabem_potential": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _i64, _vp, _vp], _int),
     "gcabem_packages_build": ([_i64, _vp, _i64, _vp, _i64] + [_vp] * 7 + [_i64] + [_vp] * 7
                               + [_i64, _int, ctypes.POINTER(_vp)], _int),
     "gcabem_packages_sizes": ([_vp, _vp], _int),

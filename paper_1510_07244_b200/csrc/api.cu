@@ -707,6 +707,33 @@ int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_
     return GCABEM_OK;
 }
 
+int gcabem_potential(gcabem_mesh_t mesh, int equation, int layer, double kappa, int order,
+                     const double *gauss_pts, const double *gauss_wts, int64_t npts,
+                     const double *points, double *out) {
+    GC_ARG(mesh && out && (points || npts == 0), "null argument");
+    if (int rc = check_kind(equation, layer, kappa)) return rc;
+    GC_ARG(order >= 1 && order <= 8, "potential order outside [1, 8]");
+    GC_ARG(npts >= 0, "negative size");
+    if (npts == 0) return GCABEM_OK;
+    GC_CUDA(cudaSetDevice(mesh->device));
+    if (int rc = ensure_disjoint_rule(mesh->device, order, gauss_pts, gauss_wts)) return rc;
+    // sum of the x-side Duffy weights (gx = 2 cancels the reference-triangle area)
+    double xw = 0.0;
+    for (int a = 0; a < order; ++a)
+        for (int b = 0; b < order; ++b) xw += (gauss_wts[a] * gauss_wts[b]) * gauss_pts[a];
+    cudaStream_t s = mesh->stream;
+    DevBuf<double> dp;
+    DevBuf<double2> dout;
+    GC_CUDA(dp.upload(points, 3 * npts, s));
+    GC_CUDA(dout.alloc(npts * mesh->nt));
+    GC_CUDA(launch_potential(kind_of(equation, layer), order, mesh->charts.p, mesh->nt, dp.p, npts,
+                             xw, dout.p, kappa, s));
+    GC_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double2) * npts * mesh->nt,
+                            cudaMemcpyDeviceToHost, s));
+    GC_CUDA(cudaStreamSynchronize(s));
+    return GCABEM_OK;
+}
+
 int gcabem_fp64_probe(int device, double *tflops) {
     GC_ARG(tflops, "null argument");
     GC_CUDA(cudaSetDevice(device));

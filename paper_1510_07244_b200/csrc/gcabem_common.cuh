@@ -66,6 +66,9 @@ cudaError_t launch_green(int equation, const Chart *charts, const int2 *tasks, i
                          const int64_t *panel_at, const int32_t *panels, const int64_t *out_at,
                          int nsrc, const double *src, const double *duffy, int nq, double *out,
                          double kappa, cudaStream_t s);
+cudaError_t launch_potential(int kind, int order, const Chart *charts, int64_t nt,
+                             const double *pts, int64_t npts, double xw, double2 *out,
+                             double kappa, cudaStream_t s);
 cudaError_t launch_fp64_probe(double *sink, int iters, int blocks, cudaStream_t s);
 
 }  // namespace gcabem

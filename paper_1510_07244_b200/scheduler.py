@@ -43,7 +43,8 @@ __all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "A
            "split_block", "ListBuilder", "batch_quadrature", "execute_list", "run_assembly",
            "make_payloads", "BackendError", "SchedulerConfigError", "CUDA_BACKEND",
            "BATCH_BACKEND", "SCALAR_BACKEND", "DEFAULT_MAXSIZE", "BYTES_PER_PAIR",
-           "PAIR_RECORD_BYTES", "VALUE_BYTES", "SINGULAR_CASES", "AssemblyPlan"]
+           "PAIR_RECORD_BYTES", "VALUE_BYTES", "SINGULAR_CASES", "AssemblyPlan",
+           "DeviceLayout", "potential_batch", "clear_package_cache"]
 
 
 @dataclass(frozen=True)
@@ -541,3 +542,26 @@ def _split_range(pk, rng, n, dq, sq):
     cuts = np.searchsorted(cum, cum[-1] * np.arange(1, n) / n, side="left") + 1
     edges = np.maximum.accumulate(np.concatenate([[0], np.minimum(cuts, hi - lo), [hi - lo]]))
     return [(int(edges[k]), int(edges[k + 1])) for k in range(n)]
+
+
+def potential_batch(mesh: SurfaceMesh, spec: KernelSpec, points: np.ndarray,
+                    order: int = 3, device: int | None = None) -> np.ndarray:
+    """Per-panel potentials at off-surface points (scheduler.py:508-534), on
+    the device: each point is a zero-extent target panel whose Gramian 2
+    cancels the reference-triangle area of the x half; returns the
+    (npoints, npanels) matrix of plain panel integrals of the kernel field."""
+    from .pairquad import default_device
+    points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    dev = default_device() if device is None else device
+    dm = device_mesh(mesh, dev)
+    g = gauss_legendre(order)
+    gp, gw = nat.f64(g.points), nat.f64(g.weights)
+    out = np.empty((points.shape[0], mesh.num_triangles), dtype=np.complex128)
+    eq, layer = spec.code
+    nat.check(nat.lib().gcabem_potential(dm.handle, eq, layer, float(spec.kappa), int(order),
+                                         nat.ptr(gp), nat.ptr(gw), points.shape[0],
+                                         nat.ptr(points), nat.ptr(out)))
+    bad = ~np.all(np.isfinite(out), axis=1)
+    if np.any(bad):
+        raise ValueError(f"evaluation point {int(np.flatnonzero(bad)[0])} lies on the surface")
+    return out

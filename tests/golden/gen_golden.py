@@ -316,6 +316,34 @@ def gen_assembly(meta):
     np.savez_compressed(os.path.join(HERE, "assembly.npz"), **out)
 
 
+def gen_potential_and_dump():
+    """scheduler.py:508 potential_batch; h2.py:195 dump (GCAMAT01 wire bytes)."""
+    out = {}
+    m = mesh.build_sphere_mesh(2)
+    pts = np.array([[0.0, 0.0, 1.7], [1.2, -0.8, 0.9], [0.1, 0.2, 0.3], [-0.4, 0.0, -0.2],
+                    [3.0, 2.0, -1.0]])
+    out["points"] = pts
+    for name, spec in SPECS.items():
+        for order in (2, 3):
+            out[f"{name}_{order}"] = scheduler.potential_batch(m, spec, pts, order)
+    np.savez_compressed(os.path.join(HERE, "potential_L2.npz"), **out)
+    t = cluster.build_cluster_tree(m, 16)
+    bt = cluster.build_block_tree(t, t, 2.0)
+    M = scheduler.run_assembly(m, bt, SPECS["L-SLP"], {}, {}, _inline_params(), (3, 5))
+    h2.dump(M, os.path.join(HERE, "L2_laplace_single.gcamat"))
+    m3 = mesh.build_sphere_mesh(3)
+    t3 = cluster.build_cluster_tree(m3, 16)
+    bt3 = cluster.build_block_tree(t3, t3, 2.0)
+    ops, _ = gca.build_interpolation_operators(m3, bt3, SPECS["L-SLP"], gca.GcaParams())
+    M3 = scheduler.run_assembly(m3, bt3, SPECS["L-SLP"], ops, ops, _inline_params(), (2, 3))
+    import gzip
+    tmp = os.path.join(HERE, "L3_laplace_single_23.gcamat")
+    h2.dump(M3, tmp)
+    with open(tmp, "rb") as fh, open(tmp + ".gz", "wb") as gz:
+        gz.write(gzip.compress(fh.read(), 9))
+    os.remove(tmp)
+
+
 def main():
     meta = {"reference": "gcabem " + getattr(gcabem, "__version__", "0.1.0"),
             "numpy": np.__version__}
@@ -330,6 +358,7 @@ def main():
     gen_trees()
     gen_gca(meta)
     gen_assembly(meta)
+    gen_potential_and_dump()
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("ok")

@@ -323,3 +323,26 @@ def test_sampled_parity_helmholtz_small_phase(layer):
                              for l in leaf_of])
         scale = np.abs(ref) if layer == "single" else np.maximum(np.abs(ref), leaf_max)
         assert float(np.max(np.abs(got - ref) / scale)) <= TOL
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_potential_batch_vs_reference(gload, name):
+    """scheduler.potential_batch (scheduler.py:508-534) on the device."""
+    g = gload("potential_L2.npz")
+    m = mesh.build_sphere_mesh(2)
+    for order in (2, 3):
+        got = scheduler.potential_batch(m, spec_of(name), g["points"], order)
+        assert rel_err(got.ravel(), g[f"{name}_{order}"].ravel()) <= TOL
+    with pytest.raises(ValueError):
+        scheduler.potential_batch(m, spec_of(name), m.vertices[:1], 3)
+
+
+def test_gcamat01_dump_of_device_matrix(tmp_path, gload):
+    from paper_1510_07244_b200 import h2
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), "laplace")
+    M = scheduler.run_assembly(m, bt, kernels.KernelSpec("laplace", "single"), ops, ops,
+                               scheduler.SchedulerParams(), (3, 5))
+    h2.dump(M, tmp_path / "m.gcamat")
+    L = h2.load(tmp_path / "m.gcamat")
+    assert L.checksum() == M.checksum()

@@ -243,3 +243,23 @@ def test_native_trees_match_python(level):
         assert len(ba.nodes) == len(bb.nodes)
         assert list(ba.nodes) == list(bb.nodes)
         assert list(ba.leaves) == list(bb.leaves)
+
+
+def test_gcamat01_roundtrip_reference_files(tmp_path):
+    """h2.load reads the reference's GCAMAT01 files and h2.dump writes them
+    back byte for byte (h2.py:195-314)."""
+    import gzip
+    import os
+    from paper_1510_07244_b200 import h2
+    g = os.path.join(os.path.dirname(__file__), "golden")
+    l3 = tmp_path / "l3.gcamat"
+    l3.write_bytes(gzip.decompress(open(os.path.join(g, "L3_laplace_single_23.gcamat.gz"),
+                                        "rb").read()))
+    for src in (os.path.join(g, "L2_laplace_single.gcamat"), str(l3)):
+        M = h2.load(src)
+        out = tmp_path / "out.gcamat"
+        h2.dump(M, out)
+        assert out.read_bytes() == open(src, "rb").read()
+    import json
+    ref = json.load(open(os.path.join(g, "golden.json")))["checksums"]
+    assert h2.load(str(l3)).checksum() == ref["L3/laplace/single/2-3"]
