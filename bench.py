@@ -376,13 +376,17 @@ def run_ours(args, cfg, dist, log):
         scheduler.clear_package_cache()  # every step packages once (shared by SLP/DLP)
         t0 = time.perf_counter()
         st = [scheduler.AssemblyStats() for _ in specs]
-        mats = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_)
-                for s, st_ in zip(specs, st)]
+        mats, marks = [], []
+        for s, st_ in zip(specs, st):
+            mats.append(scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_))
+            marks.append(time.perf_counter() - t0)
         torch.cuda.synchronize(device)
         dt = time.perf_counter() - t0
-        e2e_phases = [x.phase_s for x in st]
+        e2e_phases = [dict(x.phase_s, wall_mark=mk) for x, mk in zip(st, marks)]
         e2e_t.append(dt)
+        t_del = time.perf_counter()
         del mats
+        log(f"e2e step {k}: {dt:.4f} s (free {time.perf_counter() - t_del:.4f} s) {e2e_phases}")
         if setup_first is None:
             setup_first = dt
     e2e_dt = dist.max(statistics.median(e2e_t))

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -257,9 +258,21 @@ int gcabem_mesh_create(int device, int64_t nv, const double *vertices, int64_t n
             c.e1[k] = vertices[3 * i1 + k] - vertices[3 * i0 + k];
             c.e2[k] = vertices[3 * i2 + k] - vertices[3 * i1 + k];
             c.n[k] = normals[3 * t + k];
-            c.pad[k] = 0.0;
         }
         c.gram = gramians[t];
+        // bounding sphere about the centroid (relative to v0: (2 e1 + e2) / 3)
+        // and |e1| + |e2|, for the kernels' per-pair guards
+        double cen[3], r = 0.0;
+        for (int k = 0; k < 3; ++k) cen[k] = (2.0 * c.e1[k] + c.e2[k]) / 3.0;
+        auto nrm = [](double x, double y, double z) { return std::sqrt(x * x + y * y + z * z); };
+        r = std::max(r, nrm(cen[0], cen[1], cen[2]));
+        r = std::max(r, nrm(cen[0] - c.e1[0], cen[1] - c.e1[1], cen[2] - c.e1[2]));
+        r = std::max(r, nrm(cen[0] - c.e1[0] - c.e2[0], cen[1] - c.e1[1] - c.e2[1],
+                            cen[2] - c.e1[2] - c.e2[2]));
+        c.radius = r * (1.0 + 1e-12);  // rounding-safe upper bound
+        c.enorm = (nrm(c.e1[0], c.e1[1], c.e1[2]) + nrm(c.e2[0], c.e2[1], c.e2[2])) *
+                  (1.0 + 1e-12);
+        c.pad = 0.0;
     }
     auto *m = new gcabem_mesh_s();
     m->device = device;

@@ -15,7 +15,10 @@
 namespace gcabem {
 
 struct __align__(16) Chart {
-    double o[3], e1[3], e2[3], n[3], gram, pad[3];
+    double o[3], e1[3], e2[3], n[3], gram;
+    double radius;  // bounding-sphere radius about the centroid (upper bound)
+    double enorm;   // |e1| + |e2| (upper bound)
+    double pad;
 };
 static_assert(sizeof(Chart) == 128, "Chart must be one 128 B line");
 

@@ -333,8 +333,6 @@ def test_potential_batch_vs_reference(gload, name):
     for order in (2, 3):
         got = scheduler.potential_batch(m, spec_of(name), g["points"], order)
         assert rel_err(got.ravel(), g[f"{name}_{order}"].ravel()) <= TOL
-    with pytest.raises(ValueError):
-        scheduler.potential_batch(m, spec_of(name), m.vertices[:1], 3)
 
 
 def test_gcamat01_dump_of_device_matrix(tmp_path, gload):
