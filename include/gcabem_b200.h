@@ -28,10 +28,12 @@ extern "C" {
 #define GCABEM_ERR_ARG 1      /* invalid argument (ValueError on the Python side) */
 #define GCABEM_ERR_CUDA 2     /* CUDA runtime failure (BackendError) */
 #define GCABEM_ERR_NODEV 3    /* no CUDA device visible (BackendError) */
+#define GCABEM_ERR_GCA 4      /* GCA construction failure (gca.GcaError, gca.py:43) */
 
 typedef struct gcabem_mesh_s *gcabem_mesh_t;
 typedef struct gcabem_plan_s *gcabem_plan_t;
 typedef struct gcabem_layout_s *gcabem_layout_t;
+typedef struct gcabem_gca_s *gcabem_gca_t;
 
 /* ---- library / device ------------------------------------------------- */
 int gcabem_version(void);
@@ -109,6 +111,23 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
                          const int64_t *blocks, int64_t npanels, const int64_t *panels,
                          int64_t nitems, const int64_t *items, const uint8_t *perms,
                          gcabem_layout_t *out);
+/* The same from the flat package arrays of packaging.make_packages (leaves
+ * [leaf_lo, leaf_hi) only; payload indices relative to leaf_lo): the block
+ * and item gathers run natively instead of in numpy. */
+int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t leaf_hi,
+                                int64_t nleaves, const int64_t *leaf_shape,
+                                const int64_t *leaf_base, const int64_t *leaf_rows_at,
+                                const int64_t *leaf_cols_at, int64_t npanels,
+                                const int64_t *panels, int64_t nblocks, const int64_t *blk_leaf,
+                                const int64_t *blk_r0, const int64_t *blk_nr,
+                                const int64_t *blk_c0, const int64_t *blk_nc, int64_t nitems,
+                                const int8_t *item_case, const int64_t *item_tri_x,
+                                const int64_t *item_tri_y, const int64_t *item_leaf,
+                                const int64_t *item_offset, const uint8_t *perms,
+                                gcabem_layout_t *out);
+/* {payload_len, blocks, tasks, disjoint pairs, vertex, edge, identical items,
+ * uploaded bytes} */
+int gcabem_layout_info(gcabem_layout_t layout, int64_t *info8);
 int gcabem_layout_release(gcabem_layout_t layout);
 int gcabem_plan_create_on(gcabem_layout_t layout, int equation, int layer, double kappa,
                           int disjoint_n, const double *gauss_pts, const double *gauss_wts,
@@ -208,6 +227,39 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
                      const double *A, double epsilon, int64_t max_rank, int nthreads,
                      int64_t *out_rank, int64_t *out_rows, int64_t *out_cols,
                      double *out_resid);
+
+/* ---- GCA interpolation operators of many clusters -------------------------
+ * Replaces gca.build_interpolation_operators' per-cluster loop (reference
+ * gca.py:285-310 -> build_interpolation_operator :259-282): for every
+ * cluster c (ids cl_ids, panels perm[cl_first[c] .. + cl_size[c]], bounding
+ * box box_lo/box_hi (ncl,3)) the device evaluates the Green matrix against
+ * green_sources(box, delta, m) (gca.py:83-133; Gauss rule gauss_pts/wts of
+ * order m on [0,1], scene_diameter for degenerate boxes) with the Duffy
+ * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
+ * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
+ * nthreads threads, overlapped with the next batch (batch_bytes of Green
+ * matrix per launch; 0 = 256 MiB). Results: gcabem_gca_sizes (rank per
+ * cluster, phase seconds {device wait, host, total, batches}), then
+ * gcabem_gca_fetch (row pivots concatenated; V blocks |t| x rank row-major,
+ * float64 for Laplace, complex128 for Helmholtz, concatenated).
+ * GCABEM_ERR_GCA: "cluster <id>: zero Green matrix" / "singular ACA pivot
+ * block" as the reference's GcaError. */
+int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl,
+                     const int64_t *cl_ids, const int64_t *cl_first, const int64_t *cl_size,
+                     const double *box_lo, const double *box_hi, int64_t nperm,
+                     const int64_t *perm, double delta, int m, const double *gauss_pts,
+                     const double *gauss_wts, double scene_diameter, int64_t nduffy,
+                     const double *duffy, double epsilon, int nthreads, int64_t batch_bytes,
+                     gcabem_gca_t *out);
+int gcabem_gca_sizes(gcabem_gca_t g, int64_t *ranks, double *phase4);
+int gcabem_gca_fetch(gcabem_gca_t g, int64_t *rows, double *V);
+int gcabem_gca_free(gcabem_gca_t g);
+/* One cluster's operator from a host Green matrix A (nr x nc row-major,
+ * float64 or interleaved complex128): ACA + cond check + refined V solve
+ * (gca.py:259-282). rows and V must hold min(nr, nc) pivots / nr x min(nr, nc)
+ * values; *rank receives the rank. */
+int gcabem_gca_operator(int is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
+                        int64_t *rank, int64_t *rows, double *V);
 
 /* ---- potential evaluation --------------------------------------------------
  * Replaces scheduler.potential_batch (scheduler.py:508-534): out (npts x nt,

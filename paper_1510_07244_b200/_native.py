@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgcabem_b200.so")
 
-ERR_ARG, ERR_CUDA, ERR_NODEV = 1, 2, 3
+ERR_ARG, ERR_CUDA, ERR_NODEV, ERR_GCA = 1, 2, 3, 4
 
 
 class BackendError(RuntimeError):
@@ -49,6 +49,10 @@ _SIGS = {
     "gcabem_layout_create": ([_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp,
                               ctypes.POINTER(_vp)], _int),
     "gcabem_layout_release": ([_vp], _int),
+    "gcabem_layout_info": ([_vp, _vp], _int),
+    "gcabem_layout_from_packages": ([_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64]
+                                    + [_vp] * 5 + [_i64] + [_vp] * 6 + [ctypes.POINTER(_vp)],
+                                    _int),
     "gcabem_plan_create_on": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp,
                                ctypes.POINTER(_vp)], _int),
     "gcabem_plan_download": ([_vp, _vp], _int),
@@ -74,6 +78,13 @@ _SIGS = {
     "gcabem_tree_sizes": ([_vp, _vp], _int),
     "gcabem_tree_fetch": ([_vp] * 9, _int),
     "gcabem_tree_free": ([_vp], _int),
+    "gcabem_gca_build": ([_vp, _int, _dbl, _i64] + [_vp] * 5 + [_i64, _vp, _dbl, _int, _vp, _vp,
+                                                     _dbl, _i64, _vp, _dbl, _int, _i64,
+                                                     ctypes.POINTER(_vp)], _int),
+    "gcabem_gca_sizes": ([_vp, _vp, _vp], _int),
+    "gcabem_gca_fetch": ([_vp, _vp, _vp], _int),
+    "gcabem_gca_free": ([_vp], _int),
+    "gcabem_gca_operator": ([_int, _vp, _i64, _i64, _dbl, _vp, _vp, _vp], _int),
     "gcabem_aca_batch": ([_int, _i64, _vp, _i64, _vp, _dbl, _i64, _int, _vp, _vp, _vp, _vp],
                          _int),
 }
@@ -105,6 +116,9 @@ def check(rc: int) -> None:
     msg = lib().gcabem_last_error().decode(errors="replace")
     if rc == ERR_ARG:
         raise ValueError(msg)
+    if rc == ERR_GCA:
+        from .gca import GcaError
+        raise GcaError(msg)
     raise BackendError(msg)
 
 

@@ -14,13 +14,23 @@
 #include <cmath>
 #include <cstdint>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "gcabem_b200.h"
+#include "internal.h"
 
-int gcabem_internal_error(int code, const char *msg);  // api.cu
+// Compiled twice: as is (baseline x86-64) and from aca_avx2.cpp with -mavx2
+// (GCABEM_ACA_AVX2); the baseline unit dispatches at run time. Both builds
+// perform the same IEEE operations in the same order (no FMA contraction),
+// so results do not depend on the CPU.
+#ifdef GCABEM_ACA_AVX2
+#define GCABEM_ACA_NS aca_avx2
+#else
+#define GCABEM_ACA_NS aca_base
+#endif
 
-namespace {
+namespace GCABEM_ACA_NS {
 
 struct Cx {
     double re, im;
@@ -65,6 +75,70 @@ struct Ops<Cx> {
     static double dotc_im(Cx a, Cx b) { return a.re * b.im - a.im * b.re; }
 };
 
+// sum conj(a_k) b_k with four partial sums
+template <typename T>
+Cx dotc(const T *a, const T *b, int64_t n) {
+    using O = Ops<T>;
+    double r[4] = {0, 0, 0, 0}, i[4] = {0, 0, 0, 0};
+    int64_t k = 0;
+    for (; k + 4 <= n; k += 4)
+        for (int l = 0; l < 4; ++l) {
+            r[l] += O::dotc_re(a[k + l], b[k + l]);
+            i[l] += O::dotc_im(a[k + l], b[k + l]);
+        }
+    for (; k < n; ++k) {
+        r[0] += O::dotc_re(a[k], b[k]);
+        i[0] += O::dotc_im(a[k], b[k]);
+    }
+    return {(r[0] + r[1]) + (r[2] + r[3]), (i[0] + i[1]) + (i[2] + i[3])};
+}
+
+// np.argmax(np.abs(x)) with masked entries read as 0.0 (first index wins
+// ties). Complex magnitudes are hypot as numpy's; a squared-magnitude pass
+// first narrows the candidates to those within 1e-12 of the maximum, so
+// hypot runs on a handful of entries (the squares carry < 4 ulp error, far
+// inside that window).
+template <typename T>
+int64_t argmax_mag(const T *x, int64_t n, const char *mask, double *best_out) {
+    using O = Ops<T>;
+    int64_t jp = 0;
+    double best = -1.0;
+    if constexpr (std::is_same<T, Cx>::value) {
+        double smax = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            const double s = (mask && mask[j]) ? 0.0 : O::norm2(x[j]);
+            smax = std::max(smax, s);
+        }
+        const double thr = smax > 1e-290 ? smax * (1.0 - 1e-12) : 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (mask && mask[j]) {
+                if (0.0 > best) {
+                    best = 0.0;
+                    jp = j;
+                }
+                continue;
+            }
+            if (thr > 0.0 && O::norm2(x[j]) < thr) continue;
+            const double a = O::mag(x[j]);
+            if (a > best) {
+                best = a;
+                jp = j;
+            }
+        }
+        if (thr > 0.0 && best < 0.0) best = 0.0;
+    } else {
+        for (int64_t j = 0; j < n; ++j) {
+            const double a = (mask && mask[j]) ? 0.0 : O::mag(x[j]);
+            if (a > best) {
+                best = a;
+                jp = j;
+            }
+        }
+    }
+    if (best_out) *best_out = best;
+    return jp;
+}
+
 template <typename T>
 void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
              int64_t *cols, int64_t *rank, double *resid) {
@@ -91,15 +165,7 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
             const T ui = U[m][i];
             for (int64_t j = 0; j < nc; ++j) r[j] = O::sub(r[j], O::mul(ui, W[m][j]));
         }
-        int64_t jp = 0;
-        double best = -1.0;
-        for (int64_t j = 0; j < nc; ++j) {
-            const double a = O::mag(r[j]);
-            if (a > best) {
-                best = a;
-                jp = j;
-            }
-        }
+        const int64_t jp = argmax_mag<T>(r.data(), nc, nullptr, nullptr);
         used[i] = 1;
         if (O::zero(r[jp])) {
             next = nr;
@@ -113,23 +179,18 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
             const T wj = W[m][jp];
             for (int64_t q = 0; q < nr; ++q) c[q] = O::sub(c[q], O::mul(wj, U[m][q]));
         }
-        double nu = 0.0, nw = 0.0;
-        for (int64_t q = 0; q < nr; ++q) nu += O::norm2(c[q]);
-        for (int64_t j = 0; j < nc; ++j) nw += O::norm2(w[j]);
-        nu = std::sqrt(nu);
-        nw = std::sqrt(nw);
+        // norms and the cross terms of the Frobenius estimate: four partial
+        // sums (vectorisable; the reference's np.linalg.norm / np.vdot are
+        // BLAS reductions with their own association, so no order is "the"
+        // reference order here -- only the elementwise residual updates
+        // above decide pivots and follow the reference exactly)
+        const double nu = std::sqrt(dotc<T>(c.data(), c.data(), nr).re);
+        const double nw = std::sqrt(dotc<T>(w.data(), w.data(), nc).re);
         double cross = 0.0;
         for (size_t m = 0; m < U.size(); ++m) {
-            double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-            for (int64_t q = 0; q < nr; ++q) {
-                ar += O::dotc_re(U[m][q], c[q]);
-                ai += O::dotc_im(U[m][q], c[q]);
-            }
-            for (int64_t j = 0; j < nc; ++j) {
-                br += O::dotc_re(W[m][j], w[j]);
-                bi += O::dotc_im(W[m][j], w[j]);
-            }
-            cross += ar * br - ai * bi;  // Re((u^H c) (w_m^H w))
+            const Cx a = dotc<T>(U[m].data(), c.data(), nr);
+            const Cx b = dotc<T>(W[m].data(), w.data(), nc);
+            cross += a.re * b.re - a.im * b.im;  // Re((u^H c) (w_m^H w))
         }
         U.emplace_back(c.begin(), c.end());
         W.emplace_back(std::move(w));
@@ -139,21 +200,279 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
         est2 = std::max(est2 + nu * nu * nw * nw + 2.0 * cross, 0.0);
         res = nu * nw;
         if (res <= eps * std::sqrt(est2)) break;
-        int64_t nb = 0;
-        double mb = -1.0;
-        for (int64_t q = 0; q < nr; ++q) {
-            const double a = used[q] ? 0.0 : O::mag(c[q]);
-            if (a > mb) {
-                mb = a;
-                nb = q;
-            }
-        }
+        double mb = 0.0;
+        const int64_t nb = argmax_mag<T>(c.data(), nr, used.data(), &mb);
         next = mb == 0.0 ? nr : nb;
     }
     *rank = k;
     *resid = res;
 }
 
+// ---------------------------------------------------------------------------
+// GCA operator of one cluster (reference gca.py:248-282): pivot-block
+// condition check (np.linalg.cond, 2-norm), V = A[:, cols] inv(B) by LU with
+// partial pivoting of B^T (numpy solve = LAPACK gesv on B^T, pivot choice by
+// |re| + |im| as izamax), two refinement sweeps with the reference's early
+// exit. V parity is within roundoff x cond(B) of LAPACK, not bitwise.
+
+inline Cx cadd(Cx a, Cx b) { return {a.re + b.re, a.im + b.im}; }
+inline double abs1(double x) { return std::fabs(x); }
+inline double abs1(Cx x) { return std::fabs(x.re) + std::fabs(x.im); }
+inline double add_(double a, double b) { return a + b; }
+inline Cx add_(Cx a, Cx b) { return cadd(a, b); }
+template <typename T>
+T one();
+template <>
+double one<double>() { return 1.0; }
+template <>
+Cx one<Cx>() { return Cx{1.0, 0.0}; }
+
+// 2-norm condition number by one-sided (Hestenes) Jacobi SVD of the r x r
+// row-major block: rotate column pairs until mutually orthogonal; the
+// singular values are the final column norms (relative accuracy).
+template <typename T>
+double cond2(const T *B, int64_t r) {
+    using O = Ops<T>;
+    // column-major copy
+    std::vector<T> a((size_t)(r * r));
+    for (int64_t i = 0; i < r; ++i)
+        for (int64_t j = 0; j < r; ++j) a[(size_t)(j * r + i)] = B[i * r + j];
+    // rounding in the pair inner products is ~eps sqrt(r) relative: a
+    // tighter stop would never be met
+    const double tol = 4.0 * 2.220446049250313e-16 * (double)std::max<int64_t>(r, 4);
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        bool rotated = false;
+        for (int64_t p = 0; p < r - 1; ++p) {
+            T *ap = a.data() + p * r;
+            for (int64_t q = p + 1; q < r; ++q) {
+                T *aq = a.data() + q * r;
+                double alpha = 0.0, beta = 0.0, gr = 0.0, gi = 0.0;
+                for (int64_t i = 0; i < r; ++i) {
+                    alpha += O::norm2(ap[i]);
+                    beta += O::norm2(aq[i]);
+                    gr += O::dotc_re(ap[i], aq[i]);
+                    gi += O::dotc_im(ap[i], aq[i]);
+                }
+                const double g = std::hypot(gr, gi);
+                if (g == 0.0 || g <= tol * std::sqrt(alpha * beta)) continue;
+                rotated = true;
+                // a_q <- e^{-i phi} a_q makes the pair's inner product real
+                // (= g); then a real rotation zeroes it.
+                const double zeta = (beta - alpha) / (2.0 * g);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) /
+                                 (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+                const double pr = gr / g, pi = gi / g;  // e^{i phi}
+                for (int64_t i = 0; i < r; ++i) {
+                    T x = ap[i], y = aq[i];
+                    if constexpr (std::is_same<T, Cx>::value) {
+                        y = Cx{y.re * pr + y.im * pi, y.im * pr - y.re * pi};  // e^{-i phi} y
+                        ap[i] = Cx{c * x.re - s * y.re, c * x.im - s * y.im};
+                        aq[i] = Cx{s * x.re + c * y.re, s * x.im + c * y.im};
+                    } else {
+                        y = y * pr;
+                        ap[i] = c * x - s * y;
+                        aq[i] = s * x + c * y;
+                    }
+                }
+            }
+        }
+        if (!rotated) break;
+    }
+    double smax = 0.0, smin = HUGE_VAL;
+    for (int64_t j = 0; j < r; ++j) {
+        double n2 = 0.0;
+        for (int64_t i = 0; i < r; ++i) n2 += O::norm2(a[(size_t)(j * r + i)]);
+        const double sv = std::sqrt(n2);
+        smax = std::max(smax, sv);
+        smin = std::min(smin, sv);
+    }
+    return smin > 0.0 ? smax / smin : HUGE_VAL;
+}
+
+// LU with partial pivoting of M (r x r, row-major) and multi-RHS solves on
+// row-major (r x n) right-hand sides (inner loops run along n: contiguous).
+template <typename T>
+struct LU {
+    int64_t r = 0;
+    std::vector<T> m;
+    std::vector<int64_t> piv;
+    bool factor(const T *M, int64_t n) {
+        using O = Ops<T>;
+        r = n;
+        m.assign(M, M + n * n);
+        piv.resize(n);
+        for (int64_t k = 0; k < n; ++k) {
+            int64_t p = k;
+            double best = abs1(m[k * n + k]);
+            for (int64_t i = k + 1; i < n; ++i) {
+                const double v = abs1(m[i * n + k]);
+                if (v > best) {
+                    best = v;
+                    p = i;
+                }
+            }
+            piv[k] = p;
+            if (best == 0.0) return false;
+            if (p != k)
+                for (int64_t j = 0; j < n; ++j) std::swap(m[k * n + j], m[p * n + j]);
+            const T d = m[k * n + k];
+            for (int64_t i = k + 1; i < n; ++i) {
+                const T l = O::div(m[i * n + k], d);
+                m[i * n + k] = l;
+                for (int64_t j = k + 1; j < n; ++j)
+                    m[i * n + j] = O::sub(m[i * n + j], O::mul(l, m[k * n + j]));
+            }
+        }
+        return true;
+    }
+    // X (r x n, row-major) <- M^-1 X
+    void solve(T *X, int64_t n) const {
+        using O = Ops<T>;
+        for (int64_t k = 0; k < r; ++k)
+            if (piv[k] != k)
+                for (int64_t q = 0; q < n; ++q) std::swap(X[k * n + q], X[piv[k] * n + q]);
+        for (int64_t i = 1; i < r; ++i) {
+            T *xi = X + i * n;
+            for (int64_t j = 0; j < i; ++j) {
+                const T l = m[i * r + j];
+                const T *xj = X + j * n;
+                for (int64_t q = 0; q < n; ++q) xi[q] = O::sub(xi[q], O::mul(l, xj[q]));
+            }
+        }
+        for (int64_t i = r - 1; i >= 0; --i) {
+            T *xi = X + i * n;
+            for (int64_t j = i + 1; j < r; ++j) {
+                const T u = m[i * r + j];
+                const T *xj = X + j * n;
+                for (int64_t q = 0; q < n; ++q) xi[q] = O::sub(xi[q], O::mul(u, xj[q]));
+            }
+            const T d = m[i * r + i];
+            for (int64_t q = 0; q < n; ++q) xi[q] = O::div(xi[q], d);
+        }
+    }
+};
+
+// np.linalg.cond(B) <= 1e14 (2-norm), decided from the Frobenius condition
+// kF = |B|_F |B^-1|_F, which brackets it: kF / r <= cond2 <= kF. Only in
+// the ambiguous window does the exact Jacobi SVD run.
+template <typename T>
+bool cond_ok(const T *B, const LU<T> &luT, int64_t r) {
+    using O = Ops<T>;
+    std::vector<T> Y((size_t)(r * r), T());
+    for (int64_t i = 0; i < r; ++i) Y[i * r + i] = O::div(one<T>(), one<T>());
+    luT.solve(Y.data(), r);  // (B^T)^-1, same Frobenius norm as B^-1
+    double fb = 0.0, fi = 0.0;
+    for (int64_t e = 0; e < r * r; ++e) {
+        fb += O::norm2(B[e]);
+        fi += O::norm2(Y[e]);
+    }
+    const double kf = std::sqrt(fb) * std::sqrt(fi);
+    if (!(kf == kf)) return false;
+    if (kf <= 0.5e14) return true;
+    if (kf >= 2e14 * (double)r) return false;
+    return cond2<T>(B, r) <= 1e14;
+}
+
+template <typename T>
+int operator_one(const T *A, int64_t nr, int64_t nc, double eps, std::vector<int64_t> &rows_out,
+                 std::vector<double> &V_out) {
+    using O = Ops<T>;
+    const int64_t cap = std::min(nr, nc);
+    std::vector<int64_t> rows(cap), cols(cap);
+    for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
+        int64_t k = 0;
+        double resid = 0.0;
+        aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
+        if (k == 0) return 1;
+        // pivot block B[a][b] = A[rows[a], cols[b]], and M = B^T
+        std::vector<T> B((size_t)(k * k)), M((size_t)(k * k));
+        for (int64_t a = 0; a < k; ++a)
+            for (int64_t b = 0; b < k; ++b) {
+                B[a * k + b] = A[rows[a] * nc + cols[b]];
+                M[b * k + a] = B[a * k + b];
+            }
+        LU<T> lu;
+        if (!lu.factor(M.data(), k)) continue;  // exactly singular: cond = inf
+        if (!cond_ok<T>(B.data(), lu, k)) continue;
+        // X = V^T (k x nr) solves M X = A_cols^T
+        std::vector<T> RHS((size_t)(k * nr)), X, R((size_t)(k * nr));
+        double amax = 0.0;
+        for (int64_t q = 0; q < nr; ++q)
+            for (int64_t b = 0; b < k; ++b) {
+                const T v = A[q * nc + cols[b]];
+                RHS[b * nr + q] = v;
+                amax = std::max(amax, O::mag(v));
+            }
+        X = RHS;
+        lu.solve(X.data(), nr);
+        const double lim = 1e-15 * std::max(amax, 1.0);
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            // R^T = A_cols^T - B^T V^T = RHS - M X
+            R = RHS;
+            for (int64_t b = 0; b < k; ++b) {
+                T *rb = R.data() + b * nr;
+                for (int64_t l = 0; l < k; ++l) {
+                    const T mbl = M[b * k + l];
+                    const T *xl = X.data() + l * nr;
+                    for (int64_t q = 0; q < nr; ++q) rb[q] = O::sub(rb[q], O::mul(mbl, xl[q]));
+                }
+            }
+            double rmax = 0.0;
+            for (const T &v : R) rmax = std::max(rmax, O::mag(v));
+            if (rmax <= lim) break;
+            lu.solve(R.data(), nr);
+            for (size_t e = 0; e < X.size(); ++e) X[e] = add_(X[e], R[e]);
+        }
+        rows_out.assign(rows.begin(), rows.begin() + k);
+        const int w = std::is_same<T, Cx>::value ? 2 : 1;
+        V_out.resize((size_t)(nr * k * w));
+        T *V = reinterpret_cast<T *>(V_out.data());
+        for (int64_t q = 0; q < nr; ++q)
+            for (int64_t b = 0; b < k; ++b) V[q * k + b] = X[b * nr + q];
+        return 0;
+    }
+    return 2;
+}
+
+// entry points of this build
+void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps, int64_t cap,
+               int64_t *rows, int64_t *cols, int64_t *rank, double *resid) {
+    if (is_complex)
+        aca_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, eps, cap, rows, cols, rank, resid);
+    else
+        aca_one<double>(A, nr, nc, eps, cap, rows, cols, rank, resid);
+}
+
+int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
+                   std::vector<int64_t> &rows, std::vector<double> &V) {
+    if (is_complex)
+        return operator_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, epsilon, rows, V);
+    return operator_one<double>(A, nr, nc, epsilon, rows, V);
+}
+
+}  // namespace GCABEM_ACA_NS
+
+#ifndef GCABEM_ACA_AVX2
+namespace aca_avx2 {
+void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps, int64_t cap,
+               int64_t *rows, int64_t *cols, int64_t *rank, double *resid);
+int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
+                   std::vector<int64_t> &rows, std::vector<double> &V);
+}  // namespace aca_avx2
+
+namespace {
+bool use_avx2() {
+    static const bool yes = __builtin_cpu_supports("avx2");
+    return yes;
+}
+void aca_dispatch(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps,
+                  int64_t cap, int64_t *rows, int64_t *cols, int64_t *rank, double *resid) {
+    if (use_avx2())
+        aca_avx2::aca_entry(is_complex, A, nr, nc, eps, cap, rows, cols, rank, resid);
+    else
+        aca_base::aca_entry(is_complex, A, nr, nc, eps, cap, rows, cols, rank, resid);
+}
 }  // namespace
 
 extern "C" int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at,
@@ -171,12 +490,9 @@ extern "C" int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows
             const int64_t r0 = rows_at[c], nr = rows_at[c + 1] - r0;
             int64_t cap = std::min(nr, ncols);
             if (max_rank > 0) cap = std::min(cap, max_rank);
-            if (is_complex)
-                aca_one<Cx>(reinterpret_cast<const Cx *>(A) + r0 * ncols, nr, ncols, epsilon, cap,
-                            out_rows + r0, out_cols + r0, out_rank + c, out_resid + c);
-            else
-                aca_one<double>(A + r0 * ncols, nr, ncols, epsilon, cap, out_rows + r0,
-                                out_cols + r0, out_rank + c, out_resid + c);
+            const int64_t w = is_complex ? 2 : 1;
+            aca_dispatch(is_complex != 0, A + r0 * ncols * w, nr, ncols, epsilon, cap,
+                         out_rows + r0, out_cols + r0, out_rank + c, out_resid + c);
         }
     };
     std::vector<std::thread> th;
@@ -186,3 +502,32 @@ extern "C" int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows
     for (auto &t : th) t.join();
     return GCABEM_OK;
 }
+
+namespace gcabem {
+int gca_operator(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
+                 std::vector<int64_t> &rows, std::vector<double> &V) {
+    if (use_avx2()) return aca_avx2::operator_entry(is_complex, A, nr, nc, epsilon, rows, V);
+    return aca_base::operator_entry(is_complex, A, nr, nc, epsilon, rows, V);
+}
+}  // namespace gcabem
+
+// Host entry for one matrix (tests, gca._operator_from_green): rows and V
+// sized for the rank cap min(nr, nc).
+extern "C" int gcabem_gca_operator(int is_complex, const double *A, int64_t nr, int64_t nc,
+                                   double epsilon, int64_t *rank, int64_t *rows, double *V) {
+    if (!A || !rank || !rows || !V || nr <= 0 || nc <= 0 || !(epsilon > 0.0))
+        return gcabem_internal_error(GCABEM_ERR_ARG, "gca_operator: bad arguments");
+    std::vector<int64_t> r;
+    std::vector<double> v;
+    const int rc = gcabem::gca_operator(is_complex != 0, A, nr, nc, epsilon, r, v);
+    if (rc == 1) return gcabem_internal_error(GCABEM_ERR_GCA, "zero Green matrix");
+    if (rc == 2)
+        return gcabem_internal_error(GCABEM_ERR_GCA,
+                                     "singular ACA pivot block (condition above 1e+14)");
+    *rank = (int64_t)r.size();
+    std::copy(r.begin(), r.end(), rows);
+    std::copy(v.begin(), v.end(), V);
+    return GCABEM_OK;
+}
+
+#endif  // !GCABEM_ACA_AVX2

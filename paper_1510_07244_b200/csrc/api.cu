@@ -14,6 +14,7 @@
 
 #include "gcabem_b200.h"
 #include "gcabem_common.cuh"
+#include "internal.h"
 
 using namespace gcabem;
 
@@ -38,33 +39,6 @@ int set_error(int code, const std::string &msg) {
     do {                                                              \
         if (!(cond)) return set_error(GCABEM_ERR_ARG, (msg));         \
     } while (0)
-
-// RAII device buffer
-template <typename T>
-struct DevBuf {
-    T *p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf &) = delete;
-    DevBuf &operator=(const DevBuf &) = delete;
-    ~DevBuf() { release(); }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    cudaError_t alloc(size_t count) {
-        release();
-        n = count;
-        if (count == 0) return cudaSuccess;
-        return cudaMalloc(&p, sizeof(T) * count);
-    }
-    cudaError_t upload(const T *host, size_t count, cudaStream_t s) {
-        cudaError_t e = alloc(count);
-        if (e != cudaSuccess || count == 0) return e;
-        return cudaMemcpyAsync(p, host, sizeof(T) * count, cudaMemcpyHostToDevice, s);
-    }
-};
 
 std::mutex g_rule_mutex;
 std::set<std::pair<int, int>> g_rules_loaded;  // (device, order)
@@ -105,14 +79,6 @@ std::vector<double> pack_rule(int64_t q, const double *xs, const double *ys, con
 // Error hook for the other translation units (packaging.cpp).
 int gcabem_internal_error(int code, const char *msg) { return set_error(code, msg); }
 
-struct gcabem_mesh_s {
-    int device = 0;
-    int64_t nv = 0, nt = 0;
-    cudaStream_t stream = nullptr;
-    DevBuf<double> V;
-    DevBuf<int32_t> T;
-    DevBuf<Chart> charts;
-};
 
 // Device layout of one package set: uploaded once, shared by every plan
 // (operator) assembled from the same packages (e.g. SLP and DLP).
@@ -453,6 +419,66 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
         GC_CUDA(e);
     }
     *out = L;
+    return GCABEM_OK;
+}
+
+int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t leaf_hi,
+                                int64_t nleaves, const int64_t *leaf_shape,
+                                const int64_t *leaf_base, const int64_t *leaf_rows_at,
+                                const int64_t *leaf_cols_at, int64_t npanels,
+                                const int64_t *panels, int64_t nblocks, const int64_t *blk_leaf,
+                                const int64_t *blk_r0, const int64_t *blk_nr,
+                                const int64_t *blk_c0, const int64_t *blk_nc, int64_t nitems,
+                                const int8_t *item_case, const int64_t *item_tri_x,
+                                const int64_t *item_tri_y, const int64_t *item_leaf,
+                                const int64_t *item_offset, const uint8_t *perms,
+                                gcabem_layout_t *out) {
+    GC_ARG(mesh && out, "null argument");
+    GC_ARG(0 <= leaf_lo && leaf_lo <= leaf_hi && leaf_hi <= nleaves, "bad leaf range");
+    const int64_t base0 = leaf_base[leaf_lo];
+    // WorkBlocks of the leaf range -> {base, ld, nr, nc, rows_at, cols_at, leaf}
+    std::vector<int64_t> blocks;
+    blocks.reserve(7 * (size_t)nblocks);
+    for (int64_t b = 0; b < nblocks; ++b) {
+        const int64_t lf = blk_leaf[b];
+        GC_ARG(lf >= 0 && lf < nleaves, "block leaf out of range");
+        if (lf < leaf_lo || lf >= leaf_hi) continue;
+        const int64_t ld = leaf_shape[2 * lf + 1];
+        blocks.insert(blocks.end(), {leaf_base[lf] - base0 + blk_r0[b] * ld + blk_c0[b], ld,
+                                     blk_nr[b], blk_nc[b], leaf_rows_at[lf] + blk_r0[b],
+                                     leaf_cols_at[lf] + blk_c0[b], lf});
+    }
+    // singular items of the range, grouped by case (stable: generation order)
+    std::vector<int64_t> items;
+    std::vector<uint8_t> pm;
+    items.reserve(4 * (size_t)nitems);
+    pm.reserve(6 * (size_t)nitems);
+    for (int c = 1; c <= 3; ++c)
+        for (int64_t k = 0; k < nitems; ++k) {
+            if (item_case[k] != c) continue;
+            const int64_t lf = item_leaf[k];
+            GC_ARG(lf >= 0 && lf < nleaves, "item leaf out of range");
+            if (lf < leaf_lo || lf >= leaf_hi) continue;
+            items.insert(items.end(), {(int64_t)c, item_tri_x[k], item_tri_y[k],
+                                       leaf_base[lf] - base0 + item_offset[k]});
+            pm.insert(pm.end(), perms + 6 * k, perms + 6 * k + 6);
+        }
+    return gcabem_layout_create(mesh, leaf_base[leaf_hi] - base0, (int64_t)blocks.size() / 7,
+                                blocks.data(), npanels, panels, (int64_t)items.size() / 4,
+                                items.data(), pm.data(), out);
+}
+
+int gcabem_layout_info(gcabem_layout_t L, int64_t *info8) {
+    GC_ARG(L && info8, "null argument");
+    int64_t pairs = 0;
+    for (int64_t v : L->block_pairs) pairs += v;
+    info8[0] = L->payload_len;
+    info8[1] = (int64_t)L->block_pairs.size();
+    info8[2] = L->ntasks;
+    info8[3] = pairs;
+    for (int c = 0; c < 3; ++c) info8[4 + c] = L->case_at[c + 1] - L->case_at[c];
+    info8[7] = (int64_t)(L->blocks.n * sizeof(BlockDesc) + L->tasks.n * sizeof(int2) +
+                         L->panels.n * sizeof(int32_t) + L->items.n * sizeof(SingItem));
     return GCABEM_OK;
 }
 

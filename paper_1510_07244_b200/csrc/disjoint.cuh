@@ -1,0 +1,237 @@
+// Disjoint-rule pair quadrature (reference pairquad.py:27-92 over
+// quadrature.py:108's factored Duffy rule): constant-memory rule tables,
+// the expanded/direct evaluation forms and disjoint_kernel<N, KIND>.
+// Instantiated per order range in disjoint_o*.cu (parallel compilation).
+#pragma once
+#include "device_math.cuh"
+
+namespace gcabem {
+
+// ---------------------------------------------------------------------------
+// disjoint rule, factored: x = (a, a b), y = (c, c d), w = (wa wb a)(wc wd c)
+
+static __constant__ double c_gauss[MAX_ORDER + 1][MAX_ORDER];  // 1D Gauss points on [0,1]
+__host__ __device__ constexpr int duffy_offset(int n) { return (n - 1) * n * (2 * n - 1) / 6; }
+constexpr int DUFFY_TOTAL = duffy_offset(MAX_ORDER + 1);
+static __constant__ double c_duffy_t[DUFFY_TOTAL];  // t = a*b   (s = a = c_gauss[n][p / n])
+static __constant__ double c_duffy_w[DUFFY_TOTAL];  // (wa*wb)*a  == duffy_panel_rule weights
+
+// every translation unit that includes this header owns a copy of the
+// tables (static __constant__); its upload_tables() fills that copy
+static cudaError_t upload_tables(int n, const double *g, const double *gw) {
+    double t[MAX_ORDER * MAX_ORDER], w[MAX_ORDER * MAX_ORDER];
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            t[a * n + b] = g[a] * g[b];             // quadrature.py:95 a*b
+            w[a * n + b] = (gw[a] * gw[b]) * g[a];  // quadrature.py:96
+        }
+    cudaError_t e = cudaMemcpyToSymbol(c_gauss, g, sizeof(double) * n,
+                                       sizeof(double) * MAX_ORDER * n);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_duffy_t, t, sizeof(double) * n * n,
+                           sizeof(double) * duffy_offset(n));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(c_duffy_w, w, sizeof(double) * n * n,
+                              sizeof(double) * duffy_offset(n));
+}
+
+// Two evaluation forms for the disjoint rule x = (a, ab), y = (c, cd):
+//
+//  direct    d_pq = xo_p - g_c u_d  (3 DFMA), r^2 = |d|^2 (3)
+//  expanded  r^2 = |xo_p|^2 - 2 g_c (xo_p . u_d) + g_c^2 |u_d|^2
+//            = fma(g_c, fma(g_c, |u_d|^2, -2 xo.u_d), |xo|^2)   (2 DFMA)
+//
+// with xo_p = (ox - oy) + a e1x + ab e2x and u_d = e1y + g_d e2y. The expanded
+// form cancels when the pair is close: its rounding error is below
+// eps * S^2 / r_min^2 with S = |ox-oy| + |e1x| + |e2x| + |e1y| + |e2y| and
+// r_min a lower bound of the pair distance (bounding spheres). Pairs with
+// S^2 <= EXPANDED_MAX_RATIO * r_min^2 (error < 2.3e-13, measured < 3e-15)
+// take it; the rest (about 1% of near-field pairs) the direct form.
+constexpr double EXPANDED_MAX_RATIO = 1024.0;
+
+
+template <int N, int KIND, bool SMALL>
+__device__ __forceinline__ void disjoint_expanded(const double dO[3], const double e1x[3],
+                                                  const double e2x[3], const double e1y[3],
+                                                  const double e2y[3], const double n[3],
+                                                  double kappa, double phi0, double &acc_re,
+                                                  double &acc_im) {
+    constexpr bool DL = (KIND == L_DLP || KIND == H_DLP);
+    double uu[N], un[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        const double gd = c_gauss[N][d];
+        const double ux = fma(gd, e2y[0], e1y[0]);
+        const double uy = fma(gd, e2y[1], e1y[1]);
+        const double uz = fma(gd, e2y[2], e1y[2]);
+        uu[d] = fma(ux, ux, fma(uy, uy, uz * uz));
+        un[d] = DL ? fma(ux, n[0], fma(uy, n[1], uz * n[2])) : 0.0;
+    }
+    // -2 xo . u_d = (-2 xo . e1y) + g_d (-2 xo . e2y): two dots per x point
+    const double f1[3] = {-2.0 * e1y[0], -2.0 * e1y[1], -2.0 * e1y[2]};
+    const double f2[3] = {-2.0 * e2y[0], -2.0 * e2y[1], -2.0 * e2y[2]};
+#pragma unroll 1
+    for (int p = 0; p < N * N; ++p) {
+        const double s = c_gauss[N][p / N];
+        const double t = c_duffy_t[duffy_offset(N) + p];
+        const double wx = c_duffy_w[duffy_offset(N) + p];
+        const double xo0 = fma(t, e2x[0], fma(s, e1x[0], dO[0]));
+        const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
+        const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
+        const double xx = fma(xo0, xo0, fma(xo1, xo1, xo2 * xo2));
+        const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
+        const double a2 = fma(xo0, f1[0], fma(xo1, f1[1], xo2 * f1[2]));
+        const double b2 = fma(xo0, f2[0], fma(xo1, f2[1], xo2 * f2[2]));
+        double in_re = 0.0, in_im = 0.0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+            const double m2b = fma(c_gauss[N][d], b2, a2);
+#pragma unroll
+            for (int c = 0; c < N; ++c) {
+                const double gc = c_gauss[N][c];
+                const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+                const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
+                const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
+                point_accumulate<KIND, SMALL>(r2, dn, wy, kappa, phi0, in_re, in_im);
+            }
+        }
+        acc_re = fma(wx, in_re, acc_re);
+        if (KIND == H_SLP || KIND == H_DLP) acc_im = fma(wx, in_im, acc_im);
+    }
+}
+
+template <int N, int KIND, bool SMALL>
+__device__ __forceinline__ void disjoint_direct(const double dO[3], const double e1x[3],
+                                                const double e2x[3], const double e1y[3],
+                                                const double e2y[3], const double n[3],
+                                                double kappa, double phi0, double &acc_re,
+                                                double &acc_im) {
+    constexpr bool DL = (KIND == L_DLP || KIND == H_DLP);
+    double ux[N], uy[N], uz[N], un[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        const double gd = c_gauss[N][d];
+        ux[d] = fma(gd, e2y[0], e1y[0]);
+        uy[d] = fma(gd, e2y[1], e1y[1]);
+        uz[d] = fma(gd, e2y[2], e1y[2]);
+        un[d] = DL ? fma(ux[d], n[0], fma(uy[d], n[1], uz[d] * n[2])) : 0.0;
+    }
+#pragma unroll 1
+    for (int p = 0; p < N * N; ++p) {
+        const double s = c_gauss[N][p / N];
+        const double t = c_duffy_t[duffy_offset(N) + p];
+        const double wx = c_duffy_w[duffy_offset(N) + p];
+        const double xo0 = fma(t, e2x[0], fma(s, e1x[0], dO[0]));
+        const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
+        const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
+        const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
+        double in_re = 0.0, in_im = 0.0;
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+            const double gc = c_gauss[N][c];
+#pragma unroll
+            for (int d = 0; d < N; ++d) {
+                const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+                const double dx = fma(-gc, ux[d], xo0);
+                const double dy = fma(-gc, uy[d], xo1);
+                const double dz = fma(-gc, uz[d], xo2);
+                const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
+                const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
+                point_accumulate<KIND, SMALL>(r2, dn, wy, kappa, phi0, in_re, in_im);
+            }
+        }
+        acc_re = fma(wx, in_re, acc_re);
+        if (KIND == H_SLP || KIND == H_DLP) acc_im = fma(wx, in_im, acc_im);
+    }
+}
+
+// One thread = one panel pair of one WorkBlock; a CTA = DISJOINT_TPB
+// consecutive (row-major) pairs of one block. Rule constants are
+// compile-time offsets into constant memory (DFMA operands), so the inner
+// N^2 loop issues no loads. Pairs that share a vertex are written as 0: the
+// singular pass of the same plan overwrites every one of them (the overwrite
+// protocol, scheduler.py:9-12), so their disjoint-rule value (non-finite for
+// identical pairs) is never observable.
+template <int N, int KIND>
+__global__ void __launch_bounds__(DISJOINT_TPB)
+disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
+                const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
+                const int32_t *__restrict__ panels, double2 *__restrict__ payload,
+                double kappa) {
+    const int2 task = tasks[blockIdx.x];
+    const BlockDesc b = blocks[task.x];
+    const int k = task.y + threadIdx.x;
+    if (k >= b.nr * b.nc) return;
+    const int i = k / b.nc;
+    const int j = k - i * b.nc;
+    const int tx = panels[b.rows_at + i], ty = panels[b.cols_at + j];
+    double2 *dst = payload + b.base + (int64_t)i * b.ld + j;
+    {
+        const int a0 = T[3 * tx], a1 = T[3 * tx + 1], a2 = T[3 * tx + 2];
+        const int b0 = T[3 * ty], b1 = T[3 * ty + 1], b2 = T[3 * ty + 2];
+        if (a0 == b0 || a0 == b1 || a0 == b2 || a1 == b0 || a1 == b1 || a1 == b2 ||
+            a2 == b0 || a2 == b1 || a2 == b2) {
+            *dst = make_double2(0.0, 0.0);
+            return;
+        }
+    }
+    const Chart *cx = charts + tx;
+    const Chart *cy = charts + ty;
+    double dO[3], e1x[3], e2x[3], e1y[3], e2y[3], n[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        dO[c] = cx->o[c] - cy->o[c];
+        e1x[c] = cx->e1[c];
+        e2x[c] = cx->e2[c];
+        e1y[c] = cy->e1[c];
+        e2y[c] = cy->e2[c];
+        if (KIND == L_DLP || KIND == H_DLP) n[c] = cy->n[c];
+    }
+    const double gx = cx->gram, gy = cy->gram;
+    const double rx = cx->radius, ry = cy->radius;
+    // centroid difference: dO + (2 e1x + e2x)/3 - (2 e1y + e2y)/3
+    double dc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        dc[c] = fma(1.0 / 3.0, (2.0 * e1x[c] + e2x[c]) - (2.0 * e1y[c] + e2y[c]), dO[c]);
+    const double dcen = norm3(dc[0], dc[1], dc[2]);
+    const double rmin = dcen - rx - ry;
+    const double S = norm3(dO[0], dO[1], dO[2]) + cx->enorm + cy->enorm;
+    double re = 0.0, im = 0.0;
+    const bool expanded = rmin > 0.0 && S * S <= EXPANDED_MAX_RATIO * rmin * rmin;
+    constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
+    // Helmholtz phase about the centroid distance: |kappa r - kappa D| <= kappa (rx + ry)
+    const double phi0 = HELM ? kappa * dcen : 0.0;
+    const bool small = HELM && kappa * (rx + ry) <= SMALL_PHASE_MAX;
+    if (small) {
+        if (expanded)
+            disjoint_expanded<N, KIND, true>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+        else
+            disjoint_direct<N, KIND, true>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+        rotate(phi0, re, im);
+    } else {
+        if (expanded)
+            disjoint_expanded<N, KIND, false>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+        else
+            disjoint_direct<N, KIND, false>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+    }
+    finish_pair<KIND>(re, im, gx, gy, dst);
+}
+
+template <int N>
+static cudaError_t launch_disjoint_n(int kind, const Chart *charts, const int32_t *T,
+                                     const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                     const int32_t *panels, double2 *payload, double kappa,
+                                     cudaStream_t s) {
+    const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
+    switch (kind) {
+        case L_SLP: disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
+        case L_DLP: disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
+        case H_SLP: disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
+        default:    disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
+    }
+    return cudaGetLastError();
+}
+
+
+}  // namespace gcabem

@@ -1,0 +1,325 @@
+// GCA interpolation operators of many clusters (reference
+// gca.build_interpolation_operators, gca.py:285-310), as one native pipeline:
+//
+//   device   Green matrices of a batch of clusters (green_box_kernel: sources
+//            generated on the device from the enlarged boxes), D2H into one of
+//            two pinned staging buffers;
+//   host     ACA + pivot-block check + refined V solve per cluster
+//            (gca_operator, aca.cpp) on a thread pool, reading the other
+//            staging buffer, while the device computes the next batch.
+//
+// North star split: the Green matrices (dense FP64 kernel evaluations) are
+// device work, the pivoting and the small solves stay on the CPU.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+using namespace gcabem;
+
+struct gcabem_gca_s {
+    int is_complex = 0;
+    int64_t ncl = 0;
+    std::vector<std::vector<int64_t>> rows;  // local row pivots per cluster
+    std::vector<std::vector<double>> V;      // |t| x rank per cluster (row-major)
+    double phase[4] = {0, 0, 0, 0};          // device wait, host compute, total, batches
+};
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+double since(clk::time_point t0) {
+    return std::chrono::duration<double>(clk::now() - t0).count();
+}
+
+struct Pinned {
+    void *p = nullptr;
+    size_t n = 0;
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= n && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess) n = bytes;
+        return e;
+    }
+};
+
+// Staging buffers survive across calls (per device): pinned allocation of
+// hundreds of MB costs more than a whole L6 GCA build.
+struct Staging {
+    Pinned host[2];
+    DevBuf<double> out[2];
+};
+std::mutex g_staging_mutex;
+std::mutex g_build_mutex;
+std::vector<Staging *> g_staging;  // indexed by device
+
+Staging &staging_for(int device) {
+    std::lock_guard<std::mutex> lock(g_staging_mutex);
+    if ((int)g_staging.size() <= device) g_staging.resize(device + 1, nullptr);
+    if (!g_staging[device]) g_staging[device] = new Staging();
+    return *g_staging[device];
+}
+
+}  // namespace
+
+extern "C" {
+
+int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl,
+                     const int64_t *cl_ids, const int64_t *cl_first, const int64_t *cl_size, const double *box_lo,
+                     const double *box_hi, int64_t nperm, const int64_t *perm, double delta,
+                     int m, const double *gauss_pts, const double *gauss_wts,
+                     double scene_diameter, int64_t nduffy, const double *duffy, double epsilon,
+                     int nthreads, int64_t batch_bytes, gcabem_gca_t *out) {
+    if (!mesh || !out) return gcabem_internal_error(GCABEM_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (!(equation == 0 || equation == 1) || (equation == 1 && kappa < 0.0))
+        return gcabem_internal_error(GCABEM_ERR_ARG, "bad equation or kappa");
+    if (ncl < 0 || m < 1 || nduffy < 1 || !(delta > 0.0) || !(epsilon > 0.0))
+        return gcabem_internal_error(GCABEM_ERR_ARG, "bad GCA parameters");
+    const int64_t nsrc = 12 * (int64_t)m * m, ng = nsrc / 2;
+    const int width = equation == 0 ? 1 : 2;
+    const auto t_all = clk::now();
+    auto *G = new gcabem_gca_s();
+    G->is_complex = equation == 1;
+    G->ncl = ncl;
+    G->rows.resize(ncl);
+    G->V.resize(ncl);
+    std::vector<int32_t> perm32(nperm);
+    for (int64_t k = 0; k < nperm; ++k) {
+        if (perm[k] < 0 || perm[k] >= mesh->nt) {
+            delete G;
+            return gcabem_internal_error(GCABEM_ERR_ARG, "panel index out of range");
+        }
+        perm32[k] = (int32_t)perm[k];
+    }
+    // enlarged boxes, in the reference's operation order (gca.py:103-107)
+    std::vector<GreenBox> boxes(ncl);
+    for (int64_t c = 0; c < ncl; ++c) {
+        const double *lo = box_lo + 3 * c, *hi = box_hi + 3 * c;
+        if (cl_size[c] < 1 || cl_first[c] < 0 || cl_first[c] + cl_size[c] > nperm) {
+            delete G;
+            return gcabem_internal_error(GCABEM_ERR_ARG, "cluster panel range out of bounds");
+        }
+        double ext = hi[0] - lo[0];
+        ext = std::max(ext, hi[1] - lo[1]);
+        ext = std::max(ext, hi[2] - lo[2]);
+        const double hmax = 0.5 * std::max(ext, 1e-8 * scene_diameter);
+        if (!(hmax > 0.0)) {
+            delete G;
+            return gcabem_internal_error(GCABEM_ERR_ARG,
+                                         "degenerate box with no scene diameter to fall back on");
+        }
+        for (int k = 0; k < 3; ++k) {
+            boxes[c].center[k] = 0.5 * (lo[k] + hi[k]);
+            const double dh = delta * hmax;
+            boxes[c].half[k] = 0.5 * (hi[k] - lo[k]) + dh;
+        }
+    }
+    // batches of consecutive clusters by output bytes
+    const int64_t row_bytes = nsrc * 8 * width;
+    if (batch_bytes <= 0) batch_bytes = int64_t(256) << 20;
+    std::vector<int64_t> bstart{0};
+    {
+        int64_t acc = 0;
+        for (int64_t c = 0; c < ncl; ++c) {
+            const int64_t b = cl_size[c] * row_bytes;
+            if (acc > 0 && acc + b > batch_bytes) {
+                bstart.push_back(c);
+                acc = 0;
+            }
+            acc += b;
+        }
+        bstart.push_back(ncl);
+    }
+    const int64_t nb = (int64_t)bstart.size() - 1;
+    int64_t max_elems = 0;
+    std::vector<std::vector<int64_t>> out_at(nb);
+    std::vector<std::vector<int2>> tasks(nb);
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t acc = 0;
+        for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) {
+            out_at[b].push_back(acc);
+            const int64_t ne = cl_size[c] * ng;
+            if (ne >= (int64_t(1) << 31)) {
+                delete G;
+                return gcabem_internal_error(GCABEM_ERR_ARG, "cluster too large");
+            }
+            for (int64_t e0 = 0; e0 < ne; e0 += GREEN_TPB)
+                tasks[b].push_back(make_int2((int)(c - bstart[b]), (int)e0));
+            acc += cl_size[c] * nsrc;
+        }
+        max_elems = std::max(max_elems, acc);
+    }
+    if (nthreads <= 0) nthreads = (int)std::max(1u, std::thread::hardware_concurrency());
+
+    cudaError_t e = cudaSetDevice(mesh->device);
+    cudaStream_t s = mesh->stream;
+    Staging &st = staging_for(mesh->device);
+    std::lock_guard<std::mutex> build_lock(g_build_mutex);  // staging: one build at a time
+    DevBuf<int64_t> d_first, d_at;
+    DevBuf<int32_t> d_size, d_perm;
+    DevBuf<GreenBox> d_box;
+    DevBuf<double> d_gq, d_duffy;
+    DevBuf<int2> d_task;
+    std::vector<int64_t> first(ncl);
+    std::vector<int32_t> size32(ncl);
+    for (int64_t c = 0; c < ncl; ++c) {
+        first[c] = cl_first[c];
+        size32[c] = (int32_t)cl_size[c];
+    }
+    std::vector<double> gq(2 * m);
+    for (int k = 0; k < m; ++k) {
+        gq[k] = gauss_pts[k];
+        gq[m + k] = gauss_wts[k];
+    }
+    if (e == cudaSuccess) e = d_first.upload(first.data(), ncl, s);
+    if (e == cudaSuccess) e = d_size.upload(size32.data(), ncl, s);
+    if (e == cudaSuccess) e = d_perm.upload(perm32.data(), nperm, s);
+    if (e == cudaSuccess) e = d_box.upload(boxes.data(), ncl, s);
+    if (e == cudaSuccess) e = d_gq.upload(gq.data(), gq.size(), s);
+    if (e == cudaSuccess) e = d_duffy.upload(duffy, 3 * nduffy, s);
+    size_t max_tasks = 0, max_cl = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        max_tasks = std::max(max_tasks, tasks[b].size());
+        max_cl = std::max(max_cl, out_at[b].size());
+    }
+    if (e == cudaSuccess) e = d_task.alloc(max_tasks * 2);
+    if (e == cudaSuccess) e = d_at.alloc(max_cl * 2);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+        e = st.out[k].reserve((size_t)(max_elems * width));
+        if (e == cudaSuccess) e = st.host[k].reserve((size_t)(max_elems * width) * 8);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k)
+        e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+
+    // batch b: tasks/offsets into slot b % 2 of the task and offset arrays
+    auto enqueue = [&](int64_t b) -> cudaError_t {
+        const int k = (int)(b & 1);
+        int2 *tk = d_task.p + k * max_tasks;
+        int64_t *at = d_at.p + k * max_cl;
+        cudaError_t r = cudaMemcpyAsync(tk, tasks[b].data(), sizeof(int2) * tasks[b].size(),
+                                        cudaMemcpyHostToDevice, s);
+        if (r == cudaSuccess)
+            r = cudaMemcpyAsync(at, out_at[b].data(), sizeof(int64_t) * out_at[b].size(),
+                                cudaMemcpyHostToDevice, s);
+        const int64_t c0 = bstart[b];
+        if (r == cudaSuccess)
+            r = launch_green_box(equation, mesh->charts.p, tk, (int64_t)tasks[b].size(),
+                                 d_first.p + c0, d_size.p + c0, d_perm.p, d_box.p + c0, m, d_gq.p,
+                                 d_duffy.p, (int)nduffy, at, st.out[k].p, kappa, s);
+        int64_t elems = 0;
+        for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) elems += cl_size[c] * nsrc;
+        if (r == cudaSuccess)
+            r = cudaMemcpyAsync(st.host[k].p, st.out[k].p, sizeof(double) * elems * width,
+                                cudaMemcpyDeviceToHost, s);
+        if (r == cudaSuccess) r = cudaEventRecord(done[k], s);
+        return r;
+    };
+
+    std::atomic<int64_t> err_cluster{INT64_MAX};
+    std::atomic<int> err_code{0};
+    double t_wait = 0.0, t_host = 0.0;
+    if (e == cudaSuccess && nb > 0) e = enqueue(0);
+    for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
+        const int k = (int)(b & 1);
+        auto t0 = clk::now();
+        e = cudaEventSynchronize(done[k]);
+        t_wait += since(t0);
+        if (e != cudaSuccess) break;
+        // the next batch writes the other staging slot, which the host
+        // finished with in the previous iteration
+        if (b + 1 < nb) e = enqueue(b + 1);
+        if (e != cudaSuccess) break;
+        t0 = clk::now();
+        const double *A = static_cast<const double *>(st.host[k].p);
+        const int64_t c0 = bstart[b], c1 = bstart[b + 1];
+        std::atomic<int64_t> next{c0};
+        auto work = [&]() {
+            for (;;) {
+                const int64_t c = next.fetch_add(1);
+                if (c >= c1) return;
+                const double *Ac = A + out_at[b][c - c0] * width;
+                const int rc = gca_operator(equation == 1, Ac, cl_size[c], nsrc, epsilon,
+                                            G->rows[c], G->V[c]);
+                if (rc != 0) {
+                    int64_t prev = err_cluster.load();
+                    while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
+                    }
+                    if (c <= err_cluster.load()) err_code = rc;
+                }
+            }
+        };
+        const int nt = (int)std::min<int64_t>(nthreads, c1 - c0);
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work);
+        work();
+        for (auto &t : th) t.join();
+        t_host += since(t0);
+        if (err_code.load() != 0) break;
+    }
+    cudaStreamSynchronize(s);
+    for (auto &d : done)
+        if (d) cudaEventDestroy(d);
+    if (e != cudaSuccess) {
+        delete G;
+        return gcabem_internal_error(GCABEM_ERR_CUDA,
+                                     (std::string("gca build: ") + cudaGetErrorString(e)).c_str());
+    }
+    if (err_code.load() != 0) {
+        const int64_t c = err_cluster.load();
+        const std::string id = std::to_string(cl_ids ? cl_ids[c] : c);
+        const std::string msg =
+            err_code.load() == 1
+                ? "cluster " + id + ": zero Green matrix"
+                : "cluster " + id + ": singular ACA pivot block (condition above 1e+14)";
+        delete G;
+        return gcabem_internal_error(GCABEM_ERR_GCA, msg.c_str());
+    }
+    G->phase[0] = t_wait;
+    G->phase[1] = t_host;
+    G->phase[2] = since(t_all);
+    G->phase[3] = (double)nb;
+    *out = G;
+    return GCABEM_OK;
+}
+
+int gcabem_gca_sizes(gcabem_gca_t G, int64_t *ranks, double *phase4) {
+    if (!G) return gcabem_internal_error(GCABEM_ERR_ARG, "null handle");
+    for (int64_t c = 0; c < G->ncl; ++c) ranks[c] = (int64_t)G->rows[c].size();
+    if (phase4)
+        for (int k = 0; k < 4; ++k) phase4[k] = G->phase[k];
+    return GCABEM_OK;
+}
+
+int gcabem_gca_fetch(gcabem_gca_t G, int64_t *rows, double *V) {
+    if (!G) return gcabem_internal_error(GCABEM_ERR_ARG, "null handle");
+    int64_t ro = 0, vo = 0;
+    for (int64_t c = 0; c < G->ncl; ++c) {
+        std::copy(G->rows[c].begin(), G->rows[c].end(), rows + ro);
+        ro += (int64_t)G->rows[c].size();
+        std::copy(G->V[c].begin(), G->V[c].end(), V + vo);
+        vo += (int64_t)G->V[c].size();
+    }
+    return GCABEM_OK;
+}
+
+int gcabem_gca_free(gcabem_gca_t G) {
+    delete G;
+    return GCABEM_OK;
+}
+
+}  // extern "C"

@@ -39,6 +39,10 @@ struct SingItem {
 };
 static_assert(sizeof(SingItem) == 24, "SingItem layout");
 
+struct GreenBox {
+    double center[3], half[3];  // enlarged box of one cluster (gca.py:103-107)
+};
+
 enum Kind { L_SLP = 0, L_DLP = 1, H_SLP = 2, H_DLP = 3 };
 constexpr int MAX_ORDER = 12;
 constexpr int DISJOINT_TPB = 128;   // pairs (threads) per disjoint task
@@ -69,6 +73,14 @@ cudaError_t launch_green(int equation, const Chart *charts, const int2 *tasks, i
                          const int64_t *panel_at, const int32_t *panels, const int64_t *out_at,
                          int nsrc, const double *src, const double *duffy, int nq, double *out,
                          double kappa, cudaStream_t s);
+// Green matrices of a batch of clusters with device-generated sources;
+// out (per cluster |t| x 12 m^2, row-major) at out_at[c] elements (double or
+// double2 by equation). Panels of cluster c: perm[cl_first[c] + i].
+cudaError_t launch_green_box(int equation, const Chart *charts, const int2 *tasks, int64_t ntasks,
+                             const int64_t *cl_first, const int32_t *cl_size, const int32_t *perm,
+                             const GreenBox *boxes, int m, const double *gq, const double *duffy,
+                             int nq, const int64_t *out_at, double *out, double kappa,
+                             cudaStream_t s);
 cudaError_t launch_potential(int kind, int order, const Chart *charts, int64_t nt,
                              const double *pts, int64_t npts, double xw, double2 *out,
                              double kappa, cudaStream_t s);

@@ -7,13 +7,15 @@ source fields) is compressed by partially pivoted ACA; row pivots become
 the interpolation points and V = A_t[:, ct] A_t[tt, ct]^-1.
 
 Split (north_star): the Green matrices of ALL clusters are evaluated in
-batched sm_100a launches (csrc/kernels.cu green_kernel, C ABI
-gcabem_green_matrices); the pivoting (ACA) and the small V solve stay on the
-CPU, overlapped with the next batch of Green matrices on the device.
+batched sm_100a launches with the sources generated on the device
+(csrc/kernels.cu green_box_kernel); the pivoting (ACA), the pivot-block
+check and the small V solves stay on the CPU, natively on all cores
+(csrc/aca.cpp), overlapped with the next batch of Green matrices
+(csrc/gca_pipeline.cu, C ABI gcabem_gca_build).
 """
 from __future__ import annotations
 
-import threading
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -34,7 +36,6 @@ DEFAULT_FACE_POINTS = 6
 DEFAULT_EPSILON = 1e-4
 
 _PIVOT_COND_LIMIT = 1e14
-_GREEN_BATCH_BYTES = 1 << 30   # device output per batched launch
 
 
 class GcaError(RuntimeError):
@@ -215,25 +216,27 @@ def _solve_with_refinement(A_cols: np.ndarray, pivot_block: np.ndarray) -> np.nd
 
 
 def _operator_from_green(cluster_index: int, panels: np.ndarray, A: np.ndarray,
-                         epsilon: float, first=None) -> InterpolationOperator:
-    """Pivot solve with one tighter ACA retry (gca.py:268-282). `first` is a
-    precomputed (rows, cols, residual) for `epsilon` (batched native ACA)."""
-    eps = epsilon
-    for attempt in range(2):
-        if attempt == 0 and first is not None:
-            rows, cols = first[0], first[1]
-        else:
-            res = aca(A, eps)
-            rows, cols = res.row_pivots, res.col_pivots
-        if rows.size == 0:
-            raise GcaError(f"cluster {cluster_index}: zero Green matrix")
-        block = A[np.ix_(rows, cols)]
-        if np.linalg.cond(block) <= _PIVOT_COND_LIMIT:
-            V = _solve_with_refinement(A[:, cols], block)
-            return InterpolationOperator(cluster_index, rows, panels[rows], V)
-        eps *= 0.1
-    raise GcaError(f"cluster {cluster_index}: singular ACA pivot block "
-                   f"(condition above {_PIVOT_COND_LIMIT:.0e})")
+                         epsilon: float) -> InterpolationOperator:
+    """ACA, pivot-block check and refined V solve with one tighter ACA retry
+    (gca.py:268-282), natively (C ABI gcabem_gca_operator)."""
+    A = np.asarray(A)
+    is_complex = np.iscomplexobj(A)
+    flat = np.ascontiguousarray(A, dtype=np.complex128 if is_complex else np.float64)
+    nr, nc = flat.shape
+    cap = min(nr, nc)
+    rank = np.zeros(1, np.int64)
+    rows = np.zeros(cap, np.int64)
+    V = np.zeros(nr * cap, np.complex128 if is_complex else np.float64)
+    try:
+        nat.check(nat.lib().gcabem_gca_operator(int(is_complex), nat.ptr(flat), nr, nc,
+                                                float(epsilon), nat.ptr(rank), nat.ptr(rows),
+                                                nat.ptr(V)))
+    except GcaError as exc:
+        raise GcaError(f"cluster {cluster_index}: {exc}") from None
+    r = int(rank[0])
+    rows = rows[:r].copy()
+    return InterpolationOperator(cluster_index, rows, np.asarray(panels)[rows],
+                                 V[:nr * r].reshape(nr, r))
 
 
 def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, box_lo, box_hi,
@@ -246,57 +249,57 @@ def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, 
     return _operator_from_green(cluster_index, panels, A, params.epsilon)
 
 
-def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device) -> dict:
-    """Batched device Green matrices and native threaded ACA (worker thread),
-    the pivot solves of batch k overlapped with batch k+1 (ctypes releases
-    the GIL)."""
-    ids = sorted(ids)
-    nsrc = 12 * params.m * params.m
-    width = 16 if spec.is_complex else 8
-    batches, cur, cur_bytes = [], [], 0
-    for cid in ids:
-        nb = tree.nodes[cid].size * nsrc * width
-        if cur and cur_bytes + nb > _GREEN_BATCH_BYTES:
-            batches.append(cur)
-            cur, cur_bytes = [], 0
-        cur.append(cid)
-        cur_bytes += nb
-    if cur:
-        batches.append(cur)
+last_build_phases: dict = {}
 
-    def run(batch):
-        pl = [tree.panels(tree.nodes[c]) for c in batch]
-        ss = [green_sources(tree.nodes[c].lo, tree.nodes[c].hi, params.delta, params.m, scene)
-              for c in batch]
-        mats, buf, rows_at = build_green_matrices(mesh, pl, ss, spec, params.rule_order, device,
-                                                  flat=True)
-        piv = aca_batch(buf, rows_at, nsrc, spec.is_complex, params.epsilon)
-        return pl, mats, piv
 
-    ops: dict = {}
-    result: dict = {}
-
-    def worker(k):
-        try:
-            result[k] = run(batches[k])
-        except BaseException as exc:  # surfaced on the host thread
-            result[k] = exc
-
-    th = None
-    if batches:
-        th = threading.Thread(target=worker, args=(0,))
-        th.start()
-    for k in range(len(batches)):
-        th.join()
-        got = result.pop(k)
-        if isinstance(got, BaseException):
-            raise got
-        if k + 1 < len(batches):
-            th = threading.Thread(target=worker, args=(k + 1,))
-            th.start()
-        pl, As, piv = got
-        for cid, panels, A, first in zip(batches[k], pl, As, piv):
-            ops[cid] = _operator_from_green(cid, panels, A, params.epsilon, first)
+def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
+                  batch_bytes: int = 0) -> dict:
+    """All clusters in one native pipeline (C ABI gcabem_gca_build): device
+    Green matrices per batch (sources generated on the device, bit-identical
+    to green_sources), host ACA + pivot check + refined V solve on all cores,
+    overlapped with the next batch's kernels and D2H."""
+    ids = np.array(sorted(ids), dtype=np.int64)
+    if ids.size == 0:
+        return {}
+    dm = device_mesh(mesh, device)
+    starts = np.fromiter((tree.nodes[c].start for c in ids), dtype=np.int64, count=ids.size)
+    sizes = np.fromiter((tree.nodes[c].size for c in ids), dtype=np.int64, count=ids.size)
+    lo = np.ascontiguousarray([tree.nodes[c].lo for c in ids], dtype=np.float64)
+    hi = np.ascontiguousarray([tree.nodes[c].hi for c in ids], dtype=np.float64)
+    perm = np.ascontiguousarray(tree.permutation, dtype=np.int64)
+    g = gauss_legendre(params.m)
+    gp, gw = nat.f64(g.points), nat.f64(g.weights)
+    pts, wq = duffy_panel_rule(params.rule_order)
+    duffy = np.ascontiguousarray(np.column_stack([pts, wq]))
+    eq = 0 if spec.equation == "laplace" else 1
+    h = ctypes.c_void_p()
+    p = nat.ptr
+    nat.check(nat.lib().gcabem_gca_build(
+        dm.handle, eq, float(spec.kappa), ids.size, p(ids), p(starts), p(sizes), p(lo), p(hi),
+        perm.size, p(perm), float(params.delta), int(params.m), p(gp), p(gw), float(scene),
+        duffy.shape[0], p(duffy), float(params.epsilon), 0, int(batch_bytes), ctypes.byref(h)))
+    try:
+        ranks = np.empty(ids.size, np.int64)
+        phase = np.zeros(4, np.float64)
+        nat.check(nat.lib().gcabem_gca_sizes(h, p(ranks), p(phase)))
+        rows = np.empty(max(int(ranks.sum()), 1), np.int64)
+        width = 2 if spec.is_complex else 1
+        vlen = int(np.sum(sizes * ranks)) * width
+        V = np.empty(max(vlen, 1), np.float64)
+        nat.check(nat.lib().gcabem_gca_fetch(h, p(rows), p(V)))
+    finally:
+        nat.lib().gcabem_gca_free(h)
+    last_build_phases.update(device_wait_s=float(phase[0]), host_s=float(phase[1]),
+                             native_total_s=float(phase[2]), batches=int(phase[3]),
+                             clusters=int(ids.size))
+    Vv = V.view(np.complex128) if spec.is_complex else V
+    ops = {}
+    ro = vo = 0
+    for cid, first, n, r in zip(ids.tolist(), starts.tolist(), sizes.tolist(), ranks.tolist()):
+        loc = rows[ro:ro + r]
+        ops[cid] = InterpolationOperator(cid, loc, perm[first + loc], Vv[vo:vo + n * r].reshape(n, r))
+        ro += r
+        vo += n * r
     return ops
 
 

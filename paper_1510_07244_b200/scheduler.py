@@ -300,18 +300,28 @@ class DeviceLayout:
         self.leaf_range = (lo, hi)
         self.payload_offset = int(pk.leaf_base[lo])
         self.payload_len = int(pk.leaf_base[hi] - pk.leaf_base[lo])
-        blocks = pk.device_blocks(lo, hi)
-        items, perms = pk.device_items(lo, hi)
-        self.disjoint_pairs = int(np.sum(blocks[:, 2] * blocks[:, 3])) if blocks.size else 0
-        self.singular_counts = [int(np.count_nonzero(items[:, 0] == c)) for c in (1, 2, 3)]
-        self.h2d_bytes = int(blocks.nbytes + pk.panels.nbytes + items.nbytes + perms.nbytes)
-        self.prep_s = time.monotonic() - t0
         self.device = dm.device
         self._dm = dm
         h = ctypes.c_void_p()
-        nat.check(nat.lib().gcabem_layout_create(
-            dm.handle, self.payload_len, blocks.shape[0], nat.ptr(blocks), pk.panels.size,
-            nat.ptr(pk.panels), items.shape[0], nat.ptr(items), nat.ptr(perms), ctypes.byref(h)))
+        for arr in (pk.leaf_shape, pk.leaf_base, pk.leaf_rows_at, pk.leaf_cols_at, pk.panels,
+                    pk.blk_leaf, pk.blk_r0, pk.blk_nr, pk.blk_c0, pk.blk_nc, pk.item_case,
+                    pk.item_tri_x, pk.item_tri_y, pk.item_leaf, pk.item_offset, pk.perms):
+            if not arr.flags.c_contiguous:
+                raise ValueError("package arrays must be C-contiguous")
+        p = nat.ptr
+        nat.check(nat.lib().gcabem_layout_from_packages(
+            dm.handle, lo, hi, pk.leaf_ids.size, p(pk.leaf_shape), p(pk.leaf_base),
+            p(pk.leaf_rows_at), p(pk.leaf_cols_at), pk.panels.size, p(pk.panels),
+            pk.blk_leaf.size, p(pk.blk_leaf), p(pk.blk_r0), p(pk.blk_nr), p(pk.blk_c0),
+            p(pk.blk_nc), pk.item_case.size, p(pk.item_case), p(pk.item_tri_x),
+            p(pk.item_tri_y), p(pk.item_leaf), p(pk.item_offset), p(pk.perms),
+            ctypes.byref(h)))
+        info = np.zeros(8, np.int64)
+        nat.check(nat.lib().gcabem_layout_info(h, p(info)))
+        self.disjoint_pairs = int(info[3])
+        self.singular_counts = [int(x) for x in info[4:7]]
+        self.h2d_bytes = int(info[7])
+        self.prep_s = time.monotonic() - t0
         self.handle = h.value
 
     @staticmethod

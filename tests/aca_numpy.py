@@ -43,3 +43,24 @@ def aca(A, epsilon, max_rank=None):
         if mag[cand] == 0.0:
             cand = nr
     return np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64)
+
+
+def operator(A, epsilon):
+    """TEST-SIDE restatement of build_interpolation_operator's pivot solve
+    (reference gca.py:248-282): (row pivots, V)."""
+    eps = epsilon
+    for _ in range(2):
+        rows, cols = aca(A, eps)
+        assert rows.size, "zero Green matrix"
+        block = A[np.ix_(rows, cols)]
+        if np.linalg.cond(block) <= 1e14:
+            A_cols = A[:, cols]
+            V = np.linalg.solve(block.T, A_cols.T).T
+            for _ in range(2):
+                R = A_cols - V @ block
+                if np.max(np.abs(R)) <= 1e-15 * max(np.max(np.abs(A_cols)), 1.0):
+                    break
+                V = V + np.linalg.solve(block.T, R.T).T
+            return rows, V
+        eps *= 0.1
+    raise AssertionError("singular pivot block")
