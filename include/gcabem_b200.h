@@ -238,8 +238,9 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
  * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
  * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
  * nthreads threads, overlapped with the next batch (batch_bytes of Green
- * matrix per launch; 0 = 256 MiB). Results: gcabem_gca_sizes (rank per
- * cluster, phase seconds {device wait, host, total, batches}), then
+ * matrix per launch, 4 launches in flight; 0 = 128 MiB). Results: gcabem_gca_sizes (rank per
+ * cluster, phase6 {device wait s, pipeline wall s, total s, batches, host
+ * thread-seconds, threads}), then
  * gcabem_gca_fetch (row pivots concatenated; V blocks |t| x rank row-major,
  * float64 for Laplace, complex128 for Helmholtz, concatenated).
  * GCABEM_ERR_GCA: "cluster <id>: zero Green matrix" / "singular ACA pivot
@@ -251,7 +252,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                      const double *gauss_wts, double scene_diameter, int64_t nduffy,
                      const double *duffy, double epsilon, int nthreads, int64_t batch_bytes,
                      gcabem_gca_t *out);
-int gcabem_gca_sizes(gcabem_gca_t g, int64_t *ranks, double *phase4);
+int gcabem_gca_sizes(gcabem_gca_t g, int64_t *ranks, double *phase6);
 int gcabem_gca_fetch(gcabem_gca_t g, int64_t *rows, double *V);
 int gcabem_gca_free(gcabem_gca_t g);
 /* One cluster's operator from a host Green matrix A (nr x nc row-major,

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <memory>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -28,7 +30,8 @@ struct gcabem_gca_s {
     int64_t ncl = 0;
     std::vector<std::vector<int64_t>> rows;  // local row pivots per cluster
     std::vector<std::vector<double>> V;      // |t| x rank per cluster (row-major)
-    double phase[4] = {0, 0, 0, 0};          // device wait, host compute, total, batches
+    // device wait, pipeline wall, total, batches, host thread-seconds, threads
+    double phase[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -57,9 +60,10 @@ struct Pinned {
 
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
+constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
 struct Staging {
-    Pinned host[2];
-    DevBuf<double> out[2];
+    Pinned host[SLOTS];
+    DevBuf<double> out[SLOTS];
 };
 std::mutex g_staging_mutex;
 std::mutex g_build_mutex;
@@ -129,7 +133,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     // batches of consecutive clusters by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
-    if (batch_bytes <= 0) batch_bytes = int64_t(256) << 20;
+    if (batch_bytes <= 0) batch_bytes = int64_t(128) << 20;
     std::vector<int64_t> bstart{0};
     {
         int64_t acc = 0;
@@ -195,20 +199,20 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         max_tasks = std::max(max_tasks, tasks[b].size());
         max_cl = std::max(max_cl, out_at[b].size());
     }
-    if (e == cudaSuccess) e = d_task.alloc(max_tasks * 2);
-    if (e == cudaSuccess) e = d_at.alloc(max_cl * 2);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    if (e == cudaSuccess) e = d_task.alloc(max_tasks * SLOTS);
+    if (e == cudaSuccess) e = d_at.alloc(max_cl * SLOTS);
+    for (int k = 0; k < SLOTS && e == cudaSuccess; ++k) {
         e = st.out[k].reserve((size_t)(max_elems * width));
         if (e == cudaSuccess) e = st.host[k].reserve((size_t)(max_elems * width) * 8);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaEvent_t done[2] = {nullptr, nullptr};
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k)
+    cudaEvent_t done[SLOTS] = {};
+    for (int k = 0; k < SLOTS && e == cudaSuccess; ++k)
         e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
 
-    // batch b: tasks/offsets into slot b % 2 of the task and offset arrays
+    // batch b uses slot b % SLOTS (tasks, offsets, device output, staging)
     auto enqueue = [&](int64_t b) -> cudaError_t {
-        const int k = (int)(b & 1);
+        const int k = (int)(b % SLOTS);
         int2 *tk = d_task.p + k * max_tasks;
         int64_t *at = d_at.p + k * max_cl;
         cudaError_t r = cudaMemcpyAsync(tk, tasks[b].data(), sizeof(int2) * tasks[b].size(),
@@ -230,47 +234,83 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         return r;
     };
 
+    // Workers pull clusters in batch order from one queue (no per-batch
+    // barrier: a long cluster only delays its own slot); the calling thread
+    // issues batches into free slots and publishes each batch when its D2H
+    // has landed.
+    std::vector<int64_t> batch_of(ncl);
+    for (int64_t b = 0; b < nb; ++b)
+        for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) batch_of[c] = b;
+    std::unique_ptr<std::atomic<int64_t>[]> remaining(new std::atomic<int64_t>[nb > 0 ? nb : 1]);
+    for (int64_t b = 0; b < nb; ++b) remaining[b] = bstart[b + 1] - bstart[b];
+    std::vector<char> ready(nb, 0);
+    std::mutex mu;
+    std::condition_variable cv;
+    bool abort = false;
+    std::atomic<int64_t> next{0};
     std::atomic<int64_t> err_cluster{INT64_MAX};
     std::atomic<int> err_code{0};
-    double t_wait = 0.0, t_host = 0.0;
-    if (e == cudaSuccess && nb > 0) e = enqueue(0);
-    for (int64_t b = 0; b < nb && e == cudaSuccess; ++b) {
-        const int k = (int)(b & 1);
-        auto t0 = clk::now();
-        e = cudaEventSynchronize(done[k]);
-        t_wait += since(t0);
-        if (e != cudaSuccess) break;
-        // the next batch writes the other staging slot, which the host
-        // finished with in the previous iteration
-        if (b + 1 < nb) e = enqueue(b + 1);
-        if (e != cudaSuccess) break;
-        t0 = clk::now();
-        const double *A = static_cast<const double *>(st.host[k].p);
-        const int64_t c0 = bstart[b], c1 = bstart[b + 1];
-        std::atomic<int64_t> next{c0};
-        auto work = [&]() {
-            for (;;) {
-                const int64_t c = next.fetch_add(1);
-                if (c >= c1) return;
-                const double *Ac = A + out_at[b][c - c0] * width;
-                const int rc = gca_operator(equation == 1, Ac, cl_size[c], nsrc, epsilon,
-                                            G->rows[c], G->V[c]);
-                if (rc != 0) {
-                    int64_t prev = err_cluster.load();
-                    while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
-                    }
-                    if (c <= err_cluster.load()) err_code = rc;
-                }
+    std::vector<double> busy(nthreads, 0.0);
+    auto worker = [&](int tid) {
+        for (;;) {
+            const int64_t c = next.fetch_add(1);
+            if (c >= ncl) return;
+            const int64_t b = batch_of[c];
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return ready[b] || abort; });
+                if (abort) return;
             }
-        };
-        const int nt = (int)std::min<int64_t>(nthreads, c1 - c0);
-        std::vector<std::thread> th;
-        for (int t = 1; t < nt; ++t) th.emplace_back(work);
-        work();
-        for (auto &t : th) t.join();
-        t_host += since(t0);
-        if (err_code.load() != 0) break;
+            const auto t0 = clk::now();
+            const double *A = static_cast<const double *>(st.host[b % SLOTS].p) +
+                              out_at[b][c - bstart[b]] * width;
+            const int rc = gca_operator(equation == 1, A, cl_size[c], nsrc, epsilon, G->rows[c],
+                                        G->V[c]);
+            if (rc != 0) {
+                int64_t prev = err_cluster.load();
+                while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
+                }
+                if (c <= err_cluster.load()) err_code = rc;
+            }
+            busy[tid] += since(t0);
+            if (remaining[b].fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> lk(mu);
+                cv.notify_all();
+            }
+        }
+    };
+    double t_wait = 0.0;
+    const auto t_pipe = clk::now();
+    std::vector<std::thread> th;
+    if (e == cudaSuccess)
+        for (int t = 0; t < nthreads; ++t) th.emplace_back(worker, t);
+    int64_t issued = 0, completed = 0;
+    while (e == cudaSuccess && completed < nb) {
+        while (e == cudaSuccess && issued < nb &&
+               (issued < SLOTS || remaining[issued - SLOTS].load() == 0))
+            e = enqueue(issued++);
+        if (e != cudaSuccess) break;
+        if (completed < issued) {
+            const auto t0 = clk::now();
+            e = cudaEventSynchronize(done[completed % SLOTS]);
+            t_wait += since(t0);
+            std::lock_guard<std::mutex> lk(mu);
+            ready[completed++] = 1;
+            cv.notify_all();
+        } else {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return remaining[issued - SLOTS].load() == 0; });
+        }
     }
+    if (e != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+        cv.notify_all();
+    }
+    for (auto &t : th) t.join();
+    double t_host = 0.0;
+    for (double x : busy) t_host += x;
+    G->phase[1] = since(t_pipe);
     cudaStreamSynchronize(s);
     for (auto &d : done)
         if (d) cudaEventDestroy(d);
@@ -290,9 +330,10 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         return gcabem_internal_error(GCABEM_ERR_GCA, msg.c_str());
     }
     G->phase[0] = t_wait;
-    G->phase[1] = t_host;
     G->phase[2] = since(t_all);
     G->phase[3] = (double)nb;
+    G->phase[4] = t_host;
+    G->phase[5] = (double)nthreads;
     *out = G;
     return GCABEM_OK;
 }
@@ -301,7 +342,7 @@ int gcabem_gca_sizes(gcabem_gca_t G, int64_t *ranks, double *phase4) {
     if (!G) return gcabem_internal_error(GCABEM_ERR_ARG, "null handle");
     for (int64_t c = 0; c < G->ncl; ++c) ranks[c] = (int64_t)G->rows[c].size();
     if (phase4)
-        for (int k = 0; k < 4; ++k) phase4[k] = G->phase[k];
+        for (int k = 0; k < 6; ++k) phase4[k] = G->phase[k];
     return GCABEM_OK;
 }
 

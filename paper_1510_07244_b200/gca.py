@@ -16,6 +16,8 @@ check and the small V solves stay on the CPU, natively on all cores
 from __future__ import annotations
 
 import ctypes
+import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -252,16 +254,25 @@ def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, 
 last_build_phases: dict = {}
 
 
+def _host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
                   batch_bytes: int = 0) -> dict:
     """All clusters in one native pipeline (C ABI gcabem_gca_build): device
     Green matrices per batch (sources generated on the device, bit-identical
     to green_sources), host ACA + pivot check + refined V solve on all cores,
     overlapped with the next batch's kernels and D2H."""
+    t0 = time.perf_counter()
     ids = np.array(sorted(ids), dtype=np.int64)
     if ids.size == 0:
         return {}
     dm = device_mesh(mesh, device)
+    t_mesh = time.perf_counter() - t0
     starts = np.fromiter((tree.nodes[c].start for c in ids), dtype=np.int64, count=ids.size)
     sizes = np.fromiter((tree.nodes[c].size for c in ids), dtype=np.int64, count=ids.size)
     lo = np.ascontiguousarray([tree.nodes[c].lo for c in ids], dtype=np.float64)
@@ -274,13 +285,15 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
     eq = 0 if spec.equation == "laplace" else 1
     h = ctypes.c_void_p()
     p = nat.ptr
+    t1 = time.perf_counter()
     nat.check(nat.lib().gcabem_gca_build(
         dm.handle, eq, float(spec.kappa), ids.size, p(ids), p(starts), p(sizes), p(lo), p(hi),
         perm.size, p(perm), float(params.delta), int(params.m), p(gp), p(gw), float(scene),
-        duffy.shape[0], p(duffy), float(params.epsilon), 0, int(batch_bytes), ctypes.byref(h)))
+        duffy.shape[0], p(duffy), float(params.epsilon), _host_threads(), int(batch_bytes),
+        ctypes.byref(h)))
     try:
         ranks = np.empty(ids.size, np.int64)
-        phase = np.zeros(4, np.float64)
+        phase = np.zeros(6, np.float64)
         nat.check(nat.lib().gcabem_gca_sizes(h, p(ranks), p(phase)))
         rows = np.empty(max(int(ranks.sum()), 1), np.int64)
         width = 2 if spec.is_complex else 1
@@ -289,9 +302,7 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
         nat.check(nat.lib().gcabem_gca_fetch(h, p(rows), p(V)))
     finally:
         nat.lib().gcabem_gca_free(h)
-    last_build_phases.update(device_wait_s=float(phase[0]), host_s=float(phase[1]),
-                             native_total_s=float(phase[2]), batches=int(phase[3]),
-                             clusters=int(ids.size))
+    t2 = time.perf_counter()
     Vv = V.view(np.complex128) if spec.is_complex else V
     ops = {}
     ro = vo = 0
@@ -300,6 +311,11 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
         ops[cid] = InterpolationOperator(cid, loc, perm[first + loc], Vv[vo:vo + n * r].reshape(n, r))
         ro += r
         vo += n * r
+    last_build_phases.update(device_wait_s=float(phase[0]), pipeline_s=float(phase[1]),
+                             native_total_s=float(phase[2]), batches=int(phase[3]),
+                             host_thread_s=float(phase[4]), threads=int(phase[5]),
+                             clusters=int(ids.size), mesh_s=t_mesh, prep_s=t1 - t0 - t_mesh,
+                             call_s=t2 - t1, wrap_s=time.perf_counter() - t2)
     return ops
 
 
@@ -308,9 +324,19 @@ def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec
     """Operators for every cluster in an admissible block (gca.py:285-310);
     (row_ops, col_ops) — the same dict for a shared cluster tree."""
     device = default_device() if device is None else device
+    t0 = time.perf_counter()
     scene = mesh.diameter()
-    row_ids = {b.row for b in block_tree.leaves if b.kind == "admissible"}
-    col_ids = {b.col for b in block_tree.leaves if b.kind == "admissible"}
+    native = getattr(block_tree, "_native_leaves", None)
+    if native is not None:  # native block tree: leaf arrays, no per-leaf objects
+        arr = native[0]
+        adm = arr[:, 2] == 0
+        row_ids = set(np.unique(arr[adm, 0]).tolist())
+        col_ids = set(np.unique(arr[adm, 1]).tolist())
+    else:
+        row_ids = {b.row for b in block_tree.leaves if b.kind == "admissible"}
+        col_ids = {b.col for b in block_tree.leaves if b.kind == "admissible"}
+    last_build_phases.clear()
+    last_build_phases["ids_s"] = time.perf_counter() - t0
     if block_tree.row_tree is block_tree.col_tree:
         ops = _ops_for_tree(mesh, block_tree.row_tree, row_ids | col_ids, spec, params, scene,
                             device)
