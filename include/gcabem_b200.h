@@ -175,8 +175,9 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
                           gcabem_packages_t *out);
 /* sizes[9]: {L, payload_len, npanels, nblocks, nlists, nitems, 0, 0, 0} */
 int gcabem_packages_sizes(gcabem_packages_t pk, int64_t *sizes);
-/* blocks: nblocks x 5 {leaf, r0, nr, c0, nc}; items: nitems x 6 {case 1..3,
- * tri_x, tri_y, leaf, offset in leaf, generating block}; perms nitems x 6. */
+/* Planar (field-major) outputs: blocks 5 x nblocks {leaf, r0, nr, c0, nc};
+ * items 6 x nitems {case 1..3, tri_x, tri_y, leaf, offset in leaf,
+ * generating block}; perms nitems x 6 (perm_x, perm_y). */
 int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_shape,
                           int64_t *leaf_base, int64_t *rows_at, int64_t *cols_at,
                           uint8_t *flagged, int64_t *blocks, int64_t *blk_list, int64_t *items,
@@ -238,7 +239,7 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
  * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
  * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
  * nthreads threads, overlapped with the next batch (batch_bytes of Green
- * matrix per launch, 4 launches in flight; 0 = 128 MiB). Results: gcabem_gca_sizes (rank per
+ * matrix per launch, 4 launches in flight; 0 = 32 MiB). Results: gcabem_gca_sizes (rank per
  * cluster, phase6 {device wait s, pipeline wall s, total s, batches, host
  * thread-seconds, threads}), then
  * gcabem_gca_fetch (row pivots concatenated; V blocks |t| x rank row-major,

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -21,6 +24,21 @@ using namespace gcabem;
 namespace {
 
 thread_local std::string g_error;
+
+// GCABEM_TRACE=1: stage timings of the host-side set-up paths on stderr
+struct Trace {
+    const char *who;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    bool on = std::getenv("GCABEM_TRACE") != nullptr;
+    explicit Trace(const char *w) : who(w) {}
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[%s] %-12s %8.2f ms\n", who, what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 int set_error(int code, const std::string &msg) {
     g_error = msg;
@@ -76,6 +94,22 @@ std::vector<double> pack_rule(int64_t q, const double *xs, const double *ys, con
 
 }  // namespace
 
+namespace gcabem {
+cudaError_t pool_init(int device) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(device)) return cudaSuccess;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e == cudaSuccess) done.insert(device);
+    return e;
+}
+}  // namespace gcabem
+
 // Error hook for the other translation units (packaging.cpp).
 int gcabem_internal_error(int code, const char *msg) { return set_error(code, msg); }
 
@@ -102,7 +136,7 @@ struct gcabem_plan_s {
     int kind = 0, order = 0;
     double kappa = 0.0;
     int64_t payload_len = 0;
-    DevBuf<double2> payload;
+    PoolBuf<double2> payload;
     DevBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -320,6 +354,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
     GC_ARG(payload_len >= 0 && nblocks >= 0 && npanels >= 0 && nitems >= 0, "negative size");
     GC_ARG(nblocks < (int64_t(1) << 31), "too many blocks");
     GC_CUDA(cudaSetDevice(mesh->device));
+    Trace tr("layout");
     auto *L = new gcabem_layout_s();
     L->mesh = mesh;
     L->payload_len = payload_len;
@@ -356,6 +391,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
         for (int64_t k0 = 0; k0 < L->block_pairs[b]; k0 += DISJOINT_TPB)
             tasks[t++] = make_int2((int)b, (int)k0);
     }
+    tr.mark("blocks+tasks");
     std::vector<int32_t> pan(npanels);
     for (int64_t k = 0; k < npanels; ++k) {
         if (panels[k] < 0 || panels[k] >= mesh->nt) return fail("panel index out of range");
@@ -405,6 +441,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
         if (!ok) return fail("bad singular item (index, permutation or chart)");
         L->item_out[q] = it.out;
     }
+    tr.mark("items");
     L->ntasks = ntasks;
     L->case_at[0] = 0;
     for (int c = 1; c <= 3; ++c) L->case_at[c] = L->case_at[c - 1] + counts[c];
@@ -414,6 +451,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
     if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
     if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    tr.mark("upload");
     if (e != cudaSuccess) {
         delete L;
         GC_CUDA(e);
@@ -435,6 +473,7 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                                 gcabem_layout_t *out) {
     GC_ARG(mesh && out, "null argument");
     GC_ARG(0 <= leaf_lo && leaf_lo <= leaf_hi && leaf_hi <= nleaves, "bad leaf range");
+    Trace tr("from_pk");
     const int64_t base0 = leaf_base[leaf_lo];
     // WorkBlocks of the leaf range -> {base, ld, nr, nc, rows_at, cols_at, leaf}
     std::vector<int64_t> blocks;
@@ -463,6 +502,7 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                                        leaf_base[lf] - base0 + item_offset[k]});
             pm.insert(pm.end(), perms + 6 * k, perms + 6 * k + 6);
         }
+    tr.mark("gather");
     return gcabem_layout_create(mesh, leaf_base[leaf_hi] - base0, (int64_t)blocks.size() / 7,
                                 blocks.data(), npanels, panels, (int64_t)items.size() / 4,
                                 items.data(), pm.data(), out);
@@ -514,7 +554,8 @@ int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kap
     p->payload_len = L->payload_len;
     cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = p->payload.alloc(p->payload_len);
+    if (e == cudaSuccess) e = pool_init(mesh->device);
+    if (e == cudaSuccess) e = p->payload.alloc(p->payload_len, p->stream);
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         p->sq[c] = sq ? sq[c] : 0;
         if (p->sq[c] > 0 && L->case_at[c + 1] > L->case_at[c])

@@ -133,7 +133,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     // batches of consecutive clusters by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
-    if (batch_bytes <= 0) batch_bytes = int64_t(128) << 20;
+    if (batch_bytes <= 0) batch_bytes = int64_t(32) << 20;
     std::vector<int64_t> bstart{0};
     {
         int64_t acc = 0;

@@ -44,6 +44,35 @@ struct DevBuf {
     }
 };
 
+// Stream-ordered allocation from the device's default memory pool, whose
+// release threshold is raised once per device so freed blocks stay cached:
+// payloads of hundreds of MB are allocated and released per assembly call,
+// and cudaMalloc/cudaFree of that size cost milliseconds each.
+cudaError_t pool_init(int device);
+
+template <typename T>
+struct PoolBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    PoolBuf() = default;
+    PoolBuf(const PoolBuf &) = delete;
+    PoolBuf &operator=(const PoolBuf &) = delete;
+    ~PoolBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count, cudaStream_t stream) {
+        release();
+        n = count;
+        s = stream;
+        if (count == 0) return cudaSuccess;
+        return cudaMallocAsync(reinterpret_cast<void **>(&p), sizeof(T) * count, stream);
+    }
+};
+
 }  // namespace gcabem
 
 struct gcabem_mesh_s {

@@ -9,6 +9,9 @@
 // std::thread workers with a count / prefix-sum / fill pass so item order is
 // independent of the thread count.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -30,8 +33,13 @@ struct Packages {
     std::vector<uint8_t> flagged;       // L
     std::vector<int64_t> blk;           // B x 5 {leaf, r0, nr, c0, nc}
     std::vector<int64_t> blk_list;      // B
-    std::vector<int64_t> items;         // S x 6 {case, tri_x, tri_y, leaf, offset, block}
-    std::vector<uint8_t> perms;         // S x 6
+    // corrective items are counted at build time and written straight into
+    // the caller's arrays at fetch time (no intermediate copy)
+    std::vector<int64_t> fb;            // flagged blocks
+    std::vector<int64_t> cnt;           // item prefix sums over fb (F + 1)
+    std::vector<int64_t> triangles;     // nt x 3 copy for the fill pass
+    int nthreads = 1;
+    int64_t S = 0;
 };
 
 constexpr int64_t BYTES_PER_PAIR = 32;
@@ -67,6 +75,11 @@ inline void perm_for(const int64_t *v, const bool *shared, uint8_t *perm) {
         if (!shared[s]) perm[k++] = (uint8_t)s;
 }
 
+inline int count3(const int64_t *a, const int64_t *b) {
+    return (a[0] == b[0]) + (a[0] == b[1]) + (a[0] == b[2]) + (a[1] == b[0]) + (a[1] == b[1]) +
+           (a[1] == b[2]) + (a[2] == b[0]) + (a[2] == b[1]) + (a[2] == b[2]);
+}
+
 void parallel_for(int64_t n, int nthreads, const std::function<void(int64_t, int64_t)> &fn) {
     if (nthreads <= 1 || n < 1024) {
         fn(0, n);
@@ -98,6 +111,15 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
                           const int64_t *col_piv, int64_t maxsize, int nthreads,
                           gcabem_packages_t *out) {
     auto fail = [](const char *m) { return gcabem_internal_error(GCABEM_ERR_ARG, m); };
+    static const bool trace = std::getenv("GCABEM_TRACE") != nullptr;
+    auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (!trace) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[packages] %-10s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t_start).count());
+        t_start = now;
+    };
     if (!out) return fail("null output");
     *out = nullptr;
     if (maxsize < BYTES_PER_PAIR) return fail("maxsize smaller than one pair record (32 B)");
@@ -158,6 +180,7 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
         P.flagged[k] = touch ? 1 : 0;
     }
     P.payload_len = P.leaf_base[nleaves];
+    mark("leaves");
     // split + greedy lists
     P.blk.reserve(5 * nleaves);
     for (int64_t k = 0; k < nleaves; ++k) {
@@ -185,6 +208,7 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
         }
         P.nlists = B ? lid + 1 : 0;
     }
+    mark("split");
     // corrective scan of flagged blocks: count, prefix sum, fill
     std::vector<int64_t> fb;
     for (int64_t b = 0; b < B; ++b)
@@ -201,6 +225,7 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
         return P.panels[P.cols_at[q[0]] + q[3] + j];
     };
     bool bad_index = false;
+    bool three_shared = false;
     // vertex triples of one block's row/col panels, staged contiguously
     auto stage = [&](int64_t b, std::vector<int64_t> &ra, std::vector<int64_t> &ca,
                      std::vector<int64_t> &rt, std::vector<int64_t> &ct) {
@@ -223,11 +248,6 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
         }
         return true;
     };
-    auto count3 = [](const int64_t *a, const int64_t *b) {
-        return (a[0] == b[0]) + (a[0] == b[1]) + (a[0] == b[2]) + (a[1] == b[0]) +
-               (a[1] == b[1]) + (a[1] == b[2]) + (a[2] == b[0]) + (a[2] == b[1]) +
-               (a[2] == b[2]);
-    };
     parallel_for(F, nthreads, [&](int64_t lo, int64_t hi) {
         std::vector<int64_t> ra, ca, rt, ct;
         for (int64_t f = lo; f < hi; ++f) {
@@ -239,7 +259,11 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
             const int64_t nr = (int64_t)rt.size(), nc = (int64_t)ct.size();
             int64_t n = 0;
             for (int64_t i = 0; i < nr; ++i)
-                for (int64_t j = 0; j < nc; ++j) n += count3(&ra[3 * i], &ca[3 * j]) > 0;
+                for (int64_t j = 0; j < nc; ++j) {
+                    const int s = count3(&ra[3 * i], &ca[3 * j]);
+                    n += s > 0;
+                    if (s >= 3 && rt[i] != ct[j]) three_shared = true;
+                }
             cnt[f + 1] = n;
         }
     });
@@ -247,58 +271,17 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
         delete pk;
         return fail("panel index out of range");
     }
-    for (int64_t f = 0; f < F; ++f) cnt[f + 1] += cnt[f];
-    const int64_t S = cnt[F];
-    P.items.resize(6 * S);
-    P.perms.resize(6 * S);
-    bool three_shared = false;
-    parallel_for(F, nthreads, [&](int64_t lo, int64_t hi) {
-        std::vector<int64_t> ra, ca, rt, ct;
-        for (int64_t f = lo; f < hi; ++f) {
-            if (cnt[f + 1] == cnt[f]) continue;
-            const int64_t b = fb[f];
-            const int64_t leaf = P.blk[5 * b], r0 = P.blk[5 * b + 1], nr = P.blk[5 * b + 2];
-            const int64_t c0 = P.blk[5 * b + 3], nc = P.blk[5 * b + 4];
-            const int64_t ld = P.leaf_shape[2 * leaf + 1];
-            stage(b, ra, ca, rt, ct);
-            int64_t w = cnt[f];
-            for (int64_t i = 0; i < nr; ++i) {
-                const int64_t *va = &ra[3 * i];
-                for (int64_t j = 0; j < nc; ++j) {
-                    const int64_t *vb = &ca[3 * j];
-                    const int s = count3(va, vb);
-                    if (!s) continue;
-                    const int64_t tx = rt[i], ty = ct[j];
-                    int64_t *it = &P.items[6 * w];
-                    uint8_t *pm = &P.perms[6 * w];
-                    ++w;
-                    if (tx == ty) {
-                        it[0] = 3;
-                        for (int q = 0; q < 3; ++q) pm[q] = pm[3 + q] = (uint8_t)q;
-                    } else {
-                        if (s >= 3) three_shared = true;
-                        it[0] = std::min(s, 3);
-                        bool sa[3], sb[3];
-                        for (int q = 0; q < 3; ++q) {
-                            sa[q] = va[q] == vb[0] || va[q] == vb[1] || va[q] == vb[2];
-                            sb[q] = vb[q] == va[0] || vb[q] == va[1] || vb[q] == va[2];
-                        }
-                        perm_for(va, sa, pm);
-                        perm_for(vb, sb, pm + 3);
-                    }
-                    it[1] = tx;
-                    it[2] = ty;
-                    it[3] = leaf;
-                    it[4] = (r0 + i) * ld + c0 + j;
-                    it[5] = b;
-                }
-            }
-        }
-    });
     if (three_shared) {
         delete pk;
         return fail("distinct triangles share 3 vertices");
     }
+    mark("count");
+    for (int64_t f = 0; f < F; ++f) cnt[f + 1] += cnt[f];
+    P.S = cnt[F];
+    P.fb = std::move(fb);
+    P.cnt = std::move(cnt);
+    P.triangles.assign(triangles, triangles + 3 * nt);
+    P.nthreads = nthreads;
     *out = pk;
     return GCABEM_OK;
 }
@@ -311,7 +294,7 @@ int gcabem_packages_sizes(gcabem_packages_t pk, int64_t *sizes) {
     sizes[2] = (int64_t)pk->panels.size();
     sizes[3] = (int64_t)pk->blk.size() / 5;
     sizes[4] = pk->nlists;
-    sizes[5] = (int64_t)pk->items.size() / 6;
+    sizes[5] = pk->S;
     sizes[6] = sizes[7] = sizes[8] = 0;
     return GCABEM_OK;
 }
@@ -322,19 +305,81 @@ int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_s
                           uint8_t *flagged, int64_t *blocks, int64_t *blk_list, int64_t *items,
                           uint8_t *perms) {
     if (!pk) return GCABEM_ERR_ARG;
+    Packages &P = *pk;
     auto cp = [](void *dst, const void *src, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, src, bytes);
     };
-    cp(panels, pk->panels.data(), pk->panels.size() * 8);
-    cp(leaf_shape, pk->leaf_shape.data(), pk->leaf_shape.size() * 8);
-    cp(leaf_base, pk->leaf_base.data(), pk->leaf_base.size() * 8);
-    cp(rows_at, pk->rows_at.data(), pk->rows_at.size() * 8);
-    cp(cols_at, pk->cols_at.data(), pk->cols_at.size() * 8);
-    cp(flagged, pk->flagged.data(), pk->flagged.size());
-    cp(blocks, pk->blk.data(), pk->blk.size() * 8);
-    cp(blk_list, pk->blk_list.data(), pk->blk_list.size() * 8);
-    cp(items, pk->items.data(), pk->items.size() * 8);
-    cp(perms, pk->perms.data(), pk->perms.size());
+    cp(panels, P.panels.data(), P.panels.size() * 8);
+    cp(leaf_shape, P.leaf_shape.data(), P.leaf_shape.size() * 8);
+    cp(leaf_base, P.leaf_base.data(), P.leaf_base.size() * 8);
+    cp(rows_at, P.rows_at.data(), P.rows_at.size() * 8);
+    cp(cols_at, P.cols_at.data(), P.cols_at.size() * 8);
+    cp(flagged, P.flagged.data(), P.flagged.size());
+    // field-major: each field is one contiguous array on the Python side
+    const int64_t B = (int64_t)P.blk.size() / 5, S = P.S;
+    if (blocks)
+        for (int f = 0; f < 5; ++f)
+            for (int64_t b = 0; b < B; ++b) blocks[f * B + b] = P.blk[5 * b + f];
+    cp(blk_list, P.blk_list.data(), P.blk_list.size() * 8);
+    if (!items || !perms || S == 0) return GCABEM_OK;
+    // corrective items of the flagged blocks in argwhere (row-major) order,
+    // block after block; block f's items start at cnt[f]
+    const int64_t F = (int64_t)P.fb.size();
+    const int64_t *T = P.triangles.data();
+    int64_t *o_case = items, *o_tx = items + S, *o_ty = items + 2 * S, *o_leaf = items + 3 * S,
+            *o_off = items + 4 * S, *o_blk = items + 5 * S;
+    parallel_for(F, P.nthreads, [&](int64_t lo, int64_t hi) {
+        std::vector<int64_t> ra, ca, rt, ct;
+        for (int64_t f = lo; f < hi; ++f) {
+            if (P.cnt[f + 1] == P.cnt[f]) continue;
+            const int64_t b = P.fb[f];
+            const int64_t leaf = P.blk[5 * b], r0 = P.blk[5 * b + 1], nr = P.blk[5 * b + 2];
+            const int64_t c0 = P.blk[5 * b + 3], nc = P.blk[5 * b + 4];
+            const int64_t ld = P.leaf_shape[2 * leaf + 1];
+            ra.resize(3 * nr);
+            ca.resize(3 * nc);
+            rt.resize(nr);
+            ct.resize(nc);
+            for (int64_t i = 0; i < nr; ++i) {
+                rt[i] = P.panels[P.rows_at[leaf] + r0 + i];
+                std::memcpy(&ra[3 * i], T + 3 * rt[i], 24);
+            }
+            for (int64_t j = 0; j < nc; ++j) {
+                ct[j] = P.panels[P.cols_at[leaf] + c0 + j];
+                std::memcpy(&ca[3 * j], T + 3 * ct[j], 24);
+            }
+            int64_t w = P.cnt[f];
+            for (int64_t i = 0; i < nr; ++i) {
+                const int64_t *va = &ra[3 * i];
+                for (int64_t j = 0; j < nc; ++j) {
+                    const int64_t *vb = &ca[3 * j];
+                    const int s = count3(va, vb);
+                    if (!s) continue;
+                    const int64_t tx = rt[i], ty = ct[j];
+                    uint8_t *pm = perms + 6 * w;
+                    if (tx == ty) {
+                        o_case[w] = 3;
+                        for (int q = 0; q < 3; ++q) pm[q] = pm[3 + q] = (uint8_t)q;
+                    } else {
+                        o_case[w] = std::min(s, 3);
+                        bool sa[3], sb[3];
+                        for (int q = 0; q < 3; ++q) {
+                            sa[q] = va[q] == vb[0] || va[q] == vb[1] || va[q] == vb[2];
+                            sb[q] = vb[q] == va[0] || vb[q] == va[1] || vb[q] == va[2];
+                        }
+                        perm_for(va, sa, pm);
+                        perm_for(vb, sb, pm + 3);
+                    }
+                    o_tx[w] = tx;
+                    o_ty[w] = ty;
+                    o_leaf[w] = leaf;
+                    o_off[w] = (r0 + i) * ld + c0 + j;
+                    o_blk[w] = b;
+                    ++w;
+                }
+            }
+        }
+    });
     return GCABEM_OK;
 }
 

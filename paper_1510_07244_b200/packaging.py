@@ -223,24 +223,23 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         rows_at = np.empty(L, np.int64)
         cols_at = np.empty(L, np.int64)
         flagged = np.empty(L, np.uint8)
-        blocks = np.empty((nblk, 5), np.int64)
+        blocks = np.empty((5, nblk), np.int64)   # field-major
         blk_list = np.empty(nblk, np.int64)
-        items = np.empty((nit, 6), np.int64)
+        items = np.empty((6, nit), np.int64)
         perms = np.empty((nit, 6), np.uint8)
         nat.check(nat.lib().gcabem_packages_fetch(
             h, p(panels), p(shape), p(base), p(rows_at), p(cols_at), p(flagged), p(blocks),
             p(blk_list), p(items), p(perms)))
     finally:
         nat.lib().gcabem_packages_free(h)
-    col = np.ascontiguousarray
     return AssemblyPackages(
         maxsize=int(maxsize), leaf_ids=leaf_ids, leaf_shape=shape, leaf_base=base,
         panels=panels, leaf_rows_at=rows_at, leaf_cols_at=cols_at,
-        leaf_flagged=flagged.astype(bool), blk_leaf=col(blocks[:, 0]), blk_r0=col(blocks[:, 1]),
-        blk_nr=col(blocks[:, 2]), blk_c0=col(blocks[:, 3]), blk_nc=col(blocks[:, 4]),
-        blk_list=blk_list, n_disjoint_lists=nlists, item_case=items[:, 0].astype(np.int8),
-        item_tri_x=col(items[:, 1]), item_tri_y=col(items[:, 2]), item_leaf=col(items[:, 3]),
-        item_offset=col(items[:, 4]), item_src_block=col(items[:, 5]), perms=perms)
+        leaf_flagged=flagged.astype(bool), blk_leaf=blocks[0], blk_r0=blocks[1],
+        blk_nr=blocks[2], blk_c0=blocks[3], blk_nc=blocks[4], blk_list=blk_list,
+        n_disjoint_lists=nlists, item_case=items[0].astype(np.int8), item_tri_x=items[1],
+        item_tri_y=items[2], item_leaf=items[3], item_offset=items[4],
+        item_src_block=items[5], perms=perms)
 
 
 def shard_leaves(pk: AssemblyPackages, nshards: int, disjoint_q: int, singular_q=None):
