@@ -472,40 +472,116 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                                 const int64_t *item_offset, const uint8_t *perms,
                                 gcabem_layout_t *out) {
     GC_ARG(mesh && out, "null argument");
+    *out = nullptr;
     GC_ARG(0 <= leaf_lo && leaf_lo <= leaf_hi && leaf_hi <= nleaves, "bad leaf range");
+    GC_ARG(npanels >= 0 && nblocks >= 0 && nitems >= 0, "negative size");
+    GC_CUDA(cudaSetDevice(mesh->device));
     Trace tr("from_pk");
-    const int64_t base0 = leaf_base[leaf_lo];
-    // WorkBlocks of the leaf range -> {base, ld, nr, nc, rows_at, cols_at, leaf}
-    std::vector<int64_t> blocks;
-    blocks.reserve(7 * (size_t)nblocks);
+    const int64_t base0 = leaf_base[leaf_lo], plen = leaf_base[leaf_hi] - base0;
+    auto *L = new gcabem_layout_s();
+    L->mesh = mesh;
+    L->payload_len = plen;
+    auto fail = [&](const char *msg) {
+        delete L;
+        return set_error(GCABEM_ERR_ARG, msg);
+    };
+    // blocks of the leaf range -> descriptors, fixed-size tasks
+    std::vector<BlockDesc> bd;
+    bd.reserve((size_t)nblocks);
+    int64_t ntasks = 0, prev_leaf = -1;
     for (int64_t b = 0; b < nblocks; ++b) {
         const int64_t lf = blk_leaf[b];
-        GC_ARG(lf >= 0 && lf < nleaves, "block leaf out of range");
+        if (lf < 0 || lf >= nleaves || lf < prev_leaf) return fail("block leaves out of order");
+        prev_leaf = lf;
         if (lf < leaf_lo || lf >= leaf_hi) continue;
-        const int64_t ld = leaf_shape[2 * lf + 1];
-        blocks.insert(blocks.end(), {leaf_base[lf] - base0 + blk_r0[b] * ld + blk_c0[b], ld,
-                                     blk_nr[b], blk_nc[b], leaf_rows_at[lf] + blk_r0[b],
-                                     leaf_cols_at[lf] + blk_c0[b], lf});
+        const int64_t ld = leaf_shape[2 * lf + 1], nr = blk_nr[b], nc = blk_nc[b];
+        const int64_t base = leaf_base[lf] - base0 + blk_r0[b] * ld + blk_c0[b];
+        const int64_t ra = leaf_rows_at[lf] + blk_r0[b], ca = leaf_cols_at[lf] + blk_c0[b];
+        if (!(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31)) ||
+            !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
+            !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= plen)))
+            return fail("block descriptor out of bounds");
+        bd.push_back(BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0});
+        L->block_task_at.push_back(ntasks);
+        L->block_leaf.push_back(lf);
+        L->block_base.push_back(base);
+        L->block_pairs.push_back(nr * nc);
+        ntasks += (nr * nc + DISJOINT_TPB - 1) / DISJOINT_TPB;
     }
-    // singular items of the range, grouped by case (stable: generation order)
-    std::vector<int64_t> items;
-    std::vector<uint8_t> pm;
-    items.reserve(4 * (size_t)nitems);
-    pm.reserve(6 * (size_t)nitems);
-    for (int c = 1; c <= 3; ++c)
-        for (int64_t k = 0; k < nitems; ++k) {
-            if (item_case[k] != c) continue;
-            const int64_t lf = item_leaf[k];
-            GC_ARG(lf >= 0 && lf < nleaves, "item leaf out of range");
-            if (lf < leaf_lo || lf >= leaf_hi) continue;
-            items.insert(items.end(), {(int64_t)c, item_tri_x[k], item_tri_y[k],
-                                       leaf_base[lf] - base0 + item_offset[k]});
-            pm.insert(pm.end(), perms + 6 * k, perms + 6 * k + 6);
-        }
-    tr.mark("gather");
-    return gcabem_layout_create(mesh, leaf_base[leaf_hi] - base0, (int64_t)blocks.size() / 7,
-                                blocks.data(), npanels, panels, (int64_t)items.size() / 4,
-                                items.data(), pm.data(), out);
+    L->block_task_at.push_back(ntasks);
+    const int64_t B = (int64_t)bd.size();
+    std::vector<int2> tasks((size_t)ntasks);
+    for (int64_t b = 0; b < B; ++b) {
+        int64_t t = L->block_task_at[b];
+        for (int64_t k0 = 0; k0 < L->block_pairs[b]; k0 += DISJOINT_TPB)
+            tasks[t++] = make_int2((int)b, (int)k0);
+    }
+    std::vector<int32_t> pan((size_t)npanels);
+    for (int64_t k = 0; k < npanels; ++k) {
+        if (panels[k] < 0 || panels[k] >= mesh->nt) return fail("panel index out of range");
+        pan[k] = (int32_t)panels[k];
+    }
+    tr.mark("blocks+tasks");
+    // singular items of the range grouped by case (counting sort, stable)
+    int64_t counts[4] = {0, 0, 0, 0};
+    for (int64_t k = 0; k < nitems; ++k) {
+        const int c = item_case[k];
+        const int64_t lf = item_leaf[k];
+        if (c < 1 || c > 3 || lf < 0 || lf >= nleaves) return fail("bad singular item");
+        if (lf >= leaf_lo && lf < leaf_hi) counts[c]++;
+    }
+    L->case_at[0] = 0;
+    for (int c = 1; c <= 3; ++c) L->case_at[c] = L->case_at[c - 1] + counts[c];
+    const int64_t S = L->case_at[3];
+    std::vector<SingItem> si((size_t)S);
+    L->item_out.resize((size_t)S);
+    int64_t at[4] = {0, L->case_at[0], L->case_at[1], L->case_at[2]};
+    for (int64_t k = 0; k < nitems; ++k) {
+        const int64_t lf = item_leaf[k];
+        if (lf < leaf_lo || lf >= leaf_hi) continue;
+        const int c = item_case[k];
+        SingItem &it = si[at[c]];
+        it.out = leaf_base[lf] - base0 + item_offset[k];
+        it.tri_x = (int32_t)item_tri_x[k];
+        it.tri_y = (int32_t)item_tri_y[k];
+        const uint8_t *pm = perms + 6 * k;
+        it.px[0] = pm[0]; it.px[1] = pm[1]; it.px[2] = pm[2];
+        it.py[0] = pm[3]; it.py[1] = pm[4]; it.py[2] = pm[5];
+        it.pad[0] = it.pad[1] = 0;
+        bool ok = it.out >= 0 && it.out < plen && item_tri_x[k] >= 0 &&
+                  item_tri_x[k] < mesh->nt && item_tri_y[k] >= 0 && item_tri_y[k] < mesh->nt &&
+                  pm[0] < 3 && pm[1] < 3 && pm[2] < 3 && pm[3] < 3 && pm[4] < 3 && pm[5] < 3;
+        ok = ok && (c != 3 || (it.tri_x == it.tri_y && pm[0] == pm[3] && pm[1] == pm[4] &&
+                               pm[2] == pm[5]));
+        if (!ok) return fail("bad singular item (index, permutation or chart)");
+        L->item_out[at[c]] = it.out;
+        ++at[c];
+    }
+    // chunked execution looks items up by payload index inside a case: sort a
+    // case only if its generation order is not already ascending (it is,
+    // unless a flagged leaf was split by columns)
+    for (int c = 0; c < 3; ++c) {
+        const int64_t a0 = L->case_at[c], a1 = L->case_at[c + 1];
+        if (std::is_sorted(L->item_out.begin() + a0, L->item_out.begin() + a1)) continue;
+        std::stable_sort(si.begin() + a0, si.begin() + a1,
+                         [](const SingItem &x, const SingItem &y) { return x.out < y.out; });
+        for (int64_t q = a0; q < a1; ++q) L->item_out[q] = si[q].out;
+    }
+    tr.mark("items");
+    L->ntasks = ntasks;
+    cudaStream_t s = mesh->stream;
+    cudaError_t e = L->blocks.upload(bd.data(), bd.size(), s);
+    if (e == cudaSuccess) e = L->tasks.upload(tasks.data(), tasks.size(), s);
+    if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
+    if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    tr.mark("upload");
+    if (e != cudaSuccess) {
+        delete L;
+        GC_CUDA(e);
+    }
+    *out = L;
+    return GCABEM_OK;
 }
 
 int gcabem_layout_info(gcabem_layout_t L, int64_t *info8) {

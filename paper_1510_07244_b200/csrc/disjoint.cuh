@@ -50,7 +50,7 @@ static cudaError_t upload_tables(int n, const double *g, const double *gw) {
 constexpr double EXPANDED_MAX_RATIO = 1024.0;
 
 
-template <int N, int KIND, bool SMALL>
+template <int N, int KIND, int PH>
 __device__ __forceinline__ void disjoint_expanded(const double dO[3], const double e1x[3],
                                                   const double e2x[3], const double e1y[3],
                                                   const double e2y[3], const double n[3],
@@ -92,7 +92,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
                 const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
                 const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                point_accumulate<KIND, SMALL>(r2, dn, wy, kappa, phi0, in_re, in_im);
+                point_accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in_re, in_im);
             }
         }
         acc_re = fma(wx, in_re, acc_re);
@@ -100,7 +100,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
     }
 }
 
-template <int N, int KIND, bool SMALL>
+template <int N, int KIND, int PH>
 __device__ __forceinline__ void disjoint_direct(const double dO[3], const double e1x[3],
                                                 const double e2x[3], const double e1y[3],
                                                 const double e2y[3], const double n[3],
@@ -137,7 +137,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
                 const double dz = fma(-gc, uz[d], xo2);
                 const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                point_accumulate<KIND, SMALL>(r2, dn, wy, kappa, phi0, in_re, in_im);
+                point_accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in_re, in_im);
             }
         }
         acc_re = fma(wx, in_re, acc_re);
@@ -202,18 +202,31 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
     // Helmholtz phase about the centroid distance: |kappa r - kappa D| <= kappa (rx + ry)
     const double phi0 = HELM ? kappa * dcen : 0.0;
-    const bool small = HELM && kappa * (rx + ry) <= SMALL_PHASE_MAX;
-    if (small) {
-        if (expanded)
-            disjoint_expanded<N, KIND, true>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
-        else
-            disjoint_direct<N, KIND, true>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
-        rotate(phi0, re, im);
+    if constexpr (HELM) {
+        const double dmax = kappa * (rx + ry);
+        if (dmax <= TINY_PHASE_MAX) {
+            if (expanded)
+                disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+            else
+                disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+            rotate(phi0, re, im);
+        } else if (dmax <= SMALL_PHASE_MAX) {
+            if (expanded)
+                disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+            else
+                disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+            rotate(phi0, re, im);
+        } else {
+            if (expanded)
+                disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+            else
+                disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+        }
     } else {
         if (expanded)
-            disjoint_expanded<N, KIND, false>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+            disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
         else
-            disjoint_direct<N, KIND, false>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+            disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
     }
     finish_pair<KIND>(re, im, gx, gy, dst);
 }

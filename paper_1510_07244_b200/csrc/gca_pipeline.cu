@@ -60,7 +60,7 @@ struct Pinned {
 
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
-constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
+constexpr int SLOTS = 12;  // batches in flight: device output + pinned staging each
 struct Staging {
     Pinned host[SLOTS];
     DevBuf<double> out[SLOTS];
@@ -133,7 +133,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     // batches of consecutive clusters by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
-    if (batch_bytes <= 0) batch_bytes = int64_t(32) << 20;
+    if (batch_bytes <= 0) batch_bytes = int64_t(48) << 20;
     std::vector<int64_t> bstart{0};
     {
         int64_t acc = 0;
