@@ -239,7 +239,7 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
  * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
  * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
  * nthreads threads, overlapped with the next batch (batch_bytes of Green
- * matrix per launch, 12 launches in flight; 0 = 48 MiB). Results: gcabem_gca_sizes (rank per
+ * matrix per launch, 4 launches in flight; 0 = 32 MiB). Results: gcabem_gca_sizes (rank per
  * cluster, phase6 {device wait s, pipeline wall s, total s, batches, host
  * thread-seconds, threads}), then
  * gcabem_gca_fetch (row pivots concatenated; V blocks |t| x rank row-major,

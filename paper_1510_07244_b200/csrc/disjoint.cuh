@@ -161,20 +161,21 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const int2 task = tasks[blockIdx.x];
     const BlockDesc b = blocks[task.x];
     const int k = task.y + threadIdx.x;
-    if (k >= b.nr * b.nc) return;
-    const int i = k / b.nc;
-    const int j = k - i * b.nc;
+    // no early exit before the warp votes below: every lane of the CTA's
+    // four full warps reaches them
+    const bool inb = k < b.nr * b.nc;
+    const int i = inb ? k / b.nc : 0;
+    const int j = inb ? k - i * b.nc : 0;
     const int tx = panels[b.rows_at + i], ty = panels[b.cols_at + j];
     double2 *dst = payload + b.base + (int64_t)i * b.ld + j;
+    bool shared;
     {
         const int a0 = T[3 * tx], a1 = T[3 * tx + 1], a2 = T[3 * tx + 2];
         const int b0 = T[3 * ty], b1 = T[3 * ty + 1], b2 = T[3 * ty + 2];
-        if (a0 == b0 || a0 == b1 || a0 == b2 || a1 == b0 || a1 == b1 || a1 == b2 ||
-            a2 == b0 || a2 == b1 || a2 == b2) {
-            *dst = make_double2(0.0, 0.0);
-            return;
-        }
+        shared = a0 == b0 || a0 == b1 || a0 == b2 || a1 == b0 || a1 == b1 || a1 == b2 ||
+                 a2 == b0 || a2 == b1 || a2 == b2;
     }
+    const bool active = inb && !shared;
     const Chart *cx = charts + tx;
     const Chart *cy = charts + ty;
     double dO[3], e1x[3], e2x[3], e1y[3], e2y[3], n[3] = {0.0, 0.0, 0.0};
@@ -198,19 +199,30 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const double rmin = dcen - rx - ry;
     const double S = norm3(dO[0], dO[1], dO[2]) + cx->enorm + cy->enorm;
     double re = 0.0, im = 0.0;
-    const bool expanded = rmin > 0.0 && S * S <= EXPANDED_MAX_RATIO * rmin * rmin;
+    // evaluation form and phase tier are chosen per WARP (votes over the
+    // active lanes): a lane that needs the direct form or a longer phase
+    // polynomial takes its whole warp along instead of splitting it into
+    // serialised branches
+    const bool expanded =
+        __all_sync(0xffffffffu, !active || (rmin > 0.0 && S * S <= EXPANDED_MAX_RATIO * rmin * rmin));
     constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
     // Helmholtz phase about the centroid distance: |kappa r - kappa D| <= kappa (rx + ry)
     const double phi0 = HELM ? kappa * dcen : 0.0;
+    const double dmax = HELM && active ? kappa * (rx + ry) : 0.0;
+    const bool tiny = __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
+    const bool smallp = __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
+    if (!active) {
+        if (inb) *dst = make_double2(0.0, 0.0);
+        return;
+    }
     if constexpr (HELM) {
-        const double dmax = kappa * (rx + ry);
-        if (dmax <= TINY_PHASE_MAX) {
+        if (tiny) {
             if (expanded)
                 disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
             else
                 disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
             rotate(phi0, re, im);
-        } else if (dmax <= SMALL_PHASE_MAX) {
+        } else if (smallp) {
             if (expanded)
                 disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
             else

@@ -60,7 +60,7 @@ struct Pinned {
 
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
-constexpr int SLOTS = 12;  // batches in flight: device output + pinned staging each
+constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
 struct Staging {
     Pinned host[SLOTS];
     DevBuf<double> out[SLOTS];
@@ -133,7 +133,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     // batches of consecutive clusters by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
-    if (batch_bytes <= 0) batch_bytes = int64_t(48) << 20;
+    if (batch_bytes <= 0) batch_bytes = int64_t(32) << 20;
     std::vector<int64_t> bstart{0};
     {
         int64_t acc = 0;
@@ -234,8 +234,10 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         return r;
     };
 
-    // Workers pull clusters in batch order from one queue (no per-batch
-    // barrier: a long cluster only delays its own slot); the calling thread
+    // Workers pull clusters in batch order from one queue and copy their
+    // cluster's Green matrix out of the staging slot before working on it, so
+    // a slot is free again as soon as all its clusters are claimed (no
+    // per-batch barrier, no wait on the slowest cluster); the calling thread
     // issues batches into free slots and publishes each batch when its D2H
     // has landed.
     std::vector<int64_t> batch_of(ncl);
@@ -252,6 +254,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     std::atomic<int> err_code{0};
     std::vector<double> busy(nthreads, 0.0);
     auto worker = [&](int tid) {
+        std::vector<double> Aown;
         for (;;) {
             const int64_t c = next.fetch_add(1);
             if (c >= ncl) return;
@@ -264,8 +267,13 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
             const auto t0 = clk::now();
             const double *A = static_cast<const double *>(st.host[b % SLOTS].p) +
                               out_at[b][c - bstart[b]] * width;
-            const int rc = gca_operator(equation == 1, A, cl_size[c], nsrc, epsilon, G->rows[c],
-                                        G->V[c]);
+            Aown.assign(A, A + cl_size[c] * nsrc * width);
+            if (remaining[b].fetch_sub(1) == 1) {  // slot b % SLOTS drained
+                std::lock_guard<std::mutex> lk(mu);
+                cv.notify_all();
+            }
+            const int rc = gca_operator(equation == 1, Aown.data(), cl_size[c], nsrc, epsilon,
+                                        G->rows[c], G->V[c]);
             if (rc != 0) {
                 int64_t prev = err_cluster.load();
                 while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
@@ -273,10 +281,6 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                 if (c <= err_cluster.load()) err_code = rc;
             }
             busy[tid] += since(t0);
-            if (remaining[b].fetch_sub(1) == 1) {
-                std::lock_guard<std::mutex> lk(mu);
-                cv.notify_all();
-            }
         }
     };
     double t_wait = 0.0;
