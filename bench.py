@@ -69,14 +69,19 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            # NCCL needs one GPU per rank; fewer GPUs than ranks (a smoke test
+            # of the launch on one device) falls back to gloo for the barrier
+            # and the max -- neither is on the data path
+            ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+            backend = "nccl" if ngpu >= self.world else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend)
-            self.torch, self.dist = torch, dist
+            self.torch, self.dist, self.backend = torch, dist, backend
 
     def barrier(self):
         if self.world > 1:
@@ -86,7 +91,7 @@ class Dist:
         if self.world == 1:
             return x
         t = self.torch.tensor([x], dtype=self.torch.float64,
-                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+                              device="cuda" if self.backend == "nccl" else "cpu")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -292,7 +297,7 @@ def run_ours(args, cfg, dist, log):
     from paper_1510_07244_b200 import kernels, scheduler
     from paper_1510_07244_b200._native import require_device
 
-    device = dist.local if torch.cuda.device_count() > 1 else 0
+    device = dist.local % max(torch.cuda.device_count(), 1)
     require_device(device)
     torch.cuda.set_device(device)
     info = devmod.device_info(device)

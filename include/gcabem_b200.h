@@ -34,6 +34,7 @@ typedef struct gcabem_mesh_s *gcabem_mesh_t;
 typedef struct gcabem_plan_s *gcabem_plan_t;
 typedef struct gcabem_layout_s *gcabem_layout_t;
 typedef struct gcabem_gca_s *gcabem_gca_t;
+typedef struct gcabem_h2_s *gcabem_h2_t;
 
 /* ---- library / device ------------------------------------------------- */
 int gcabem_version(void);
@@ -262,6 +263,26 @@ int gcabem_gca_free(gcabem_gca_t g);
  * values; *rank receives the rank. */
 int gcabem_gca_operator(int is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
                         int64_t *rank, int64_t *rows, double *V);
+
+/* ---- device-resident compressed operator and matvec ------------------------
+ * Replaces h2.matvec (reference h2.py:49-71): y = sum over leaves of dense
+ * P x[s] and admissible V_t (P (V_s^T x[s])), in the permuted index space of
+ * the row / column trees (row_perm, col_perm). leaf_desc (nleaves x 7):
+ * {row_start, row_size, col_start, col_size, dense, row_op, col_op};
+ * leaf_base: payload offset per leaf (complex128 payload, payload_len);
+ * rowop_desc / colop_desc (n x 4): {cluster start, size, rank, offset in V};
+ * V: all bases stacked (complex128, v_len). The product is a sequence of
+ * gathers with a fixed summation order: bitwise reproducible. x, y host
+ * complex128; device_ms (nullable) gets the device time of the product. */
+int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *row_perm,
+                     const int64_t *col_perm, int64_t nleaves, const int64_t *leaf_desc,
+                     const int64_t *leaf_base, int64_t payload_len, const double *payload,
+                     int64_t nrowops, const int64_t *rowop_desc, int64_t ncolops,
+                     const int64_t *colop_desc, int64_t v_len, const double *V,
+                     gcabem_h2_t *out);
+int gcabem_h2_matvec(gcabem_h2_t h, const double *x, double *y, float *device_ms);
+int gcabem_h2_info(gcabem_h2_t h, double *bytes_per_product);
+int gcabem_h2_free(gcabem_h2_t h);
 
 /* ---- potential evaluation --------------------------------------------------
  * Replaces scheduler.potential_batch (scheduler.py:508-534): out (npts x nt,

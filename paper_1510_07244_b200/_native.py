@@ -85,6 +85,11 @@ _SIGS = {
     "gcabem_gca_fetch": ([_vp, _vp, _vp], _int),
     "gcabem_gca_free": ([_vp], _int),
     "gcabem_gca_operator": ([_int, _vp, _i64, _i64, _dbl, _vp, _vp, _vp], _int),
+    "gcabem_h2_create": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp,
+                          _i64, _vp, _i64, _vp, ctypes.POINTER(_vp)], _int),
+    "gcabem_h2_matvec": ([_vp, _vp, _vp, _vp], _int),
+    "gcabem_h2_info": ([_vp, _vp], _int),
+    "gcabem_h2_free": ([_vp], _int),
     "gcabem_aca_batch": ([_int, _i64, _vp, _i64, _vp, _dbl, _i64, _int, _vp, _vp, _vp, _vp],
                          _int),
 }

@@ -25,20 +25,6 @@ namespace {
 
 thread_local std::string g_error;
 
-// GCABEM_TRACE=1: stage timings of the host-side set-up paths on stderr
-struct Trace {
-    const char *who;
-    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-    bool on = std::getenv("GCABEM_TRACE") != nullptr;
-    explicit Trace(const char *w) : who(w) {}
-    void mark(const char *what) {
-        if (!on) return;
-        const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[%s] %-12s %8.2f ms\n", who, what,
-                     std::chrono::duration<double, std::milli>(now - t).count());
-        t = now;
-    }
-};
 
 int set_error(int code, const std::string &msg) {
     g_error = msg;

@@ -95,6 +95,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     const int64_t nsrc = 12 * (int64_t)m * m, ng = nsrc / 2;
     const int width = equation == 0 ? 1 : 2;
     const auto t_all = clk::now();
+    Trace tr("gca");
     auto *G = new gcabem_gca_s();
     G->is_complex = equation == 1;
     G->ncl = ncl;
@@ -131,6 +132,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
             boxes[c].half[k] = 0.5 * (hi[k] - lo[k]) + dh;
         }
     }
+    tr.mark("boxes");
     // batches of consecutive clusters by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
     if (batch_bytes <= 0) batch_bytes = int64_t(32) << 20;
@@ -167,6 +169,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         max_elems = std::max(max_elems, acc);
     }
     if (nthreads <= 0) nthreads = (int)std::max(1u, std::thread::hardware_concurrency());
+    tr.mark("batches");
 
     cudaError_t e = cudaSetDevice(mesh->device);
     cudaStream_t s = mesh->stream;
@@ -206,6 +209,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         if (e == cudaSuccess) e = st.host[k].reserve((size_t)(max_elems * width) * 8);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    tr.mark("uploads");
     cudaEvent_t done[SLOTS] = {};
     for (int k = 0; k < SLOTS && e == cudaSuccess; ++k)
         e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
@@ -312,6 +316,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         cv.notify_all();
     }
     for (auto &t : th) t.join();
+    tr.mark("pipeline");
     double t_host = 0.0;
     for (double x : busy) t_host += x;
     G->phase[1] = since(t_pipe);
@@ -333,6 +338,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         delete G;
         return gcabem_internal_error(GCABEM_ERR_GCA, msg.c_str());
     }
+    tr.mark("finish");
     G->phase[0] = t_wait;
     G->phase[2] = since(t_all);
     G->phase[3] = (double)nb;

@@ -3,7 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "gcabem_b200.h"
@@ -12,6 +15,21 @@
 int gcabem_internal_error(int code, const char *msg);  // api.cu
 
 namespace gcabem {
+
+// GCABEM_TRACE=1: stage timings of the host-side set-up paths on stderr
+struct Trace {
+    const char *who;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    bool on = std::getenv("GCABEM_TRACE") != nullptr;
+    explicit Trace(const char *w) : who(w) {}
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[%s] %-12s %8.2f ms\n", who, what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 template <typename T>
 struct DevBuf {

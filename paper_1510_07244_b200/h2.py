@@ -109,27 +109,137 @@ def _coupling_block(M: GCAMatrix, leaf) -> np.ndarray:
     return M.row_ops[leaf.row].V @ M.payloads[leaf.index] @ M.col_ops[leaf.col].V.T
 
 
+def _leaf_arrays(M: GCAMatrix):
+    """(L, 7) {row_start, row_size, col_start, col_size, dense, row_op, col_op}
+    in block-tree preorder plus the flat payload and per-leaf offsets, and
+    the operator tables {start, size, rank, v_offset} with their stacked V
+    (complex128). Operator indices follow sorted cluster ids."""
+    bt = M.block_tree
+    rt, ct = bt.row_tree, bt.col_tree
+    native = getattr(bt, "_native_leaves", None)
+    if native is not None:
+        arr = native[0]
+        lrow, lcol, ldense = arr[:, 0], arr[:, 1], arr[:, 2].astype(bool)
+        lids = bt.leaves._idx if hasattr(bt.leaves, "_idx") else \
+            np.array([l.index for l in bt.leaves], dtype=np.int64)
+    else:
+        lrow = np.array([l.row for l in bt.leaves], dtype=np.int64)
+        lcol = np.array([l.col for l in bt.leaves], dtype=np.int64)
+        ldense = np.array([l.kind == "dense" for l in bt.leaves], dtype=bool)
+        lids = np.array([l.index for l in bt.leaves], dtype=np.int64)
+    rstart = np.fromiter((n.start for n in rt.nodes), np.int64, len(rt.nodes))
+    rsize = np.fromiter((n.size for n in rt.nodes), np.int64, len(rt.nodes))
+    if ct is rt:
+        cstart, csize = rstart, rsize
+    else:
+        cstart = np.fromiter((n.start for n in ct.nodes), np.int64, len(ct.nodes))
+        csize = np.fromiter((n.size for n in ct.nodes), np.int64, len(ct.nodes))
+
+    def op_table(ops, start, size, used):
+        ids = sorted(c for c in ops if c in used)
+        pos = {c: k for k, c in enumerate(ids)}
+        desc = np.zeros((max(len(ids), 1), 4), np.int64)
+        Vs, off = [], 0
+        for k, c in enumerate(ids):
+            V = np.asarray(ops[c].V)
+            desc[k] = (start[c], size[c], V.shape[1], off)
+            Vs.append(np.ascontiguousarray(V, dtype=np.complex128).ravel())
+            off += V.size
+        return pos, desc, Vs
+    adm = ~ldense
+    rpos, rdesc, rV = op_table(M.row_ops, rstart, rsize, set(lrow[adm].tolist()))
+    cpos, cdesc, cV = op_table(M.col_ops, cstart, csize, set(lcol[adm].tolist()))
+    nr_v = sum(v.size for v in rV)
+    cdesc[:, 3] += nr_v
+    V = np.concatenate(rV + cV) if rV or cV else np.zeros(1, np.complex128)
+    L = lrow.size
+    desc = np.empty((L, 7), np.int64)
+    desc[:, 0], desc[:, 1] = rstart[lrow], rsize[lrow]
+    desc[:, 2], desc[:, 3] = cstart[lcol], csize[lcol]
+    desc[:, 4] = ldense
+    desc[:, 5] = [rpos.get(int(r), -1) if a_ else -1 for r, a_ in zip(lrow, adm)]
+    desc[:, 6] = [cpos.get(int(c), -1) if a_ else -1 for c, a_ in zip(lcol, adm)]
+    P = M.payloads
+    if isinstance(P, LeafPayloads) and not P._over and not P._gone and \
+            np.array_equal(P._ids, lids):
+        buf, base = P.buffer, P._base[:-1]
+    else:
+        parts = [np.ascontiguousarray(P[int(k)], dtype=np.complex128).ravel() for k in lids]
+        base = np.concatenate([[0], np.cumsum([q.size for q in parts])[:-1]]).astype(np.int64)
+        buf = np.concatenate(parts) if parts else np.zeros(1, np.complex128)
+    return (desc, np.ascontiguousarray(base, dtype=np.int64),
+            np.ascontiguousarray(buf, dtype=np.complex128), (rdesc, len(rpos)),
+            (cdesc, len(cpos)), np.ascontiguousarray(V))
+
+
+class DeviceH2:
+    """A GCAMatrix resident on one device (payload, bases, index plans) with a
+    deterministic matrix-vector product (C ABI gcabem_h2_*; csrc/h2_matvec.cu)."""
+
+    def __init__(self, M: GCAMatrix, device: int | None = None):
+        import ctypes
+        from . import _native as nat
+        from .pairquad import default_device
+        self.device = default_device() if device is None else device
+        nat.require_device(self.device)
+        desc, base, buf, (rdesc, nro), (cdesc, nco), V = _leaf_arrays(M)
+        rows, cols = M.shape
+        rp = np.ascontiguousarray(M.block_tree.row_tree.permutation, dtype=np.int64)
+        cp = np.ascontiguousarray(M.block_tree.col_tree.permutation, dtype=np.int64)
+        h = ctypes.c_void_p()
+        p = nat.ptr
+        nat.check(nat.lib().gcabem_h2_create(
+            self.device, rows, cols, p(rp), p(cp), desc.shape[0], p(desc), p(base), buf.size,
+            p(buf), nro, p(rdesc), nco, p(cdesc), V.size, p(V), ctypes.byref(h)))
+        self.handle = h.value
+        self.shape = (rows, cols)
+        bpp = ctypes.c_double()
+        nat.check(nat.lib().gcabem_h2_info(self.handle, ctypes.byref(bpp)))
+        self.bytes_per_product = bpp.value
+        self.last_device_ms = None
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        import ctypes
+        from . import _native as nat
+        x = np.asarray(x)
+        if x.shape != (self.shape[1],):
+            raise ValueError(f"dimension mismatch: operator {self.shape}, vector {x.shape}")
+        xc = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.empty(self.shape[0], dtype=np.complex128)
+        ms = ctypes.c_float()
+        nat.check(nat.lib().gcabem_h2_matvec(self.handle, nat.ptr(xc), nat.ptr(y),
+                                             ctypes.byref(ms)))
+        self.last_device_ms = ms.value
+        return y
+
+    def close(self) -> None:
+        from . import _native as nat
+        h, self.handle = getattr(self, "handle", None), None
+        if h and nat._lib is not None:
+            nat._lib.gcabem_h2_free(h)
+
+    def __del__(self):
+        self.close()
+
+
+def device_matrix(M: GCAMatrix, device: int | None = None) -> DeviceH2:
+    """The device-resident copy of M (built once, cached on M)."""
+    dev = getattr(M, "_device_h2", None)
+    if dev is None or (device is not None and dev.device != device):
+        dev = DeviceH2(M, device)
+        object.__setattr__(M, "_device_h2", dev)
+    return dev
+
+
 def matvec(M: GCAMatrix, x: np.ndarray) -> np.ndarray:
-    """y = M x, leaves accumulated in preorder (h2.py:49-71). The column-side
-    operator is conj(V_s), so its conjugate transpose is the plain V_s^T."""
+    """y = M x (h2.py:49-71) on the device: dense leaves P x[s], admissible
+    leaves V_t (P (V_s^T x[s])), summed in a fixed order (bitwise
+    reproducible). The matrix is uploaded once and cached on M."""
     rows, cols = M.shape
     x = np.asarray(x)
     if x.shape != (cols,):
         raise ValueError(f"dimension mismatch: operator {M.shape}, vector {x.shape}")
-    rt, ct = M.block_tree.row_tree, M.block_tree.col_tree
-    xp = np.asarray(x, dtype=np.complex128)[ct.permutation]
-    yp = np.zeros(rows, dtype=np.complex128)
-    for leaf in M.block_tree.leaves:
-        t, s = rt.nodes[leaf.row], ct.nodes[leaf.col]
-        xs = xp[s.start:s.start + s.size]
-        P = M.payloads[leaf.index]
-        if leaf.kind == "dense":
-            yp[t.start:t.start + t.size] += P @ xs
-        else:
-            yp[t.start:t.start + t.size] += M.row_ops[leaf.row].V @ (P @ (M.col_ops[leaf.col].V.T @ xs))
-    y = np.empty(rows, dtype=np.complex128)
-    y[rt.permutation] = yp
-    return y
+    return device_matrix(M).matvec(x)
 
 
 def to_dense(M: GCAMatrix, cap: int = DENSE_EXPANSION_CAP) -> np.ndarray:

@@ -292,3 +292,26 @@ def test_gcamat01_roundtrip_reference_files(tmp_path):
     import json
     ref = json.load(open(os.path.join(g, "golden.json")))["checksums"]
     assert h2.load(str(l3)).checksum() == ref["L3/laplace/single/2-3"]
+
+
+def test_device_matvec_tables_restate_reference_matvec():
+    """h2._leaf_arrays (the tables the device product runs on) drive the staged
+    algorithm of csrc/h2_matvec.cu to the reference leaf-loop product, on a
+    GCAMATO1 reference file (L3 Laplace SLP): no device needed."""
+    import gzip
+    import os
+    import h2_numpy
+    from paper_1510_07244_b200 import h2
+    g = os.path.join(os.path.dirname(__file__), "golden")
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "l3.gcamat")
+        with open(path, "wb") as fh:
+            fh.write(gzip.decompress(open(os.path.join(g, "L3_laplace_single_23.gcamat.gz"),
+                                          "rb").read()))
+        M = h2.load(path)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(M.shape[1]) + 1j * rng.standard_normal(M.shape[1])
+    ref = h2_numpy.matvec_reference(M, x)
+    got = h2_numpy.matvec_staged(M, x)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
