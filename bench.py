@@ -400,6 +400,29 @@ def run_ours(args, cfg, dist, log):
     e2e_pairs = (pk_total_pairs(pk, len(specs))) * dist.world
     e2e_value = e2e_pairs / e2e_dt
 
+    # solve-phase product on the device-resident operator (h2.matvec, SURVEY
+    # 8(f)2): HBM-bound, reported against the measured copy bandwidth
+    matvec_line = None
+    if not args.no_matvec:
+        from paper_1510_07244_b200 import h2
+        M = scheduler.run_assembly(m, bt, specs[0], ops, ops, params, cfg["orders"])
+        D = h2.DeviceH2(M, device)
+        rng = np.random.default_rng(0)
+        x = rng.standard_normal(M.shape[1]) + 1j * rng.standard_normal(M.shape[1])
+        for _ in range(3):
+            D.matvec(x)
+        mv_ms = []
+        for _ in range(10):
+            D.matvec(x)
+            mv_ms.append(D.last_device_ms)
+        mv = statistics.median(mv_ms)
+        hbm = _hbm_peak()
+        gbs = D.bytes_per_product / (mv * 1e-3) / 1e9
+        matvec_line = {"operator": specs[0].layer, "device_ms": mv,
+                       "bytes_per_product": int(D.bytes_per_product), "GB_s": gbs,
+                       "hbm_peak_GB_s": hbm, "frac": gbs / hbm if hbm else None}
+        D.close()
+        del M
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         import oracle
@@ -437,9 +460,20 @@ def run_ours(args, cfg, dist, log):
         "device": info["name"], "wall_s_timed": wall, "plan_upload_s": plan_s,
         "flops_per_step": {s.layer: f for s, f in zip(specs, fl)},
     }
+    if matvec_line is not None:
+        line["matvec"] = matvec_line
     if cpu is not None:
         line["cpu_baseline"] = cpu
     return line if dist.rank == 0 else None
+
+
+def _hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json, else the
+    profiling recipe's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6550.0
 
 
 def pk_total_pairs(pk, n_ops: int) -> int:
@@ -457,6 +491,7 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-matvec", action="store_true")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]
