@@ -35,6 +35,7 @@ typedef struct gcabem_plan_s *gcabem_plan_t;
 typedef struct gcabem_layout_s *gcabem_layout_t;
 typedef struct gcabem_gca_s *gcabem_gca_t;
 typedef struct gcabem_h2_s *gcabem_h2_t;
+typedef struct gcabem_p1_s *gcabem_p1_t;
 
 /* ---- library / device ------------------------------------------------- */
 int gcabem_version(void);
@@ -283,6 +284,33 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
 int gcabem_h2_matvec(gcabem_h2_t h, const double *x, double *y, float *device_ms);
 int gcabem_h2_info(gcabem_h2_t h, double *bytes_per_product);
 int gcabem_h2_free(gcabem_h2_t h);
+
+/* ---- piecewise-linear (P1) near field ------------------------------------
+ * Extension beyond the reference's P0 assembly (BASELINE
+ * config 4). Per near-field pair of the layout (build it from the dense
+ * leaves only), the 3 x 3 local matrix M[a][b] = g_x g_y sum_q w_q
+ * lambda_a(x_q) k lambda_b(y_q), lambda = (1 - s, s - t, t) -- the reference's
+ * integrate_pair(..., basis_x=lambda_a, basis_y=lambda_b) (quadrature.py:
+ * 223-271) -- in the triangles' stored vertex order; then the vertex x vertex
+ * near-field matrix (CSR, columns ascending) by a deterministic gather-sum
+ * (fixed contribution order, no atomics). create builds the scatter plan
+ * (device radix sort of the 9 entry keys); execute runs the local matrices
+ * and the gather; info {nv, nnz, pairs, singular items} + ms {local, gather};
+ * download: row_ptr (nv + 1), col (nnz), values (nnz complex128), local
+ * (nullable; pairs x 9 complex128, payload order). */
+int gcabem_p1_create(gcabem_layout_t layout, int equation, int layer, double kappa,
+                     int disjoint_n, const double *gauss_pts, const double *gauss_wts,
+                     const int64_t *sq, const double *const *srule, gcabem_p1_t *out);
+int gcabem_p1_execute(gcabem_p1_t p1);
+int gcabem_p1_info(gcabem_p1_t p1, int64_t *info4, float *ms2);
+int gcabem_p1_download(gcabem_p1_t p1, int64_t *row_ptr, int32_t *col, double *values,
+                       double *local);
+int gcabem_p1_destroy(gcabem_p1_t p1);
+/* P1 local matrices of caller-given pairs under any 4D rule (n x 9 complex128). */
+int gcabem_p1_batch(gcabem_mesh_t mesh, int equation, int layer, double kappa, int64_t n,
+                    const int64_t *tri_x, const int64_t *tri_y, const uint8_t *perm_x,
+                    const uint8_t *perm_y, int64_t nq, const double *xs, const double *ys,
+                    const double *w, double *out);
 
 /* ---- potential evaluation --------------------------------------------------
  * Replaces scheduler.potential_batch (scheduler.py:508-534): out (npts x nt,

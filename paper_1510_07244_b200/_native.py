@@ -90,6 +90,14 @@ _SIGS = {
     "gcabem_h2_matvec": ([_vp, _vp, _vp, _vp], _int),
     "gcabem_h2_info": ([_vp, _vp], _int),
     "gcabem_h2_free": ([_vp], _int),
+    "gcabem_p1_create": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)],
+                         _int),
+    "gcabem_p1_execute": ([_vp], _int),
+    "gcabem_p1_info": ([_vp, _vp, _vp], _int),
+    "gcabem_p1_download": ([_vp, _vp, _vp, _vp, _vp], _int),
+    "gcabem_p1_destroy": ([_vp], _int),
+    "gcabem_p1_batch": ([_vp, _int, _int, _dbl, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp,
+                         _vp], _int),
     "gcabem_aca_batch": ([_int, _i64, _vp, _i64, _vp, _dbl, _i64, _int, _vp, _vp, _vp, _vp],
                          _int),
 }

@@ -100,22 +100,6 @@ cudaError_t pool_init(int device) {
 int gcabem_internal_error(int code, const char *msg) { return set_error(code, msg); }
 
 
-// Device layout of one package set: uploaded once, shared by every plan
-// (operator) assembled from the same packages (e.g. SLP and DLP).
-struct gcabem_layout_s {
-    gcabem_mesh_t mesh = nullptr;
-    int64_t payload_len = 0;
-    DevBuf<BlockDesc> blocks;
-    DevBuf<int2> tasks;
-    int64_t ntasks = 0;
-    DevBuf<int32_t> panels;
-    DevBuf<SingItem> items;
-    int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])
-    // host copies for chunked execution
-    std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
-    std::atomic<int> refs{1};
-};
-
 struct gcabem_plan_s {
     gcabem_mesh_t mesh = nullptr;
     gcabem_layout_t L = nullptr;

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <vector>
 
 #include "gcabem_b200.h"
@@ -100,6 +101,22 @@ struct gcabem_mesh_s {
     gcabem::DevBuf<double> V;
     gcabem::DevBuf<int32_t> T;
     gcabem::DevBuf<gcabem::Chart> charts;
+};
+
+// Device layout of one package set: uploaded once, shared by every plan
+// (operator) assembled from the same packages (e.g. SLP and DLP).
+struct gcabem_layout_s {
+    gcabem_mesh_t mesh = nullptr;
+    int64_t payload_len = 0;
+    gcabem::DevBuf<gcabem::BlockDesc> blocks;
+    gcabem::DevBuf<int2> tasks;
+    int64_t ntasks = 0;
+    gcabem::DevBuf<int32_t> panels;
+    gcabem::DevBuf<gcabem::SingItem> items;
+    int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])
+    // host copies for chunked execution
+    std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
+    std::atomic<int> refs{1};
 };
 
 // Dense host kernels of the GCA operator construction (aca.cpp).

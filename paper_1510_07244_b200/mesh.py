@@ -164,6 +164,85 @@ def build_sphere_mesh(level: int) -> SurfaceMesh:
     return make_surface_mesh(V, T)
 
 
+def _smoothstep(x):
+    x = np.clip(x, 0.0, 1.0)
+    return x * x * (3.0 - 2.0 * x)
+
+
+def build_crankshaft_mesh(num_triangles: int = 65536, seed: int = 0,
+                          n_theta: int | None = None) -> SurfaceMesh:
+    """Closed, outward-oriented crankshaft-like surface (BASELINE config 4;
+    the reference has no such generator): a tube along z with
+    a stepped radius profile -- main journals, crank webs, offset crank pins
+    at seeded throw angles -- smooth transitions, and fan caps at both ends.
+    Deterministic for a given (num_triangles, seed).
+
+    num_triangles = 2 n_theta (n_z + 1): n_theta ring vertices, n_z quad
+    rows (two triangles each) plus two fans of n_theta triangles. With the
+    default n_theta = 128, 65536 triangles give n_z = 255."""
+    if n_theta is None:
+        n_theta = 128 if num_triangles >= 4096 else 16
+    if n_theta < 3 or num_triangles % (2 * n_theta) or num_triangles // (2 * n_theta) < 2:
+        raise MeshError(f"num_triangles must be 2 * n_theta * (n_z + 1) with n_z >= 1 "
+                        f"(n_theta = {n_theta})")
+    n_z = num_triangles // (2 * n_theta) - 1
+    rng = np.random.default_rng(seed)
+    # segments along z: J (journal) W (web) P (pin) W J W P W J ... ending in J
+    n_throws = 4
+    kinds = ["J"]
+    for _ in range(n_throws):
+        kinds += ["W", "P", "W", "J"]
+    seg_len = {"J": 0.30, "W": 0.10, "P": 0.26}
+    lengths = np.array([seg_len[k] * (1.0 + 0.1 * rng.uniform(-1.0, 1.0)) for k in kinds])
+    z_edges = np.concatenate([[0.0], np.cumsum(lengths)])
+    radius = {"J": 0.22, "W": 0.55, "P": 0.20}
+    throw = 0.32
+    angles = rng.permutation(n_throws) * (2.0 * np.pi / n_throws) + rng.uniform(-0.2, 0.2,
+                                                                               n_throws)
+    # vertex rings on a z grid; radius and centre blend smoothly at segment ends
+    z = np.linspace(0.0, z_edges[-1], n_z + 1)
+    r = np.zeros_like(z)
+    cx = np.zeros_like(z)
+    cy = np.zeros_like(z)
+    width = 0.03
+    pin = 0
+    for k, kind in enumerate(kinds):
+        w_in = _smoothstep((z - z_edges[k] + width) / (2.0 * width))
+        w_out = 1.0 - _smoothstep((z - z_edges[k + 1] + width) / (2.0 * width))
+        w = w_in * w_out
+        r += w * radius[kind]
+        if kind == "P":
+            cx += w * throw * np.cos(angles[pin])
+            cy += w * throw * np.sin(angles[pin])
+        if kind == "W":  # webs carry half the throw of the adjacent pin
+            a = angles[min(pin, n_throws - 1)]
+            cx += w * 0.5 * throw * np.cos(a)
+            cy += w * 0.5 * throw * np.sin(a)
+        if kind == "P":
+            pin += 1
+    r = np.maximum(r, 0.12)
+    theta = np.arange(n_theta) * (2.0 * np.pi / n_theta)
+    V = np.empty(((n_z + 1) * n_theta + 2, 3))
+    ring = np.arange(n_theta)
+    for i in range(n_z + 1):
+        V[i * n_theta + ring, 0] = cx[i] + r[i] * np.cos(theta)
+        V[i * n_theta + ring, 1] = cy[i] + r[i] * np.sin(theta)
+        V[i * n_theta + ring, 2] = z[i]
+    bottom, top = (n_z + 1) * n_theta, (n_z + 1) * n_theta + 1
+    V[bottom] = (cx[0], cy[0], z[0])
+    V[top] = (cx[-1], cy[-1], z[-1])
+    T = []
+    nxt = (ring + 1) % n_theta
+    for i in range(n_z):
+        a, b = i * n_theta + ring, i * n_theta + nxt
+        c, d = (i + 1) * n_theta + nxt, (i + 1) * n_theta + ring
+        T.append(np.stack([a, b, c], axis=1))
+        T.append(np.stack([a, c, d], axis=1))
+    T.append(np.stack([np.full(n_theta, bottom), nxt, ring], axis=1))
+    T.append(np.stack([np.full(n_theta, top), n_z * n_theta + ring, n_z * n_theta + nxt], axis=1))
+    return make_surface_mesh(V, np.concatenate(T).astype(np.int64))
+
+
 def chart(mesh: SurfaceMesh, tri: int, perm=(0, 1, 2)) -> AffineChart:
     """Chart of one triangle with vertices in order `perm` (mesh.py:192-204)."""
     if not 0 <= tri < mesh.num_triangles:

@@ -344,6 +344,61 @@ def gen_potential_and_dump():
     os.remove(tmp)
 
 
+def gen_p1():
+    """P1 local matrices M[a][b] = integrate_pair(chart_x, chart_y, spec, rule,
+    normal_y, basis_x=lambda_a, basis_y=lambda_b) (quadrature.py:223-271) on a
+    small crankshaft surface (geometry from our generator, everything else
+    from the reference), stored in the triangles' stored vertex order."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1510_07244_b200.mesh import build_crankshaft_mesh
+    g = build_crankshaft_mesh(2048, seed=1)
+    m = mesh.make_surface_mesh(g.vertices, g.triangles)
+    rng = np.random.default_rng(11)
+    tri = m.triangles
+    nt = m.num_triangles
+    shared = np.zeros((nt, nt), dtype=np.int8)
+    for a_ in range(3):
+        for b_ in range(3):
+            shared += (tri[:, a_][:, None] == tri[:, b_][None, :]).astype(np.int8)
+    mid = m.midpoints()
+    picks = {}
+    disj = np.argwhere(shared == 0)
+    d = np.linalg.norm(mid[disj[:, 0]] - mid[disj[:, 1]], axis=1)
+    near = disj[np.argsort(d, kind="stable")[rng.choice(3000, 24, replace=False)]]
+    far = disj[rng.choice(len(disj), 16, replace=False)]
+    picks["disjoint"] = np.concatenate([near, far])
+    for case, cnt in (("vertex", 1), ("edge", 2)):
+        cand = np.argwhere(shared == cnt)
+        picks[case] = cand[rng.choice(len(cand), 32, replace=False)]
+    ids = rng.choice(nt, 24, replace=False)
+    picks["identical"] = np.stack([ids, ids], axis=1)
+    lam = [lambda p: 1.0 - p[:, 0], lambda p: p[:, 0] - p[:, 1], lambda p: p[:, 1]]
+    out = {"vertices": m.vertices, "triangles": m.triangles}
+    for case, pairs in picks.items():
+        out[f"pairs_{case}"] = pairs
+        n = 3 if case == "disjoint" else 5
+        rule = quadrature.build_rule(case, n)
+        perms = []
+        for name in ("L-SLP", "L-DLP", "H-SLP", "H-DLP"):
+            spec = SPECS[name]
+            vals = np.zeros((len(pairs), 3, 3), dtype=np.complex128)
+            for k, (tx, ty) in enumerate(pairs):
+                cls = quadrature.classify_pair(m, int(tx), int(ty))
+                assert cls.case == case
+                if name == "L-SLP":
+                    perms.append(list(cls.perm_x) + list(cls.perm_y))
+                cx = mesh.chart(m, int(tx), cls.perm_x)
+                cy = mesh.chart(m, int(ty), cls.perm_y)
+                for a_ in range(3):
+                    for b_ in range(3):
+                        v = quadrature.integrate_pair(cx, cy, spec, rule, m.normals[int(ty)],
+                                                      basis_x=lam[a_], basis_y=lam[b_])
+                        vals[k, cls.perm_x[a_], cls.perm_y[b_]] = v
+            out[f"p1_{case}_{name}"] = vals
+        out[f"perms_{case}"] = np.array(perms, dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "p1_crank.npz"), **out)
+
+
 def main():
     meta = {"reference": "gcabem " + getattr(gcabem, "__version__", "0.1.0"),
             "numpy": np.__version__}
@@ -359,10 +414,14 @@ def main():
     gen_gca(meta)
     gen_assembly(meta)
     gen_potential_and_dump()
+    gen_p1()
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
     print("ok")
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["p1"]:
+        gen_p1()
+        sys.exit(0)
     sys.exit(main())

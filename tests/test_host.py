@@ -315,3 +315,40 @@ def test_device_matvec_tables_restate_reference_matvec():
     ref = h2_numpy.matvec_reference(M, x)
     got = h2_numpy.matvec_staged(M, x)
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_crankshaft_mesh_closed_oriented_deterministic():
+    m = mesh.build_crankshaft_mesh(65536, seed=0)
+    assert m.num_triangles == 65536
+    e = np.concatenate([m.triangles[:, [0, 1]], m.triangles[:, [1, 2]], m.triangles[:, [2, 0]]])
+    key = e[:, 0] * m.num_vertices + e[:, 1]
+    rev = e[:, 1] * m.num_vertices + e[:, 0]
+    assert np.unique(key).size == key.size              # each directed edge once
+    assert np.array_equal(np.sort(key), np.sort(rev))   # closed, consistently oriented
+    assert m.num_vertices - key.size // 2 + m.num_triangles == 2
+    V = m.vertices[m.triangles]
+    assert np.einsum("ij,ij->i", V[:, 0], np.cross(V[:, 1], V[:, 2])).sum() > 0  # outward
+    m2 = mesh.build_crankshaft_mesh(65536, seed=0)
+    assert np.array_equal(m.vertices, m2.vertices)
+    assert not np.array_equal(m.vertices, mesh.build_crankshaft_mesh(65536, seed=1).vertices)
+
+
+def test_p1_numpy_restatement_matches_reference_golden(gload):
+    """The test-side P1 oracle reproduces the reference's integrate_pair with
+    P1 bases (golden p1_crank.npz, generated from the reference)."""
+    import p1_numpy
+    from paper_1510_07244_b200 import kernels as K, quadrature as Q
+    g = gload("p1_crank.npz")
+    m = mesh.make_surface_mesh(g["vertices"], g["triangles"])
+    specs = {"L-SLP": K.KernelSpec("laplace", "single"), "L-DLP": K.KernelSpec("laplace", "double"),
+             "H-SLP": K.KernelSpec("helmholtz", "single", 4.0),
+             "H-DLP": K.KernelSpec("helmholtz", "double", 4.0)}
+    for case in ("disjoint", "vertex", "edge", "identical"):
+        pairs, perms = g[f"pairs_{case}"], g[f"perms_{case}"]
+        rule = Q.build_rule(case, 3 if case == "disjoint" else 5)
+        for name, spec in specs.items():
+            ref = g[f"p1_{case}_{name}"]
+            for k, (tx, ty) in enumerate(pairs):
+                got = p1_numpy.local_matrix(m, spec, rule, tx, ty, perms[k, :3], perms[k, 3:])
+                scale = np.max(np.abs(ref[k]))
+                assert np.max(np.abs(got - ref[k])) <= 1e-12 * scale, (case, name, k)
