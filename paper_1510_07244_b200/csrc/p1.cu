@@ -416,6 +416,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     const int64_t P = L->payload_len;
     if (9 * P >= (int64_t(1) << 31))
         return gcabem_internal_error(GCABEM_ERR_ARG, "P1 near field too large for one plan");
+    Trace tr("p1_create");
     auto *p = new gcabem_p1_s();
     p->L = L;
     ++L->refs;
@@ -440,6 +441,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
     if (e == cudaSuccess) e = pool_init(mesh->device);
     if (e == cudaSuccess) e = p->local.alloc(9 * P, s);
+    tr.mark("rules+local");
     // scatter plan: sort the 9 P entry keys, run-length encode, row pointers
     const int64_t E = 9 * P;
     DevBuf<uint64_t> keys, keys_out, ukeys;
@@ -481,6 +483,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     int64_t nnz = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&nnz, d_nnz.p, 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    tr.mark("sort+rle");
     if (E == 0) nnz = 0;
     // segment offsets: exclusive scan of the run lengths (nnz + 1 entries;
     // counts[nnz] is zeroed first so the last offset is the total)
@@ -498,6 +501,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    tr.mark("csr");
     if (e != cudaSuccess) {
         gcabem_p1_destroy(p);
         return gcabem_internal_error(GCABEM_ERR_CUDA,

@@ -395,11 +395,18 @@ def test_p1_local_matrices_vs_reference_golden(gload, case):
     m = mesh.make_surface_mesh(g["vertices"], g["triangles"])
     pairs, perms = g[f"pairs_{case}"], g[f"perms_{case}"]
     rule = Q.build_rule(case, 3 if case == "disjoint" else 5)
-    for name, spec in SPECS.items():
+    for name, (eq, layer, kappa) in SPECS.items():
+        spec = kernels.KernelSpec(eq, layer, kappa)
         got = p1.local_matrices(m, spec, rule, pairs[:, 0], pairs[:, 1], perms[:, :3],
                                 perms[:, 3:])
         ref = g[f"p1_{case}_{name}"]
         scale = np.max(np.abs(ref), axis=(1, 2))
+        if layer == "double":
+            # P2 rule: coplanar pairs (flat parts of the crankshaft) have DLP
+            # entries that are pure roundoff in the reference (~1e-21); they
+            # are compared on the pair's single-layer scale
+            slp = g[f"p1_{case}_{name[0]}-SLP"]
+            scale = np.maximum(scale, np.max(np.abs(slp), axis=(1, 2)))
         err = np.max(np.abs(got - ref), axis=(1, 2))
         assert np.all(err <= 1e-12 * scale), (name, float(np.max(err / scale)))
 
@@ -408,11 +415,11 @@ def test_p1_local_matrices_vs_reference_golden(gload, case):
                                             ("helmholtz", "double", 4.0)])
 def test_p1_near_field_scatter_vs_oracle(eq, layer, kappa):
     """P1 near-field matrix (device local matrices + deterministic gather
-    scatter) vs the numpy oracle's np.add.at scatter on a 2048-triangle
+    scatter) vs the numpy oracle's np.add.at scatter on a 1024-triangle
     crankshaft; row-scaled 1e-12; two executions bitwise identical."""
     import p1_numpy
     from paper_1510_07244_b200 import p1
-    m = mesh.build_crankshaft_mesh(2048, seed=1)
+    m = mesh.build_crankshaft_mesh(1024, seed=1, n_theta=16)
     t = cluster.build_cluster_tree(m, 16)
     bt = cluster.build_block_tree(t, t, 2.0)
     spec = kernels.KernelSpec(eq, layer, kappa)
