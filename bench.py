@@ -55,6 +55,10 @@ CONFIGS = {
                orders=(3, 5), near_only=False,
                workload="C3: Helmholtz kappa=4 SLP+DLP full H2 setup, sphere 131072 "
                         "triangles, orders 3/5"),
+    "c5": dict(level=8, equation="helmholtz", kappa=4.0, layers=("single", "double"),
+               orders=(3, 3), near_only=False,
+               workload="C5: Helmholtz kappa=4 SLP+DLP scaling sweep, sphere 524288 triangles, "
+                        "disjoint and singular order n swept together (--order)"),
     "c4": dict(crankshaft=65536, equation="helmholtz", kappa=4.0, layers=("double",),
                orders=(3, 5), near_only=True, p1=True,
                workload="C4: Helmholtz kappa=4 DLP, piecewise-linear basis, crankshaft-like "
@@ -470,12 +474,13 @@ def run_ours(args, cfg, dist, log):
     params = scheduler.SchedulerParams(backends=(scheduler.Backend("cuda", devices=(device,)),))
     h2d = sum(p.h2d_bytes for p in plans)
     d2h = sum(p.payload_len * 16 for p in plans)
-    warm = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"])
-            for s in specs]  # warm the path and the pinned pool (both buffers live at once)
-    del warm
     setup_first = None
     e2e_phases = []
-    for k in range(max(1, args.e2e_steps)):
+    if args.e2e_steps > 0:
+        warm = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"])
+                for s in specs]  # warm the path and the pinned pool (both buffers live)
+        del warm
+    for k in range(args.e2e_steps):
         dist.barrier()
         scheduler.clear_package_cache()  # every step packages once (shared by SLP/DLP)
         t0 = time.perf_counter()
@@ -493,9 +498,9 @@ def run_ours(args, cfg, dist, log):
         log(f"e2e step {k}: {dt:.4f} s (free {time.perf_counter() - t_del:.4f} s) {e2e_phases}")
         if setup_first is None:
             setup_first = dt
-    e2e_dt = dist.max(statistics.median(e2e_t))
+    e2e_dt = dist.max(statistics.median(e2e_t)) if e2e_t else None
     e2e_pairs = (pk_total_pairs(pk, len(specs))) * dist.world
-    e2e_value = e2e_pairs / e2e_dt
+    e2e_value = e2e_pairs / e2e_dt if e2e_dt else None
 
     # solve-phase product on the device-resident operator (h2.matvec, SURVEY
     # 8(f)2): HBM-bound, reported against the measured copy bandwidth
@@ -532,8 +537,9 @@ def run_ours(args, cfg, dist, log):
     h2_setup = {"trees_s": round(setup_t["trees_s"], 3), "gca_s": round(setup_t["gca_s"], 3),
                 "gca_phases_s": {k: round(v, 4) if isinstance(v, float) else v
                                  for k, v in setup_t.get("gca_phases", {}).items()},
-                "assembly_slp_dlp_s": round(setup_first, 4),
-                "total_s": round(setup_t["trees_s"] + setup_t["gca_s"] + setup_first, 3)}
+                "assembly_slp_dlp_s": round(setup_first, 4) if setup_first else None,
+                "total_s": round(setup_t["trees_s"] + setup_t["gca_s"] + setup_first, 3)
+                if setup_first else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -589,9 +595,14 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--order", type=int, default=None,
+                    help="override the quadrature orders (disjoint n = singular n), e.g. C5")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.order is not None:
+        cfg["orders"] = (args.order, args.order)
+        cfg["workload"] += f", orders {args.order}/{args.order}"
     dist = Dist()
 
     def log(msg):
