@@ -50,48 +50,75 @@ __device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
     return acc;
 }
 
-// one thread per (item, component): out[out_at[it] + k] = sum_i M[i, k] v[v_at + i]
-// for k < width (M row-major nrows x width) -- used for xs_s = V_s^T xp[s]
-__global__ void tmatvec_kernel(const int64_t *__restrict__ task_item,
-                               const int32_t *__restrict__ task_k0, int64_t ntasks,
-                               const int64_t *__restrict__ m_at, const int32_t *__restrict__ nrows,
-                               const int32_t *__restrict__ width,
-                               const int64_t *__restrict__ v_at, const int64_t *__restrict__ out_at,
-                               const double2 *__restrict__ M, const double2 *__restrict__ v,
-                               double2 *__restrict__ out) {
+// xs = M^T v for one item per CTA (M row-major nrows x width, width <=
+// TM_MAX): warp w takes rows w, w + 4, ...; lane l owns components l, l + 32,
+// ... (a row read is coalesced); the four warps' partial sums are added in
+// warp order at the end -- fixed association, deterministic.
+constexpr int TM_MAX = 128;
+__global__ void __launch_bounds__(MV_TPB)
+tmatvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_k0,
+               int64_t ntasks, const int64_t *__restrict__ m_at,
+               const int32_t *__restrict__ nrows, const int32_t *__restrict__ width,
+               const int64_t *__restrict__ v_at, const int64_t *__restrict__ out_at,
+               const double2 *__restrict__ M, const double2 *__restrict__ v,
+               double2 *__restrict__ out) {
+    __shared__ double2 part[MV_TPB / 32][TM_MAX];
     const int64_t t = blockIdx.x;
     if (t >= ntasks) return;
     const int64_t it = task_item[t];
-    const int k = task_k0[t] + threadIdx.x;
-    const int w = width[it];
-    if (k >= w) return;
-    const double2 *Mi = M + m_at[it] + k;
+    const int w = width[it], n = nrows[it];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double2 *Mi = M + m_at[it];
     const double2 *vi = v + v_at[it];
-    double2 acc = make_double2(0.0, 0.0);
-    const int n = nrows[it];
-    for (int i = 0; i < n; ++i) acc = cmac(acc, Mi[(int64_t)i * w], vi[i]);
-    out[out_at[it] + k] = acc;
+    double2 acc[TM_MAX / 32];
+#pragma unroll
+    for (int q = 0; q < TM_MAX / 32; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int i = warp; i < n; i += MV_TPB / 32) {
+        const double2 x = vi[i];
+#pragma unroll
+        for (int q = 0; q < TM_MAX / 32; ++q)
+            if (lane + 32 * q < w) acc[q] = cmac(acc[q], Mi[(int64_t)i * w + lane + 32 * q], x);
+    }
+#pragma unroll
+    for (int q = 0; q < TM_MAX / 32; ++q) part[warp][lane + 32 * q] = acc[q];
+    __syncthreads();
+    for (int k = threadIdx.x; k < w; k += MV_TPB) {
+        double2 s = part[0][k];
+#pragma unroll
+        for (int q = 1; q < MV_TPB / 32; ++q) {
+            s.x += part[q][k].x;
+            s.y += part[q][k].y;
+        }
+        out[out_at[it] + k] = s;
+    }
 }
 
-// one thread per (item, row): out[out_at[it] + r] = sum_j M[r, j] v[v_at + j]
-// (M row-major rows x ncols) -- dense leaves P xp[s], admissible P xs_s, V_t z_t
-__global__ void matvec_kernel(const int64_t *__restrict__ task_item,
-                              const int32_t *__restrict__ task_r0, int64_t ntasks,
-                              const int64_t *__restrict__ m_at, const int32_t *__restrict__ rows,
-                              const int32_t *__restrict__ cols, const int64_t *__restrict__ v_at,
-                              const int64_t *__restrict__ out_at, const double2 *__restrict__ M,
-                              const double2 *__restrict__ v, double2 *__restrict__ out) {
+// out[out_at[it] + r] = sum_j M[r, j] v[v_at + j] (M row-major rows x cols):
+// one WARP per row, lanes stride the columns (coalesced row reads), then a
+// fixed butterfly reduction -- deterministic. A task covers 4 rows.
+__global__ void __launch_bounds__(MV_TPB)
+matvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_r0,
+              int64_t ntasks, const int64_t *__restrict__ m_at, const int32_t *__restrict__ rows,
+              const int32_t *__restrict__ cols, const int64_t *__restrict__ v_at,
+              const int64_t *__restrict__ out_at, const double2 *__restrict__ M,
+              const double2 *__restrict__ v, double2 *__restrict__ out) {
     const int64_t t = blockIdx.x;
     if (t >= ntasks) return;
     const int64_t it = task_item[t];
-    const int r = task_r0[t] + threadIdx.x;
-    if (r >= rows[it]) return;
+    const int r = task_r0[t] + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows[it]) return;  // whole warp leaves together
     const int nc = cols[it];
     const double2 *Mr = M + m_at[it] + (int64_t)r * nc;
     const double2 *vv = v + v_at[it];
     double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j < nc; ++j) acc = cmac(acc, Mr[j], vv[j]);
-    out[out_at[it] + r] = acc;
+    for (int j = lane; j < nc; j += 32) acc = cmac(acc, Mr[j], vv[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) out[out_at[it] + r] = acc;
 }
 
 // CSR gather-sum: out[i] = sum_{p in [at[i], at[i+1])} src[idx[p]] (in order)
@@ -118,14 +145,21 @@ struct Batch {
     std::vector<int32_t> task_r0;
     DevBuf<int64_t> d_m_at, d_v_at, d_out_at, d_task_item;
     DevBuf<int32_t> d_rows, d_cols, d_task_r0;
-    void add(int64_t m, int32_t r, int32_t c, int64_t v, int64_t o, int32_t tasks_over) {
+    // tasks_over rows (or 1 task per item when step <= 0), `step` per task
+    void add(int64_t m, int32_t r, int32_t c, int64_t v, int64_t o, int32_t tasks_over,
+             int32_t step) {
         const int64_t it = (int64_t)m_at.size();
         m_at.push_back(m);
         rows.push_back(r);
         cols.push_back(c);
         v_at.push_back(v);
         out_at.push_back(o);
-        for (int32_t r0 = 0; r0 < tasks_over; r0 += MV_TPB) {
+        if (step <= 0) {
+            task_item.push_back(it);
+            task_r0.push_back(0);
+            return;
+        }
+        for (int32_t r0 = 0; r0 < tasks_over; r0 += step) {
             task_item.push_back(it);
             task_r0.push_back(r0);
         }
@@ -194,7 +228,11 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
     for (int64_t o = 0; o < ncolops; ++o) {
         const int64_t *d = colop_desc + 4 * o;
         xs_at[o + 1] = xs_at[o] + d[2];
-        H->colop.add(d[3], (int32_t)d[1], (int32_t)d[2], d[0], xs_at[o], (int32_t)d[2]);
+        if (d[2] > TM_MAX) {
+            delete H;
+            return fail("h2_create: rank above 128");
+        }
+        H->colop.add(d[3], (int32_t)d[1], (int32_t)d[2], d[0], xs_at[o], 0, 0);
     }
     // leaves: dense rows into cbuf, admissible rows into wbuf
     std::vector<int64_t> c_at(nleaves, -1), w_at(nleaves, -1);
@@ -213,7 +251,8 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
                 return fail("h2_create: dense leaf payload out of bounds");
             }
             c_at[l] = nc_total;
-            H->leafmv.add(leaf_base[l], (int32_t)nr, (int32_t)ncl, c0, nc_total, (int32_t)nr);
+            H->leafmv.add(leaf_base[l], (int32_t)nr, (int32_t)ncl, c0, nc_total, (int32_t)nr,
+                          MV_TPB / 32);
             nc_total += nr;
         } else {
             const int64_t ro = d[5], co = d[6];
@@ -241,7 +280,8 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
         const int64_t *d = leaf_desc + 7 * l;
         const int64_t ro = d[5], co = d[6];
         const int64_t kr = rowop_desc[4 * ro + 2], kc = colop_desc[4 * co + 2];
-        coup.add(leaf_base[l], (int32_t)kr, (int32_t)kc, xs_at[co], w_at[l], (int32_t)kr);
+        coup.add(leaf_base[l], (int32_t)kr, (int32_t)kc, xs_at[co], w_at[l], (int32_t)kr,
+                 MV_TPB / 32);
     }
     // row operators: z_t = sum of w over its leaves (preorder), u_t = V_t z_t
     std::vector<int64_t> z_at_h(1, 0), z_idx_h, zoff(nrowops + 1, 0);
@@ -260,7 +300,7 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
         const int64_t *d = rowop_desc + 4 * o;
         u_at[o] = nu_total;
         H->rowop.add(d[3], (int32_t)d[1], (int32_t)d[2], zoff[o], nc_total + nu_total,
-                     (int32_t)d[1]);
+                     (int32_t)d[1], MV_TPB / 32);
         nu_total += d[1];
     }
     // output CSR over permuted rows: dense leaf rows (preorder), then row
