@@ -94,31 +94,26 @@ tmatvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict_
 }
 
 // out[out_at[it] + r] = sum_j M[r, j] v[v_at + j] (M row-major rows x cols):
-// one WARP per row, lanes stride the columns (coalesced row reads), then a
-// fixed butterfly reduction -- deterministic. A task covers 4 rows.
+// one thread per ROW of the whole batch (tasks are the flattened rows of all
+// items, in item order): a warp streams 32 consecutive rows, which for
+// consecutive leaves are consecutive in the payload buffer -- no idle lanes
+// for 16-row leaves, each thread's row a contiguous run of cache lines.
 __global__ void __launch_bounds__(MV_TPB)
 matvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_r0,
               int64_t ntasks, const int64_t *__restrict__ m_at, const int32_t *__restrict__ rows,
               const int32_t *__restrict__ cols, const int64_t *__restrict__ v_at,
               const int64_t *__restrict__ out_at, const double2 *__restrict__ M,
               const double2 *__restrict__ v, double2 *__restrict__ out) {
-    const int64_t t = blockIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * MV_TPB + threadIdx.x;
     if (t >= ntasks) return;
     const int64_t it = task_item[t];
-    const int r = task_r0[t] + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (r >= rows[it]) return;  // whole warp leaves together
+    const int r = task_r0[t];
     const int nc = cols[it];
     const double2 *Mr = M + m_at[it] + (int64_t)r * nc;
     const double2 *vv = v + v_at[it];
     double2 acc = make_double2(0.0, 0.0);
-    for (int j = lane; j < nc; j += 32) acc = cmac(acc, Mr[j], vv[j]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-    }
-    if (lane == 0) out[out_at[it] + r] = acc;
+    for (int j = 0; j < nc; ++j) acc = cmac(acc, Mr[j], vv[j]);
+    out[out_at[it] + r] = acc;
 }
 
 // CSR gather-sum: out[i] = sum_{p in [at[i], at[i+1])} src[idx[p]] (in order)
@@ -252,7 +247,7 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
             }
             c_at[l] = nc_total;
             H->leafmv.add(leaf_base[l], (int32_t)nr, (int32_t)ncl, c0, nc_total, (int32_t)nr,
-                          MV_TPB / 32);
+                          1);
             nc_total += nr;
         } else {
             const int64_t ro = d[5], co = d[6];
@@ -281,7 +276,7 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
         const int64_t ro = d[5], co = d[6];
         const int64_t kr = rowop_desc[4 * ro + 2], kc = colop_desc[4 * co + 2];
         coup.add(leaf_base[l], (int32_t)kr, (int32_t)kc, xs_at[co], w_at[l], (int32_t)kr,
-                 MV_TPB / 32);
+                 1);
     }
     // row operators: z_t = sum of w over its leaves (preorder), u_t = V_t z_t
     std::vector<int64_t> z_at_h(1, 0), z_idx_h, zoff(nrowops + 1, 0);
@@ -300,7 +295,7 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
         const int64_t *d = rowop_desc + 4 * o;
         u_at[o] = nu_total;
         H->rowop.add(d[3], (int32_t)d[1], (int32_t)d[2], zoff[o], nc_total + nu_total,
-                     (int32_t)d[1], MV_TPB / 32);
+                     (int32_t)d[1], 1);
         nu_total += d[1];
     }
     // output CSR over permuted rows: dense leaf rows (preorder), then row
@@ -367,7 +362,7 @@ cudaError_t run_matvec(gcabem_h2_s *H, Batch &b, const double2 *M, const double2
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
             b.d_out_at.p, M, v, out);
     else
-        matvec_kernel<<<(unsigned)nt, MV_TPB, 0, H->stream>>>(
+        matvec_kernel<<<(unsigned)((nt + MV_TPB - 1) / MV_TPB), MV_TPB, 0, H->stream>>>(
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
             b.d_out_at.p, M, v, out);
     return cudaGetLastError();
