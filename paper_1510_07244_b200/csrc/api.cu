@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <set>
 #include <string>
 #include <utility>
@@ -430,6 +431,38 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
     return GCABEM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// split [0, n) over up to `maxt` std::threads (inline below `grain`)
+template <typename F>
+void par_for(int64_t n, int64_t grain, F fn) {
+    const int maxt = (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+    const int nt = (int)std::min<int64_t>(maxt, std::max<int64_t>(1, n / std::max<int64_t>(grain, 1)));
+    if (nt <= 1) {
+        fn(0, n, 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t chunk = (n + nt - 1) / nt;
+    for (int t = 1; t < nt; ++t) {
+        const int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+        if (lo < hi) th.emplace_back(fn, lo, hi, t);
+    }
+    fn(0, std::min(n, chunk), 0);
+    for (auto &x : th) x.join();
+}
+
+// pinned staging for layout uploads (grow-only, one user at a time)
+std::mutex g_arena_mutex;
+void *g_arena = nullptr;
+size_t g_arena_bytes = 0;
+
+}  // namespace
+
+extern "C" {
+
 int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t leaf_hi,
                                 int64_t nleaves, const int64_t *leaf_shape,
                                 const int64_t *leaf_base, const int64_t *leaf_rows_at,
@@ -448,84 +481,147 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     GC_CUDA(cudaSetDevice(mesh->device));
     Trace tr("from_pk");
     const int64_t base0 = leaf_base[leaf_lo], plen = leaf_base[leaf_hi] - base0;
+    // blocks are in leaf order: the range is one contiguous run
+    for (int64_t b = 1; b < nblocks; ++b)
+        GC_ARG(blk_leaf[b] >= blk_leaf[b - 1], "block leaves out of order");
+    GC_ARG(nblocks == 0 || (blk_leaf[0] >= 0 && blk_leaf[nblocks - 1] < nleaves),
+           "block leaf out of range");
+    const int64_t b0 = std::lower_bound(blk_leaf, blk_leaf + nblocks, leaf_lo) - blk_leaf;
+    const int64_t b1 = std::lower_bound(blk_leaf, blk_leaf + nblocks, leaf_hi) - blk_leaf;
+    const int64_t B = b1 - b0;
     auto *L = new gcabem_layout_s();
     L->mesh = mesh;
     L->payload_len = plen;
-    auto fail = [&](const char *msg) {
-        delete L;
-        return set_error(GCABEM_ERR_ARG, msg);
-    };
-    // blocks of the leaf range -> descriptors, fixed-size tasks
-    std::vector<BlockDesc> bd;
-    bd.reserve((size_t)nblocks);
-    int64_t ntasks = 0, prev_leaf = -1;
-    for (int64_t b = 0; b < nblocks; ++b) {
-        const int64_t lf = blk_leaf[b];
-        if (lf < 0 || lf >= nleaves || lf < prev_leaf) return fail("block leaves out of order");
-        prev_leaf = lf;
-        if (lf < leaf_lo || lf >= leaf_hi) continue;
-        const int64_t ld = leaf_shape[2 * lf + 1], nr = blk_nr[b], nc = blk_nc[b];
-        const int64_t base = leaf_base[lf] - base0 + blk_r0[b] * ld + blk_c0[b];
-        const int64_t ra = leaf_rows_at[lf] + blk_r0[b], ca = leaf_cols_at[lf] + blk_c0[b];
-        if (!(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31)) ||
-            !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
-            !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= plen)))
-            return fail("block descriptor out of bounds");
-        bd.push_back(BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0});
-        L->block_task_at.push_back(ntasks);
-        L->block_leaf.push_back(lf);
-        L->block_base.push_back(base);
-        L->block_pairs.push_back(nr * nc);
-        ntasks += (nr * nc + DISJOINT_TPB - 1) / DISJOINT_TPB;
-    }
-    L->block_task_at.push_back(ntasks);
-    const int64_t B = (int64_t)bd.size();
-    std::vector<int2> tasks((size_t)ntasks);
+    L->block_task_at.resize(B + 1);
+    L->block_leaf.resize(B);
+    L->block_base.resize(B);
+    L->block_pairs.resize(B);
+    int64_t ntasks = 0;
     for (int64_t b = 0; b < B; ++b) {
-        int64_t t = L->block_task_at[b];
-        for (int64_t k0 = 0; k0 < L->block_pairs[b]; k0 += DISJOINT_TPB)
-            tasks[t++] = make_int2((int)b, (int)k0);
+        const int64_t np = blk_nr[b0 + b] * blk_nc[b0 + b];
+        L->block_task_at[b] = ntasks;
+        L->block_pairs[b] = np;
+        ntasks += (np + DISJOINT_TPB - 1) / DISJOINT_TPB;
     }
-    std::vector<int32_t> pan((size_t)npanels);
-    for (int64_t k = 0; k < npanels; ++k) {
-        if (panels[k] < 0 || panels[k] >= mesh->nt) return fail("panel index out of range");
-        pan[k] = (int32_t)panels[k];
+    L->block_task_at[B] = ntasks;
+    // singular items of the range: per-chunk case counts (stable counting sort)
+    constexpr int MAXT = 8;
+    int64_t cnt[MAXT][4] = {};
+    std::atomic<bool> bad{false};
+    const int64_t ichunk = std::max<int64_t>(1, (nitems + MAXT - 1) / MAXT);
+    // fixed item slots [slot * ichunk, (slot + 1) * ichunk): thread-count independent
+    const int64_t slot_grain = nitems < (1 << 16) ? MAXT : 1;
+    par_for(MAXT, slot_grain, [&](int64_t slo, int64_t shi, int) {
+        for (int64_t slot = slo; slot < shi; ++slot) {
+            const int64_t c0 = slot * ichunk, c1 = std::min(nitems, c0 + ichunk);
+            for (int64_t k = c0; k < c1; ++k) {
+                const int c = item_case[k];
+                const int64_t lf = item_leaf[k];
+                if (c < 1 || c > 3 || lf < 0 || lf >= nleaves) {
+                    bad = true;
+                    continue;
+                }
+                if (lf >= leaf_lo && lf < leaf_hi) cnt[slot][c]++;
+            }
+        }
+    });
+    if (bad) {
+        delete L;
+        return set_error(GCABEM_ERR_ARG, "bad singular item");
     }
-    tr.mark("blocks+tasks");
-    // singular items of the range grouped by case (counting sort, stable)
-    int64_t counts[4] = {0, 0, 0, 0};
-    for (int64_t k = 0; k < nitems; ++k) {
-        const int c = item_case[k];
-        const int64_t lf = item_leaf[k];
-        if (c < 1 || c > 3 || lf < 0 || lf >= nleaves) return fail("bad singular item");
-        if (lf >= leaf_lo && lf < leaf_hi) counts[c]++;
-    }
+    int64_t chunk_at[MAXT][4] = {};
     L->case_at[0] = 0;
-    for (int c = 1; c <= 3; ++c) L->case_at[c] = L->case_at[c - 1] + counts[c];
+    {
+        int64_t run = 0;
+        for (int c = 1; c <= 3; ++c) {
+            for (int s = 0; s < MAXT; ++s) {
+                chunk_at[s][c] = run;
+                run += cnt[s][c];
+            }
+            L->case_at[c] = run;
+        }
+    }
     const int64_t S = L->case_at[3];
-    std::vector<SingItem> si((size_t)S);
-    L->item_out.resize((size_t)S);
-    int64_t at[4] = {0, L->case_at[0], L->case_at[1], L->case_at[2]};
-    for (int64_t k = 0; k < nitems; ++k) {
-        const int64_t lf = item_leaf[k];
-        if (lf < leaf_lo || lf >= leaf_hi) continue;
-        const int c = item_case[k];
-        SingItem &it = si[at[c]];
-        it.out = leaf_base[lf] - base0 + item_offset[k];
-        it.tri_x = (int32_t)item_tri_x[k];
-        it.tri_y = (int32_t)item_tri_y[k];
-        const uint8_t *pm = perms + 6 * k;
-        it.px[0] = pm[0]; it.px[1] = pm[1]; it.px[2] = pm[2];
-        it.py[0] = pm[3]; it.py[1] = pm[4]; it.py[2] = pm[5];
-        it.pad[0] = it.pad[1] = 0;
-        bool ok = it.out >= 0 && it.out < plen && item_tri_x[k] >= 0 &&
-                  item_tri_x[k] < mesh->nt && item_tri_y[k] >= 0 && item_tri_y[k] < mesh->nt &&
-                  pm[0] < 3 && pm[1] < 3 && pm[2] < 3 && pm[3] < 3 && pm[4] < 3 && pm[5] < 3;
-        ok = ok && (c != 3 || (it.tri_x == it.tri_y && pm[0] == pm[3] && pm[1] == pm[4] &&
-                               pm[2] == pm[5]));
-        if (!ok) return fail("bad singular item (index, permutation or chart)");
-        L->item_out[at[c]] = it.out;
-        ++at[c];
+    L->item_out.resize(S);
+    tr.mark("counts");
+    // one pinned arena: [BlockDesc B | int2 ntasks | int32 npanels | SingItem S]
+    auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t off_t = align(sizeof(BlockDesc) * B), off_p = off_t + align(sizeof(int2) * ntasks),
+                 off_s = off_p + align(sizeof(int32_t) * npanels),
+                 total = off_s + align(sizeof(SingItem) * S);
+    std::lock_guard<std::mutex> arena_lock(g_arena_mutex);
+    if (total > g_arena_bytes) {
+        if (g_arena) cudaFreeHost(g_arena);
+        g_arena = nullptr;
+        g_arena_bytes = 0;
+        cudaError_t e = cudaHostAlloc(&g_arena, std::max<size_t>(total, size_t(64) << 20),
+                                      cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            delete L;
+            GC_CUDA(e);
+        }
+        g_arena_bytes = std::max<size_t>(total, size_t(64) << 20);
+    }
+    char *arena = static_cast<char *>(g_arena);
+    BlockDesc *bd = reinterpret_cast<BlockDesc *>(arena);
+    int2 *tasks = reinterpret_cast<int2 *>(arena + off_t);
+    int32_t *pan = reinterpret_cast<int32_t *>(arena + off_p);
+    SingItem *si = reinterpret_cast<SingItem *>(arena + off_s);
+    par_for(B, 1 << 14, [&](int64_t lo, int64_t hi, int) {
+        for (int64_t b = lo; b < hi; ++b) {
+            const int64_t g = b0 + b, lf = blk_leaf[g];
+            const int64_t ld = leaf_shape[2 * lf + 1], nr = blk_nr[g], nc = blk_nc[g];
+            const int64_t base = leaf_base[lf] - base0 + blk_r0[g] * ld + blk_c0[g];
+            const int64_t ra = leaf_rows_at[lf] + blk_r0[g], ca = leaf_cols_at[lf] + blk_c0[g];
+            if (!(nr >= 0 && nc >= 0 && nr * nc < (int64_t(1) << 31)) ||
+                !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
+                !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= plen)))
+                bad = true;
+            bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
+            L->block_leaf[b] = lf;
+            L->block_base[b] = base;
+            int64_t t = L->block_task_at[b];
+            for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
+                tasks[t++] = make_int2((int)b, (int)k0);
+        }
+    });
+    par_for(npanels, 1 << 16, [&](int64_t lo, int64_t hi, int) {
+        for (int64_t k = lo; k < hi; ++k) {
+            if (panels[k] < 0 || panels[k] >= mesh->nt) bad = true;
+            pan[k] = (int32_t)panels[k];
+        }
+    });
+    par_for(MAXT, slot_grain, [&](int64_t slo, int64_t shi, int) {
+        for (int64_t slot = slo; slot < shi; ++slot) {
+            const int64_t c0 = slot * ichunk, c1 = std::min(nitems, c0 + ichunk);
+            int64_t at[4] = {0, chunk_at[slot][1], chunk_at[slot][2], chunk_at[slot][3]};
+            for (int64_t k = c0; k < c1; ++k) {
+                const int64_t lf = item_leaf[k];
+                if (lf < leaf_lo || lf >= leaf_hi) continue;
+                const int c = item_case[k];
+                SingItem &it = si[at[c]];
+                it.out = leaf_base[lf] - base0 + item_offset[k];
+                it.tri_x = (int32_t)item_tri_x[k];
+                it.tri_y = (int32_t)item_tri_y[k];
+                const uint8_t *pm = perms + 6 * k;
+                it.px[0] = pm[0]; it.px[1] = pm[1]; it.px[2] = pm[2];
+                it.py[0] = pm[3]; it.py[1] = pm[4]; it.py[2] = pm[5];
+                it.pad[0] = it.pad[1] = 0;
+                bool ok = it.out >= 0 && it.out < plen && item_tri_x[k] >= 0 &&
+                          item_tri_x[k] < mesh->nt && item_tri_y[k] >= 0 &&
+                          item_tri_y[k] < mesh->nt && pm[0] < 3 && pm[1] < 3 && pm[2] < 3 &&
+                          pm[3] < 3 && pm[4] < 3 && pm[5] < 3;
+                ok = ok && (c != 3 || (it.tri_x == it.tri_y && pm[0] == pm[3] &&
+                                       pm[1] == pm[4] && pm[2] == pm[5]));
+                if (!ok) bad = true;
+                L->item_out[at[c]] = it.out;
+                ++at[c];
+            }
+        }
+    });
+    if (bad) {
+        delete L;
+        return set_error(GCABEM_ERR_ARG, "bad block, panel or singular item");
     }
     // chunked execution looks items up by payload index inside a case: sort a
     // case only if its generation order is not already ascending (it is,
@@ -533,18 +629,22 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     for (int c = 0; c < 3; ++c) {
         const int64_t a0 = L->case_at[c], a1 = L->case_at[c + 1];
         if (std::is_sorted(L->item_out.begin() + a0, L->item_out.begin() + a1)) continue;
-        std::stable_sort(si.begin() + a0, si.begin() + a1,
+        std::stable_sort(si + a0, si + a1,
                          [](const SingItem &x, const SingItem &y) { return x.out < y.out; });
         for (int64_t q = a0; q < a1; ++q) L->item_out[q] = si[q].out;
     }
-    tr.mark("items");
+    tr.mark("fill");
     L->ntasks = ntasks;
     cudaStream_t s = mesh->stream;
-    cudaError_t e = L->blocks.upload(bd.data(), bd.size(), s);
-    if (e == cudaSuccess) e = L->tasks.upload(tasks.data(), tasks.size(), s);
-    if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
-    if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
+    cudaError_t e = L->blocks.alloc(B);
+    if (e == cudaSuccess) e = L->tasks.alloc(ntasks);
+    if (e == cudaSuccess) e = L->panels.alloc(npanels);
+    if (e == cudaSuccess) e = L->items.alloc(S);
+    if (e == cudaSuccess && B) e = cudaMemcpyAsync(L->blocks.p, bd, sizeof(BlockDesc) * B, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && ntasks) e = cudaMemcpyAsync(L->tasks.p, tasks, sizeof(int2) * ntasks, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && npanels) e = cudaMemcpyAsync(L->panels.p, pan, sizeof(int32_t) * npanels, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && S) e = cudaMemcpyAsync(L->items.p, si, sizeof(SingItem) * S, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the arena is reused after this
     tr.mark("upload");
     if (e != cudaSuccess) {
         delete L;

@@ -174,7 +174,28 @@ def _leaf_arrays(bt: BlockTree):
     return _cached(_leaf_cache, bt, build)
 
 
+_op_cache: dict = {}
+
+
 def _op_arrays(ops: dict, nnodes: int):
+    """Pivot arrays of an operator dict, cached while the dict holds the same
+    operator objects (ops dicts cannot be weak-referenced: the entry keeps a
+    fingerprint of (cluster, operator identity) pairs and is replaced when it
+    no longer matches)."""
+    fp = (nnodes, tuple((k, id(v)) for k, v in ops.items()))
+    with _cache_lock:
+        hit = _op_cache.get(id(ops))
+    if hit is not None and hit[0] == fp:
+        return hit[2]
+    val = _op_arrays_build(ops, nnodes)
+    with _cache_lock:
+        if len(_op_cache) > 16:
+            _op_cache.clear()
+        _op_cache[id(ops)] = (fp, ops, val)
+    return val
+
+
+def _op_arrays_build(ops: dict, nnodes: int):
     at = np.zeros(nnodes + 1, dtype=np.int64)
     pivs = []
     for cid in sorted(ops):
