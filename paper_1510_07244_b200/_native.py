@@ -13,7 +13,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgcabem_b200.so")
+# GCABEM_LIB_PATH: load a variant build (occupancy / flag experiments)
+LIB_PATH = os.environ.get("GCABEM_LIB_PATH") or os.path.join(HERE, "libgcabem_b200.so")
 
 ERR_ARG, ERR_CUDA, ERR_NODEV, ERR_GCA = 1, 2, 3, 4
 

@@ -152,8 +152,14 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // singular pass of the same plan overwrites every one of them (the overwrite
 // protocol, scheduler.py:9-12), so their disjoint-rule value (non-finite for
 // identical pairs) is never observable.
+// resident CTAs per SM the register allocation must allow (per kind; 1 =
+// compiler's choice). Overridable at build time for occupancy experiments.
+#ifndef GCABEM_DISJOINT_MINB
+#define GCABEM_DISJOINT_MINB(KIND) 1
+#endif
+
 template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB)
+__global__ void __launch_bounds__(DISJOINT_TPB, GCABEM_DISJOINT_MINB(KIND))
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,
