@@ -417,7 +417,8 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
     L->case_at[0] = 0;
     for (int c = 1; c <= 3; ++c) L->case_at[c] = L->case_at[c - 1] + counts[c];
     cudaStream_t s = mesh->stream;
-    cudaError_t e = L->blocks.upload(bd.data(), bd.size(), s);
+    cudaError_t e = pool_init(mesh->device);
+    if (e == cudaSuccess) e = L->blocks.upload(bd.data(), bd.size(), s);
     if (e == cudaSuccess) e = L->tasks.upload(tasks.data(), tasks.size(), s);
     if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
     if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
@@ -636,10 +637,11 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     tr.mark("fill");
     L->ntasks = ntasks;
     cudaStream_t s = mesh->stream;
-    cudaError_t e = L->blocks.alloc(B);
-    if (e == cudaSuccess) e = L->tasks.alloc(ntasks);
-    if (e == cudaSuccess) e = L->panels.alloc(npanels);
-    if (e == cudaSuccess) e = L->items.alloc(S);
+    cudaError_t e = pool_init(mesh->device);
+    if (e == cudaSuccess) e = L->blocks.alloc(B, s);
+    if (e == cudaSuccess) e = L->tasks.alloc(ntasks, s);
+    if (e == cudaSuccess) e = L->panels.alloc(npanels, s);
+    if (e == cudaSuccess) e = L->items.alloc(S, s);
     if (e == cudaSuccess && B) e = cudaMemcpyAsync(L->blocks.p, bd, sizeof(BlockDesc) * B, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && ntasks) e = cudaMemcpyAsync(L->tasks.p, tasks, sizeof(int2) * ntasks, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && npanels) e = cudaMemcpyAsync(L->panels.p, pan, sizeof(int32_t) * npanels, cudaMemcpyHostToDevice, s);

@@ -90,6 +90,11 @@ struct PoolBuf {
         if (count == 0) return cudaSuccess;
         return cudaMallocAsync(reinterpret_cast<void **>(&p), sizeof(T) * count, stream);
     }
+    cudaError_t upload(const T *host, size_t count, cudaStream_t stream) {
+        cudaError_t e = alloc(count, stream);
+        if (e != cudaSuccess || count == 0) return e;
+        return cudaMemcpyAsync(p, host, sizeof(T) * count, cudaMemcpyHostToDevice, stream);
+    }
 };
 
 }  // namespace gcabem
@@ -108,11 +113,12 @@ struct gcabem_mesh_s {
 struct gcabem_layout_s {
     gcabem_mesh_t mesh = nullptr;
     int64_t payload_len = 0;
-    gcabem::DevBuf<gcabem::BlockDesc> blocks;
-    gcabem::DevBuf<int2> tasks;
+    // stream-ordered pool allocations (layouts are created per assembly call)
+    gcabem::PoolBuf<gcabem::BlockDesc> blocks;
+    gcabem::PoolBuf<int2> tasks;
     int64_t ntasks = 0;
-    gcabem::DevBuf<int32_t> panels;
-    gcabem::DevBuf<gcabem::SingItem> items;
+    gcabem::PoolBuf<int32_t> panels;
+    gcabem::PoolBuf<gcabem::SingItem> items;
     int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])
     // host copies for chunked execution
     std::vector<int64_t> block_task_at, block_leaf, block_base, block_pairs, item_out;
