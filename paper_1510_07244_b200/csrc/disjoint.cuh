@@ -153,13 +153,13 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // protocol, scheduler.py:9-12), so their disjoint-rule value (non-finite for
 // identical pairs) is never observable.
 // resident CTAs per SM the register allocation must allow, per kind:
-// L-DLP 6 (80 registers), Helmholtz 5 (102); measured on the B200 against
+// L-SLP 7 (72 registers), L-DLP 6 (80), Helmholtz 5 (<= 102); measured on the B200 against
 // the compiler's choice (96 / 128 registers): +1% (C2 L-DLP) and +10% (C3
 // H-DLP) from the extra warps hiding the FP64 dependency latency, despite a
 // few spilled bytes in the cold full-sincos tier. Overridable at build time
 // (-DGCABEM_DISJOINT_MINB(K)=...) for experiments.
 #ifndef GCABEM_DISJOINT_MINB
-#define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 1 ? 6 : ((KIND) >= 2 ? 5 : 1))
+#define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 0 ? 7 : ((KIND) == 1 ? 6 : 5))
 #endif
 
 template <int N, int KIND>
