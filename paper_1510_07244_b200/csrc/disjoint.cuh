@@ -156,14 +156,15 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // L-SLP 7 (72 registers), L-DLP 6 (80), Helmholtz 5 (<= 102); measured on the B200 against
 // the compiler's choice (96 / 128 registers): +1% (C2 L-DLP) and +10% (C3
 // H-DLP) from the extra warps hiding the FP64 dependency latency, despite a
-// few spilled bytes in the cold full-sincos tier. Overridable at build time
+// few spilled bytes in the cold full-sincos tier (orders above 7 keep the
+// compiler's choice: they would spill heavily). Overridable at build time
 // (-DGCABEM_DISJOINT_MINB(K)=...) for experiments.
 #ifndef GCABEM_DISJOINT_MINB
 #define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 0 ? 7 : ((KIND) == 1 ? 6 : 5))
 #endif
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB, GCABEM_DISJOINT_MINB(KIND))
+__global__ void __launch_bounds__(DISJOINT_TPB, N <= 7 ? GCABEM_DISJOINT_MINB(KIND) : 1)
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,

@@ -338,6 +338,14 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         delete G;
         return gcabem_internal_error(GCABEM_ERR_GCA, msg.c_str());
     }
+    d_first.release();
+    d_at.release();
+    d_size.release();
+    d_perm.release();
+    d_box.release();
+    d_gq.release();
+    d_duffy.release();
+    d_task.release();
     tr.mark("finish");
     G->phase[0] = t_wait;
     G->phase[2] = since(t_all);
