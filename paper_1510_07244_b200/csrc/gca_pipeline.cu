@@ -64,9 +64,9 @@ constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging e
 struct Staging {
     Pinned host[SLOTS];
     DevBuf<double> out[SLOTS];
+    std::mutex busy;  // one build per device at a time (builds on other devices run in parallel)
 };
 std::mutex g_staging_mutex;
-std::mutex g_build_mutex;
 std::vector<Staging *> g_staging;  // indexed by device
 
 Staging &staging_for(int device) {
@@ -81,7 +81,8 @@ Staging &staging_for(int device) {
 extern "C" {
 
 int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl,
-                     const int64_t *cl_ids, const int64_t *cl_first, const int64_t *cl_size, const double *box_lo,
+                     const int64_t *cl_ids, const int64_t *cl_first, const int64_t *cl_size,
+                     const double *box_lo,
                      const double *box_hi, int64_t nperm, const int64_t *perm, double delta,
                      int m, const double *gauss_pts, const double *gauss_wts,
                      double scene_diameter, int64_t nduffy, const double *duffy, double epsilon,
@@ -174,12 +175,15 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     cudaError_t e = cudaSetDevice(mesh->device);
     cudaStream_t s = mesh->stream;
     Staging &st = staging_for(mesh->device);
-    std::lock_guard<std::mutex> build_lock(g_build_mutex);  // staging: one build at a time
-    DevBuf<int64_t> d_first, d_at;
-    DevBuf<int32_t> d_size, d_perm;
-    DevBuf<GreenBox> d_box;
-    DevBuf<double> d_gq, d_duffy;
-    DevBuf<int2> d_task;
+    std::lock_guard<std::mutex> build_lock(st.busy);
+    // per-call buffers from the device pool (stream-ordered: no implicit
+    // device-wide synchronisation on free)
+    if (e == cudaSuccess) e = pool_init(mesh->device);
+    PoolBuf<int64_t> d_first, d_at;
+    PoolBuf<int32_t> d_size, d_perm;
+    PoolBuf<GreenBox> d_box;
+    PoolBuf<double> d_gq, d_duffy;
+    PoolBuf<int2> d_task;
     std::vector<int64_t> first(ncl);
     std::vector<int32_t> size32(ncl);
     for (int64_t c = 0; c < ncl; ++c) {
@@ -202,14 +206,16 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         max_tasks = std::max(max_tasks, tasks[b].size());
         max_cl = std::max(max_cl, out_at[b].size());
     }
-    if (e == cudaSuccess) e = d_task.alloc(max_tasks * SLOTS);
-    if (e == cudaSuccess) e = d_at.alloc(max_cl * SLOTS);
+    if (e == cudaSuccess) e = d_task.alloc(max_tasks * SLOTS, s);
+    if (e == cudaSuccess) e = d_at.alloc(max_cl * SLOTS, s);
+    tr.mark("uploads");
     for (int k = 0; k < SLOTS && e == cudaSuccess; ++k) {
         e = st.out[k].reserve((size_t)(max_elems * width));
         if (e == cudaSuccess) e = st.host[k].reserve((size_t)(max_elems * width) * 8);
     }
+    tr.mark("staging");
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    tr.mark("uploads");
+    tr.mark("sync");
     cudaEvent_t done[SLOTS] = {};
     for (int k = 0; k < SLOTS && e == cudaSuccess; ++k)
         e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
@@ -323,6 +329,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     cudaStreamSynchronize(s);
     for (auto &d : done)
         if (d) cudaEventDestroy(d);
+    tr.mark("sync+events");
     if (e != cudaSuccess) {
         delete G;
         return gcabem_internal_error(GCABEM_ERR_CUDA,

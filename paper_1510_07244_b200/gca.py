@@ -265,7 +265,7 @@ def _host_threads() -> int:
 
 
 def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
-                  batch_bytes: int = 0) -> dict:
+                  batch_bytes: int = 0, threads: int | None = None) -> dict:
     """All clusters in one native pipeline (C ABI gcabem_gca_build): device
     Green matrices per batch (sources generated on the device, bit-identical
     to green_sources), host ACA + pivot check + refined V solve on all cores,
@@ -292,7 +292,8 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
     nat.check(nat.lib().gcabem_gca_build(
         dm.handle, eq, float(spec.kappa), ids.size, p(ids), p(starts), p(sizes), p(lo), p(hi),
         perm.size, p(perm), float(params.delta), int(params.m), p(gp), p(gw), float(scene),
-        duffy.shape[0], p(duffy), float(params.epsilon), _host_threads(), int(batch_bytes),
+        duffy.shape[0], p(duffy), float(params.epsilon), threads or _host_threads(),
+        int(batch_bytes),
         ctypes.byref(h)))
     try:
         ranks = np.empty(ids.size, np.int64)
@@ -322,11 +323,49 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
     return ops
 
 
+def _ops_multi(mesh, tree, ids, spec, params, scene, devices) -> dict:
+    """Clusters split into contiguous id ranges balanced by panel count, one
+    native pipeline per device running concurrently (the ctypes call releases
+    the GIL; no exchange step: every cluster is independent, gca.py:295-302),
+    host threads shared evenly."""
+    ids = sorted(ids)
+    if len(devices) == 1 or len(ids) < 2 * len(devices):
+        return _ops_for_tree(mesh, tree, ids, spec, params, scene, devices[0])
+    w = np.cumsum([tree.nodes[c].size for c in ids]).astype(np.float64)
+    cuts = np.searchsorted(w, w[-1] * np.arange(1, len(devices)) / len(devices)) + 1
+    parts = np.split(np.array(ids, dtype=np.int64), np.minimum(cuts, len(ids)))
+    share = max(1, _host_threads() // len(devices))
+    out, errs = [None] * len(parts), []
+
+    def run(k):
+        try:
+            out[k] = _ops_for_tree(mesh, tree, parts[k].tolist(), spec, params, scene,
+                                   devices[k], threads=share)
+        except BaseException as exc:  # re-raised on the caller's thread
+            errs.append(exc)
+    import threading
+    th = [threading.Thread(target=run, args=(k,)) for k in range(len(parts)) if parts[k].size]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    ops: dict = {}
+    for o in out:
+        if o:
+            ops.update(o)
+    return dict(sorted(ops.items()))
+
+
 def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
-                                  params: GcaParams, device: int | None = None):
+                                  params: GcaParams, device=None):
     """Operators for every cluster in an admissible block (gca.py:285-310);
-    (row_ops, col_ops) — the same dict for a shared cluster tree."""
-    device = default_device() if device is None else device
+    (row_ops, col_ops) — the same dict for a shared cluster tree. `device`
+    may be a sequence of devices: the clusters are then partitioned across
+    them (balanced by panel count) and built concurrently."""
+    devices = tuple(device) if isinstance(device, (tuple, list)) else \
+        (default_device() if device is None else device,)
     t0 = time.perf_counter()
     scene = mesh.diameter()
     native = getattr(block_tree, "_native_leaves", None)
@@ -341,9 +380,9 @@ def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec
     last_build_phases.clear()
     last_build_phases["ids_s"] = time.perf_counter() - t0
     if block_tree.row_tree is block_tree.col_tree:
-        ops = _ops_for_tree(mesh, block_tree.row_tree, row_ids | col_ids, spec, params, scene,
-                            device)
+        ops = _ops_multi(mesh, block_tree.row_tree, row_ids | col_ids, spec, params, scene,
+                         devices)
         return ops, ops
-    return (_ops_for_tree(mesh, block_tree.row_tree, row_ids, spec, params, scene, device),
-            _ops_for_tree(mesh, block_tree.col_tree, col_ids, spec, params, scene, device))
+    return (_ops_multi(mesh, block_tree.row_tree, row_ids, spec, params, scene, devices),
+            _ops_multi(mesh, block_tree.col_tree, col_ids, spec, params, scene, devices))
 

@@ -54,8 +54,12 @@ def assemble_operator(mesh: SurfaceMesh, spec: KernelSpec, config: PipelineConfi
     block_tree = build_trees(mesh, config) if trees is None else trees
     t0 = time.monotonic()
     if ops is None:
+        # the GCA operators use the devices of the disjoint backend: several
+        # devices partition the clusters
+        devices = config.scheduler.backend_for("disjoint").devices
         row_ops, col_ops = build_interpolation_operators(
-            mesh, block_tree, KernelSpec(spec.equation, "single", spec.kappa), config.gca)
+            mesh, block_tree, KernelSpec(spec.equation, "single", spec.kappa), config.gca,
+            device=tuple(devices))
     else:
         row_ops, col_ops = ops
     t1 = time.monotonic()

@@ -435,3 +435,16 @@ def test_p1_near_field_scatter_vs_oracle(eq, layer, kappa):
     _, _, d2 = plan.download()
     assert np.array_equal(d1, d2)
     plan.close()
+
+
+def test_gca_multi_device_partition_equals_single():
+    """Clusters partitioned over several devices (here the same device
+    twice: the partition and merge logic) give the single-device operators."""
+    m, t, bt = sphere_setup(4)
+    spec = kernels.KernelSpec("helmholtz", "single", 4.0)
+    one, _ = gca.build_interpolation_operators(m, bt, spec, gca.GcaParams(), device=0)
+    two, _ = gca.build_interpolation_operators(m, bt, spec, gca.GcaParams(), device=(0, 0, 0))
+    assert list(one) == list(two)
+    for c in one:
+        assert np.array_equal(one[c].pivots_global, two[c].pivots_global)
+        assert np.array_equal(one[c].V, two[c].V)
