@@ -359,6 +359,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     G->phase[3] = (double)nb;
     G->phase[4] = t_host;
     G->phase[5] = (double)nthreads;
+    tr.mark("return");
     *out = G;
     return GCABEM_OK;
 }

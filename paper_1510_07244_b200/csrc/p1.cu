@@ -69,7 +69,7 @@ __device__ __forceinline__ void p1_disjoint_pair(const double dO[3], const doubl
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         double in[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-#pragma unroll 1  // N points in flight, not N^2: register pressure (18 accumulators)
+#pragma unroll
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
 #pragma unroll
@@ -130,9 +130,10 @@ __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy
         }
 }
 
-// 3 CTAs per SM: 164 registers, no spills (242 and 2 CTAs unconstrained)
+// unconstrained registers (242, 2 CTAs/SM): measured faster on the B200 than
+// 3 CTAs/SM with the y loop rolled (34.2 vs 30.6 ms at C4) -- ILP wins here
 template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB, 3)
+__global__ void __launch_bounds__(DISJOINT_TPB)
 p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                    const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                    const int32_t *__restrict__ panels, double2 *__restrict__ local,
