@@ -398,19 +398,11 @@ struct LU {
                 for (int64_t q = 0; q < n; ++q) std::swap(X[k * n + q], X[piv[k] * n + q]);
         for (int64_t i = 1; i < r; ++i) {
             T *xi = X + i * n;
-            for (int64_t j = 0; j < i; ++j) {
-                const T l = m[i * r + j];
-                const T *xj = X + j * n;
-                for (int64_t q = 0; q < n; ++q) xi[q] = O::sub(xi[q], O::mul(l, xj[q]));
-            }
+            for (int64_t j = 0; j < i; ++j) mulsub<T>(xi, m[i * r + j], X + j * n, n);
         }
         for (int64_t i = r - 1; i >= 0; --i) {
             T *xi = X + i * n;
-            for (int64_t j = i + 1; j < r; ++j) {
-                const T u = m[i * r + j];
-                const T *xj = X + j * n;
-                for (int64_t q = 0; q < n; ++q) xi[q] = O::sub(xi[q], O::mul(u, xj[q]));
-            }
+            for (int64_t j = i + 1; j < r; ++j) mulsub<T>(xi, m[i * r + j], X + j * n, n);
             const T d = m[i * r + i];
             for (int64_t q = 0; q < n; ++q) xi[q] = O::div(xi[q], d);
         }
@@ -476,11 +468,7 @@ int operator_one(const T *A, int64_t nr, int64_t nc, double eps, std::vector<int
             R = RHS;
             for (int64_t b = 0; b < k; ++b) {
                 T *rb = R.data() + b * nr;
-                for (int64_t l = 0; l < k; ++l) {
-                    const T mbl = M[b * k + l];
-                    const T *xl = X.data() + l * nr;
-                    for (int64_t q = 0; q < nr; ++q) rb[q] = O::sub(rb[q], O::mul(mbl, xl[q]));
-                }
+                for (int64_t l = 0; l < k; ++l) mulsub<T>(rb, M[b * k + l], X.data() + l * nr, nr);
             }
             double rmax = 0.0;
             for (const T &v : R) rmax = std::max(rmax, O::mag(v));
