@@ -10,9 +10,6 @@
 // use the reference's operation order (r -= u_i * v), magnitudes are fabs /
 // hypot as numpy's abs, complex division follows numpy's Smith scheme.
 #include <algorithm>
-#if defined(__AVX2__)
-#include <immintrin.h>
-#endif
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -96,66 +93,15 @@ Cx dotc(const T *a, const T *b, int64_t n) {
     return {(r[0] + r[1]) + (r[2] + r[3]), (i[0] + i[1]) + (i[2] + i[3])};
 }
 
-// x[j] -= s * y[j] (the residual updates): the same IEEE operations in both
-// builds; the AVX2 build does two complex (or four real) per instruction with
-// the products ordered exactly as the scalar cmul, so results are identical.
+// x[j] -= s * y[j] (the residual updates and the LU sweeps); the compiler
+// vectorises it in the AVX2 build (hand-written intrinsics measured no faster
+// on the B200 host)
 template <typename T>
 inline void mulsub(T *x, T s, const T *y, int64_t n) {
     using O = Ops<T>;
     for (int64_t j = 0; j < n; ++j) x[j] = O::sub(x[j], O::mul(s, y[j]));
 }
 
-#if defined(__AVX2__) && !defined(GCABEM_NO_INTRIN)
-template <>
-inline void mulsub<Cx>(Cx *x, Cx s, const Cx *y, int64_t n) {
-    double *xd = reinterpret_cast<double *>(x);
-    const double *yd = reinterpret_cast<const double *>(y);
-    const __m256d sr = _mm256_set1_pd(s.re), si = _mm256_set1_pd(s.im);
-    int64_t j = 0;
-    for (; j + 2 <= n; j += 2) {
-        const __m256d w = _mm256_loadu_pd(yd + 2 * j);
-        const __m256d t1 = _mm256_mul_pd(sr, w);                               // sr*wr, sr*wi
-        const __m256d t2 = _mm256_mul_pd(si, _mm256_permute_pd(w, 0x5));       // si*wi, si*wr
-        const __m256d prod = _mm256_addsub_pd(t1, t2);  // sr*wr - si*wi, sr*wi + si*wr
-        _mm256_storeu_pd(xd + 2 * j, _mm256_sub_pd(_mm256_loadu_pd(xd + 2 * j), prod));
-    }
-    for (; j < n; ++j) x[j] = csub(x[j], cmul(s, y[j]));
-}
-
-// dotc with the generic version's association: lanes k % 4 accumulate
-// (a.re b.re + a.im b.im) and (a.re b.im - a.im b.re)
-template <>
-inline Cx dotc<Cx>(const Cx *a, const Cx *b, int64_t n) {
-    const double *ad = reinterpret_cast<const double *>(a);
-    const double *bd = reinterpret_cast<const double *>(b);
-    __m256d acc01 = _mm256_setzero_pd(), acc23 = _mm256_setzero_pd();  // (re, im, re, im)
-    int64_t k = 0;
-    for (; k + 4 <= n; k += 4) {
-        for (int h = 0; h < 2; ++h) {
-            const __m256d A = _mm256_loadu_pd(ad + 2 * (k + 2 * h));
-            const __m256d B = _mm256_loadu_pd(bd + 2 * (k + 2 * h));
-            const __m256d p = _mm256_mul_pd(A, B);                           // ar br, ai bi
-            const __m256d q = _mm256_mul_pd(A, _mm256_permute_pd(B, 0x5));   // ar bi, ai br
-            const __m256d re = _mm256_hadd_pd(p, p);                          // ar br + ai bi
-            const __m256d im = _mm256_hsub_pd(q, q);                          // ar bi - ai br
-            const __m256d v = _mm256_blend_pd(re, im, 0xA);
-            if (h == 0)
-                acc01 = _mm256_add_pd(acc01, v);
-            else
-                acc23 = _mm256_add_pd(acc23, v);
-        }
-    }
-    double l01[4], l23[4];
-    _mm256_storeu_pd(l01, acc01);
-    _mm256_storeu_pd(l23, acc23);
-    double r[4] = {l01[0], l01[2], l23[0], l23[2]}, i[4] = {l01[1], l01[3], l23[1], l23[3]};
-    for (; k < n; ++k) {
-        r[0] += a[k].re * b[k].re + a[k].im * b[k].im;
-        i[0] += a[k].re * b[k].im - a[k].im * b[k].re;
-    }
-    return {(r[0] + r[1]) + (r[2] + r[3]), (i[0] + i[1]) + (i[2] + i[3])};
-}
-#endif
 
 // np.argmax(np.abs(x)) with masked entries read as 0.0 (first index wins
 // ties). Complex magnitudes are hypot as numpy's; a squared-magnitude pass
