@@ -374,18 +374,35 @@ int gcabem_gca_sizes(gcabem_gca_t G, int64_t *ranks, double *phase4) {
 
 int gcabem_gca_fetch(gcabem_gca_t G, int64_t *rows, double *V) {
     if (!G) return gcabem_internal_error(GCABEM_ERR_ARG, "null handle");
-    int64_t ro = 0, vo = 0;
+    // offsets, then a threaded copy (the caller's fresh buffer is
+    // page-faulted by the copying threads in parallel)
+    std::vector<int64_t> ro(G->ncl + 1, 0), vo(G->ncl + 1, 0);
     for (int64_t c = 0; c < G->ncl; ++c) {
-        std::copy(G->rows[c].begin(), G->rows[c].end(), rows + ro);
-        ro += (int64_t)G->rows[c].size();
-        std::copy(G->V[c].begin(), G->V[c].end(), V + vo);
-        vo += (int64_t)G->V[c].size();
+        ro[c + 1] = ro[c] + (int64_t)G->rows[c].size();
+        vo[c + 1] = vo[c] + (int64_t)G->V[c].size();
     }
+    const int nt = (int)std::min<int64_t>(16, std::max<int64_t>(1, G->ncl / 256));
+    std::atomic<int64_t> next{0};
+    auto work = [&]() {
+        for (;;) {
+            const int64_t c0 = next.fetch_add(64);
+            if (c0 >= G->ncl) return;
+            for (int64_t c = c0; c < std::min<int64_t>(G->ncl, c0 + 64); ++c) {
+                std::copy(G->rows[c].begin(), G->rows[c].end(), rows + ro[c]);
+                std::copy(G->V[c].begin(), G->V[c].end(), V + vo[c]);
+            }
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work);
+    work();
+    for (auto &t : th) t.join();
     return GCABEM_OK;
 }
 
 int gcabem_gca_free(gcabem_gca_t G) {
-    delete G;
+    // hundreds of MB in thousands of blocks: release them off the caller's path
+    if (G) std::thread([G]() { delete G; }).detach();
     return GCABEM_OK;
 }
 
