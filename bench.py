@@ -349,12 +349,14 @@ def run_ours_p1(args, cfg, dist, log):
     ms_max = dist.max(ms)
     value = pairs * dist.world / (ms_max * 1e-3)
     local_ms = statistics.mean(t["local"] for t in per)
-    from paper_1510_07244_b200.roofline import pair_flops
+    from paper_1510_07244_b200.roofline import p1_pair_flops
     nd = plan.num_pairs - plan.num_singular
     sq = plan.singular_q
     counts = [int(np.count_nonzero(plan.packages.item_case == c)) for c in (1, 2, 3)]
-    fl = pair_flops(spec, "disjoint", cfg["orders"][0] ** 4) * nd + \
-        sum(pair_flops(spec, "singular", q) * c for q, c in zip(sq, counts))
+    n0 = cfg["orders"][0]
+    fl = p1_pair_flops(spec, "disjoint", n0 ** 4, n0) * nd + \
+        sum(p1_pair_flops(spec, "singular", q, cfg["orders"][1]) * c
+            for q, c in zip(sq, counts))
     from paper_1510_07244_b200 import device as devmod
     peak = devmod.fp64_peak_tflops(device)
     achieved = fl / (local_ms * 1e-3) / 1e12
@@ -376,8 +378,8 @@ def run_ours_p1(args, cfg, dist, log):
                    "parallelism": f"weak x{dist.world}, no collectives"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
-                     "kernel": "p1 local matrices (P0 algorithmic flops per pair; the 3x3 "
-                               "basis weighting is not credited)",
+                     "kernel": "p1 local matrices (disjoint + singular launches; flops per "
+                               "roofline.p1_pair_flops: P0 point work + the basis weighting)",
                      "peak_source": "measured DFMA probe (gcabem_fp64_probe), this device"},
         "e2e": {"value": pairs * dist.world / e2e_dt, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_dt},

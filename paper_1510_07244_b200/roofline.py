@@ -24,3 +24,21 @@ def point_flops(spec, family: str) -> int:
 def pair_flops(spec, family: str, q: int) -> int:
     """Flops of one pair integral with a Q-point rule."""
     return q * point_flops(spec, family) + PAIR_OVERHEAD
+
+
+def p1_pair_flops(spec, family: str, q: int, order: int) -> int:
+    """Flops of one P1 local (3 x 3) matrix with a Q-point rule: the P0 point
+    work plus the basis weighting the minimal algorithm must do. Disjoint
+    (factored) rule: per point 3 real-weighted accumulations of the kernel
+    value (2 flops each, x2 for complex), per x point 9 accumulations of the
+    y-side sums (36 flops complex / 18 real) shared by the N^2 y points.
+    Singular rules: per point the two barycentric triples (4), the weight
+    products (3), 3 scalings of the kernel value and 9 accumulations
+    (complex: 6 + 36; real: 3 + 18). Per pair the 9 Gramian scalings."""
+    cplx = spec.equation == "helmholtz"
+    base = point_flops(spec, family)
+    if family == "disjoint":
+        extra = (12 if cplx else 6) + (36 if cplx else 18) / (order * order)
+    else:
+        extra = 7 + (42 if cplx else 21)
+    return int(q * (base + extra)) + 9 * PAIR_OVERHEAD
