@@ -218,7 +218,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     tr.mark("sync");
     cudaEvent_t done[SLOTS] = {};
     for (int k = 0; k < SLOTS && e == cudaSuccess; ++k)
-        e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+        e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming | cudaEventBlockingSync);
 
     // batch b uses slot b % SLOTS (tasks, offsets, device output, staging)
     auto enqueue = [&](int64_t b) -> cudaError_t {
