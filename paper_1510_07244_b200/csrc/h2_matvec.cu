@@ -94,26 +94,38 @@ tmatvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict_
 }
 
 // out[out_at[it] + r] = sum_j M[r, j] v[v_at + j] (M row-major rows x cols):
-// one thread per ROW of the whole batch (tasks are the flattened rows of all
-// items, in item order): a warp streams 32 consecutive rows, which for
-// consecutive leaves are consecutive in the payload buffer -- no idle lanes
-// for 16-row leaves, each thread's row a contiguous run of cache lines.
+// RPG lanes per row over the flattened rows of the batch (tasks are rows, in
+// item order): lane g of a row group reads columns g, g + RPG, ..., so one
+// load instruction covers 32 / RPG rows x RPG consecutive elements (full
+// 128 B segments), then a fixed butterfly over the group -- deterministic.
+constexpr int RPG = 8;
 __global__ void __launch_bounds__(MV_TPB)
 matvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_r0,
               int64_t ntasks, const int64_t *__restrict__ m_at, const int32_t *__restrict__ rows,
               const int32_t *__restrict__ cols, const int64_t *__restrict__ v_at,
               const int64_t *__restrict__ out_at, const double2 *__restrict__ M,
               const double2 *__restrict__ v, double2 *__restrict__ out) {
-    const int64_t t = (int64_t)blockIdx.x * MV_TPB + threadIdx.x;
-    if (t >= ntasks) return;
-    const int64_t it = task_item[t];
-    const int r = task_r0[t];
-    const int nc = cols[it];
-    const double2 *Mr = M + m_at[it] + (int64_t)r * nc;
-    const double2 *vv = v + v_at[it];
+    const int64_t gt = (int64_t)blockIdx.x * MV_TPB + threadIdx.x;
+    const int64_t t = gt / RPG;
+    const int g = (int)(gt % RPG);
+    const bool live = t < ntasks;
     double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j < nc; ++j) acc = cmac(acc, Mr[j], vv[j]);
-    out[out_at[it] + r] = acc;
+    int64_t it = 0;
+    int r = 0;
+    if (live) {
+        it = task_item[t];
+        r = task_r0[t];
+        const int nc = cols[it];
+        const double2 *Mr = M + m_at[it] + (int64_t)r * nc;
+        const double2 *vv = v + v_at[it];
+        for (int j = g; j < nc; j += RPG) acc = cmac(acc, Mr[j], vv[j]);
+    }
+#pragma unroll
+    for (int o = RPG / 2; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (live && g == 0) out[out_at[it] + r] = acc;
 }
 
 // CSR gather-sum: out[i] = sum_{p in [at[i], at[i+1])} src[idx[p]] (in order)
@@ -362,7 +374,7 @@ cudaError_t run_matvec(gcabem_h2_s *H, Batch &b, const double2 *M, const double2
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
             b.d_out_at.p, M, v, out);
     else
-        matvec_kernel<<<(unsigned)((nt + MV_TPB - 1) / MV_TPB), MV_TPB, 0, H->stream>>>(
+        matvec_kernel<<<(unsigned)((nt * RPG + MV_TPB - 1) / MV_TPB), MV_TPB, 0, H->stream>>>(
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
             b.d_out_at.p, M, v, out);
     return cudaGetLastError();
