@@ -50,47 +50,77 @@ __device__ __forceinline__ double2 cmac(double2 acc, double2 a, double2 b) {
     return acc;
 }
 
-// xs = M^T v for one item per CTA (M row-major nrows x width, width <=
-// TM_MAX): warp w takes rows w, w + 4, ...; lane l owns components l, l + 32,
-// ... (a row read is coalesced); the four warps' partial sums are added in
-// warp order at the end -- fixed association, deterministic.
+// xs = M^T v (M row-major nrows x width, width <= TM_MAX), split into
+// tasks of TM_ROWS rows: warp w of the task's CTA takes rows w, w + 4, ...;
+// lane l owns components l, l + 32, ... (a row read is coalesced); the
+// warps' partials are added in warp order into the task's partial vector,
+// and treduce_kernel sums the tasks of an item in task order -- fixed
+// association, deterministic, and a large cluster spreads over many CTAs.
 constexpr int TM_MAX = 128;
+constexpr int TM_ROWS = 128;
 __global__ void __launch_bounds__(MV_TPB)
-tmatvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_k0,
+tmatvec_kernel(const int64_t *__restrict__ task_item, const int32_t *__restrict__ task_r0,
                int64_t ntasks, const int64_t *__restrict__ m_at,
                const int32_t *__restrict__ nrows, const int32_t *__restrict__ width,
-               const int64_t *__restrict__ v_at, const int64_t *__restrict__ out_at,
+               const int64_t *__restrict__ v_at, const int64_t *__restrict__ part_at,
                const double2 *__restrict__ M, const double2 *__restrict__ v,
-               double2 *__restrict__ out) {
-    __shared__ double2 part[MV_TPB / 32][TM_MAX];
+               double2 *__restrict__ part) {
+    __shared__ double2 sp[MV_TPB / 32][TM_MAX];
     const int64_t t = blockIdx.x;
     if (t >= ntasks) return;
     const int64_t it = task_item[t];
     const int w = width[it], n = nrows[it];
+    const int r0 = task_r0[t], r1 = min(n, r0 + TM_ROWS);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double2 *Mi = M + m_at[it];
     const double2 *vi = v + v_at[it];
     double2 acc[TM_MAX / 32];
 #pragma unroll
     for (int q = 0; q < TM_MAX / 32; ++q) acc[q] = make_double2(0.0, 0.0);
-    for (int i = warp; i < n; i += MV_TPB / 32) {
+    for (int i = r0 + warp; i < r1; i += MV_TPB / 32) {
         const double2 x = vi[i];
 #pragma unroll
         for (int q = 0; q < TM_MAX / 32; ++q)
             if (lane + 32 * q < w) acc[q] = cmac(acc[q], Mi[(int64_t)i * w + lane + 32 * q], x);
     }
 #pragma unroll
-    for (int q = 0; q < TM_MAX / 32; ++q) part[warp][lane + 32 * q] = acc[q];
+    for (int q = 0; q < TM_MAX / 32; ++q) sp[warp][lane + 32 * q] = acc[q];
     __syncthreads();
     for (int k = threadIdx.x; k < w; k += MV_TPB) {
-        double2 s = part[0][k];
+        double2 s = sp[0][k];
 #pragma unroll
         for (int q = 1; q < MV_TPB / 32; ++q) {
-            s.x += part[q][k].x;
-            s.y += part[q][k].y;
+            s.x += sp[q][k].x;
+            s.y += sp[q][k].y;
         }
-        out[out_at[it] + k] = s;
+        part[part_at[t] + k] = s;
     }
+}
+
+// out[out_at[it] + k] = sum over the item's tasks (in order) of their partials
+__global__ void treduce_kernel(const int64_t *__restrict__ item_task_at,
+                               const int64_t *__restrict__ part_at,
+                               const int32_t *__restrict__ width,
+                               const int64_t *__restrict__ out_at, const int64_t *__restrict__ ek_at,
+                               int64_t nitems, int64_t nk, const double2 *__restrict__ part,
+                               double2 *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * MV_TPB + threadIdx.x;
+    if (e >= nk) return;
+    // item of component e: binary search in ek_at (prefix of widths)
+    int64_t lo = 0, hi = nitems;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ek_at[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int64_t it = lo;
+    const int k = (int)(e - ek_at[it]);
+    double2 s = make_double2(0.0, 0.0);
+    for (int64_t t = item_task_at[it]; t < item_task_at[it + 1]; ++t) {
+        const double2 p = part[part_at[t] + k];
+        s.x += p.x;
+        s.y += p.y;
+    }
+    out[out_at[it] + k] = s;
 }
 
 // out[out_at[it] + r] = sum_j M[r, j] v[v_at + j] (M row-major rows x cols):
@@ -193,7 +223,10 @@ struct gcabem_h2_s {
     DevBuf<double2> payload, V, xh, xp, xs, yp, cbuf, wbuf, zbuf;
     DevBuf<int32_t> row_perm, col_perm;
     DevBuf<int64_t> z_at, z_idx, y_at, y_idx;
-    Batch colop;   // xs_s = V_s^T xp[s]            (tmatvec)
+    Batch colop;   // xs_s = V_s^T xp[s]            (tmatvec, TM_ROWS-row tasks)
+    DevBuf<int64_t> d_part_at, d_item_task_at, d_ek_at;
+    DevBuf<double2> part;
+    int64_t nk = 0;
     Batch leafmv;  // dense leaves: c = P xp[s]      (matvec)
     Batch coup;    // admissible leaves: w = P xs_s  (matvec)
     Batch rowop;   // u_t = V_t z_t                  (matvec)
@@ -239,7 +272,7 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
             delete H;
             return fail("h2_create: rank above 128");
         }
-        H->colop.add(d[3], (int32_t)d[1], (int32_t)d[2], d[0], xs_at[o], 0, 0);
+        H->colop.add(d[3], (int32_t)d[1], (int32_t)d[2], d[0], xs_at[o], (int32_t)d[1], TM_ROWS);
     }
     // leaves: dense rows into cbuf, admissible rows into wbuf
     std::vector<int64_t> c_at(nleaves, -1), w_at(nleaves, -1);
@@ -350,6 +383,21 @@ int gcabem_h2_create(int device, int64_t nrows, int64_t ncols, const int64_t *ro
     if (e == cudaSuccess) e = H->y_at.upload(y_at_h.data(), y_at_h.size(), s);
     if (e == cudaSuccess) e = H->y_idx.upload(y_idx_h.data(), std::max<size_t>(y_idx_h.size(), 1), s);
     if (e == cudaSuccess) e = H->colop.upload(s);
+    {   // partial-sum layout of the chunked transposed products
+        const Batch &b = H->colop;
+        std::vector<int64_t> part_at(b.task_item.size() + 1, 0), item_task_at(ncolops + 1, 0);
+        for (size_t t = 0; t < b.task_item.size(); ++t) {
+            part_at[t + 1] = part_at[t] + b.cols[b.task_item[t]];
+            item_task_at[b.task_item[t] + 1] = (int64_t)t + 1;
+        }
+        for (int64_t o = 0; o < ncolops; ++o)
+            item_task_at[o + 1] = std::max(item_task_at[o + 1], item_task_at[o]);
+        H->nk = xs_at[ncolops];
+        if (e == cudaSuccess) e = H->d_part_at.upload(part_at.data(), part_at.size(), s);
+        if (e == cudaSuccess) e = H->d_item_task_at.upload(item_task_at.data(), item_task_at.size(), s);
+        if (e == cudaSuccess) e = H->d_ek_at.upload(xs_at.data(), xs_at.size(), s);
+        if (e == cudaSuccess) e = H->part.alloc(std::max<int64_t>(part_at.back(), 1));
+    }
     if (e == cudaSuccess) e = H->leafmv.upload(s);
     if (e == cudaSuccess) e = H->rowop.upload(s);
     if (e == cudaSuccess) e = coup.upload(s);
@@ -369,11 +417,16 @@ cudaError_t run_matvec(gcabem_h2_s *H, Batch &b, const double2 *M, const double2
                        double2 *out, bool transposed) {
     const int64_t nt = b.ntasks();
     if (nt == 0) return cudaSuccess;
-    if (transposed)
+    if (transposed) {
         tmatvec_kernel<<<(unsigned)nt, MV_TPB, 0, H->stream>>>(
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
-            b.d_out_at.p, M, v, out);
-    else
+            H->d_part_at.p, M, v, H->part.p);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || H->nk == 0) return e;
+        treduce_kernel<<<(unsigned)((H->nk + MV_TPB - 1) / MV_TPB), MV_TPB, 0, H->stream>>>(
+            H->d_item_task_at.p, H->d_part_at.p, b.d_cols.p, b.d_out_at.p, H->d_ek_at.p,
+            (int64_t)b.m_at.size(), H->nk, H->part.p, out);
+    } else
         matvec_kernel<<<(unsigned)((nt * RPG + MV_TPB - 1) / MV_TPB), MV_TPB, 0, H->stream>>>(
             b.d_task_item.p, b.d_task_r0.p, nt, b.d_m_at.p, b.d_rows.p, b.d_cols.p, b.d_v_at.p,
             b.d_out_at.p, M, v, out);
