@@ -328,6 +328,7 @@ def run_ours_p1(args, cfg, dist, log):
     t0 = time.perf_counter()
     A = plan.assemble()
     t_first = time.perf_counter() - t0
+    del A
     pairs = plan.num_pairs
     log(f"c4: nt={m.num_triangles} nv={m.num_vertices} near pairs={pairs} "
         f"singular={plan.num_singular} nnz={plan.nnz} plan {t_plan:.3f}s first {t_first:.3f}s")
@@ -362,6 +363,7 @@ def run_ours_p1(args, cfg, dist, log):
     achieved = fl / (local_ms * 1e-3) / 1e12
     e2e_t = []
     for _ in range(max(1, args.e2e_steps)):
+        A = None  # release the previous matrix: its pinned buffers return to the pool
         t0 = time.perf_counter()
         A = plan.assemble()
         e2e_t.append(time.perf_counter() - t0)

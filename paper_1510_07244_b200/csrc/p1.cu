@@ -203,6 +203,53 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
 }
 
 // --- generic rule (singular items, index batches) ---------------------------
+// the singular-rule point loop of one pair (rule staged through shared
+// memory in chunks; every thread walks the same points)
+template <int KIND, int PH>
+__device__ __forceinline__ void p1_generic_rule(bool valid, const double dO[3],
+                                                const double e1x[3], const double e2x[3],
+                                                const double e1y[3], const double e2y[3],
+                                                const double ny[3], const double *__restrict__ rule,
+                                                int64_t q, double kappa, double phi0,
+                                                double acc[9][2]) {
+    __shared__ double sr[RULE_CHUNK * 5];
+    for (int64_t base = 0; base < q; base += RULE_CHUNK) {
+        const int cnt = (int)min((int64_t)RULE_CHUNK, q - base);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cnt * 5; e += blockDim.x) sr[e] = rule[base * 5 + e];
+        __syncthreads();
+        if (!valid) continue;
+        for (int k = 0; k < cnt; ++k) {
+            const double xs = sr[5 * k], xt = sr[5 * k + 1];
+            const double ys = sr[5 * k + 2], yt = sr[5 * k + 3], w = sr[5 * k + 4];
+            double d[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double xp = fma(xt, e2x[c], fma(xs, e1x[c], dO[c]));
+                d[c] = fma(-yt, e2y[c], fma(-ys, e1y[c], xp));
+            }
+            const double r2 = fma(d[0], d[0], fma(d[1], d[1], d[2] * d[2]));
+            double dn = 0.0;
+            if (KIND == L_DLP || KIND == H_DLP)
+                dn = fma(d[0], ny[0], fma(d[1], ny[1], d[2] * ny[2]));
+            double kr, ki;
+            point_value<KIND, PH>(r2, dn, kappa, phi0, kr, ki);
+            const double lx[3] = {1.0 - xs, xs - xt, xt};
+            const double ly[3] = {w * (1.0 - ys), w * (ys - yt), w * yt};
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                const double ur = ly[b] * kr, ui = ly[b] * ki;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    acc[3 * a + b][0] = fma(lx[a], ur, acc[3 * a + b][0]);
+                    if (KIND == H_SLP || KIND == H_DLP)
+                        acc[3 * a + b][1] = fma(lx[a], ui, acc[3 * a + b][1]);
+                }
+            }
+        }
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(GENERIC_TPB)
 p1_generic_kernel(const double *__restrict__ V, const int32_t *__restrict__ T,
@@ -237,43 +284,30 @@ p1_generic_kernel(const double *__restrict__ V, const int32_t *__restrict__ T,
     double acc[9][2];
 #pragma unroll
     for (int e = 0; e < 9; ++e) acc[e][0] = acc[e][1] = 0.0;
-    __shared__ double sr[RULE_CHUNK * 5];
-    for (int64_t base = 0; base < q; base += RULE_CHUNK) {
-        const int cnt = (int)min((int64_t)RULE_CHUNK, q - base);
-        __syncthreads();
-        for (int e = threadIdx.x; e < cnt * 5; e += blockDim.x) sr[e] = rule[base * 5 + e];
-        __syncthreads();
-        if (!valid) continue;
-        for (int k = 0; k < cnt; ++k) {
-            const double xs = sr[5 * k], xt = sr[5 * k + 1];
-            const double ys = sr[5 * k + 2], yt = sr[5 * k + 3], w = sr[5 * k + 4];
-            double d[3];
+    // Helmholtz phase about the centroid distance, tier CTA-uniform (the
+    // rule loop stages shared memory with __syncthreads), as generic_kernel
+    constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
+    double phi0 = 0.0;
+    int tier = 0;
+    if constexpr (HELM) {
+        double dc[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double xp = fma(xt, e2x[c], fma(xs, e1x[c], dO[c]));
-                d[c] = fma(-yt, e2y[c], fma(-ys, e1y[c], xp));
-            }
-            const double r2 = fma(d[0], d[0], fma(d[1], d[1], d[2] * d[2]));
-            double dn = 0.0;
-            if (KIND == L_DLP || KIND == H_DLP)
-                dn = fma(d[0], ny[0], fma(d[1], ny[1], d[2] * ny[2]));
-            double kr, ki;
-            point_value<KIND, 0>(r2, dn, kappa, 0.0, kr, ki);
-            const double lx[3] = {1.0 - xs, xs - xt, xt};
-            const double ly[3] = {w * (1.0 - ys), w * (ys - yt), w * yt};
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                const double ur = ly[b] * kr, ui = ly[b] * ki;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    acc[3 * a + b][0] = fma(lx[a], ur, acc[3 * a + b][0]);
-                    if (KIND == H_SLP || KIND == H_DLP)
-                        acc[3 * a + b][1] = fma(lx[a], ui, acc[3 * a + b][1]);
-                }
-            }
-        }
+        for (int c = 0; c < 3; ++c)
+            dc[c] = fma(1.0 / 3.0, (2.0 * e1x[c] + e2x[c]) - (2.0 * e1y[c] + e2y[c]), dO[c]);
+        phi0 = kappa * norm3(dc[0], dc[1], dc[2]);
+        const double rsum = valid ? charts[it.tri_x].radius + charts[it.tri_y].radius : 0.0;
+        if (__syncthreads_and(!valid || kappa * rsum <= TINY_PHASE_MAX))
+            tier = 2;
+        else if (__syncthreads_and(!valid || kappa * rsum <= SMALL_PHASE_MAX))
+            tier = 1;
     }
-    if (valid) p1_finish<KIND>(acc, gx, gy, false, 0.0, it.px, it.py, local + 9 * it.out);
+    if (tier == 2)
+        p1_generic_rule<KIND, 2>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, phi0, acc);
+    else if (tier == 1)
+        p1_generic_rule<KIND, 1>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, phi0, acc);
+    else
+        p1_generic_rule<KIND, 0>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, 0.0, acc);
+    if (valid) p1_finish<KIND>(acc, gx, gy, tier > 0, phi0, it.px, it.py, local + 9 * it.out);
 }
 
 // --- scatter plan and gather-sum --------------------------------------------
