@@ -88,6 +88,30 @@ class _LeafSubset:
             yield self._leaves[int(k)]
 
 
+class VertexCSR:
+    """The P1 near-field matrix (vertex x vertex) as raw CSR arrays in pinned
+    host memory: indptr, indices (int32, ascending per row), data
+    (complex128). to_scipy() wraps them without copying (scipy's format
+    checks cost more than the device assembly at C4, so they are not paid on
+    the assembly path)."""
+
+    def __init__(self, indptr, indices, data, n):
+        self.indptr, self.indices, self.data = indptr, indices, data
+        self.shape = (n, n)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indices.size)
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        ip = self.indptr.astype(np.int32) if self.nnz < 2 ** 31 - 1 else self.indptr
+        return sp.csr_matrix((self.data, self.indices, ip), shape=self.shape, copy=False)
+
+    def toarray(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+
 class NearFieldP1:
     """Device plan of the P1 near-field matrix of one kernel: packages of the
     dense leaves, the scatter plan (CSR pattern + contribution order), and
@@ -143,15 +167,11 @@ class NearFieldP1:
         res = (indptr, indices[:self.nnz], data[:self.nnz])
         return res + (local,) if with_local else res
 
-    def assemble(self):
-        """execute() + the near-field matrix as scipy.sparse.csr_matrix (nv x nv)."""
-        import scipy.sparse as sp
+    def assemble(self) -> VertexCSR:
+        """execute() + the near-field matrix (VertexCSR; .to_scipy() for scipy)."""
         self.execute()
         indptr, indices, data = self.download()
-        n = self.num_vertices
-        if self.nnz < 2 ** 31 - 1:  # int32 index arrays: scipy keeps the buffers (no copy)
-            indptr = indptr.astype(np.int32)
-        return sp.csr_matrix((data, indices, indptr), shape=(n, n), copy=False)
+        return VertexCSR(indptr, indices, data, self.num_vertices)
 
     def close(self) -> None:
         h, self.handle = getattr(self, "handle", None), None
@@ -166,8 +186,8 @@ class NearFieldP1:
 
 
 def assemble_near_field(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
-                        orders=(3, 5), device: int | None = None):
-    """P1 near-field matrix (scipy CSR, vertex x vertex) of `spec` on the device."""
+                        orders=(3, 5), device: int | None = None) -> VertexCSR:
+    """P1 near-field matrix (vertex x vertex CSR) of `spec` on the device."""
     plan = NearFieldP1(mesh, block_tree, spec, orders, device)
     try:
         return plan.assemble()
