@@ -44,6 +44,12 @@ int gcabem_device_count(int *count);
 /* name (>= 256 bytes), SM count, SM clock kHz */
 int gcabem_device_info(int device, char *name, int *sm_count, int *clock_khz);
 
+/* Return the caches the library keeps across calls to the driver: the
+ * device memory pool's free blocks (payloads and layouts are pool
+ * allocations that stay cached), the GCA staging ring and the pinned layout
+ * arena of `device`. Live plans, layouts and matrices are unaffected. */
+int gcabem_release_cached(int device);
+
 /* Pinned host memory for payload buffers (cudaHostAlloc / cudaFreeHost). */
 int gcabem_host_alloc(int64_t nbytes, void **ptr);
 int gcabem_host_free(void *ptr);

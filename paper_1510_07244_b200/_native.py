@@ -39,6 +39,7 @@ _SIGS = {
                            _int),
     "gcabem_host_alloc": ([_i64, ctypes.POINTER(_vp)], _int),
     "gcabem_host_free": ([_vp], _int),
+    "gcabem_release_cached": ([_int], _int),
     "gcabem_pair_values": ([_int, _int, _int, _dbl, _i64] + [_vp] * 9 + [_i64] + [_vp] * 4, _int),
     "gcabem_mesh_create": ([_int, _i64, _vp, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)], _int),
     "gcabem_mesh_destroy": ([_vp], _int),
@@ -213,6 +214,11 @@ class _PinnedPool:
 
 
 _POOL = _PinnedPool()
+
+
+def pinned_pool_clear() -> None:
+    """Free the cached (unused) pinned blocks."""
+    _POOL.clear()
 
 
 class _PinnedBlock:

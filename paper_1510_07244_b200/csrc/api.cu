@@ -962,6 +962,22 @@ int gcabem_potential(gcabem_mesh_t mesh, int equation, int layer, double kappa, 
     return GCABEM_OK;
 }
 
+int gcabem_release_cached(int device) {
+    GC_CUDA(cudaSetDevice(device));
+    GC_CUDA(cudaDeviceSynchronize());
+    gca_release_staging(device);
+    {
+        std::lock_guard<std::mutex> lock(g_arena_mutex);
+        if (g_arena) cudaFreeHost(g_arena);
+        g_arena = nullptr;
+        g_arena_bytes = 0;
+    }
+    cudaMemPool_t pool;
+    GC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    GC_CUDA(cudaMemPoolTrimTo(pool, 0));
+    return GCABEM_OK;
+}
+
 int gcabem_fp64_probe(int device, double *tflops) {
     GC_ARG(tflops, "null argument");
     GC_CUDA(cudaSetDevice(device));

@@ -78,6 +78,18 @@ Staging &staging_for(int device) {
 
 }  // namespace
 
+void gcabem::gca_release_staging(int device) {
+    Staging *st = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_staging_mutex);
+        if (device < (int)g_staging.size()) std::swap(st, g_staging[device]);
+    }
+    if (st) {
+        std::lock_guard<std::mutex> busy(st->busy);  // wait for a running build
+    }
+    delete st;
+}
+
 extern "C" {
 
 int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl,

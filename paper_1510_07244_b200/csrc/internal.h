@@ -68,6 +68,8 @@ struct DevBuf {
 // payloads of hundreds of MB are allocated and released per assembly call,
 // and cudaMalloc/cudaFree of that size cost milliseconds each.
 cudaError_t pool_init(int device);
+// free the GCA pipeline's staging ring of `device` (gca_pipeline.cu)
+void gca_release_staging(int device);
 
 template <typename T>
 struct PoolBuf {

@@ -43,29 +43,25 @@ __device__ __forceinline__ void point_value(double r2, double dn, double kappa, 
     point_accumulate<KIND, PH>(r2, dn, 1.0, kappa, phi0, re, im);
 }
 
-// --- disjoint rule, factored (x = (a, ab), y = (c, cd)) ----------------------
-// EXP: the expanded r^2 = |xo|^2 - 2 g_c (xo . u_d) + g_c^2 |u_d|^2 (2 DFMA per
-// point, taken under the same per-warp guard as disjoint_kernel), else the
-// direct form d = xo - g_c u_d.
-template <int N, int KIND, int PH, bool EXP>
+// --- disjoint rule, factored (x = (a, ab), y = (c, cd)), direct form -------
+// (the expanded r^2 form of disjoint_kernel measured slower here: with 18
+// accumulators the kernel is register-bound, 254 vs 242 registers)
+template <int N, int KIND, int PH>
 __device__ __forceinline__ void p1_disjoint_pair(const double dO[3], const double e1x[3],
                                                  const double e2x[3], const double e1y[3],
                                                  const double e2y[3], const double n[3],
                                                  double kappa, double phi0, double acc[9][2]) {
     constexpr bool DL = (KIND == L_DLP || KIND == H_DLP);
     constexpr bool CPLX = (KIND == H_SLP || KIND == H_DLP);
-    double ux[N], uy[N], uz[N], uu[N], un[N];
+    double ux[N], uy[N], uz[N], un[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) {
         const double gd = c_gauss[N][d];
         ux[d] = fma(gd, e2y[0], e1y[0]);
         uy[d] = fma(gd, e2y[1], e1y[1]);
         uz[d] = fma(gd, e2y[2], e1y[2]);
-        uu[d] = EXP ? fma(ux[d], ux[d], fma(uy[d], uy[d], uz[d] * uz[d])) : 0.0;
         un[d] = DL ? fma(ux[d], n[0], fma(uy[d], n[1], uz[d] * n[2])) : 0.0;
     }
-    const double f1[3] = {-2.0 * e1y[0], -2.0 * e1y[1], -2.0 * e1y[2]};
-    const double f2[3] = {-2.0 * e2y[0], -2.0 * e2y[1], -2.0 * e2y[2]};
 #pragma unroll 1
     for (int p = 0; p < N * N; ++p) {
         const double s = c_gauss[N][p / N];
@@ -75,12 +71,6 @@ __device__ __forceinline__ void p1_disjoint_pair(const double dO[3], const doubl
         const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
-        double xx = 0.0, a2 = 0.0, b2 = 0.0;
-        if (EXP) {
-            xx = fma(xo0, xo0, fma(xo1, xo1, xo2 * xo2));
-            a2 = fma(xo0, f1[0], fma(xo1, f1[1], xo2 * f1[2]));
-            b2 = fma(xo0, f2[0], fma(xo1, f2[1], xo2 * f2[2]));
-        }
         double in[3][2] = {{0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
         for (int c = 0; c < N; ++c) {
@@ -89,15 +79,10 @@ __device__ __forceinline__ void p1_disjoint_pair(const double dO[3], const doubl
             for (int d = 0; d < N; ++d) {
                 const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
                 const double ty = c_duffy_t[duffy_offset(N) + c * N + d];  // = gc gd
-                double r2;
-                if (EXP) {
-                    r2 = fma(gc, fma(gc, uu[d], fma(c_gauss[N][d], b2, a2)), xx);
-                } else {
-                    const double dx = fma(-gc, ux[d], xo0);
-                    const double dy = fma(-gc, uy[d], xo1);
-                    const double dz = fma(-gc, uz[d], xo2);
-                    r2 = fma(dx, dx, fma(dy, dy, dz * dz));
-                }
+                const double dx = fma(-gc, ux[d], xo0);
+                const double dy = fma(-gc, uy[d], xo1);
+                const double dz = fma(-gc, uz[d], xo2);
+                const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
                 double kr, ki;
                 point_value<KIND, PH>(r2, dn, kappa, phi0, kr, ki);
@@ -192,11 +177,6 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     const double dmax = HELM && active ? kappa * (cx->radius + cy->radius) : 0.0;
     const bool tiny = __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
     const bool smallp = __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
-    // expanded-form guard of disjoint_kernel, voted per warp
-    const double rmin = norm3(dc[0], dc[1], dc[2]) - cx->radius - cy->radius;
-    const double S = norm3(dO[0], dO[1], dO[2]) + cx->enorm + cy->enorm;
-    const bool expanded = __all_sync(
-        0xffffffffu, !active || (rmin > 0.0 && S * S <= EXPANDED_MAX_RATIO * rmin * rmin));
     if (!active) {
         // singular pairs are overwritten by the singular pass; keep them 0
         if (inb)
@@ -210,21 +190,14 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     if constexpr (HELM) {
         const int ph = tiny ? 2 : (smallp ? 1 : 0);
         rot = ph > 0;
-        const double ph0 = rot ? phi0 : 0.0;
-        if (expanded) {
-            if (ph == 2) p1_disjoint_pair<N, KIND, 2, true>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-            else if (ph == 1) p1_disjoint_pair<N, KIND, 1, true>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-            else p1_disjoint_pair<N, KIND, 0, true>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-        } else {
-            if (ph == 2) p1_disjoint_pair<N, KIND, 2, false>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-            else if (ph == 1) p1_disjoint_pair<N, KIND, 1, false>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-            else p1_disjoint_pair<N, KIND, 0, false>(dO, e1x, e2x, e1y, e2y, n, kappa, ph0, acc);
-        }
-    } else {
-        if (expanded)
-            p1_disjoint_pair<N, KIND, 0, true>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+        if (ph == 2)
+            p1_disjoint_pair<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
+        else if (ph == 1)
+            p1_disjoint_pair<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
         else
-            p1_disjoint_pair<N, KIND, 0, false>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+            p1_disjoint_pair<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+    } else {
+        p1_disjoint_pair<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
     }
     const uint8_t id[3] = {0, 1, 2};
     p1_finish<KIND>(acc, cx->gram, cy->gram, rot, phi0, id, id, dst);

@@ -82,3 +82,11 @@ def device_info(device: int = 0) -> dict:
 
 def as_i64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def release_cached(device: int = 0) -> None:
+    """Give the library's cross-call caches on `device` back to the driver
+    (device memory pool free blocks, GCA staging ring, pinned layout arena)."""
+    nat.require_device(device)
+    nat.check(nat.lib().gcabem_release_cached(device))
+    nat.pinned_pool_clear()

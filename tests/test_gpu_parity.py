@@ -448,3 +448,19 @@ def test_gca_multi_device_partition_equals_single():
     for c in one:
         assert np.array_equal(one[c].pivots_global, two[c].pivots_global)
         assert np.array_equal(one[c].V, two[c].V)
+
+
+def test_release_cached_then_reassemble(gload):
+    """Dropping the library's caches (pool, staging, arena) between two
+    assemblies changes nothing in the result."""
+    from paper_1510_07244_b200 import device as devmod
+    g = gload("gca_L3.npz")
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(g, "laplace")
+    spec = kernels.KernelSpec("laplace", "single", 0.0)
+    a = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
+    first = np.array(a.buffer)
+    del a
+    devmod.release_cached(0)
+    b = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
+    assert np.array_equal(first, b.buffer)
