@@ -481,16 +481,18 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     tr.mark("rules+local");
     // scatter plan: sort the 9 P entry keys, run-length encode, row pointers
     const int64_t E = 9 * P;
-    DevBuf<uint64_t> keys, keys_out, ukeys;
-    DevBuf<int32_t> vals, counts;
-    DevBuf<int64_t> d_nnz;
-    DevBuf<char> tmp;
+    // plan temporaries from the device pool (stream-ordered: tens of GB at C4,
+    // whose cudaMalloc/cudaFree would each synchronise the device)
+    PoolBuf<uint64_t> keys, keys_out, ukeys;
+    PoolBuf<int32_t> vals, counts;
+    PoolBuf<int64_t> d_nnz;
+    PoolBuf<char> tmp;
     int end_bit = 1;
     while (end_bit < 64 && ((uint64_t)1 << end_bit) < (uint64_t)mesh->nv * (uint64_t)mesh->nv)
         ++end_bit;
-    if (e == cudaSuccess) e = keys.alloc(std::max<int64_t>(E, 1));
-    if (e == cudaSuccess) e = keys_out.alloc(std::max<int64_t>(E, 1));
-    if (e == cudaSuccess) e = vals.alloc(std::max<int64_t>(E, 1));
+    if (e == cudaSuccess) e = keys.alloc(std::max<int64_t>(E, 1), s);
+    if (e == cudaSuccess) e = keys_out.alloc(std::max<int64_t>(E, 1), s);
+    if (e == cudaSuccess) e = vals.alloc(std::max<int64_t>(E, 1), s);
     if (e == cudaSuccess) e = p->src.alloc(std::max<int64_t>(E, 1));
     if (e == cudaSuccess && L->ntasks > 0) {
         p1_keys_kernel<<<(unsigned)L->ntasks, DISJOINT_TPB, 0, s>>>(
@@ -501,16 +503,16 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     if (e == cudaSuccess)
         e = cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_out.p, vals.p, p->src.p,
                                             (int)E, 0, end_bit, s);
-    if (e == cudaSuccess) e = ukeys.alloc(std::max<int64_t>(E, 1));
-    if (e == cudaSuccess) e = counts.alloc(E + 1);
-    if (e == cudaSuccess) e = d_nnz.alloc(1);
+    if (e == cudaSuccess) e = ukeys.alloc(std::max<int64_t>(E, 1), s);
+    if (e == cudaSuccess) e = counts.alloc(E + 1, s);
+    if (e == cudaSuccess) e = d_nnz.alloc(1, s);
     if (e == cudaSuccess)
         e = cub::DeviceRunLengthEncode::Encode(nullptr, tb2, keys_out.p, ukeys.p, counts.p,
                                                d_nnz.p, (int)E, s);
     if (e == cudaSuccess) e = p->seg.alloc(E + 1);
     if (e == cudaSuccess)
         e = cub::DeviceScan::ExclusiveSum(nullptr, tb3, counts.p, p->seg.p, (int)E + 1, s);
-    if (e == cudaSuccess) e = tmp.alloc(std::max(tb, std::max(tb2, tb3)));
+    if (e == cudaSuccess) e = tmp.alloc(std::max(tb, std::max(tb2, tb3)), s);
     if (e == cudaSuccess && E > 0)
         e = cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_out.p, vals.p, p->src.p,
                                             (int)E, 0, end_bit, s);
