@@ -8,5 +8,5 @@ if [ "${PROFILE:-0}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py > gpurun_out/launches.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:disjoint_kernel -c 2 -o gpurun_out/prof_disjoint -f python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 fi
-./tools/math_probe > gpurun_out/math_probe.json 2>&1
+[ -x tools/math_probe ] && ./tools/math_probe > gpurun_out/math_probe.json 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -3 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -8 gpurun_out/bench.err
