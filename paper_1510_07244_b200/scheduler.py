@@ -412,10 +412,13 @@ class AssemblyPlan:
         return {"disjoint": ms[0], "singular": ms[1], "total": ms[2]}
 
     def flops(self) -> dict:
-        """Algorithmic FP64 flops of one execute (SURVEY §8(d) convention)."""
+        """Algorithmic FP64 flops of one execute (SURVEY §8(d) convention). The
+        disjoint launch skips the pairs that share a vertex (it writes 0 and the
+        singular pass overwrites them), so they are not credited to it."""
         from .roofline import pair_flops
         dq = self.orders[0] ** 4
-        dis = pair_flops(self.spec, "disjoint", dq) * self.disjoint_pairs
+        computed = self.disjoint_pairs - sum(self.singular_counts)
+        dis = pair_flops(self.spec, "disjoint", dq) * computed
         sing = sum(pair_flops(self.spec, "singular", q) * n
                    for q, n in zip(self.singular_q, self.singular_counts))
         return {"disjoint": dis, "singular": sing}
