@@ -140,6 +140,14 @@ int gcabem_layout_release(gcabem_layout_t layout);
 int gcabem_plan_create_on(gcabem_layout_t layout, int equation, int layer, double kappa,
                           int disjoint_n, const double *gauss_pts, const double *gauss_wts,
                           const int64_t *sq, const double *const *srule, gcabem_plan_t *out);
+/* Fused plan of BOTH layers of one equation (the pipelines that need V and K,
+ * solver.py:279-282): every kernel evaluates r, 1/r and the phase once per
+ * quadrature point and accumulates the single and the double layer into two
+ * payloads (same layout). Download with gcabem_plan_execute_download2 /
+ * gcabem_plan_download2 (host = single layer, host2 = double layer). */
+int gcabem_plan_create_pair(gcabem_layout_t layout, int equation, double kappa, int disjoint_n,
+                            const double *gauss_pts, const double *gauss_wts, const int64_t *sq,
+                            const double *const *srule, gcabem_plan_t *out);
 /* Launch all kernels on the plan stream (async). The payload is zeroed first
  * (make_payloads semantics), then disjoint, then singular overwrites. */
 int gcabem_plan_execute(gcabem_plan_t plan);
@@ -148,8 +156,10 @@ int gcabem_plan_execute(gcabem_plan_t plan);
  * on a copy stream while chunk k+1 computes. Asynchronous: call
  * gcabem_plan_synchronize before reading `host`. */
 int gcabem_plan_execute_download(gcabem_plan_t plan, double *host, int nchunks);
+int gcabem_plan_execute_download2(gcabem_plan_t plan, double *host, double *host2, int nchunks);
 /* Copy the payload (payload_len complex128) to host memory and wait. */
 int gcabem_plan_download(gcabem_plan_t plan, double *host);
+int gcabem_plan_download2(gcabem_plan_t plan, double *host, double *host2);
 int gcabem_plan_synchronize(gcabem_plan_t plan);
 /* CUDA-event durations of the last execute, ms: [disjoint, singular, total]. */
 int gcabem_plan_timing(gcabem_plan_t plan, float *ms3);

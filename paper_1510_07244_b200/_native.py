@@ -58,6 +58,10 @@ _SIGS = {
     "gcabem_plan_create_on": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp,
                                ctypes.POINTER(_vp)], _int),
     "gcabem_plan_download": ([_vp, _vp], _int),
+    "gcabem_plan_download2": ([_vp, _vp, _vp], _int),
+    "gcabem_plan_create_pair": ([_vp, _int, _dbl, _int, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)],
+                                _int),
+    "gcabem_plan_execute_download2": ([_vp, _vp, _vp, _int], _int),
     "gcabem_plan_execute_download": ([_vp, _vp, _int], _int),
     "gcabem_plan_synchronize": ([_vp], _int),
     "gcabem_plan_timing": ([_vp, _vp], _int),

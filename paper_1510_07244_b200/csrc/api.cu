@@ -108,6 +108,7 @@ struct gcabem_plan_s {
     double kappa = 0.0;
     int64_t payload_len = 0;
     PoolBuf<double2> payload;
+    PoolBuf<double2> payload2;  // pair kinds: the double layer
     DevBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -310,7 +311,7 @@ int gcabem_batch_quadrature(gcabem_mesh_t mesh, int equation, int layer, double 
         same = items[i].tri_x == items[i].tri_y && items[i].px[0] == items[i].py[0] &&
                items[i].px[1] == items[i].py[1] && items[i].px[2] == items[i].py[2];
     GC_CUDA(launch_generic(kind_of(equation, layer), same, mesh->V.p, mesh->T.p, mesh->charts.p,
-                           di.p, n, dr.p, nq, dout.p, kappa, s));
+                           di.p, n, dr.p, nq, dout.p, nullptr, kappa, s));
     GC_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double2) * n, cudaMemcpyDeviceToHost, s));
     GC_CUDA(cudaStreamSynchronize(s));
     return GCABEM_OK;
@@ -679,12 +680,42 @@ int gcabem_layout_release(gcabem_layout_t L) {
     return GCABEM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
+                     const double *gauss_pts, const double *gauss_wts, const int64_t *sq,
+                     const double *const *srule, gcabem_plan_t *out);
+}  // namespace
+
+extern "C" {
+
 int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kappa,
                           int disjoint_n, const double *gauss_pts, const double *gauss_wts,
                           const int64_t *sq, const double *const *srule, gcabem_plan_t *out) {
     GC_ARG(L && out, "null argument");
     *out = nullptr;
     if (int rc = check_kind(equation, layer, kappa)) return rc;
+    return plan_create_kind(L, kind_of(equation, layer), kappa, disjoint_n, gauss_pts, gauss_wts,
+                            sq, srule, out);
+}
+
+int gcabem_plan_create_pair(gcabem_layout_t L, int equation, double kappa, int disjoint_n,
+                            const double *gauss_pts, const double *gauss_wts, const int64_t *sq,
+                            const double *const *srule, gcabem_plan_t *out) {
+    GC_ARG(L && out, "null argument");
+    *out = nullptr;
+    if (int rc = check_kind(equation, 1, kappa)) return rc;
+    return plan_create_kind(L, equation == 0 ? L_PAIR : H_PAIR, kappa, disjoint_n, gauss_pts,
+                            gauss_wts, sq, srule, out);
+}
+
+}  // extern "C"
+
+namespace {
+int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
+                     const double *gauss_pts, const double *gauss_wts, const int64_t *sq,
+                     const double *const *srule, gcabem_plan_t *out) {
     GC_ARG(disjoint_n >= 1 && disjoint_n <= MAX_ORDER, "disjoint order outside [1, 12]");
     gcabem_mesh_t mesh = L->mesh;
     GC_CUDA(cudaSetDevice(mesh->device));
@@ -696,7 +727,7 @@ int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kap
     p->mesh = mesh;
     p->L = L;
     ++L->refs;
-    p->kind = kind_of(equation, layer);
+    p->kind = kind;
     p->order = disjoint_n;
     p->kappa = kappa;
     p->payload_len = L->payload_len;
@@ -704,6 +735,7 @@ int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kap
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = pool_init(mesh->device);
     if (e == cudaSuccess) e = p->payload.alloc(p->payload_len, p->stream);
+    if (e == cudaSuccess && kind_pair(kind)) e = p->payload2.alloc(p->payload_len, p->stream);
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         p->sq[c] = sq ? sq[c] : 0;
         if (p->sq[c] > 0 && L->case_at[c + 1] > L->case_at[c])
@@ -718,6 +750,9 @@ int gcabem_plan_create_on(gcabem_layout_t L, int equation, int layer, double kap
     *out = p;
     return GCABEM_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int gcabem_plan_create(gcabem_mesh_t mesh, int equation, int layer, double kappa, int disjoint_n,
                        const double *gauss_pts, const double *gauss_wts, int64_t payload_len,
@@ -746,7 +781,7 @@ int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p
     cudaStream_t s = p->stream;
     const int64_t t0 = p->L->block_task_at[b0], t1 = p->L->block_task_at[b1];
     GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p + t0, t1 - t0,
-                            p->L->panels.p, p->payload.p, p->kappa, s));
+                            p->L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
     for (int c = 0; c < 3; ++c) {
         const auto first = p->L->item_out.begin() + p->L->case_at[c];
         const auto last = p->L->item_out.begin() + p->L->case_at[c + 1];
@@ -754,7 +789,8 @@ int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p
         const int64_t i1 = std::lower_bound(first, last, p1) - p->L->item_out.begin();
         if (i1 <= i0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->L->items.p + i0,
-                               i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->kappa, s));
+                               i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->payload2.p,
+                               p->kappa, s));
     }
     return GCABEM_OK;
 }
@@ -766,18 +802,21 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     gcabem_mesh_t m = p->mesh;
     GC_CUDA(cudaSetDevice(m->device));
     cudaStream_t s = p->stream;
-    if (p->payload_len > 0)
+    if (p->payload_len > 0) {
         GC_CUDA(cudaMemsetAsync(p->payload.p, 0, sizeof(double2) * p->payload_len, s));
+        if (kind_pair(p->kind))
+            GC_CUDA(cudaMemsetAsync(p->payload2.p, 0, sizeof(double2) * p->payload_len, s));
+    }
     GC_CUDA(cudaEventRecord(p->ev[0], s));
     GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p, p->L->ntasks,
-                            p->L->panels.p, p->payload.p, p->kappa, s));
+                            p->L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     for (int c = 0; c < 3; ++c) {
         const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
         if (n == 0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
                                p->L->items.p + p->L->case_at[c], n, p->srule[c].p, p->sq[c],
-                               p->payload.p, p->kappa, s));
+                               p->payload.p, p->payload2.p, p->kappa, s));
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
@@ -785,7 +824,14 @@ int gcabem_plan_execute(gcabem_plan_t p) {
 }
 
 int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
+    GC_ARG(p && !kind_pair(p->kind), "pair plans download with gcabem_plan_execute_download2");
+    return gcabem_plan_execute_download2(p, host, nullptr, nchunks);
+}
+
+int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, int nchunks) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
+    GC_ARG(!kind_pair(p->kind) || host2 || p->payload_len == 0,
+           "pair plan: the double-layer target is missing");
     GC_CUDA(cudaSetDevice(p->mesh->device));
     const int64_t B = (int64_t)p->L->block_leaf.size();
     if (nchunks < 1) nchunks = 1;
@@ -813,14 +859,21 @@ int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
         const int64_t b0 = cut[k], b1 = cut[k + 1];
         const int64_t p0 = b0 < B ? p->L->block_base[b0] : p->payload_len;
         const int64_t p1 = b1 < B ? p->L->block_base[b1] : p->payload_len;
-        if (p1 > p0)
+        if (p1 > p0) {
             GC_CUDA(cudaMemsetAsync(p->payload.p + p0, 0, sizeof(double2) * (p1 - p0), s));
+            if (kind_pair(p->kind))
+                GC_CUDA(cudaMemsetAsync(p->payload2.p + p0, 0, sizeof(double2) * (p1 - p0), s));
+        }
         if (int rc = enqueue_range(p, b0, b1, p0, p1)) return rc;
         GC_CUDA(cudaEventRecord(p->chunk_ev[k], s));
         if (p1 > p0) {
             GC_CUDA(cudaStreamWaitEvent(p->copy, p->chunk_ev[k], 0));
             GC_CUDA(cudaMemcpyAsync(host + 2 * p0, p->payload.p + p0, sizeof(double2) * (p1 - p0),
                                     cudaMemcpyDeviceToHost, p->copy));
+            if (kind_pair(p->kind))
+                GC_CUDA(cudaMemcpyAsync(host2 + 2 * p0, p->payload2.p + p0,
+                                        sizeof(double2) * (p1 - p0), cudaMemcpyDeviceToHost,
+                                        p->copy));
         }
     }
     GC_CUDA(cudaEventRecord(p->ev[1], s));
@@ -830,10 +883,17 @@ int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
 }
 
 int gcabem_plan_download(gcabem_plan_t p, double *host) {
+    return gcabem_plan_download2(p, host, nullptr);
+}
+
+int gcabem_plan_download2(gcabem_plan_t p, double *host, double *host2) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
     GC_CUDA(cudaSetDevice(p->mesh->device));
     if (p->payload_len > 0)
         GC_CUDA(cudaMemcpyAsync(host, p->payload.p, sizeof(double2) * p->payload_len,
+                                cudaMemcpyDeviceToHost, p->stream));
+    if (p->payload_len > 0 && kind_pair(p->kind) && host2)
+        GC_CUDA(cudaMemcpyAsync(host2, p->payload2.p, sizeof(double2) * p->payload_len,
                                 cudaMemcpyDeviceToHost, p->stream));
     GC_CUDA(cudaStreamSynchronize(p->stream));
     return GCABEM_OK;

@@ -54,9 +54,8 @@ template <int N, int KIND, int PH>
 __device__ __forceinline__ void disjoint_expanded(const double dO[3], const double e1x[3],
                                                   const double e2x[3], const double e1y[3],
                                                   const double e2y[3], const double n[3],
-                                                  double kappa, double phi0, double &acc_re,
-                                                  double &acc_im) {
-    constexpr bool DL = (KIND == L_DLP || KIND == H_DLP);
+                                                  double kappa, double phi0, double acc[4]) {
+    constexpr bool DL = kind_normal(KIND);
     double uu[N], un[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) {
@@ -82,7 +81,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         const double a2 = fma(xo0, f1[0], fma(xo1, f1[1], xo2 * f1[2]));
         const double b2 = fma(xo0, f2[0], fma(xo1, f2[1], xo2 * f2[2]));
-        double in_re = 0.0, in_im = 0.0;
+        double in[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int d = 0; d < N; ++d) {
             const double m2b = fma(c_gauss[N][d], b2, a2);
@@ -92,11 +91,13 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
                 const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
                 const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                point_accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in_re, in_im);
+                accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
             }
         }
-        acc_re = fma(wx, in_re, acc_re);
-        if (KIND == H_SLP || KIND == H_DLP) acc_im = fma(wx, in_im, acc_im);
+        acc[0] = fma(wx, in[0], acc[0]);
+        if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
+        if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
+        if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
     }
 }
 
@@ -104,9 +105,8 @@ template <int N, int KIND, int PH>
 __device__ __forceinline__ void disjoint_direct(const double dO[3], const double e1x[3],
                                                 const double e2x[3], const double e1y[3],
                                                 const double e2y[3], const double n[3],
-                                                double kappa, double phi0, double &acc_re,
-                                                double &acc_im) {
-    constexpr bool DL = (KIND == L_DLP || KIND == H_DLP);
+                                                double kappa, double phi0, double acc[4]) {
+    constexpr bool DL = kind_normal(KIND);
     double ux[N], uy[N], uz[N], un[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) {
@@ -125,7 +125,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
-        double in_re = 0.0, in_im = 0.0;
+        double in[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
@@ -137,11 +137,13 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
                 const double dz = fma(-gc, uz[d], xo2);
                 const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                point_accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in_re, in_im);
+                accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
             }
         }
-        acc_re = fma(wx, in_re, acc_re);
-        if (KIND == H_SLP || KIND == H_DLP) acc_im = fma(wx, in_im, acc_im);
+        acc[0] = fma(wx, in[0], acc[0]);
+        if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
+        if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
+        if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
     }
 }
 
@@ -160,7 +162,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // compiler's choice: they would spill heavily). Overridable at build time
 // (-DGCABEM_DISJOINT_MINB(K)=...) for experiments.
 #ifndef GCABEM_DISJOINT_MINB
-#define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 0 ? 7 : ((KIND) == 1 ? 6 : 5))
+#define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 0 ? 7 : ((KIND) == 1 ? 6 : ((KIND) <= 3 ? 5 : 4)))
 #endif
 
 template <int N, int KIND>
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(DISJOINT_TPB, N <= 7 ? GCABEM_DISJOINT_MINB(KI
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,
-                double kappa) {
+                double2 *__restrict__ payload2, double kappa) {
     const int2 task = tasks[blockIdx.x];
     const BlockDesc b = blocks[task.x];
     const int k = task.y + threadIdx.x;
@@ -178,7 +180,9 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const int i = inb ? k / b.nc : 0;
     const int j = inb ? k - i * b.nc : 0;
     const int tx = panels[b.rows_at + i], ty = panels[b.cols_at + j];
-    double2 *dst = payload + b.base + (int64_t)i * b.ld + j;
+    const int64_t pos = b.base + (int64_t)i * b.ld + j;
+    double2 *dst = payload + pos;
+    double2 *dst2 = kind_pair(KIND) ? payload2 + pos : nullptr;
     bool shared;
     {
         const int a0 = T[3 * tx], a1 = T[3 * tx + 1], a2 = T[3 * tx + 2];
@@ -197,7 +201,7 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
         e2x[c] = cx->e2[c];
         e1y[c] = cy->e1[c];
         e2y[c] = cy->e2[c];
-        if (KIND == L_DLP || KIND == H_DLP) n[c] = cy->n[c];
+        if (kind_normal(KIND)) n[c] = cy->n[c];
     }
     const double gx = cx->gram, gy = cy->gram;
     const double rx = cx->radius, ry = cy->radius;
@@ -209,65 +213,69 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const double dcen = norm3(dc[0], dc[1], dc[2]);
     const double rmin = dcen - rx - ry;
     const double S = norm3(dO[0], dO[1], dO[2]) + cx->enorm + cy->enorm;
-    double re = 0.0, im = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     // evaluation form and phase tier are chosen per WARP (votes over the
     // active lanes): a lane that needs the direct form or a longer phase
     // polynomial takes its whole warp along instead of splitting it into
     // serialised branches
     const bool expanded =
         __all_sync(0xffffffffu, !active || (rmin > 0.0 && S * S <= EXPANDED_MAX_RATIO * rmin * rmin));
-    constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
+    constexpr bool HELM = kind_helm(KIND);
     // Helmholtz phase about the centroid distance: |kappa r - kappa D| <= kappa (rx + ry)
     const double phi0 = HELM ? kappa * dcen : 0.0;
     const double dmax = HELM && active ? kappa * (rx + ry) : 0.0;
     const bool tiny = __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
     const bool smallp = __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
     if (!active) {
-        if (inb) *dst = make_double2(0.0, 0.0);
+        if (inb) {
+            *dst = make_double2(0.0, 0.0);
+            if (kind_pair(KIND)) *dst2 = make_double2(0.0, 0.0);
+        }
         return;
     }
     if constexpr (HELM) {
         if (tiny) {
             if (expanded)
-                disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+                disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
             else
-                disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
-            rotate(phi0, re, im);
+                disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
+            rotate_acc<KIND>(phi0, acc);
         } else if (smallp) {
             if (expanded)
-                disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
+                disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
             else
-                disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, re, im);
-            rotate(phi0, re, im);
+                disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
+            rotate_acc<KIND>(phi0, acc);
         } else {
             if (expanded)
-                disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+                disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
             else
-                disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+                disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
         }
     } else {
         if (expanded)
-            disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+            disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
         else
-            disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, re, im);
+            disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
     }
-    finish_pair<KIND>(re, im, gx, gy, dst);
+    finish_acc<KIND>(acc, gx, gy, dst, dst2);
 }
 
 template <int N>
 static cudaError_t launch_disjoint_n(int kind, const Chart *charts, const int32_t *T,
                                      const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
-                                     const int32_t *panels, double2 *payload, double kappa,
-                                     cudaStream_t s) {
+                                     const int32_t *panels, double2 *payload, double2 *payload2,
+                                     double kappa, cudaStream_t s) {
     const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
     switch (kind) {
-        case L_SLP: disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
-        case L_DLP: disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
-        case H_SLP: disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
-        default:    disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, kappa); break;
+        case L_SLP: disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case L_DLP: disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case H_SLP: disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case H_DLP: disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case L_PAIR: disjoint_kernel<N, L_PAIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        default:    disjoint_kernel<N, H_PAIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
     }
     return cudaGetLastError();
 }
-
 
 }  // namespace gcabem

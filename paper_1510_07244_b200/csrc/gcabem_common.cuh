@@ -43,7 +43,13 @@ struct GreenBox {
     double center[3], half[3];  // enlarged box of one cluster (gca.py:103-107)
 };
 
-enum Kind { L_SLP = 0, L_DLP = 1, H_SLP = 2, H_DLP = 3 };
+enum Kind { L_SLP = 0, L_DLP = 1, H_SLP = 2, H_DLP = 3,
+            // fused SLP + DLP of one equation: one evaluation of r, 1/r and the
+            // phase feeds both operators' accumulators (two payloads)
+            L_PAIR = 4, H_PAIR = 5 };
+__host__ __device__ constexpr bool kind_helm(int k) { return k == H_SLP || k == H_DLP || k == H_PAIR; }
+__host__ __device__ constexpr bool kind_normal(int k) { return k == L_DLP || k == H_DLP || k >= L_PAIR; }
+__host__ __device__ constexpr bool kind_pair(int k) { return k >= L_PAIR; }
 constexpr int MAX_ORDER = 12;
 constexpr int DISJOINT_TPB = 128;   // pairs (threads) per disjoint task
 constexpr int GENERIC_TPB = 128;
@@ -54,17 +60,19 @@ inline int kind_of(int equation, int layer) { return equation * 2 + layer; }
 
 // ---- launchers (kernels.cu) ------------------------------------------------
 cudaError_t upload_disjoint_rule(int order, const double *gauss_pts, const double *gauss_wts);
+// kind L_PAIR / H_PAIR: payload gets the single layer, payload2 the double
+// layer (payload2 unused otherwise)
 cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
                             const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
-                            const int32_t *panels, double2 *payload, double kappa,
-                            cudaStream_t s);
+                            const int32_t *panels, double2 *payload, double2 *payload2,
+                            double kappa, cudaStream_t s);
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
 // same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).
 cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int32_t *T,
                            const Chart *charts, const SingItem *items, int64_t n,
-                           const double *rule, int64_t q, double2 *payload, double kappa,
-                           cudaStream_t s);
+                           const double *rule, int64_t q, double2 *payload, double2 *payload2,
+                           double kappa, cudaStream_t s);
 // Raw charts (gcabem_pair_values): per pair 22 doubles
 // {ox,e1x,e2x, oy,e1y,e2y, ny} (21) + gx, gy packed as 24 doubles.
 cudaError_t launch_raw(int kind, const double *pairs, int64_t n, const double *rule, int64_t q,

@@ -11,19 +11,28 @@ from __future__ import annotations
 F_DISJOINT = {("laplace", "single"): 12, ("laplace", "double"): 19,
               ("helmholtz", "single"): 19, ("helmholtz", "double"): 31}
 F_SINGULAR = {k: v + 24 for k, v in F_DISJOINT.items()}
+# both layers of one equation from one point evaluation (fused pair plans): the
+# minimal shared algorithm computes d, r^2, r (and kr, sin, cos) once, so the
+# pair is credited the double layer plus what the single layer adds on top
+# (its own 1/r, weight product and accumulation: 3 flops Laplace, 7 Helmholtz)
+F_DISJOINT_PAIR = {"laplace": 19 + 3, "helmholtz": 31 + 7}
+F_SINGULAR_PAIR = {k: v + 24 for k, v in F_DISJOINT_PAIR.items()}
 PAIR_OVERHEAD = 4
 # Green-matrix entry: n^2 panel points x disjoint F (monopole SLP, dipole DLP) + 2
 GREEN_ENTRY_OVERHEAD = 2
 
 
-def point_flops(spec, family: str) -> int:
+def point_flops(spec, family: str, pair: bool = False) -> int:
+    if pair:
+        table = F_DISJOINT_PAIR if family == "disjoint" else F_SINGULAR_PAIR
+        return table[spec.equation]
     table = F_DISJOINT if family == "disjoint" else F_SINGULAR
     return table[(spec.equation, spec.layer)]
 
 
-def pair_flops(spec, family: str, q: int) -> int:
-    """Flops of one pair integral with a Q-point rule."""
-    return q * point_flops(spec, family) + PAIR_OVERHEAD
+def pair_flops(spec, family: str, q: int, pair: bool = False) -> int:
+    """Flops of one pair integral with a Q-point rule (pair: both layers)."""
+    return q * point_flops(spec, family, pair) + (2 if pair else 1) * PAIR_OVERHEAD
 
 
 def p1_pair_flops(spec, family: str, q: int, order: int) -> int:

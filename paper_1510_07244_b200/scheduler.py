@@ -44,7 +44,7 @@ __all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "A
            "make_payloads", "BackendError", "SchedulerConfigError", "CUDA_BACKEND",
            "BATCH_BACKEND", "SCALAR_BACKEND", "DEFAULT_MAXSIZE", "BYTES_PER_PAIR",
            "PAIR_RECORD_BYTES", "VALUE_BYTES", "SINGULAR_CASES", "AssemblyPlan",
-           "DeviceLayout", "potential_batch", "clear_package_cache"]
+           "DeviceLayout", "potential_batch", "clear_package_cache", "run_assembly_pair"]
 
 
 @dataclass(frozen=True)
@@ -346,10 +346,15 @@ class DeviceLayout:
 class AssemblyPlan:
     """Device plan of one operator on one device: a (shared, cached) device
     layout of the packages plus this operator's payload, executable
-    repeatedly (C ABI gcabem_plan_*). Payload stays in HBM until download()."""
+    repeatedly (C ABI gcabem_plan_*). Payload stays in HBM until download().
+
+    pair=True: BOTH layers of spec's equation in one fused plan (every kernel
+    evaluates r, 1/r and the phase once per point for the single and the
+    double layer; C ABI gcabem_plan_create_pair); download2() / the pair
+    execute_download() fill two host buffers."""
 
     def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
-                 leaf_range=None):
+                 leaf_range=None, pair: bool = False):
         t_prep = time.monotonic()
         self.layout = DeviceLayout.cached(dm, pk, leaf_range)
         lay = self.layout
@@ -370,10 +375,16 @@ class AssemblyPlan:
         self._dm = dm
         self.h2d_bytes = lay.h2d_bytes + int(sum(r.nbytes for r in rules))
         self.prep_s = time.monotonic() - t_prep
+        self.pair = bool(pair)
         h = ctypes.c_void_p()
-        nat.check(nat.lib().gcabem_plan_create_on(
-            lay.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw), nat.ptr(sq),
-            ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
+        if self.pair:
+            nat.check(nat.lib().gcabem_plan_create_pair(
+                lay.handle, eq, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw), nat.ptr(sq),
+                ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
+        else:
+            nat.check(nat.lib().gcabem_plan_create_on(
+                lay.handle, eq, layer, float(spec.kappa), dn, nat.ptr(gp), nat.ptr(gw),
+                nat.ptr(sq), ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
         self.handle = h.value
         self._keep = rules
 
@@ -387,24 +398,34 @@ class AssemblyPlan:
         """Run on an external cudaStream_t (e.g. torch.cuda.Stream.cuda_stream)."""
         nat.check(nat.lib().gcabem_plan_set_stream(self.handle, stream_handle or None))
 
-    def execute_download(self, out: np.ndarray, nchunks: int = 8) -> None:
+    def execute_download(self, out: np.ndarray, nchunks: int = 8,
+                         out2: np.ndarray | None = None) -> None:
         """Execute and stream the payload into `out` chunk by chunk (D2H of
-        chunk k overlaps the kernels of chunk k+1). Asynchronous: call
-        synchronize() before reading `out`."""
+        chunk k overlaps the kernels of chunk k+1); a pair plan also streams
+        the double layer into `out2`. Asynchronous: call synchronize()
+        before reading the targets."""
         self._check_target(out)
-        nat.check(nat.lib().gcabem_plan_execute_download(self.handle, nat.ptr(out),
-                                                         int(nchunks)))
-        self._pinned_target = out  # keep alive until synchronize
+        if self.pair:
+            self._check_target(out2)
+            nat.check(nat.lib().gcabem_plan_execute_download2(self.handle, nat.ptr(out),
+                                                              nat.ptr(out2), int(nchunks)))
+        else:
+            nat.check(nat.lib().gcabem_plan_execute_download(self.handle, nat.ptr(out),
+                                                             int(nchunks)))
+        self._pinned_target = (out, out2)  # keep alive until synchronize
 
-    def _check_target(self, out: np.ndarray) -> None:
-        if out.dtype != np.complex128 or out.size != self.payload_len or \
+    def _check_target(self, out) -> None:
+        if out is None or out.dtype != np.complex128 or out.size != self.payload_len or \
                 not out.flags.c_contiguous:
             raise ValueError("download target must be contiguous complex128 of payload_len")
 
-    def download(self, out: np.ndarray) -> None:
-        """Copy the payload into `out` (complex128, payload_len, ideally pinned)."""
+    def download(self, out: np.ndarray, out2: np.ndarray | None = None) -> None:
+        """Copy the payload into `out` (complex128, payload_len, ideally
+        pinned); a pair plan's double layer into `out2`."""
         self._check_target(out)
-        nat.check(nat.lib().gcabem_plan_download(self.handle, nat.ptr(out)))
+        if self.pair:
+            self._check_target(out2)
+        nat.check(nat.lib().gcabem_plan_download2(self.handle, nat.ptr(out), nat.ptr(out2)))
 
     def timing_ms(self) -> dict:
         ms = (ctypes.c_float * 3)()
@@ -418,8 +439,8 @@ class AssemblyPlan:
         from .roofline import pair_flops
         dq = self.orders[0] ** 4
         computed = self.disjoint_pairs - sum(self.singular_counts)
-        dis = pair_flops(self.spec, "disjoint", dq) * computed
-        sing = sum(pair_flops(self.spec, "singular", q) * n
+        dis = pair_flops(self.spec, "disjoint", dq, self.pair) * computed
+        sing = sum(pair_flops(self.spec, "singular", q, self.pair) * n
                    for q, n in zip(self.singular_q, self.singular_counts))
         return {"disjoint": dis, "singular": sing}
 
@@ -543,6 +564,74 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
     payloads = LeafPayloads(payload, pk.leaf_ids, pk.leaf_base, pk.leaf_shape)
     phase["total"] = time.monotonic() - t0
     return GCAMatrix(block_tree, row_ops, col_ops, payloads, buffer=payload)
+
+
+def run_assembly_pair(mesh: SurfaceMesh, block_tree: BlockTree, equation: str, kappa: float,
+                      row_ops: dict, col_ops: dict, params: SchedulerParams | None = None,
+                      orders: tuple = (3, 5), stats: AssemblyStats | None = None):
+    """The single- and the double-layer operator of one equation, assembled
+    together: (GCAMatrix SLP, GCAMatrix DLP), each identical in layout and
+    within roundoff in value to run_assembly() of that layer. One fused device
+    pass evaluates the distance, its inverse and the Helmholtz phase once per
+    quadrature point for both operators (the pipelines that need V and K,
+    reference solver.py:279-282, reuse trees and operators the same way)."""
+    params = params or SchedulerParams()
+    stats = stats if stats is not None else AssemblyStats()
+    spec = KernelSpec(equation, "single", kappa)
+    backend = params.backend_for("disjoint")
+    t0 = time.monotonic()
+    phase = {}
+    pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
+    phase["packaging"] = time.monotonic() - t0
+    devices = list(backend.devices)
+    sq = [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES]
+    if params.shard is not None:
+        rank, world = params.shard
+        base = shard_leaves(pk, world, orders[0] ** 4, sq)[rank]
+        ranges = [(base[0] + a, base[0] + b) for a, b in
+                  _split_range(pk, base, len(devices), orders[0] ** 4, sq)]
+    else:
+        ranges = shard_leaves(pk, len(devices), orders[0] ** 4, sq)
+    ta = time.monotonic()
+    slp = nat.pinned_empty(pk.payload_len, np.complex128)
+    dlp = nat.pinned_empty(pk.payload_len, np.complex128)
+    if params.shard is not None:
+        slp[:] = 0
+        dlp[:] = 0
+    phase["pinned_alloc"] = time.monotonic() - ta
+    plans = []
+    try:
+        ta = time.monotonic()
+        for dev, rng in zip(devices, ranges):
+            plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng, pair=True))
+        phase["plan_create"] = time.monotonic() - ta
+        phase["plan_host_prep"] = sum(p.prep_s for p in plans)
+        ta = time.monotonic()
+        for p in plans:
+            if p.payload_len:
+                sl = slice(p.payload_offset, p.payload_offset + p.payload_len)
+                p.execute_download(slp[sl], params.chunks, dlp[sl])
+        for p in plans:
+            p.synchronize()
+        phase["execute_download"] = time.monotonic() - ta
+        stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans if p.payload_len}
+    finally:
+        ta = time.monotonic()
+        for p in plans:
+            p.close()
+        phase["plan_destroy"] = time.monotonic() - ta
+    t1 = time.monotonic()
+    stats.phase_s = phase
+    stats.block_pairs += 2 * pk.block_pairs()
+    stats.corrective_items += 2 * pk.num_items
+    ev = _events(pk, backend.name, t0, t1)
+    stats.events.extend(ev + ev)
+    stats.lists_executed += 2 * len(ev)
+    stats.pairs_executed += 2 * sum(r["pairs"] for r in ev)
+    phase["total"] = time.monotonic() - t0
+    return tuple(GCAMatrix(block_tree, row_ops, col_ops,
+                           LeafPayloads(buf, pk.leaf_ids, pk.leaf_base, pk.leaf_shape),
+                           buffer=buf) for buf in (slp, dlp))
 
 
 def _split_range(pk, rng, n, dq, sq):

@@ -464,3 +464,39 @@ def test_release_cached_then_reassemble(gload):
     devmod.release_cached(0)
     b = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
     assert np.array_equal(first, b.buffer)
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+@pytest.mark.parametrize("orders", [(3, 5), (4, 5)])
+def test_run_assembly_pair_vs_oracle(gload, eq, kappa, orders):
+    """The fused SLP+DLP plan (one evaluation of r, 1/r and the phase per
+    point for both layers) against the oracle for each layer (P2 rule), and
+    against the separate single-layer plans (within roundoff)."""
+    m, bt, ops, pk = packages_for(3, eq, gload("gca_L3.npz"))
+    S, D = scheduler.run_assembly_pair(m, bt, eq, kappa, ops, ops,
+                                       scheduler.SchedulerParams(), orders)
+    for layer, M in (("single", S), ("double", D)):
+        ref = oracle_assemble(m, pk, eq, layer, kappa, orders)
+        ok, worst, nfb = p2_check(pk, M.buffer, ref, TOL, double_layer=layer == "double")
+        assert ok, (layer, worst, nfb)
+        sep = scheduler.run_assembly(m, bt, kernels.KernelSpec(eq, layer, kappa), ops, ops,
+                                     scheduler.SchedulerParams(), orders)
+        ok, worst, _ = p2_check(pk, M.buffer, sep.buffer, 1e-13, double_layer=layer == "double")
+        assert ok, (layer, "vs separate", worst)
+    assert set(S.payloads) == set(D.payloads) == {l.index for l in bt.leaves}
+
+
+def test_run_assembly_pair_sampled_L5():
+    """Fused pair plan at L5 (Helmholtz, coupling blocks included) vs the
+    separate plans on every entry (1e-12, P2 rule)."""
+    m, t, bt = sphere_setup(5)
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                       scheduler.SchedulerParams(), (3, 5))
+    for layer, M in (("single", S), ("double", D)):
+        sep = scheduler.run_assembly(m, bt, kernels.KernelSpec("helmholtz", layer, 4.0), ops,
+                                     ops, scheduler.SchedulerParams(), (3, 5))
+        ok, worst, _ = p2_check(pk, M.buffer, sep.buffer, 1e-12, double_layer=layer == "double")
+        assert ok, (layer, worst)
