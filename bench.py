@@ -418,90 +418,111 @@ def run_ours(args, cfg, dist, log):
         shard = shard_leaves(pk, dist.world, cfg["orders"][0] ** 4,
                              [build_rule(c, cfg["orders"][1]).num_points
                               for c in ("vertex", "edge", "identical")])[dist.rank]
+    fused = len(specs) == 2 and {s.layer for s in specs} == {"single", "double"} and \
+        not args.separate
     tp = time.perf_counter()
-    plans = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], shard) for s in specs]
+    sep_plans = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], shard) for s in specs]
+    pair_plan = scheduler.AssemblyPlan(dm, specs[0], pk, cfg["orders"], shard, pair=True) \
+        if fused else None
     plan_s = time.perf_counter() - tp
-    pairs_step = sum(p.disjoint_pairs + sum(p.singular_counts) for p in plans)
+    # pair integrals per step: both operators' pairs (block pairs + corrective items)
+    pairs_step = sum(p.disjoint_pairs + sum(p.singular_counts) for p in sep_plans)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
     stream = torch.cuda.Stream(device=device)
-    for p in plans:  # one timeline: both operators in order on one stream
-        p.set_stream(stream.cuda_stream)
+    for p in sep_plans + ([pair_plan] if pair_plan else []):
+        p.set_stream(stream.cuda_stream)  # one timeline on one stream
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
 
-    def step():
-        with torch.cuda.stream(stream):
-            l2_flush(flush)
-            ev0.record(stream)
-            for p in plans:
-                p.execute()
-            ev1.record(stream)
-        stream.synchronize()
-        return ev0.elapsed_time(ev1), [p.timing_ms() for p in plans]
-
-    for _ in range(args.warmup):
-        step()
-    peak = devmod.fp64_peak_tflops(device)
-    dist.barrier()
-    torch.cuda.synchronize(device)
-    per_step, disj_ms = [], []
-    with ClockSampler(device) as clk:
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            total, tm = step()
-            per_step.append(total)
-            disj_ms.append([t["disjoint"] for t in tm])
+    def time_plans(plans, steps, warmup, clk_sampler=None):
+        def step():
+            with torch.cuda.stream(stream):
+                l2_flush(flush)
+                ev0.record(stream)
+                for p in plans:
+                    p.execute()
+                ev1.record(stream)
+            stream.synchronize()
+            return ev0.elapsed_time(ev1), [p.timing_ms() for p in plans]
+        for _ in range(warmup):
+            step()
+        dist.barrier()
         torch.cuda.synchronize(device)
-        wall = time.perf_counter() - w0
-    dist.barrier()
-    ms = statistics.mean(per_step)
+        per, dis = [], []
+        w0 = time.perf_counter()
+        for _ in range(steps):
+            total, tm = step()
+            per.append(total)
+            dis.append([t["disjoint"] for t in tm])
+        torch.cuda.synchronize(device)
+        wall_ = time.perf_counter() - w0
+        dist.barrier()
+        return statistics.mean(per), np.mean(np.array(dis), axis=0), wall_
+
+    peak = devmod.fp64_peak_tflops(device)
+    main_plans = [pair_plan] if fused else sep_plans
+    with ClockSampler(device) as clk:
+        ms, dk, wall = time_plans(main_plans, args.steps, args.warmup)
     ms_max = dist.max(ms)
     # weak: every rank did pairs_step; strong: the ranks split one job
     total_pairs = pairs_step * dist.world if args.mode == "weak" else \
-        pk_total_pairs(pk, len(plans))
+        pk_total_pairs(pk, len(sep_plans))
     value = total_pairs / (ms_max * 1e-3)
+    separate = None
+    if fused:  # the same workload as two single-layer plans, for reference
+        ms_sep, dk_sep, _ = time_plans(sep_plans, args.steps, 3)
+        ms_sep = dist.max(ms_sep)
+        fl_sep = [p.flops() for p in sep_plans]
+        kd = int(np.argmax(dk_sep))
+        separate = {"value": total_pairs / (ms_sep * 1e-3), "ms_per_step": ms_sep,
+                    "dominant_kernel": f"disjoint_kernel<{cfg['orders'][0]},{specs[kd].layer}>",
+                    "dominant_frac": fl_sep[kd]["disjoint"] / (dk_sep[kd] * 1e-3) / 1e12 / peak}
 
-    # roofline of the dominant kernel: disjoint quadrature of each operator
-    fl = [p.flops() for p in plans]
-    dk = np.mean(np.array(disj_ms), axis=0)  # per plan
+    # roofline of the dominant kernel: the disjoint quadrature launch
+    fl = [p.flops() for p in main_plans]
     k_dom = int(np.argmax(dk))
     achieved = fl[k_dom]["disjoint"] / (dk[k_dom] * 1e-3) / 1e12
     share = float(np.sum(dk) / ms)
+    dom_name = "pair" if fused else specs[k_dom].layer
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{args.config}/{specs[k_dom].layer}")
+            traffic = json.load(open(prof)).get(f"{args.config}/{dom_name}")
         except (OSError, ValueError):
             traffic = None
 
     # e2e through the public API, host buffers, H2D + D2H inside
     e2e_t = []
     params = scheduler.SchedulerParams(backends=(scheduler.Backend("cuda", devices=(device,)),))
-    h2d = sum(p.h2d_bytes for p in plans)
-    d2h = sum(p.payload_len * 16 for p in plans)
+    plans = sep_plans
+    h2d = sum(p.h2d_bytes for p in main_plans)
+    d2h = sum(p.payload_len * 16 for p in sep_plans)
+
+    def assemble_both(stats_list):
+        if fused:
+            st_ = stats_list[0]
+            return list(scheduler.run_assembly_pair(m, bt, cfg["equation"], cfg["kappa"], ops,
+                                                    ops, params, cfg["orders"], st_))
+        return [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_)
+                for s, st_ in zip(specs, stats_list)]
     setup_first = None
     e2e_phases = []
     if args.e2e_steps > 0:
-        warm = [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"])
-                for s in specs]  # warm the path and the pinned pool (both buffers live)
+        warm = assemble_both([scheduler.AssemblyStats() for _ in specs])  # path + pinned pool
         del warm
     for k in range(args.e2e_steps):
         dist.barrier()
-        scheduler.clear_package_cache()  # every step packages once (shared by SLP/DLP)
+        scheduler.clear_package_cache()  # every step packages once
         t0 = time.perf_counter()
         st = [scheduler.AssemblyStats() for _ in specs]
-        mats, marks = [], []
-        for s, st_ in zip(specs, st):
-            mats.append(scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_))
-            marks.append(time.perf_counter() - t0)
+        mats = assemble_both(st)
         torch.cuda.synchronize(device)
         dt = time.perf_counter() - t0
-        e2e_phases = [dict(x.phase_s, wall_mark=mk) for x, mk in zip(st, marks)]
+        e2e_phases = [dict(x.phase_s) for x in st if x.phase_s]
         e2e_t.append(dt)
-        t_del = time.perf_counter()
         del mats
-        log(f"e2e step {k}: {dt:.4f} s (free {time.perf_counter() - t_del:.4f} s) {e2e_phases}")
+        log(f"e2e step {k}: {dt:.4f} s {e2e_phases}")
         if setup_first is None:
             setup_first = dt
     e2e_dt = dist.max(statistics.median(e2e_t)) if e2e_t else None
@@ -539,7 +560,7 @@ def run_ours(args, cfg, dist, log):
         pairs, dt, desc = cpu_sample(pk, m, cfg, args.cpu_seconds, nth, log)
         cpu = {"value": pairs / dt, "unit": UNIT, "cores": nth, "kind": "port", "sample": desc}
 
-    launches = sum(1 + sum(1 for c in p.singular_counts if c) for p in plans) * args.steps
+    launches = sum(1 + sum(1 for c in p.singular_counts if c) for p in main_plans) * args.steps
     h2_setup = {"mesh_s (input, not counted)": round(setup_t["mesh_s"], 3),
                 "trees_s": round(setup_t["trees_s"], 3), "gca_s": round(setup_t["gca_s"], 3),
                 "gca_phases_s": {k: round(v, 4) if isinstance(v, float) else v
@@ -554,11 +575,15 @@ def run_ours(args, cfg, dist, log):
         "data": f"synthetic (deterministic octahedral sphere level {cfg['level']})",
         "config": {"workload": cfg["workload"], "pairs_per_step": int(pairs_step),
                    "operators": list(cfg["layers"]), "orders": list(cfg["orders"]),
+                   "plan": "one fused SLP+DLP plan (scheduler.run_assembly_pair)" if fused
+                   else "one plan per operator (scheduler.run_assembly)",
                    "l2": "flushed between steps (512 MiB device write)",
                    "parallelism": f"{args.mode} x{dist.world}, no collectives"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"disjoint_kernel<{cfg['orders'][0]},{specs[k_dom].layer}>",
+                     "kernel": f"disjoint_kernel<{cfg['orders'][0]},{dom_name}>"
+                               + (" (fused single+double layer: r, 1/r, phase once per point; "
+                                  "flops = roofline.F_DISJOINT_PAIR)" if fused else ""),
                      "peak_source": "measured DFMA probe (gcabem_fp64_probe), this device",
                      "kernel_share_of_step": share},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -568,7 +593,8 @@ def run_ours(args, cfg, dist, log):
         "clocks": clk.summary(),
         "h2_setup": h2_setup,
         "device": info["name"], "wall_s_timed": wall, "plan_upload_s": plan_s,
-        "flops_per_step": {s.layer: f for s, f in zip(specs, fl)},
+        "flops_per_step": {("pair" if fused else s.layer): f for s, f in zip(specs, fl)},
+        "separate_plans": separate,
     }
     if matvec_line is not None:
         line["matvec"] = matvec_line
@@ -602,6 +628,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--separate", action="store_true",
+                    help="time SLP and DLP as two single-layer plans (default: one fused plan)")
     ap.add_argument("--order", type=int, default=None,
                     help="override the quadrature orders (disjoint n = singular n), e.g. C5")
     args = ap.parse_args(argv)

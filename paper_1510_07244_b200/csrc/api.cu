@@ -942,6 +942,7 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
         if (e) cudaEventDestroy(e);
     for (auto &e : p->chunk_ev) cudaEventDestroy(e);
     p->payload.release();
+    p->payload2.release();
     for (auto &r : p->srule) r.release();
     cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
     if (mine) cudaStreamDestroy(mine);
