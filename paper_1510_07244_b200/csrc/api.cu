@@ -109,7 +109,7 @@ struct gcabem_plan_s {
     int64_t payload_len = 0;
     PoolBuf<double2> payload;
     PoolBuf<double2> payload2;  // pair kinds: the double layer
-    DevBuf<double> srule[3];
+    PoolBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> chunk_ev;
@@ -734,8 +734,10 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
     cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = pool_init(mesh->device);
+    Trace tr("plan_create");
     if (e == cudaSuccess) e = p->payload.alloc(p->payload_len, p->stream);
     if (e == cudaSuccess && kind_pair(kind)) e = p->payload2.alloc(p->payload_len, p->stream);
+    tr.mark("alloc");
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         p->sq[c] = sq ? sq[c] : 0;
         if (p->sq[c] > 0 && L->case_at[c + 1] > L->case_at[c])
@@ -743,6 +745,7 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
     }
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    tr.mark("rules+sync");
     if (e != cudaSuccess) {
         gcabem_plan_destroy(p);
         GC_CUDA(e);
@@ -935,20 +938,25 @@ int gcabem_plan_payload(gcabem_plan_t p, void **dev_ptr) {
 
 int gcabem_plan_destroy(gcabem_plan_t p) {
     if (!p) return GCABEM_OK;
+    Trace tr("plan_destroy");
     cudaSetDevice(p->mesh->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->copy) cudaStreamSynchronize(p->copy);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : p->chunk_ev) cudaEventDestroy(e);
+    tr.mark("sync+events");
     p->payload.release();
     p->payload2.release();
+    tr.mark("free");
     for (auto &r : p->srule) r.release();
     cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
     if (mine) cudaStreamDestroy(mine);
     if (p->copy) cudaStreamDestroy(p->copy);
+    tr.mark("streams");
     gcabem_layout_release(p->L);
     delete p;
+    tr.mark("layout");
     return GCABEM_OK;
 }
 

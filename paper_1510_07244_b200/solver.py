@@ -68,3 +68,30 @@ def assemble_operator(mesh: SurfaceMesh, spec: KernelSpec, config: PipelineConfi
                                     config.scheduler, config.orders, stats)
     t2 = time.monotonic()
     return AssembledOperator(matrix, t1 - t0, t2 - t1, stats)
+
+
+def assemble_operator_pair(mesh: SurfaceMesh, equation: str, kappa: float,
+                           config: PipelineConfig, trees=None, ops=None):
+    """Both layers of one equation (the V and K of the reference's
+    Laplace DtN / Helmholtz Brakhage-Werner pipelines, solver.py:266-371,
+    which reuse trees and operators between them): trees, GCA operators,
+    then ONE fused device assembly (scheduler.run_assembly_pair).
+    Returns (AssembledOperator single layer, AssembledOperator double layer);
+    the setup seconds are reported on the first, the shared assembly time on
+    both."""
+    block_tree = build_trees(mesh, config) if trees is None else trees
+    t0 = time.monotonic()
+    if ops is None:
+        devices = config.scheduler.backend_for("disjoint").devices
+        row_ops, col_ops = build_interpolation_operators(
+            mesh, block_tree, KernelSpec(equation, "single", kappa), config.gca,
+            device=tuple(devices))
+    else:
+        row_ops, col_ops = ops
+    t1 = time.monotonic()
+    stats = scheduler.AssemblyStats()
+    slp, dlp = scheduler.run_assembly_pair(mesh, block_tree, equation, kappa, row_ops, col_ops,
+                                           config.scheduler, config.orders, stats)
+    t2 = time.monotonic()
+    return (AssembledOperator(slp, t1 - t0, t2 - t1, stats),
+            AssembledOperator(dlp, 0.0, t2 - t1, stats))
