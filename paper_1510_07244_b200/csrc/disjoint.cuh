@@ -159,14 +159,16 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // the compiler's choice (96 / 128 registers): +1% (C2 L-DLP) and +10% (C3
 // H-DLP) from the extra warps hiding the FP64 dependency latency, despite a
 // few spilled bytes in the cold full-sincos tier (orders above 7 keep the
-// compiler's choice: they would spill heavily). Overridable at build time
-// (-DGCABEM_DISJOINT_MINB(K)=...) for experiments.
-#ifndef GCABEM_DISJOINT_MINB
-#define GCABEM_DISJOINT_MINB(KIND) ((KIND) == 0 ? 7 : ((KIND) == 1 ? 6 : ((KIND) <= 3 ? 5 : 4)))
-#endif
+// compiler's choice: they would spill heavily); the fused pair kinds carry two
+// layers of accumulators and get fewer CTAs at the higher orders.
+constexpr int disjoint_minb(int n, int kind) {
+    return n > 7 ? 1                                     // would spill heavily
+           : kind == L_SLP ? 7 : kind == L_DLP ? 6 : kind <= H_DLP ? 5
+           : n <= 4 ? 4 : n <= 6 ? 3 : 2;               // pair kinds: 2 layers of state
+}
 
 template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB, N <= 7 ? GCABEM_DISJOINT_MINB(KIND) : 1)
+__global__ void __launch_bounds__(DISJOINT_TPB, disjoint_minb(N, KIND))
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,

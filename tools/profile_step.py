@@ -20,12 +20,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=tuple(bench.CONFIGS))
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--separate", action="store_true", help="one plan per operator")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     m, bt, ops, pk, _ = bench.build_workload(cfg, 0, lambda s: print(s, file=sys.stderr))
     dm = devmod.device_mesh(m, 0)
-    plans = [scheduler.AssemblyPlan(dm, kernels.KernelSpec(cfg["equation"], l, cfg["kappa"]),
-                                    pk, cfg["orders"]) for l in cfg["layers"]]
+    if len(cfg["layers"]) == 2 and not args.separate:  # the bench's fused SLP+DLP plan
+        plans = [scheduler.AssemblyPlan(dm, kernels.KernelSpec(cfg["equation"], "single",
+                                                               cfg["kappa"]),
+                                        pk, cfg["orders"], pair=True)]
+    else:
+        plans = [scheduler.AssemblyPlan(dm, kernels.KernelSpec(cfg["equation"], l,
+                                                               cfg["kappa"]),
+                                        pk, cfg["orders"]) for l in cfg["layers"]]
     for _ in range(args.reps):
         for p in plans:
             p.execute()
