@@ -500,3 +500,22 @@ def test_run_assembly_pair_sampled_L5():
                                      ops, scheduler.SchedulerParams(), (3, 5))
         ok, worst, _ = p2_check(pk, M.buffer, sep.buffer, 1e-12, double_layer=layer == "double")
         assert ok, (layer, worst)
+
+
+def test_pair_plan_shards_equal_single(gload):
+    """Fused pair plans: several devices of one process and process shards
+    (SchedulerParams.shard) give the unsharded payloads bit for bit."""
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), "helmholtz")
+    S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                       scheduler.SchedulerParams(), (3, 5))
+    be = scheduler.Backend("cuda", devices=(0, 0, 0))
+    S3, D3 = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                         scheduler.SchedulerParams(backends=(be,)), (3, 5))
+    assert np.array_equal(S.buffer, S3.buffer) and np.array_equal(D.buffer, D3.buffer)
+    parts = [scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                         scheduler.SchedulerParams(shard=(r, 2)), (3, 5))
+             for r in range(2)]
+    # each shard fills its own leaf range and leaves the rest zero
+    assert np.array_equal(parts[0][0].buffer + parts[1][0].buffer, S.buffer)
+    assert np.array_equal(parts[0][1].buffer + parts[1][1].buffer, D.buffer)
