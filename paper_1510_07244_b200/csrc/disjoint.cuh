@@ -161,10 +161,13 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // few spilled bytes in the cold full-sincos tier (orders above 7 keep the
 // compiler's choice: they would spill heavily); the fused pair kinds carry two
 // layers of accumulators and get fewer CTAs at the higher orders.
+#ifndef GCABEM_PAIR_MINB  // pair kinds at orders <= 4 (build-time override for A/B runs)
+#define GCABEM_PAIR_MINB 4
+#endif
 constexpr int disjoint_minb(int n, int kind) {
     return n > 7 ? 1                                     // would spill heavily
            : kind == L_SLP ? 7 : kind == L_DLP ? 6 : kind <= H_DLP ? 5
-           : n <= 4 ? 4 : n <= 6 ? 3 : 2;               // pair kinds: 2 layers of state
+           : n <= 4 ? GCABEM_PAIR_MINB : n <= 6 ? 3 : 2;  // pair kinds: 2 layers of state
 }
 
 template <int N, int KIND>

@@ -1,6 +1,6 @@
 # A/B: the in-tree library vs a variant build (GCABEM_LIB_PATH), device step only
 mkdir -p gpurun_out
-VAR=${VAR:-build/minb/libgcabem_b200.so}
+VAR=${VAR:-abvar/libgcabem_b200.so}
 for cfg in c2 c3; do
   for lib in base var; do
     if [ $lib = var ]; then export GCABEM_LIB_PATH=$PWD/$VAR; else unset GCABEM_LIB_PATH; fi
