@@ -161,13 +161,14 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // few spilled bytes in the cold full-sincos tier (orders above 7 keep the
 // compiler's choice: they would spill heavily); the fused pair kinds carry two
 // layers of accumulators and get fewer CTAs at the higher orders.
-#ifndef GCABEM_PAIR_MINB  // pair kinds at orders <= 4 (build-time override for A/B runs)
-#define GCABEM_PAIR_MINB 4
-#endif
+// pair kinds at orders <= 4: L_PAIR 4 (124 registers; 5 measured 2% slower at
+// C2), H_PAIR 5 (96 registers, +1% at C3 despite a few spilled bytes in the
+// cold full-sincos tier)
 constexpr int disjoint_minb(int n, int kind) {
     return n > 7 ? 1                                     // would spill heavily
            : kind == L_SLP ? 7 : kind == L_DLP ? 6 : kind <= H_DLP ? 5
-           : n <= 4 ? GCABEM_PAIR_MINB : n <= 6 ? 3 : 2;  // pair kinds: 2 layers of state
+           : n <= 4 ? (kind == L_PAIR ? 4 : 5)
+           : n <= 6 ? 3 : 2;                             // pair kinds: 2 layers of state
 }
 
 template <int N, int KIND>
