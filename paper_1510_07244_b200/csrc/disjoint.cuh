@@ -47,7 +47,10 @@ static cudaError_t upload_tables(int n, const double *g, const double *gw) {
 // r_min a lower bound of the pair distance (bounding spheres). Pairs with
 // S^2 <= EXPANDED_MAX_RATIO * r_min^2 (error < 2.3e-13, measured < 3e-15)
 // take it; the rest (about 1% of near-field pairs) the direct form.
-constexpr double EXPANDED_MAX_RATIO = 1024.0;
+#ifndef GCABEM_EXPANDED_MAX_RATIO
+#define GCABEM_EXPANDED_MAX_RATIO 1024.0
+#endif
+constexpr double EXPANDED_MAX_RATIO = GCABEM_EXPANDED_MAX_RATIO;
 
 
 template <int N, int KIND, int PH>
