@@ -85,7 +85,10 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
         const double a2 = fma(xo0, f1[0], fma(xo1, f1[1], xo2 * f1[2]));
         const double b2 = fma(xo0, f2[0], fma(xo1, f2[1], xo2 * f2[2]));
         double in[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+        // fused pair kinds at orders >= 6 roll the outer y loop (the fully
+        // unrolled N^2 body spills their two layers of state)
+        constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
+#pragma unroll OUTER
         for (int d = 0; d < N; ++d) {
             const double m2b = fma(c_gauss[N][d], b2, a2);
 #pragma unroll
@@ -129,7 +132,8 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         double in[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
+        constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;  // see disjoint_expanded
+#pragma unroll OUTER
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
 #pragma unroll
