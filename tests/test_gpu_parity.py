@@ -467,7 +467,7 @@ def test_release_cached_then_reassemble(gload):
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
-@pytest.mark.parametrize("orders", [(3, 5), (4, 5)])
+@pytest.mark.parametrize("orders", [(3, 5), (4, 5), (7, 5)])
 def test_run_assembly_pair_vs_oracle(gload, eq, kappa, orders):
     """The fused SLP+DLP plan (one evaluation of r, 1/r and the phase per
     point for both layers) against the oracle for each layer (P2 rule), and
