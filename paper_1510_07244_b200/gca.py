@@ -255,13 +255,10 @@ last_build_phases: dict = {}
 
 
 def _host_threads() -> int:
-    """Host threads for the ACA pool: this process's CPU set, shared evenly
-    by the processes of one node (torchrun sets LOCAL_WORLD_SIZE)."""
-    try:
-        n = len(os.sched_getaffinity(0))
-    except AttributeError:
-        n = os.cpu_count() or 1
-    return max(1, n // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
+    """Host threads for the ACA pool (packaging.host_threads: this process's
+    share of the node's CPU set)."""
+    from .packaging import host_threads
+    return host_threads()
 
 
 def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,

@@ -210,6 +210,16 @@ def _op_arrays_build(ops: dict, nnodes: int):
     return at, np.ascontiguousarray(piv)
 
 
+def host_threads() -> int:
+    """Host threads for the native host work of this process: its CPU set,
+    shared evenly by the processes of one node (torchrun LOCAL_WORLD_SIZE)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return max(1, min(32, n // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
+
+
 def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops,
                   maxsize: int, nthreads: int = 0) -> AssemblyPackages:
     if maxsize < BYTES_PER_PAIR:
@@ -227,7 +237,7 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         cat, cpiv = rat, rpiv
     else:
         cat, cpiv = _op_arrays(col_ops, cs.size)
-    nthreads = nthreads or min(os.cpu_count() or 1, 32)
+    nthreads = nthreads or host_threads()
     h = ctypes.c_void_p()
     p = nat.ptr
     nat.check(nat.lib().gcabem_packages_build(
