@@ -16,7 +16,6 @@ check and the small V solves stay on the CPU, natively on all cores
 from __future__ import annotations
 
 import ctypes
-import os
 import time
 from dataclasses import dataclass
 
