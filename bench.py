@@ -509,6 +509,7 @@ def run_ours(args, cfg, dist, log):
     setup_first = None
     e2e_phases = []
     if args.e2e_steps > 0:
+        scheduler.clear_package_cache()
         warm = assemble_both([scheduler.AssemblyStats() for _ in specs])  # path + pinned pool
         del warm
     for k in range(args.e2e_steps):

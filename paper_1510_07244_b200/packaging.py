@@ -220,23 +220,69 @@ def host_threads() -> int:
     return max(1, min(32, n // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))))
 
 
+@dataclass
+class PackageInputs:
+    """The flat arrays make_packages hands to the native builder (triangles,
+    leaves, both trees, both operators' pivots), gathered once so that
+    several leaf ranges can be packaged without re-deriving them."""
+    T: np.ndarray
+    leaves: np.ndarray
+    leaf_ids: np.ndarray
+    row: tuple      # start, size, lo, hi, perm
+    col: tuple
+    row_ops: tuple  # at, pivots
+    col_ops: tuple
+
+
+def package_inputs(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops):
+    leaves, leaf_ids = _leaf_arrays(block_tree)
+    row = _tree_arrays(block_tree.row_tree)
+    col = row if block_tree.col_tree is block_tree.row_tree else \
+        _tree_arrays(block_tree.col_tree)
+    rop = _op_arrays(row_ops, row[0].size)
+    cop = rop if (col_ops is row_ops and col is row) else _op_arrays(col_ops, col[0].size)
+    return PackageInputs(np.ascontiguousarray(triangles, dtype=np.int64), leaves, leaf_ids,
+                         row, col, rop, cop)
+
+
+def leaf_layout(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs | None = None):
+    """(leaf_ids, leaf_shape, leaf_base) of the whole payload without building
+    packages: a dense leaf holds |t| x |s| entries, an admissible leaf the
+    coupling matrix rank(t) x rank(s) (make_packages' leaf loop)."""
+    x = inputs or package_inputs(np.zeros((0, 3), np.int64), block_tree, row_ops, col_ops)
+    rz, cz = x.row[1], x.col[1]
+    rat, cat = x.row_ops[0], x.col_ops[0]
+    # one gather per side from [ranks | sizes], the dense flag picking the half
+    rtab = np.concatenate([np.diff(rat), rz])
+    ctab = rtab if cat is rat and cz is rz else np.concatenate([np.diff(cat), cz])
+    leaves = x.leaves
+    shape = np.empty((leaves.shape[0], 2), np.int64)
+    shape[:, 0] = rtab[leaves[:, 0] + leaves[:, 2] * rz.size]
+    shape[:, 1] = ctab[leaves[:, 1] + leaves[:, 2] * cz.size]
+    base = np.zeros(leaves.shape[0] + 1, np.int64)
+    np.cumsum(shape[:, 0] * shape[:, 1], out=base[1:])
+    return x.leaf_ids, shape, base
+
+
 def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops,
-                  maxsize: int, nthreads: int = 0) -> AssemblyPackages:
+                  maxsize: int, nthreads: int = 0, leaf_range=None,
+                  inputs: PackageInputs | None = None) -> AssemblyPackages:
+    """Packages of the block tree's leaves (or of the leaves [lo, hi) of
+    leaf_range, payload offsets then relative to leaf lo: the same blocks and
+    corrective items those leaves get in the whole-tree packages, list ids
+    counted from 0). `inputs`: package_inputs() of the same arguments."""
     if maxsize < BYTES_PER_PAIR:
         raise SchedulerConfigError(
             f"maxsize {maxsize} smaller than one pair record ({BYTES_PER_PAIR} B)")
-    T = np.ascontiguousarray(triangles, dtype=np.int64)
-    leaves, leaf_ids = _leaf_arrays(block_tree)
-    rs, rz, rlo, rhi, rperm = _tree_arrays(block_tree.row_tree)
-    if block_tree.col_tree is block_tree.row_tree:
-        cs, cz, clo, chi, cperm = rs, rz, rlo, rhi, rperm
-    else:
-        cs, cz, clo, chi, cperm = _tree_arrays(block_tree.col_tree)
-    rat, rpiv = _op_arrays(row_ops, rs.size)
-    if col_ops is row_ops and cs is rs:
-        cat, cpiv = rat, rpiv
-    else:
-        cat, cpiv = _op_arrays(col_ops, cs.size)
+    x = inputs or package_inputs(triangles, block_tree, row_ops, col_ops)
+    T, leaves, leaf_ids = x.T, x.leaves, x.leaf_ids
+    if leaf_range is not None:
+        lo, hi = leaf_range
+        leaves, leaf_ids = leaves[lo:hi], leaf_ids[lo:hi]
+    rs, rz, rlo, rhi, rperm = x.row
+    cs, cz, clo, chi, cperm = x.col
+    rat, rpiv = x.row_ops
+    cat, cpiv = x.col_ops
     nthreads = nthreads or host_threads()
     h = ctypes.c_void_p()
     p = nat.ptr

@@ -33,7 +33,8 @@ from .h2 import GCAMatrix, LeafPayloads
 from .kernels import KernelSpec
 from .mesh import SurfaceMesh
 from .packaging import (BYTES_PER_PAIR, PAIR_RECORD_BYTES, SINGULAR_CASES, VALUE_BYTES,
-                        AssemblyPackages, SchedulerConfigError, make_packages, shard_leaves)
+                        AssemblyPackages, SchedulerConfigError, leaf_layout, make_packages,
+                        package_inputs, shard_leaves)
 from .quadrature import QuadRule4D, build_rule, classify_pair, gauss_legendre
 
 DEFAULT_MAXSIZE = 8 * 2 ** 20
@@ -86,6 +87,10 @@ class SchedulerParams:
     shard: tuple | None = None
     # leaf-aligned chunks per device whose D2H overlaps the next chunk's kernels
     chunks: int = 8
+    # leaf-range stages of a single-device assembly whose packages are not
+    # cached yet: stage k+1 is packaged on a host thread while stage k's
+    # kernels and D2H run (1 = package everything first)
+    stages: int = 5
 
     def backend_for(self, case: str) -> Backend:
         wanted = self.affinity.get(case)
@@ -500,6 +505,151 @@ def packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
     return pk
 
 
+class StagedPackages:
+    """Packages of contiguous leaf ranges, built one range after the other on
+    a host thread (make_packages(leaf_range=...)) so that the device can work
+    on range k while range k+1 is packaged. Each range's packages are exactly
+    the whole-tree packages restricted to its leaves (payload offsets relative
+    to the range's first leaf)."""
+
+    def __init__(self, mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
+                 maxsize: int, nstages: int):
+        inputs = package_inputs(mesh.triangles, block_tree, row_ops, col_ops)
+        self.leaf_ids, self.leaf_shape, self.leaf_base = leaf_layout(block_tree, row_ops,
+                                                                     col_ops, inputs)
+        L = self.leaf_ids.size
+        self.payload_len = int(self.leaf_base[-1])
+        # leaf-aligned ranges growing geometrically (payload fractions
+        # 1, 2, 4, ... / (2^n - 1)): the first range is packaged, computed and
+        # on the wire within milliseconds, and each later range is packaged
+        # while the (longer) D2H of all earlier ones runs
+        n = max(1, min(int(nstages), L))
+        frac = np.cumsum(2.0 ** np.arange(n))[:-1] / (2.0 ** n - 1)
+        cuts = np.searchsorted(self.leaf_base, self.payload_len * frac, side="left")
+        edges = np.unique(np.concatenate([[0], np.clip(cuts, 1, L), [L]]))
+        self.ranges = [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+        self._pk = [None] * len(self.ranges)
+        self._ready = [threading.Event() for _ in self.ranges]
+        self._err = None
+        args = (mesh.triangles, block_tree, row_ops, col_ops, int(maxsize))
+
+        def work():
+            for k, rng in enumerate(self.ranges):
+                try:
+                    self._pk[k] = make_packages(*args, leaf_range=rng, inputs=inputs)
+                except BaseException as exc:  # re-raised by stage()
+                    self._err = exc
+                    for ev in self._ready[k:]:
+                        ev.set()
+                    return
+                self._ready[k].set()
+        self._thread = threading.Thread(target=work, name="gcabem-packaging", daemon=True)
+        self._thread.start()
+
+    def chunks(self, k: int, total: int) -> int:
+        """D2H chunks of range k: about `total` over all ranges, by size."""
+        lo, hi = self.ranges[k]
+        share = (self.leaf_base[hi] - self.leaf_base[lo]) / max(self.payload_len, 1)
+        return max(2, int(round(total * share)))
+
+    def stage(self, k: int) -> AssemblyPackages:
+        self._ready[k].wait()
+        if self._pk[k] is None:
+            raise self._err
+        return self._pk[k]
+
+    def offset(self, k: int) -> int:
+        return int(self.leaf_base[self.ranges[k][0]])
+
+
+def staged_packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
+                        maxsize: int, nstages: int) -> StagedPackages:
+    """StagedPackages of (block tree, operators, budget, stages), cached like
+    packages_for (a second operator from the same packages packages nothing)."""
+    key = ("staged", id(block_tree), id(row_ops), id(col_ops), int(maxsize),
+           id(mesh.triangles), int(nstages))
+    with _pk_lock:
+        hit = _pk_cache.get(key)
+    if hit is not None and hit[0]() is block_tree:
+        return hit[3]
+    sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages)
+    with _pk_lock:
+        _pk_cache[key] = (weakref.ref(block_tree), row_ops, col_ops, sp)
+    weakref.finalize(block_tree, lambda k=key: _pk_cache.pop(k, None))
+    return sp
+
+
+def _cached_packages(mesh, block_tree, row_ops, col_ops, maxsize):
+    key = (id(block_tree), id(row_ops), id(col_ops), int(maxsize), id(mesh.triangles))
+    with _pk_lock:
+        hit = _pk_cache.get(key)
+    return hit[3] if hit is not None and hit[0]() is block_tree else None
+
+
+def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, stats,
+                     device):
+    """Single-device assembly over StagedPackages: plan k is created and
+    launched (kernels + chunked D2H on its own streams) as soon as range k is
+    packaged, so packaging and layout upload of later ranges overlap the
+    device work and the D2H of earlier ones."""
+    t0 = time.monotonic()
+    phase = {}
+    sp = staged_packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes,
+                             params.stages)
+    ta = time.monotonic()
+    outs = [nat.pinned_empty(sp.payload_len, np.complex128) for _ in range(2 if pair else 1)]
+    phase["pinned_alloc"] = time.monotonic() - ta
+    dm = device_mesh(mesh, device)
+    plans, wait = [], 0.0
+    try:
+        ta = time.monotonic()
+        for k in range(len(sp.ranges)):
+            tw = time.monotonic()
+            pk = sp.stage(k)
+            wait += time.monotonic() - tw
+            p = AssemblyPlan(dm, spec, pk, orders, pair=pair)
+            plans.append(p)
+            if p.payload_len:
+                sl = slice(sp.offset(k), sp.offset(k) + p.payload_len)
+                p.execute_download(outs[0][sl], sp.chunks(k, 2 * params.chunks),
+                                   outs[1][sl] if pair else None)
+        phase["packaging_wait"] = wait
+        phase["plans_launched"] = time.monotonic() - ta
+        for p in plans:
+            p.synchronize()
+        phase["execute_download"] = time.monotonic() - ta
+        ms = [p.timing_ms() for p in plans if p.payload_len]
+        stats.device_ms = {f"device{device}": {key: sum(m[key] for m in ms)
+                                               for key in ("disjoint", "singular", "total")}}
+    finally:
+        ta = time.monotonic()
+        for p in plans:
+            p.close()
+        phase["plan_destroy"] = time.monotonic() - ta
+    t1 = time.monotonic()
+    mult = 2 if pair else 1
+    ev = []
+    for k in range(len(sp.ranges)):
+        pk = sp.stage(k)
+        stats.block_pairs += mult * pk.block_pairs()
+        stats.corrective_items += mult * pk.num_items
+        ev += _events(pk, params.backend_for("disjoint").name, t0, t1)
+    stats.events.extend(ev * mult)
+    stats.lists_executed += mult * len(ev)
+    stats.pairs_executed += mult * sum(r["pairs"] for r in ev)
+    phase["total"] = time.monotonic() - t0
+    stats.phase_s = phase
+    return tuple(GCAMatrix(block_tree, row_ops, col_ops,
+                           LeafPayloads(buf, sp.leaf_ids, sp.leaf_base, sp.leaf_shape),
+                           buffer=buf) for buf in outs)
+
+
+def _use_staged(mesh, block_tree, row_ops, col_ops, params) -> bool:
+    devices = params.backend_for("disjoint").devices
+    return (params.stages > 1 and len(devices) == 1 and params.shard is None and
+            _cached_packages(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes) is None)
+
+
 def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
                  row_ops: dict, col_ops: dict, params: SchedulerParams | None = None,
                  orders: tuple = (3, 5), stats: AssemblyStats | None = None) -> GCAMatrix:
@@ -514,6 +664,9 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
     if not params.backends:
         raise SchedulerConfigError("at least one backend required")
     backend = params.backend_for("disjoint")
+    if _use_staged(mesh, block_tree, row_ops, col_ops, params):
+        return _assemble_staged(mesh, block_tree, spec, False, row_ops, col_ops, params, orders,
+                                stats, backend.devices[0])[0]
     t0 = time.monotonic()
     phase = {}
     pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
@@ -579,6 +732,9 @@ def run_assembly_pair(mesh: SurfaceMesh, block_tree: BlockTree, equation: str, k
     stats = stats if stats is not None else AssemblyStats()
     spec = KernelSpec(equation, "single", kappa)
     backend = params.backend_for("disjoint")
+    if _use_staged(mesh, block_tree, row_ops, col_ops, params):
+        return _assemble_staged(mesh, block_tree, spec, True, row_ops, col_ops, params, orders,
+                                stats, backend.devices[0])
     t0 = time.monotonic()
     phase = {}
     pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)

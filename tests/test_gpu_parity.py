@@ -519,3 +519,30 @@ def test_pair_plan_shards_equal_single(gload):
     # each shard fills its own leaf range and leaves the rest zero
     assert np.array_equal(parts[0][0].buffer + parts[1][0].buffer, S.buffer)
     assert np.array_equal(parts[0][1].buffer + parts[1][1].buffer, D.buffer)
+
+
+@pytest.mark.parametrize("stages", [2, 5])
+def test_staged_assembly_equals_unstaged(stages):
+    """Staged assembly (leaf ranges packaged on a host thread while earlier
+    ranges run on the device) gives the unstaged payloads bit for bit, for
+    the single-operator and the fused pair call; a second operator reuses the
+    cached stage packages."""
+    m, t, bt = sphere_setup(4)
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    spec = kernels.KernelSpec("helmholtz", "double", 4.0)
+    scheduler.clear_package_cache()
+    ref = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(stages=1))
+    refS, refD = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                             scheduler.SchedulerParams(stages=1))
+    scheduler.clear_package_cache()
+    params = scheduler.SchedulerParams(stages=stages)
+    st = scheduler.AssemblyStats()
+    got = scheduler.run_assembly(m, bt, spec, ops, ops, params, stats=st)
+    assert "packaging_wait" in st.phase_s
+    assert np.array_equal(got.buffer, ref.buffer)
+    for lid in list(ref.payloads)[::37]:
+        assert np.array_equal(got.payloads[lid], ref.payloads[lid])
+    S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops, params)
+    assert np.array_equal(S.buffer, refS.buffer) and np.array_equal(D.buffer, refD.buffer)
+    scheduler.clear_package_cache()

@@ -204,6 +204,40 @@ def test_native_packaging_matches_numpy(gload, level, maxsize):
                               b.panels[b.leaf_cols_at[k]:b.leaf_cols_at[k] + nc])
 
 
+@pytest.mark.parametrize("nstages", [2, 3, 7])
+def test_staged_packages_equal_whole_tree(nstages):
+    """Leaf-range packages (the staged assembly's) are the whole-tree packages
+    restricted to their leaves: same blocks, same corrective items, payload
+    offsets shifted by the range's base; leaf_layout gives the same shapes."""
+    m, t, bt = sphere_setup(4)
+    ids = {l.row for l in bt.leaves if l.kind == "admissible"} | \
+          {l.col for l in bt.leaves if l.kind == "admissible"}
+    ops = {c: gca.InterpolationOperator(c, None, t.panels(t.nodes[c])[::-1][:20], None)
+           for c in ids}
+    full = packaging.make_packages(m.triangles, bt, ops, ops, 20000)
+    lids, shape, base = packaging.leaf_layout(bt, ops, ops)
+    assert np.array_equal(lids, full.leaf_ids)
+    assert np.array_equal(shape, full.leaf_shape)
+    assert np.array_equal(base, full.leaf_base)
+    L = full.leaf_ids.size
+    edges = np.linspace(0, L, nstages + 1).astype(int)
+    blk, items = [], []
+    for lo, hi in zip(edges[:-1], edges[1:]):
+        pk = packaging.make_packages(m.triangles, bt, ops, ops, 20000, leaf_range=(lo, hi))
+        assert np.array_equal(pk.leaf_shape, full.leaf_shape[lo:hi])
+        assert np.array_equal(pk.leaf_base, full.leaf_base[lo:hi + 1] - full.leaf_base[lo])
+        blk.append(np.stack([pk.blk_leaf + lo, pk.blk_r0, pk.blk_nr, pk.blk_c0, pk.blk_nc]))
+        items.append(np.stack([pk.item_case.astype(np.int64), pk.item_tri_x, pk.item_tri_y,
+                               pk.item_leaf + lo, pk.item_offset]))
+    want_blk = np.stack([full.blk_leaf, full.blk_r0, full.blk_nr, full.blk_c0, full.blk_nc])
+    assert np.array_equal(np.concatenate(blk, axis=1), want_blk)
+    got = np.concatenate(items, axis=1)
+    want = np.stack([full.item_case.astype(np.int64), full.item_tri_x, full.item_tri_y,
+                     full.item_leaf, full.item_offset])
+    assert got.shape == want.shape
+    assert np.array_equal(got[:, np.lexsort(got[::-1])], want[:, np.lexsort(want[::-1])])
+
+
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
 def test_native_aca_matches_numpy_restatement(eq, kappa):
     """csrc/aca.cpp (threaded batch) vs the numpy ACA on every admissible
