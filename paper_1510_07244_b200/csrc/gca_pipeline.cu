@@ -2,14 +2,17 @@
 // gca.build_interpolation_operators, gca.py:285-310), as one native pipeline:
 //
 //   device   Green matrices of a batch of clusters (green_box_kernel: sources
-//            generated on the device from the enlarged boxes), D2H into one of
-//            two pinned staging buffers;
+//            generated on the device from the enlarged boxes), D2H into a
+//            free slot of a ring of pinned staging buffers;
 //   host     ACA + pivot-block check + refined V solve per cluster
-//            (gca_operator, aca.cpp) on a thread pool, reading the other
-//            staging buffer, while the device computes the next batch.
+//            (gca_operator, aca.cpp) on a thread pool, each worker copying
+//            its cluster out of the slot first, while the device computes the
+//            next batches.
 //
-// North star split: the Green matrices (dense FP64 kernel evaluations) are
-// device work, the pivoting and the small solves stay on the CPU.
+// Clusters run largest first (the longest host jobs start early: no tail with
+// idle threads). North star split: the Green matrices (dense FP64 kernel
+// evaluations) are device work, the pivoting and the small solves stay on
+// the CPU.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -17,6 +20,7 @@
 #include <memory>
 #include <cmath>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <vector>
@@ -64,6 +68,7 @@ constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging e
 struct Staging {
     Pinned host[SLOTS];
     DevBuf<double> out[SLOTS];
+    std::vector<std::vector<double>> aown;  // per worker: its cluster's Green matrix
     std::mutex busy;  // one build per device at a time (builds on other devices run in parallel)
 };
 std::mutex g_staging_mutex;
@@ -146,14 +151,21 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         }
     }
     tr.mark("boxes");
-    // batches of consecutive clusters by output bytes
+    // processing order: largest clusters first (their host work is the
+    // longest; issued last they would leave a tail with most threads idle),
+    // ties by index. Everything below is indexed by position in this order.
+    std::vector<int64_t> ord(ncl);
+    for (int64_t c = 0; c < ncl; ++c) ord[c] = c;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int64_t a, int64_t b) { return cl_size[a] > cl_size[b]; });
+    // batches of consecutive positions by output bytes
     const int64_t row_bytes = nsrc * 8 * width;
     if (batch_bytes <= 0) batch_bytes = int64_t(32) << 20;
     std::vector<int64_t> bstart{0};
     {
         int64_t acc = 0;
         for (int64_t c = 0; c < ncl; ++c) {
-            const int64_t b = cl_size[c] * row_bytes;
+            const int64_t b = cl_size[ord[c]] * row_bytes;
             if (acc > 0 && acc + b > batch_bytes) {
                 bstart.push_back(c);
                 acc = 0;
@@ -170,14 +182,14 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         int64_t acc = 0;
         for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) {
             out_at[b].push_back(acc);
-            const int64_t ne = cl_size[c] * ng;
+            const int64_t ne = cl_size[ord[c]] * ng;
             if (ne >= (int64_t(1) << 31)) {
                 delete G;
                 return gcabem_internal_error(GCABEM_ERR_ARG, "cluster too large");
             }
             for (int64_t e0 = 0; e0 < ne; e0 += GREEN_TPB)
                 tasks[b].push_back(make_int2((int)(c - bstart[b]), (int)e0));
-            acc += cl_size[c] * nsrc;
+            acc += cl_size[ord[c]] * nsrc;
         }
         max_elems = std::max(max_elems, acc);
     }
@@ -198,9 +210,11 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     PoolBuf<int2> d_task;
     std::vector<int64_t> first(ncl);
     std::vector<int32_t> size32(ncl);
+    std::vector<GreenBox> box_ord(ncl);
     for (int64_t c = 0; c < ncl; ++c) {
-        first[c] = cl_first[c];
-        size32[c] = (int32_t)cl_size[c];
+        first[c] = cl_first[ord[c]];
+        size32[c] = (int32_t)cl_size[ord[c]];
+        box_ord[c] = boxes[ord[c]];
     }
     std::vector<double> gq(2 * m);
     for (int k = 0; k < m; ++k) {
@@ -210,7 +224,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     if (e == cudaSuccess) e = d_first.upload(first.data(), ncl, s);
     if (e == cudaSuccess) e = d_size.upload(size32.data(), ncl, s);
     if (e == cudaSuccess) e = d_perm.upload(perm32.data(), nperm, s);
-    if (e == cudaSuccess) e = d_box.upload(boxes.data(), ncl, s);
+    if (e == cudaSuccess) e = d_box.upload(box_ord.data(), ncl, s);
     if (e == cudaSuccess) e = d_gq.upload(gq.data(), gq.size(), s);
     if (e == cudaSuccess) e = d_duffy.upload(duffy, 3 * nduffy, s);
     size_t max_tasks = 0, max_cl = 0;
@@ -232,9 +246,11 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     for (int k = 0; k < SLOTS && e == cudaSuccess; ++k)
         e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming | cudaEventBlockingSync);
 
-    // batch b uses slot b % SLOTS (tasks, offsets, device output, staging)
-    auto enqueue = [&](int64_t b) -> cudaError_t {
-        const int k = (int)(b % SLOTS);
+    // batch b uses slot slot_of[b] (tasks, offsets, device output, staging),
+    // taken from the free list when the batch is issued
+    std::vector<int> slot_of(nb, -1);
+    auto enqueue = [&](int64_t b, int k) -> cudaError_t {
+        slot_of[b] = k;
         int2 *tk = d_task.p + k * max_tasks;
         int64_t *at = d_at.p + k * max_cl;
         cudaError_t r = cudaMemcpyAsync(tk, tasks[b].data(), sizeof(int2) * tasks[b].size(),
@@ -248,7 +264,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                                  d_first.p + c0, d_size.p + c0, d_perm.p, d_box.p + c0, m, d_gq.p,
                                  d_duffy.p, (int)nduffy, at, st.out[k].p, kappa, s);
         int64_t elems = 0;
-        for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) elems += cl_size[c] * nsrc;
+        for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) elems += cl_size[ord[c]] * nsrc;
         if (r == cudaSuccess)
             r = cudaMemcpyAsync(st.host[k].p, st.out[k].p, sizeof(double) * elems * width,
                                 cudaMemcpyDeviceToHost, s);
@@ -260,38 +276,48 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     // cluster's Green matrix out of the staging slot before working on it, so
     // a slot is free again as soon as all its clusters are claimed (no
     // per-batch barrier, no wait on the slowest cluster); the calling thread
-    // issues batches into free slots and publishes each batch when its D2H
-    // has landed.
+    // issues batches into whichever slots are free (a slot held by the long
+    // copy-out of a large cluster does not stall the others) and publishes
+    // each batch when its D2H has landed.
     std::vector<int64_t> batch_of(ncl);
     for (int64_t b = 0; b < nb; ++b)
         for (int64_t c = bstart[b]; c < bstart[b + 1]; ++c) batch_of[c] = b;
     std::unique_ptr<std::atomic<int64_t>[]> remaining(new std::atomic<int64_t>[nb > 0 ? nb : 1]);
     for (int64_t b = 0; b < nb; ++b) remaining[b] = bstart[b + 1] - bstart[b];
     std::vector<char> ready(nb, 0);
+    std::vector<int> free_slots;
+    for (int k = SLOTS - 1; k >= 0; --k) free_slots.push_back(k);
     std::mutex mu;
     std::condition_variable cv;
     bool abort = false;
     std::atomic<int64_t> next{0};
     std::atomic<int64_t> err_cluster{INT64_MAX};
     std::atomic<int> err_code{0};
-    std::vector<double> busy(nthreads, 0.0);
+    std::vector<double> busy(nthreads, 0.0), first_at(nthreads, -1.0), last_at(nthreads, 0.0),
+        starved(nthreads, 0.0);
+    const auto t_start = clk::now();
+    if ((int)st.aown.size() < nthreads) st.aown.resize(nthreads);
     auto worker = [&](int tid) {
-        std::vector<double> Aown;
+        std::vector<double> &Aown = st.aown[tid];  // grow-only across calls: no page faults
         for (;;) {
-            const int64_t c = next.fetch_add(1);
-            if (c >= ncl) return;
-            const int64_t b = batch_of[c];
+            const int64_t pos = next.fetch_add(1);
+            if (pos >= ncl) return;
+            const int64_t b = batch_of[pos], c = ord[pos];
+            const auto tw = clk::now();
             {
                 std::unique_lock<std::mutex> lk(mu);
                 cv.wait(lk, [&] { return ready[b] || abort; });
                 if (abort) return;
             }
             const auto t0 = clk::now();
-            const double *A = static_cast<const double *>(st.host[b % SLOTS].p) +
-                              out_at[b][c - bstart[b]] * width;
+            starved[tid] += std::chrono::duration<double>(t0 - tw).count();
+            if (first_at[tid] < 0.0) first_at[tid] = std::chrono::duration<double>(t0 - t_start).count();
+            const double *A = static_cast<const double *>(st.host[slot_of[b]].p) +
+                              out_at[b][pos - bstart[b]] * width;
             Aown.assign(A, A + cl_size[c] * nsrc * width);
-            if (remaining[b].fetch_sub(1) == 1) {  // slot b % SLOTS drained
+            if (remaining[b].fetch_sub(1) == 1) {  // slot drained: back to the free list
                 std::lock_guard<std::mutex> lk(mu);
+                free_slots.push_back(slot_of[b]);
                 cv.notify_all();
             }
             const int rc = gca_operator(equation == 1, Aown.data(), cl_size[c], nsrc, epsilon,
@@ -303,6 +329,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                 if (c <= err_cluster.load()) err_code = rc;
             }
             busy[tid] += since(t0);
+            last_at[tid] = since(t_start);
         }
     };
     double t_wait = 0.0;
@@ -312,20 +339,30 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         for (int t = 0; t < nthreads; ++t) th.emplace_back(worker, t);
     int64_t issued = 0, completed = 0;
     while (e == cudaSuccess && completed < nb) {
-        while (e == cudaSuccess && issued < nb &&
-               (issued < SLOTS || remaining[issued - SLOTS].load() == 0))
-            e = enqueue(issued++);
+        for (;;) {
+            int k = -1;
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                if (issued < nb && !free_slots.empty()) {
+                    k = free_slots.back();
+                    free_slots.pop_back();
+                }
+            }
+            if (k < 0) break;
+            e = enqueue(issued++, k);
+            if (e != cudaSuccess) break;
+        }
         if (e != cudaSuccess) break;
         if (completed < issued) {
             const auto t0 = clk::now();
-            e = cudaEventSynchronize(done[completed % SLOTS]);
+            e = cudaEventSynchronize(done[slot_of[completed]]);
             t_wait += since(t0);
             std::lock_guard<std::mutex> lk(mu);
             ready[completed++] = 1;
             cv.notify_all();
         } else {
             std::unique_lock<std::mutex> lk(mu);
-            cv.wait(lk, [&] { return remaining[issued - SLOTS].load() == 0; });
+            cv.wait(lk, [&] { return !free_slots.empty(); });
         }
     }
     if (e != cudaSuccess) {
@@ -335,6 +372,14 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     for (auto &t : th) t.join();
     tr.mark("pipeline");
+    if (tr.on && nthreads > 0)
+        std::fprintf(stderr, "[gca] workers: first cluster %.1f-%.1f ms, last done %.1f-%.1f ms, "
+                     "waiting for Green batches %.1f ms (all threads)\n",
+                     1e3 * *std::min_element(first_at.begin(), first_at.end()),
+                     1e3 * *std::max_element(first_at.begin(), first_at.end()),
+                     1e3 * *std::min_element(last_at.begin(), last_at.end()),
+                     1e3 * *std::max_element(last_at.begin(), last_at.end()),
+                     1e3 * std::accumulate(starved.begin(), starved.end(), 0.0));
     double t_host = 0.0;
     for (double x : busy) t_host += x;
     G->phase[1] = since(t_pipe);
