@@ -69,41 +69,56 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
         uu[d] = fma(ux, ux, fma(uy, uy, uz * uz));
         un[d] = DL ? fma(ux, n[0], fma(uy, n[1], uz * n[2])) : 0.0;
     }
-    // -2 xo . u_d = (-2 xo . e1y) + g_d (-2 xo . e2y): two dots per x point
-    const double f1[3] = {-2.0 * e1y[0], -2.0 * e1y[1], -2.0 * e1y[2]};
-    const double f2[3] = {-2.0 * e2y[0], -2.0 * e2y[1], -2.0 * e2y[2]};
+    // x-side quantities as polynomials in the x point (s, t) = (a, a b):
+    //   |xo|^2     = Q0 + s (2 P1 + s Q11) + t (2 P2 + 2 s Q12 + t Q22)
+    //   -2 xo.e1y  = A0 + s A1 + t A2,  -2 xo.e2y = B0 + s B1 + t B2
+    //   xo.n_y     = N0 + s N1 + t N2
+    // with xo = dO + s e1x + t e2x; the s parts once per a, 5 FMA per x point
+    auto dot = [](const double *u, const double *v) { return fma(u[0], v[0], fma(u[1], v[1], u[2] * v[2])); };
+    const double Q0 = dot(dO, dO), P1 = 2.0 * dot(dO, e1x), P2 = 2.0 * dot(dO, e2x);
+    const double Q11 = dot(e1x, e1x), Q12 = 2.0 * dot(e1x, e2x), Q22 = dot(e2x, e2x);
+    const double A0 = -2.0 * dot(dO, e1y), A1 = -2.0 * dot(e1x, e1y), A2 = -2.0 * dot(e2x, e1y);
+    const double B0 = -2.0 * dot(dO, e2y), B1 = -2.0 * dot(e1x, e2y), B2 = -2.0 * dot(e2x, e2y);
+    const double N0 = DL ? dot(dO, n) : 0.0, N1 = DL ? dot(e1x, n) : 0.0,
+                 N2 = DL ? dot(e2x, n) : 0.0;
 #pragma unroll 1
-    for (int p = 0; p < N * N; ++p) {
-        const double s = c_gauss[N][p / N];
-        const double t = c_duffy_t[duffy_offset(N) + p];
-        const double wx = c_duffy_w[duffy_offset(N) + p];
-        const double xo0 = fma(t, e2x[0], fma(s, e1x[0], dO[0]));
-        const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
-        const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
-        const double xx = fma(xo0, xo0, fma(xo1, xo1, xo2 * xo2));
-        const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
-        const double a2 = fma(xo0, f1[0], fma(xo1, f1[1], xo2 * f1[2]));
-        const double b2 = fma(xo0, f2[0], fma(xo1, f2[1], xo2 * f2[2]));
-        double in[4] = {0.0, 0.0, 0.0, 0.0};
-        // fused pair kinds at orders >= 6 roll the outer y loop (the fully
-        // unrolled N^2 body spills their two layers of state)
-        constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
+    for (int ia = 0; ia < N; ++ia) {
+        const double s = c_gauss[N][ia];
+        const double xs = fma(s, fma(s, Q11, P1), Q0);
+        const double vs = fma(s, Q12, P2);
+        const double as = fma(s, A1, A0);
+        const double bs = fma(s, B1, B0);
+        const double ns = DL ? fma(s, N1, N0) : 0.0;
+#pragma unroll 1
+        for (int ib = 0; ib < N; ++ib) {
+            const int p = ia * N + ib;
+            const double t = c_duffy_t[duffy_offset(N) + p];
+            const double wx = c_duffy_w[duffy_offset(N) + p];
+            const double xx = fma(t, fma(t, Q22, vs), xs);
+            const double xon = DL ? fma(t, N2, ns) : 0.0;
+            const double a2 = fma(t, A2, as);
+            const double b2 = fma(t, B2, bs);
+            double in[4] = {0.0, 0.0, 0.0, 0.0};
+            // fused pair kinds at orders >= 6 roll the outer y loop (the fully
+            // unrolled N^2 body spills their two layers of state)
+            constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
 #pragma unroll OUTER
-        for (int d = 0; d < N; ++d) {
-            const double m2b = fma(c_gauss[N][d], b2, a2);
+            for (int d = 0; d < N; ++d) {
+                const double m2b = fma(c_gauss[N][d], b2, a2);
 #pragma unroll
-            for (int c = 0; c < N; ++c) {
-                const double gc = c_gauss[N][c];
-                const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
-                const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
-                const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
+                for (int c = 0; c < N; ++c) {
+                    const double gc = c_gauss[N][c];
+                    const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+                    const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
+                    const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
+                    accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
+                }
             }
+            acc[0] = fma(wx, in[0], acc[0]);
+            if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
+            if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
+            if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
         }
-        acc[0] = fma(wx, in[0], acc[0]);
-        if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
-        if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
-        if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
     }
 }
 
@@ -237,8 +252,9 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     // Helmholtz phase about the centroid distance: |kappa r - kappa D| <= kappa (rx + ry)
     const double phi0 = HELM ? kappa * dcen : 0.0;
     const double dmax = HELM && active ? kappa * (rx + ry) : 0.0;
-    const bool tiny = __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
-    const bool smallp = __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
+    // kappa = 0 takes the full-sincos tier (unscaled geometry, see below)
+    const bool tiny = HELM && kappa > 0.0 && __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
+    const bool smallp = HELM && kappa > 0.0 && __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
     if (!active) {
         if (inb) {
             *dst = make_double2(0.0, 0.0);
@@ -247,18 +263,31 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
         return;
     }
     if constexpr (HELM) {
-        if (tiny) {
-            if (expanded)
-                disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
-            else
-                disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
+        if (tiny || smallp) {
+            // geometry in units of 1/kappa: kappa r = r2' y' with no product
+            // by kappa per point (the point kernels get kappa = 1); the sums
+            // come out as S / kappa (single layer) and D / kappa^2 (double)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                dO[c] *= kappa;
+                e1x[c] *= kappa;
+                e2x[c] *= kappa;
+                e1y[c] *= kappa;
+                e2y[c] *= kappa;
+            }
+            if (tiny) {
+                if (expanded)
+                    disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                else
+                    disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+            } else {
+                if (expanded)
+                    disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                else
+                    disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+            }
             rotate_acc<KIND>(phi0, acc);
-        } else if (smallp) {
-            if (expanded)
-                disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
-            else
-                disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
-            rotate_acc<KIND>(phi0, acc);
+            unscale_acc<KIND>(kappa, acc);
         } else {
             if (expanded)
                 disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
