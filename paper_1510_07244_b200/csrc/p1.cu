@@ -109,6 +109,31 @@ __device__ __forceinline__ void p1_disjoint_pair(const double dO[3], const doubl
     }
 }
 
+// geometry in units of 1/kappa (Helmholtz tiers with kappa > 0, as
+// disjoint_kernel): the point kernels get kappa = 1, the sums come out as
+// S / kappa (single layer) and D / kappa^2 (double layer)
+__device__ __forceinline__ void scale_geometry(double kappa, double dO[3], double e1x[3],
+                                               double e2x[3], double e1y[3], double e2y[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        dO[c] *= kappa;
+        e1x[c] *= kappa;
+        e2x[c] *= kappa;
+        e1y[c] *= kappa;
+        e2y[c] *= kappa;
+    }
+}
+
+template <int KIND>
+__device__ __forceinline__ void p1_unscale(double kappa, double acc[9][2]) {
+    const double f = KIND == H_DLP ? kappa * kappa : kappa;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+        acc[e][0] *= f;
+        acc[e][1] *= f;
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy, bool helm_rot,
                                           double phi0, const uint8_t *px, const uint8_t *py,
@@ -175,8 +200,9 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     constexpr bool HELM = (KIND == H_SLP || KIND == H_DLP);
     const double phi0 = HELM ? kappa * norm3(dc[0], dc[1], dc[2]) : 0.0;
     const double dmax = HELM && active ? kappa * (cx->radius + cy->radius) : 0.0;
-    const bool tiny = __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
-    const bool smallp = __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
+    // kappa = 0 takes the full-sincos tier (unscaled geometry)
+    const bool tiny = kappa > 0.0 && __all_sync(0xffffffffu, dmax <= TINY_PHASE_MAX);
+    const bool smallp = kappa > 0.0 && __all_sync(0xffffffffu, dmax <= SMALL_PHASE_MAX);
     if (!active) {
         // singular pairs are overwritten by the singular pass; keep them 0
         if (inb)
@@ -190,12 +216,16 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     if constexpr (HELM) {
         const int ph = tiny ? 2 : (smallp ? 1 : 0);
         rot = ph > 0;
-        if (ph == 2)
-            p1_disjoint_pair<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
-        else if (ph == 1)
-            p1_disjoint_pair<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, kappa, phi0, acc);
-        else
+        if (ph > 0) {
+            scale_geometry(kappa, dO, e1x, e2x, e1y, e2y);
+            if (ph == 2)
+                p1_disjoint_pair<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+            else
+                p1_disjoint_pair<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+            p1_unscale<KIND>(kappa, acc);
+        } else {
             p1_disjoint_pair<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+        }
     } else {
         p1_disjoint_pair<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
     }
@@ -297,17 +327,21 @@ p1_generic_kernel(const double *__restrict__ V, const int32_t *__restrict__ T,
             dc[c] = fma(1.0 / 3.0, (2.0 * e1x[c] + e2x[c]) - (2.0 * e1y[c] + e2y[c]), dO[c]);
         phi0 = kappa * norm3(dc[0], dc[1], dc[2]);
         const double rsum = valid ? charts[it.tri_x].radius + charts[it.tri_y].radius : 0.0;
-        if (__syncthreads_and(!valid || kappa * rsum <= TINY_PHASE_MAX))
+        if (kappa > 0.0 && __syncthreads_and(!valid || kappa * rsum <= TINY_PHASE_MAX))
             tier = 2;
-        else if (__syncthreads_and(!valid || kappa * rsum <= SMALL_PHASE_MAX))
+        else if (kappa > 0.0 && __syncthreads_and(!valid || kappa * rsum <= SMALL_PHASE_MAX))
             tier = 1;
     }
-    if (tier == 2)
-        p1_generic_rule<KIND, 2>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, phi0, acc);
-    else if (tier == 1)
-        p1_generic_rule<KIND, 1>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, phi0, acc);
-    else
+    if (tier > 0) {
+        scale_geometry(kappa, dO, e1x, e2x, e1y, e2y);
+        if (tier == 2)
+            p1_generic_rule<KIND, 2>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, 1.0, phi0, acc);
+        else
+            p1_generic_rule<KIND, 1>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, 1.0, phi0, acc);
+        p1_unscale<KIND>(kappa, acc);
+    } else {
         p1_generic_rule<KIND, 0>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, 0.0, acc);
+    }
     if (valid) p1_finish<KIND>(acc, gx, gy, tier > 0, phi0, it.px, it.py, local + 9 * it.out);
 }
 
