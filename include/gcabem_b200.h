@@ -201,6 +201,13 @@ int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_s
                           uint8_t *flagged, int64_t *blocks, int64_t *blk_list, int64_t *items,
                           uint8_t *perms);
 int gcabem_packages_free(gcabem_packages_t pk);
+/* Payload layout of the leaves alone (the leaf loop of gcabem_packages_build,
+ * make_payloads scheduler.py:411-422): leaf_shape L x 2 {rows, cols} (dense
+ * |t| x |s|, admissible rank_t x rank_s), leaf_base L + 1 prefix offsets. */
+int gcabem_leaf_layout(int64_t nleaves, const int64_t *leaves, int64_t nrow,
+                       const int64_t *row_size, const int64_t *row_op_at, int64_t ncol,
+                       const int64_t *col_size, const int64_t *col_op_at, int64_t *leaf_shape,
+                       int64_t *leaf_base);
 
 /* ---- GCA Green matrices ---------------------------------------------------
  * Replaces gca.build_green_matrix (gca.py:136-179), batched over clusters.

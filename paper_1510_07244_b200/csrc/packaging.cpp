@@ -388,4 +388,24 @@ int gcabem_packages_free(gcabem_packages_t pk) {
     return GCABEM_OK;
 }
 
+int gcabem_leaf_layout(int64_t nleaves, const int64_t *leaves, int64_t nrow,
+                       const int64_t *row_size, const int64_t *row_op_at, int64_t ncol,
+                       const int64_t *col_size, const int64_t *col_op_at, int64_t *leaf_shape,
+                       int64_t *leaf_base) {
+    if (nleaves < 0 || (nleaves > 0 && (!leaves || !leaf_shape || !leaf_base)))
+        return gcabem_internal_error(GCABEM_ERR_ARG, "leaf_layout: bad arguments");
+    leaf_base[0] = 0;
+    for (int64_t k = 0; k < nleaves; ++k) {
+        const int64_t r = leaves[3 * k], c = leaves[3 * k + 1];
+        if (r < 0 || r >= nrow || c < 0 || c >= ncol)
+            return gcabem_internal_error(GCABEM_ERR_ARG, "leaf cluster index out of range");
+        const int64_t nr = leaves[3 * k + 2] ? row_size[r] : row_op_at[r + 1] - row_op_at[r];
+        const int64_t nc = leaves[3 * k + 2] ? col_size[c] : col_op_at[c + 1] - col_op_at[c];
+        leaf_shape[2 * k] = nr;
+        leaf_shape[2 * k + 1] = nc;
+        leaf_base[k + 1] = leaf_base[k] + nr * nc;
+    }
+    return GCABEM_OK;
+}
+
 }  // extern "C"

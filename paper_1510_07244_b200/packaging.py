@@ -182,7 +182,7 @@ def _op_arrays(ops: dict, nnodes: int):
     operator objects (ops dicts cannot be weak-referenced: the entry keeps a
     fingerprint of (cluster, operator identity) pairs and is replaced when it
     no longer matches)."""
-    fp = (nnodes, tuple((k, id(v)) for k, v in ops.items()))
+    fp = (nnodes, tuple(ops.keys()), tuple(map(id, ops.values())))
     with _cache_lock:
         hit = _op_cache.get(id(ops))
     if hit is not None and hit[0] == fp:
@@ -250,17 +250,13 @@ def leaf_layout(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs |
     packages: a dense leaf holds |t| x |s| entries, an admissible leaf the
     coupling matrix rank(t) x rank(s) (make_packages' leaf loop)."""
     x = inputs or package_inputs(np.zeros((0, 3), np.int64), block_tree, row_ops, col_ops)
-    rz, cz = x.row[1], x.col[1]
-    rat, cat = x.row_ops[0], x.col_ops[0]
-    # one gather per side from [ranks | sizes], the dense flag picking the half
-    rtab = np.concatenate([np.diff(rat), rz])
-    ctab = rtab if cat is rat and cz is rz else np.concatenate([np.diff(cat), cz])
-    leaves = x.leaves
-    shape = np.empty((leaves.shape[0], 2), np.int64)
-    shape[:, 0] = rtab[leaves[:, 0] + leaves[:, 2] * rz.size]
-    shape[:, 1] = ctab[leaves[:, 1] + leaves[:, 2] * cz.size]
-    base = np.zeros(leaves.shape[0] + 1, np.int64)
-    np.cumsum(shape[:, 0] * shape[:, 1], out=base[1:])
+    L = x.leaves.shape[0]
+    shape = np.empty((L, 2), np.int64)
+    base = np.empty(L + 1, np.int64)
+    p = nat.ptr
+    nat.check(nat.lib().gcabem_leaf_layout(L, p(x.leaves), x.row[1].size, p(x.row[1]),
+                                           p(x.row_ops[0]), x.col[1].size, p(x.col[1]),
+                                           p(x.col_ops[0]), p(shape), p(base)))
     return x.leaf_ids, shape, base
 
 

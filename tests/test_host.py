@@ -238,6 +238,37 @@ def test_staged_packages_equal_whole_tree(nstages):
     assert np.array_equal(got[:, np.lexsort(got[::-1])], want[:, np.lexsort(want[::-1])])
 
 
+@pytest.mark.parametrize("nstages", [1, 3, 5, 9])
+def test_staged_packages_ranges(nstages):
+    """scheduler.StagedPackages: leaf ranges tile [0, L) in order, range 0 is
+    the first L/64 leaves, later ranges grow with the payload; each stage's
+    packages are make_packages(leaf_range) of its range; the layout equals the
+    whole-tree packages' (native gcabem_leaf_layout)."""
+    from paper_1510_07244_b200 import scheduler
+    m, t, bt = sphere_setup(4)
+    ids = {l.row for l in bt.leaves if l.kind == "admissible"} | \
+          {l.col for l in bt.leaves if l.kind == "admissible"}
+    ops = {c: gca.InterpolationOperator(c, None, t.panels(t.nodes[c])[::-1][:20], None)
+           for c in ids}
+    full = packaging.make_packages(m.triangles, bt, ops, ops, 20000)
+    sp = scheduler.StagedPackages(m, bt, ops, ops, 20000, nstages)
+    L = full.leaf_ids.size
+    assert np.array_equal(sp.leaf_base, full.leaf_base)
+    assert np.array_equal(sp.leaf_shape, full.leaf_shape)
+    assert sp.ranges[0][0] == 0 and sp.ranges[-1][1] == L
+    assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(sp.ranges, sp.ranges[1:]))
+    assert len(sp.ranges) <= nstages
+    if nstages > 1:
+        assert sp.ranges[0] == (0, max(1, L // 64))
+    for k, rng in enumerate(sp.ranges):
+        pk = sp.stage(k)
+        ref = packaging.make_packages(m.triangles, bt, ops, ops, 20000, leaf_range=rng)
+        for f in ("blk_leaf", "blk_r0", "blk_nr", "blk_c0", "blk_nc", "item_case", "item_tri_x",
+                  "item_tri_y", "item_leaf", "item_offset", "perms", "leaf_base"):
+            assert np.array_equal(getattr(pk, f), getattr(ref, f)), (k, f)
+        assert sp.offset(k) == full.leaf_base[rng[0]]
+
+
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
 def test_native_aca_matches_numpy_restatement(eq, kappa):
     """csrc/aca.cpp (threaded batch) vs the numpy ACA on every admissible

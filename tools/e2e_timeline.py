@@ -1,0 +1,28 @@
+"""Timeline of the staged e2e assembly (run_assembly_pair): per leaf range the
+times (ms from the call) it was packaged, its plan created, launched and
+synchronised, against the PCIe floor of its bytes."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.getcwd())
+import bench  # noqa: E402
+from paper_1510_07244_b200 import scheduler  # noqa: E402
+
+cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+cfg = bench.CONFIGS[cfg_name]
+m, bt, ops, pk, _ = bench.build_workload(cfg, 0, lambda s: None)
+for rep in range(4):
+    scheduler.clear_package_cache()
+    st = scheduler.AssemblyStats()
+    t0 = time.perf_counter()
+    out = scheduler.run_assembly_pair(m, bt, cfg["equation"], cfg["kappa"], ops, ops,
+                                      scheduler.SchedulerParams(stages=int(os.environ.get("STAGES", "6"))),
+                                      cfg["orders"], st)
+    dt = time.perf_counter() - t0
+    print(f"{cfg_name} total {dt * 1e3:.1f} ms  phases " +
+          " ".join(f"{k}={v * 1e3:.1f}" for k, v in st.phase_s.items()))
+    for k, t in enumerate(st.stage_times):
+        print(f"   range {k}: packaged {t[0] * 1e3:6.1f}  plan {t[1] * 1e3:6.1f}  "
+              f"launched {t[2] * 1e3:6.1f}  done {t[3] * 1e3:6.1f} ms")
+    del out
