@@ -233,7 +233,9 @@ class _PinnedBlock:
         self.size, self.ptr = _POOL.acquire(nbytes)
 
     def __del__(self):
-        if self.ptr:
+        # at interpreter teardown the module globals may already be gone:
+        # the process exit returns the memory
+        if self.ptr and _POOL is not None:
             _POOL.release(self.size, self.ptr)
         self.ptr = None
 
