@@ -376,59 +376,77 @@ bool cond_ok(const T *B, const LU<T> &luT, int64_t r) {
     return cond2<T>(B, r) <= 1e14;
 }
 
+// V = A[:, cols] B^-1 for ACA pivots (rows, cols, rank k): 0, or 2 when the
+// pivot block is singular or its condition number is above 1e14
+template <typename T>
+int solve_one(const T *A, int64_t nr, int64_t nc, int64_t k, const int64_t *rows,
+              const int64_t *cols, std::vector<int64_t> &rows_out, std::vector<double> &V_out) {
+    using O = Ops<T>;
+    // pivot block B[a][b] = A[rows[a], cols[b]], and M = B^T
+    std::vector<T> B((size_t)(k * k)), M((size_t)(k * k));
+    for (int64_t a = 0; a < k; ++a)
+        for (int64_t b = 0; b < k; ++b) {
+            B[a * k + b] = A[rows[a] * nc + cols[b]];
+            M[b * k + a] = B[a * k + b];
+        }
+    LU<T> lu;
+    if (!lu.factor(M.data(), k)) return 2;  // exactly singular: cond = inf
+    if (!cond_ok<T>(B.data(), lu, k)) return 2;
+    // X = V^T (k x nr) solves M X = A_cols^T
+    std::vector<T> RHS((size_t)(k * nr)), X, R((size_t)(k * nr));
+    double amax = 0.0;
+    for (int64_t q = 0; q < nr; ++q)
+        for (int64_t b = 0; b < k; ++b) {
+            const T v = A[q * nc + cols[b]];
+            RHS[b * nr + q] = v;
+            amax = std::max(amax, O::mag(v));
+        }
+    X = RHS;
+    lu.solve(X.data(), nr);
+    const double lim = 1e-15 * std::max(amax, 1.0);
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        // R^T = A_cols^T - B^T V^T = RHS - M X
+        R = RHS;
+        for (int64_t b = 0; b < k; ++b) {
+            T *rb = R.data() + b * nr;
+            for (int64_t l = 0; l < k; ++l) mulsub<T>(rb, M[b * k + l], X.data() + l * nr, nr);
+        }
+        double rmax = 0.0;
+        for (const T &v : R) rmax = std::max(rmax, O::mag(v));
+        if (rmax <= lim) break;
+        lu.solve(R.data(), nr);
+        for (size_t e = 0; e < X.size(); ++e) X[e] = add_(X[e], R[e]);
+    }
+    rows_out.assign(rows, rows + k);
+    const int w = std::is_same<T, Cx>::value ? 2 : 1;
+    V_out.resize((size_t)(nr * k * w));
+    T *V = reinterpret_cast<T *>(V_out.data());
+    for (int64_t q = 0; q < nr; ++q)
+        for (int64_t b = 0; b < k; ++b) V[q * k + b] = X[b * nr + q];
+    return 0;
+}
+
+// The whole operator: ACA at eps (or the given first-attempt pivots), the
+// solve, and one retry at eps / 10 when the pivot block is rejected
 template <typename T>
 int operator_one(const T *A, int64_t nr, int64_t nc, double eps, std::vector<int64_t> &rows_out,
-                 std::vector<double> &V_out) {
-    using O = Ops<T>;
+                 std::vector<double> &V_out, int64_t pre_k = -1, const int64_t *pre_rows = nullptr,
+                 const int64_t *pre_cols = nullptr) {
     const int64_t cap = std::min(nr, nc);
     std::vector<int64_t> rows(cap), cols(cap);
     for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
         int64_t k = 0;
-        double resid = 0.0;
-        aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
-        if (k == 0) return 1;
-        // pivot block B[a][b] = A[rows[a], cols[b]], and M = B^T
-        std::vector<T> B((size_t)(k * k)), M((size_t)(k * k));
-        for (int64_t a = 0; a < k; ++a)
-            for (int64_t b = 0; b < k; ++b) {
-                B[a * k + b] = A[rows[a] * nc + cols[b]];
-                M[b * k + a] = B[a * k + b];
-            }
-        LU<T> lu;
-        if (!lu.factor(M.data(), k)) continue;  // exactly singular: cond = inf
-        if (!cond_ok<T>(B.data(), lu, k)) continue;
-        // X = V^T (k x nr) solves M X = A_cols^T
-        std::vector<T> RHS((size_t)(k * nr)), X, R((size_t)(k * nr));
-        double amax = 0.0;
-        for (int64_t q = 0; q < nr; ++q)
-            for (int64_t b = 0; b < k; ++b) {
-                const T v = A[q * nc + cols[b]];
-                RHS[b * nr + q] = v;
-                amax = std::max(amax, O::mag(v));
-            }
-        X = RHS;
-        lu.solve(X.data(), nr);
-        const double lim = 1e-15 * std::max(amax, 1.0);
-        for (int sweep = 0; sweep < 2; ++sweep) {
-            // R^T = A_cols^T - B^T V^T = RHS - M X
-            R = RHS;
-            for (int64_t b = 0; b < k; ++b) {
-                T *rb = R.data() + b * nr;
-                for (int64_t l = 0; l < k; ++l) mulsub<T>(rb, M[b * k + l], X.data() + l * nr, nr);
-            }
-            double rmax = 0.0;
-            for (const T &v : R) rmax = std::max(rmax, O::mag(v));
-            if (rmax <= lim) break;
-            lu.solve(R.data(), nr);
-            for (size_t e = 0; e < X.size(); ++e) X[e] = add_(X[e], R[e]);
+        const int64_t *r = rows.data(), *c = cols.data();
+        if (attempt == 0 && pre_k >= 0) {
+            k = pre_k;
+            r = pre_rows;
+            c = pre_cols;
+        } else {
+            double resid = 0.0;
+            aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
         }
-        rows_out.assign(rows.begin(), rows.begin() + k);
-        const int w = std::is_same<T, Cx>::value ? 2 : 1;
-        V_out.resize((size_t)(nr * k * w));
-        T *V = reinterpret_cast<T *>(V_out.data());
-        for (int64_t q = 0; q < nr; ++q)
-            for (int64_t b = 0; b < k; ++b) V[q * k + b] = X[b * nr + q];
-        return 0;
+        if (k == 0) return 1;
+        if (solve_one<T>(A, nr, nc, k, r, c, rows_out, V_out) == 0) return 0;
     }
     return 2;
 }
@@ -443,10 +461,12 @@ void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double 
 }
 
 int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                   std::vector<int64_t> &rows, std::vector<double> &V) {
+                   std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
+                   const int64_t *pre_rows, const int64_t *pre_cols) {
     if (is_complex)
-        return operator_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, epsilon, rows, V);
-    return operator_one<double>(A, nr, nc, epsilon, rows, V);
+        return operator_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, epsilon, rows, V, pre_k,
+                                pre_rows, pre_cols);
+    return operator_one<double>(A, nr, nc, epsilon, rows, V, pre_k, pre_rows, pre_cols);
 }
 
 }  // namespace GCABEM_ACA_NS
@@ -456,7 +476,8 @@ namespace aca_avx2 {
 void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps, int64_t cap,
                int64_t *rows, int64_t *cols, int64_t *rank, double *resid);
 int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                   std::vector<int64_t> &rows, std::vector<double> &V);
+                   std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
+                   const int64_t *pre_rows, const int64_t *pre_cols);
 }  // namespace aca_avx2
 
 namespace {
@@ -503,9 +524,20 @@ extern "C" int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows
 
 namespace gcabem {
 int gca_operator(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                 std::vector<int64_t> &rows, std::vector<double> &V) {
-    if (use_avx2()) return aca_avx2::operator_entry(is_complex, A, nr, nc, epsilon, rows, V);
-    return aca_base::operator_entry(is_complex, A, nr, nc, epsilon, rows, V);
+                 std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
+                 const int64_t *pre_rows, const int64_t *pre_cols) {
+    if (use_avx2())
+        return aca_avx2::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, pre_k, pre_rows,
+                                        pre_cols);
+    return aca_base::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, pre_k, pre_rows,
+                                    pre_cols);
+}
+int64_t gca_aca(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
+                int64_t *rows, int64_t *cols) {
+    int64_t k = 0;
+    double resid = 0.0;
+    aca_dispatch(is_complex, A, nr, nc, epsilon, std::min(nr, nc), rows, cols, &k, &resid);
+    return k;
 }
 }  // namespace gcabem
 

@@ -173,6 +173,34 @@ def test_gca_pipeline_matches_per_cluster_path(eq, kappa):
         assert np.max(np.abs(ops[cid].V - ref.V)) <= 1e-9 * np.max(np.abs(ref.V)), cid
 
 
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+@pytest.mark.parametrize("mode", ["device", "retry"])
+def test_gca_device_vsolve_matches_host(monkeypatch, eq, kappa, mode):
+    """The V solves on the device (csrc/vsolve.cu: LU of B^T, Frobenius
+    condition bracket, two refinement sweeps, explicit roundings) against the
+    host solve of the same pipeline (GCABEM_GCA_HOST_SOLVE): identical pivots
+    on every L5 cluster, V within roundoff and bitwise equal almost
+    everywhere. `retry` hands every device solve back to the host pass (Green
+    matrix recomputed on the device, host decision)."""
+    m, t, bt = sphere_setup(5)
+    spec = kernels.KernelSpec(eq, "single", kappa)
+    params = gca.GcaParams()
+    ids = sorted({l.row for l in bt.leaves if l.kind == "admissible"})
+    monkeypatch.setenv("GCABEM_GCA_HOST_SOLVE", "1")
+    ref = gca._ops_for_tree(m, t, ids, spec, params, m.diameter(), 0)
+    monkeypatch.delenv("GCABEM_GCA_HOST_SOLVE")
+    if mode == "retry":
+        monkeypatch.setenv("GCABEM_GCA_FORCE_RETRY", "1")
+    ops = gca._ops_for_tree(m, t, ids, spec, params, m.diameter(), 0, batch_bytes=8 << 20)
+    same = 0
+    for cid in ids:
+        assert np.array_equal(ops[cid].pivots_global, ref[cid].pivots_global), cid
+        d = np.max(np.abs(ops[cid].V - ref[cid].V))
+        assert d <= 1e-12 * np.max(np.abs(ref[cid].V)), cid
+        same += int(d == 0.0)
+    assert same >= 0.9 * len(ids), (same, len(ids))
+
+
 def test_assemble_operator_pipeline():
     """solver.assemble_operator end to end (trees, device GCA, device assembly)."""
     m = mesh.build_sphere_mesh(3)
