@@ -368,6 +368,9 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     // (test hook for the retry pass)
     const bool host_solve = std::getenv("GCABEM_GCA_HOST_SOLVE") != nullptr;
     const bool force_retry = std::getenv("GCABEM_GCA_FORCE_RETRY") != nullptr;
+    // test hook: every cluster takes the host fallback (solve on the ACA
+    // pivots already found, as when no pack is free)
+    const bool force_fallback = std::getenv("GCABEM_GCA_FORCE_FALLBACK") != nullptr;
     if (!host_solve && e == cudaSuccess && !st.vring) {
         auto r = std::make_unique<VRing>();
         e = cudaStreamCreateWithFlags(&r->s, cudaStreamNonBlocking);
@@ -405,6 +408,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     // hand cluster c (Green matrix A, ACA pivots) to the device; false: no room
     auto offload = [&](int64_t c, const double *A, int64_t nr, int64_t k, const int64_t *prow,
                        const int64_t *pcol) -> bool {
+        if (force_fallback) return false;
         const int64_t need = (k * k + k * nr) * width;
         VPack *p = nullptr;
         int64_t in_off = 0;

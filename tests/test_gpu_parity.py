@@ -174,14 +174,16 @@ def test_gca_pipeline_matches_per_cluster_path(eq, kappa):
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
-@pytest.mark.parametrize("mode", ["device", "retry"])
+@pytest.mark.parametrize("mode", ["device", "retry", "fallback"])
 def test_gca_device_vsolve_matches_host(monkeypatch, eq, kappa, mode):
     """The V solves on the device (csrc/vsolve.cu: LU of B^T, Frobenius
     condition bracket, two refinement sweeps, explicit roundings) against the
     host solve of the same pipeline (GCABEM_GCA_HOST_SOLVE): identical pivots
     on every L5 cluster, V within roundoff and bitwise equal almost
     everywhere. `retry` hands every device solve back to the host pass (Green
-    matrix recomputed on the device, host decision)."""
+    matrix recomputed on the device, host decision); `fallback` solves every
+    cluster on the host from the pivots the pipeline's ACA found (the path
+    of clusters no pack had room for): bitwise the host path."""
     m, t, bt = sphere_setup(5)
     spec = kernels.KernelSpec(eq, "single", kappa)
     params = gca.GcaParams()
@@ -191,7 +193,11 @@ def test_gca_device_vsolve_matches_host(monkeypatch, eq, kappa, mode):
     monkeypatch.delenv("GCABEM_GCA_HOST_SOLVE")
     if mode == "retry":
         monkeypatch.setenv("GCABEM_GCA_FORCE_RETRY", "1")
+    if mode == "fallback":
+        monkeypatch.setenv("GCABEM_GCA_FORCE_FALLBACK", "1")
     ops = gca._ops_for_tree(m, t, ids, spec, params, m.diameter(), 0, batch_bytes=8 << 20)
+    if mode == "fallback":
+        assert all(np.array_equal(ops[c].V, ref[c].V) for c in ids)
     same = 0
     for cid in ids:
         assert np.array_equal(ops[cid].pivots_global, ref[cid].pivots_global), cid
