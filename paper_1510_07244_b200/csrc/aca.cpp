@@ -25,6 +25,7 @@
 // perform the same IEEE operations in the same order (no FMA contraction),
 // so results do not depend on the CPU.
 #ifdef GCABEM_ACA_AVX2
+#include <immintrin.h>
 #define GCABEM_ACA_NS aca_avx2
 #else
 #define GCABEM_ACA_NS aca_base
@@ -50,6 +51,27 @@ inline Cx cdiv(Cx a, Cx b) {
 }
 inline double cabs(Cx a) { return std::hypot(a.re, a.im); }
 
+// Division of many numerators by one divisor: the divisor's part of Smith's
+// scheme (branch, rat, scl) once, then per element exactly the operations of
+// cdiv(a, b) -- bitwise the per-element division without its two divides.
+struct CDivisor {
+    bool re_major;
+    double rat, scl;
+    explicit CDivisor(Cx b) : re_major(std::fabs(b.re) >= std::fabs(b.im)) {
+        if (re_major) {
+            rat = b.im / b.re;
+            scl = 1.0 / (b.re + b.im * rat);
+        } else {
+            rat = b.re / b.im;
+            scl = 1.0 / (b.im + b.re * rat);
+        }
+    }
+    Cx operator()(Cx a) const {
+        if (re_major) return {(a.re + a.im * rat) * scl, (a.im - a.re * rat) * scl};
+        return {(a.re * rat + a.im) * scl, (a.im * rat - a.re) * scl};
+    }
+};
+
 template <typename T>
 struct Ops;
 template <>
@@ -58,6 +80,11 @@ struct Ops<double> {
     static double mul(double a, double b) { return a * b; }
     static double sub(double a, double b) { return a - b; }
     static double div(double a, double b) { return a / b; }
+    struct Divider {  // real division stays a division (a * (1/b) would round differently)
+        double b;
+        explicit Divider(double d) : b(d) {}
+        double operator()(double a) const { return a / b; }
+    };
     static bool zero(double a) { return a == 0.0; }
     static double norm2(double a) { return a * a; }
     static double dotc_re(double a, double b) { return a * b; }  // Re(conj(a) b)
@@ -69,28 +96,74 @@ struct Ops<Cx> {
     static Cx mul(Cx a, Cx b) { return cmul(a, b); }
     static Cx sub(Cx a, Cx b) { return csub(a, b); }
     static Cx div(Cx a, Cx b) { return cdiv(a, b); }
+    using Divider = CDivisor;
     static bool zero(Cx a) { return a.re == 0.0 && a.im == 0.0; }
     static double norm2(Cx a) { return a.re * a.re + a.im * a.im; }
     static double dotc_re(Cx a, Cx b) { return a.re * b.re + a.im * b.im; }
     static double dotc_im(Cx a, Cx b) { return a.re * b.im - a.im * b.re; }
 };
 
-// sum conj(a_k) b_k with four partial sums
+// sum conj(a_k) b_k over the arrays as doubles, 4 at a time into two 4-lane
+// accumulators (alternating) for the products x_e y_e (real part) and
+// x_e y_(e^1) (imaginary part: lanes re*im minus im*re), combined in a fixed
+// order at the end. The AVX2 build does exactly these IEEE operations with
+// vector instructions (no FMA), so both builds agree bitwise. (The
+// reference's np.vdot / norm are BLAS reductions with their own association:
+// these sums only feed the stopping estimate, see aca_one.)
 template <typename T>
 Cx dotc(const T *a, const T *b, int64_t n) {
-    using O = Ops<T>;
-    double r[4] = {0, 0, 0, 0}, i[4] = {0, 0, 0, 0};
-    int64_t k = 0;
-    for (; k + 4 <= n; k += 4)
-        for (int l = 0; l < 4; ++l) {
-            r[l] += O::dotc_re(a[k + l], b[k + l]);
-            i[l] += O::dotc_im(a[k + l], b[k + l]);
+    constexpr int W = std::is_same<T, Cx>::value ? 2 : 1;
+    const double *x = reinterpret_cast<const double *>(a);
+    const double *y = reinterpret_cast<const double *>(b);
+    const int64_t nd = n * W, nv = nd / 4;
+    double tr = 0.0, ti = 0.0;
+    for (int64_t e = nv * 4; e < nd; e += W) {  // tail: < 4 doubles
+        tr += x[e] * y[e];
+        if (W == 2) {
+            tr += x[e + 1] * y[e + 1];
+            ti += x[e] * y[e + 1] - x[e + 1] * y[e];
         }
-    for (; k < n; ++k) {
-        r[0] += O::dotc_re(a[k], b[k]);
-        i[0] += O::dotc_im(a[k], b[k]);
     }
-    return {(r[0] + r[1]) + (r[2] + r[3]), (i[0] + i[1]) + (i[2] + i[3])};
+#ifdef GCABEM_ACA_AVX2
+    __m256d r0 = _mm256_setzero_pd(), r1 = r0, i0 = r0, i1 = r0;
+    int64_t v = 0;
+    for (; v + 2 <= nv; v += 2) {
+        const __m256d xa = _mm256_loadu_pd(x + 4 * v), ya = _mm256_loadu_pd(y + 4 * v);
+        const __m256d xb = _mm256_loadu_pd(x + 4 * v + 4), yb = _mm256_loadu_pd(y + 4 * v + 4);
+        r0 = _mm256_add_pd(r0, _mm256_mul_pd(xa, ya));
+        r1 = _mm256_add_pd(r1, _mm256_mul_pd(xb, yb));
+        if (W == 2) {
+            i0 = _mm256_add_pd(i0, _mm256_mul_pd(xa, _mm256_permute_pd(ya, 0x5)));
+            i1 = _mm256_add_pd(i1, _mm256_mul_pd(xb, _mm256_permute_pd(yb, 0x5)));
+        }
+    }
+    if (v < nv) {
+        const __m256d xa = _mm256_loadu_pd(x + 4 * v), ya = _mm256_loadu_pd(y + 4 * v);
+        r0 = _mm256_add_pd(r0, _mm256_mul_pd(xa, ya));
+        if (W == 2) i0 = _mm256_add_pd(i0, _mm256_mul_pd(xa, _mm256_permute_pd(ya, 0x5)));
+    }
+    alignas(32) double R[2][4], I[2][4];
+    _mm256_store_pd(R[0], r0);
+    _mm256_store_pd(R[1], r1);
+    _mm256_store_pd(I[0], i0);
+    _mm256_store_pd(I[1], i1);
+#else
+    double R[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, I[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    for (int64_t v = 0; v < nv; ++v) {
+        const double *xv = x + 4 * v, *yv = y + 4 * v;
+        double *rr = R[v & 1], *ii = I[v & 1];
+        for (int l = 0; l < 4; ++l) {
+            rr[l] += xv[l] * yv[l];
+            if (W == 2) ii[l] += xv[l] * yv[l ^ 1];
+        }
+    }
+#endif
+    const double re = ((R[0][0] + R[0][1]) + (R[0][2] + R[0][3])) +
+                      ((R[1][0] + R[1][1]) + (R[1][2] + R[1][3])) + tr;
+    const double im = W == 2 ? ((I[0][0] - I[0][1]) + (I[0][2] - I[0][3])) +
+                                   ((I[1][0] - I[1][1]) + (I[1][2] - I[1][3])) + ti
+                             : 0.0;
+    return {re, im};
 }
 
 // x[j] -= s * y[j] (the residual updates and the LU sweeps); the compiler
@@ -183,7 +256,8 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
         }
         std::vector<T> w(nc);
         const T piv = r[jp];
-        for (int64_t j = 0; j < nc; ++j) w[j] = O::div(r[j], piv);
+        const typename O::Divider by_piv(piv);
+        for (int64_t j = 0; j < nc; ++j) w[j] = by_piv(r[j]);
         for (int64_t q = 0; q < nr; ++q) c[q] = A[q * nc + jp];
         for (size_t m = 0; m < U.size(); ++m) {
             const T wj = W[m][jp];
@@ -326,9 +400,9 @@ struct LU {
             if (best == 0.0) return false;
             if (p != k)
                 for (int64_t j = 0; j < n; ++j) std::swap(m[k * n + j], m[p * n + j]);
-            const T d = m[k * n + k];
+            const typename O::Divider by_d(m[k * n + k]);
             for (int64_t i = k + 1; i < n; ++i) {
-                const T l = O::div(m[i * n + k], d);
+                const T l = by_d(m[i * n + k]);
                 m[i * n + k] = l;
                 for (int64_t j = k + 1; j < n; ++j)
                     m[i * n + j] = O::sub(m[i * n + j], O::mul(l, m[k * n + j]));
@@ -349,8 +423,8 @@ struct LU {
         for (int64_t i = r - 1; i >= 0; --i) {
             T *xi = X + i * n;
             for (int64_t j = i + 1; j < r; ++j) mulsub<T>(xi, m[i * r + j], X + j * n, n);
-            const T d = m[i * r + i];
-            for (int64_t q = 0; q < n; ++q) xi[q] = O::div(xi[q], d);
+            const typename O::Divider by_d(m[i * r + i]);
+            for (int64_t q = 0; q < n; ++q) xi[q] = by_d(xi[q]);
         }
     }
 };

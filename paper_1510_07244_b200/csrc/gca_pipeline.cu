@@ -654,8 +654,19 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         }
         if (e != cudaSuccess) break;
         if (completed < issued) {
+            // publish the oldest batch once its D2H has landed; meanwhile a
+            // slot freed by the workers is refilled at once (a blocking wait
+            // on the event would leave it empty until the batch lands)
             const auto t0 = clk::now();
-            e = cudaEventSynchronize(done[slot_of[completed]]);
+            const cudaError_t q = cudaEventQuery(done[slot_of[completed]]);
+            if (q == cudaErrorNotReady) {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait_for(lk, std::chrono::microseconds(100),
+                            [&] { return !free_slots.empty() && issued < nb; });
+                t_wait += since(t0);
+                continue;
+            }
+            e = q;
             t_wait += since(t0);
             std::lock_guard<std::mutex> lk(mu);
             ready[completed++] = 1;
