@@ -189,6 +189,13 @@ def build_workload(cfg, device, log):
             device=device)
         t["gca_s"] = time.perf_counter() - t1
         t["gca_phases"] = dict(gca.last_build_phases)
+        # the same build again: the first call of a process also pays its
+        # pinned staging, pack buffers and worker buffers (kept for later calls)
+        t1 = time.perf_counter()
+        gca.build_interpolation_operators(
+            m, bt, kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"]), gca.GcaParams(),
+            device=device)
+        t["gca_warm_s"] = time.perf_counter() - t1
     t2 = time.perf_counter()
     pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
     t["packaging_s"] = time.perf_counter() - t2
@@ -564,11 +571,14 @@ def run_ours(args, cfg, dist, log):
     launches = sum(1 + sum(1 for c in p.singular_counts if c) for p in main_plans) * args.steps
     h2_setup = {"mesh_s (input, not counted)": round(setup_t["mesh_s"], 3),
                 "trees_s": round(setup_t["trees_s"], 3), "gca_s": round(setup_t["gca_s"], 3),
+                "gca_warm_s (second call)": round(setup_t.get("gca_warm_s", 0.0), 3),
                 "gca_phases_s": {k: round(v, 4) if isinstance(v, float) else v
                                  for k, v in setup_t.get("gca_phases", {}).items()},
                 "assembly_slp_dlp_s": round(setup_first, 4) if setup_first else None,
                 "total_s": round(setup_t["trees_s"] + setup_t["gca_s"] + setup_first, 3)
-                if setup_first else None}
+                if setup_first else None,
+                "total_warm_s": round(setup_t["trees_s"] + setup_t.get("gca_warm_s", 0.0)
+                                      + min(e2e_t), 3) if e2e_t else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,

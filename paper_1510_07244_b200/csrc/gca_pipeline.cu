@@ -75,7 +75,7 @@ constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging e
 // finished ones. Workers never wait on the device: with no pack free they
 // solve on the host.
 constexpr int VPACKS = 8;
-constexpr int64_t VS_PACK_BYTES = int64_t(8) << 20;  // input bytes per launch
+constexpr int64_t VS_PACK_BYTES = int64_t(4) << 20;  // input bytes per launch
 constexpr int64_t VS_WAIT_WORK = 256 * 32;           // nr x k from which a worker waits for a pack
 enum VState { V_FREE, V_FILLING, V_SEALED, V_INFLIGHT };
 struct VItem {
@@ -430,7 +430,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
             }
             p = vcur;
             if (p->items.empty() && (int64_t)(p->hin.n / 8) < std::max(need, VS_PACK_BYTES / 8) &&
-                p->hin.reserve((size_t)std::max(need * 8, 2 * VS_PACK_BYTES)) != cudaSuccess) {
+                p->hin.reserve((size_t)std::max(need * 8, VS_PACK_BYTES)) != cudaSuccess) {
                 p->state = V_FREE;
                 vcur = nullptr;
                 return false;
@@ -478,12 +478,11 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         const size_t nt = p.tasks.size(), nch = p.chunks.size();
         const size_t tk_bytes = nt * sizeof(VTask), ch_bytes = nch * sizeof(int2);
         cudaStream_t vs = vr->s;
-        // pinned buffers grow in large steps (cudaHostAlloc/FreeHost cost
-        // milliseconds and FreeHost synchronises): V fits in the input's
-        // size, task lists in 1 MiB for typical packs
-        cudaError_t r = p.htk.reserve(std::max<size_t>(tk_bytes + ch_bytes, size_t(1) << 20));
-        if (r == cudaSuccess) r = p.hout.reserve(std::max(p.hin.n, (size_t)p.out_len * 8));
-        if (r == cudaSuccess) r = p.haux.reserve(std::max<size_t>(nt * sizeof(VAux), 256 << 10));
+        // pinned buffers grow in steps of at least a pack (cudaHostAlloc /
+        // FreeHost cost milliseconds and FreeHost synchronises)
+        cudaError_t r = p.htk.reserve(std::max<size_t>(tk_bytes + ch_bytes, size_t(256) << 10));
+        if (r == cudaSuccess) r = p.hout.reserve(std::max((size_t)VS_PACK_BYTES, (size_t)p.out_len * 8));
+        if (r == cudaSuccess) r = p.haux.reserve(std::max<size_t>(nt * sizeof(VAux), 64 << 10));
         if (r == cudaSuccess) r = pool_reserve(p.din, (size_t)p.in_len, vs);
         if (r == cudaSuccess) r = pool_reserve(p.dout, (size_t)p.out_len, vs);
         if (r == cudaSuccess) r = pool_reserve(p.dscr, (size_t)p.scr_len, vs);
