@@ -28,9 +28,11 @@
 #include <thread>
 #include <vector>
 
+#include "gca_vsolve.h"
 #include "internal.h"
 
 using namespace gcabem;
+using namespace gcabem::gca_detail;
 
 struct gcabem_gca_s {
     int is_complex = 0;
@@ -48,87 +50,9 @@ double since(clk::time_point t0) {
     return std::chrono::duration<double>(clk::now() - t0).count();
 }
 
-struct Pinned {
-    void *p = nullptr;
-    size_t n = 0;
-    ~Pinned() {
-        if (p) cudaFreeHost(p);
-    }
-    cudaError_t reserve(size_t bytes) {
-        if (bytes <= n && p) return cudaSuccess;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        n = 0;
-        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
-        if (e == cudaSuccess) n = bytes;
-        return e;
-    }
-};
-
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
 constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
-
-// Device V solves (vsolve.cu): workers hand each cluster's pivot block and
-// pivot columns to the pack being filled (gathered straight into its pinned
-// buffer); a launcher thread sends full packs to the device and harvests the
-// finished ones. Workers never wait on the device: with no pack free they
-// solve on the host.
-constexpr int VPACKS = 8;
-constexpr int64_t VS_PACK_BYTES = int64_t(4) << 20;  // input bytes per launch
-constexpr int64_t VS_WAIT_WORK = 256 * 32;           // nr x k from which a worker waits for a pack
-enum VState { V_FREE, V_FILLING, V_SEALED, V_INFLIGHT };
-struct VItem {
-    int64_t c, out_off, nr, k;
-    std::vector<int64_t> rows;
-};
-template <typename T>
-cudaError_t pool_reserve(PoolBuf<T> &b, size_t n, cudaStream_t s) {
-    return (b.p && b.n >= n) ? cudaSuccess : b.alloc(std::max<size_t>(n, 1), s);
-}
-struct VPack {
-    Pinned hin, hout, haux, htk;
-    PoolBuf<double> din, dout, dscr;
-    PoolBuf<VAux> daux;
-    PoolBuf<VTask> dtk;
-    PoolBuf<int2> dch;
-    cudaEvent_t ev = nullptr;
-    VState state = V_FREE;
-    int64_t seq = 0;
-    int writers = 0;
-    std::vector<VItem> items;
-    std::vector<VTask> tasks;
-    std::vector<int2> chunks;
-    int64_t in_len = 0, out_len = 0, scr_len = 0;
-    int kmax = 0;
-    void reset() {
-        items.clear();
-        tasks.clear();
-        chunks.clear();
-        in_len = out_len = scr_len = 0;
-        kmax = 0;
-        writers = 0;
-    }
-};
-struct VRing {
-    cudaStream_t s = nullptr;
-    VPack pack[VPACKS];
-    ~VRing() {
-        for (auto &p : pack) {
-            p.din.release();
-            p.dout.release();
-            p.dscr.release();
-            p.daux.release();
-            p.dtk.release();
-            p.dch.release();
-            if (p.ev) cudaEventDestroy(p.ev);
-        }
-        if (s) {
-            cudaStreamSynchronize(s);
-            cudaStreamDestroy(s);
-        }
-    }
-};
 
 struct Staging {
     Pinned host[SLOTS];
@@ -364,220 +288,23 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     const auto t_start = clk::now();
     if ((int)st.aown.size() < nthreads) st.aown.resize(nthreads);
     // device V solves unless GCABEM_GCA_HOST_SOLVE is set (the host path, for
-    // A/B and tests); GCABEM_GCA_FORCE_RETRY hands every device solve back
-    // (test hook for the retry pass)
+    // A/B and tests)
     const bool host_solve = std::getenv("GCABEM_GCA_HOST_SOLVE") != nullptr;
-    const bool force_retry = std::getenv("GCABEM_GCA_FORCE_RETRY") != nullptr;
-    // test hook: every cluster takes the host fallback (solve on the ACA
-    // pivots already found, as when no pack is free)
-    const bool force_fallback = std::getenv("GCABEM_GCA_FORCE_FALLBACK") != nullptr;
     if (!host_solve && e == cudaSuccess && !st.vring) {
         auto r = std::make_unique<VRing>();
-        e = cudaStreamCreateWithFlags(&r->s, cudaStreamNonBlocking);
-        for (auto &p : r->pack)
-            if (e == cudaSuccess)
-                e = cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming | cudaEventBlockingSync);
+        e = r->init();
         if (e == cudaSuccess) st.vring = std::move(r);
     }
-    VRing *vr = host_solve ? nullptr : st.vring.get();
-    std::mutex vmu;
-    std::condition_variable vcv;
-    VPack *vcur = nullptr;  // pack being filled
-    int64_t vseq = 0;
-    bool workers_done = false;
-    std::atomic<int64_t> n_dev{0}, n_host{0};
-    std::vector<int64_t> retry;
-    std::atomic<int> vs_err{0};
+    std::unique_ptr<VSolveQueue> vq;
+    if (!host_solve && st.vring)
+        vq = std::make_unique<VSolveQueue>(*st.vring, mesh->device, equation == 1, nsrc, G->rows,
+                                           G->V);
+    std::atomic<int64_t> n_host{0};
     auto fail = [&](int64_t c, int rc) {
         int64_t prev = err_cluster.load();
         while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
         }
         if (c <= err_cluster.load()) err_code = rc;
-    };
-    // a FREE pack as the one being filled (vmu held); nullptr if none
-    auto take_pack = [&]() -> VPack * {
-        for (auto &p : vr->pack)
-            if (p.state == V_FREE) {
-                p.reset();
-                p.state = V_FILLING;
-                p.seq = vseq++;
-                return &p;
-            }
-        return nullptr;
-    };
-    // hand cluster c (Green matrix A, ACA pivots) to the device; false: no room
-    auto offload = [&](int64_t c, const double *A, int64_t nr, int64_t k, const int64_t *prow,
-                       const int64_t *pcol) -> bool {
-        if (force_fallback) return false;
-        const int64_t need = (k * k + k * nr) * width;
-        VPack *p = nullptr;
-        int64_t in_off = 0;
-        {
-            std::unique_lock<std::mutex> lk(vmu);
-            for (;;) {
-                if (vcur && vcur->in_len + need > (int64_t)(vcur->hin.n / 8)) {
-                    vcur->state = V_SEALED;  // full: to the launcher
-                    vcur = nullptr;
-                    vcv.notify_all();
-                }
-                if (!vcur) vcur = take_pack();
-                if (vcur) break;
-                // no pack free: small clusters are solved on the host at once,
-                // large ones (whose host solve costs more than waiting) wait
-                // for the launcher to free one
-                if (nr * k < VS_WAIT_WORK || vs_err.load() != 0) return false;
-                vcv.wait(lk);
-            }
-            p = vcur;
-            if (p->items.empty() && (int64_t)(p->hin.n / 8) < std::max(need, VS_PACK_BYTES / 8) &&
-                p->hin.reserve((size_t)std::max(need * 8, VS_PACK_BYTES)) != cudaSuccess) {
-                p->state = V_FREE;
-                vcur = nullptr;
-                return false;
-            }
-            in_off = p->in_len;
-            VTask tk;
-            tk.in_off = in_off;
-            tk.out_off = p->out_len;
-            tk.scr_off = p->scr_len;
-            tk.nr = (int32_t)nr;
-            tk.k = (int32_t)k;
-            for (int64_t q0 = 0; q0 < nr; q0 += VS_ROWS)
-                p->chunks.push_back(make_int2((int)p->tasks.size(), (int)q0));
-            p->tasks.push_back(tk);
-            p->items.push_back(VItem{c, p->out_len, nr, k, std::vector<int64_t>(prow, prow + k)});
-            p->in_len += need;
-            p->out_len += nr * k * width;
-            p->scr_len += vsolve_scratch(k, nr, width);
-            p->kmax = std::max(p->kmax, (int)k);
-            ++p->writers;
-            if (p->in_len * 8 >= VS_PACK_BYTES) {
-                p->state = V_SEALED;
-                vcur = nullptr;
-            }
-        }
-        // B = A[rows, cols] and A[:, cols]^T, gathered into the pinned buffer
-        double *dst = static_cast<double *>(p->hin.p) + in_off;
-        for (int64_t a = 0; a < k; ++a)
-            for (int64_t bb = 0; bb < k; ++bb) {
-                const double *src = A + (prow[a] * nsrc + pcol[bb]) * width;
-                for (int t = 0; t < width; ++t) *dst++ = src[t];
-            }
-        for (int64_t bb = 0; bb < k; ++bb)
-            for (int64_t q = 0; q < nr; ++q) {
-                const double *src = A + (q * nsrc + pcol[bb]) * width;
-                for (int t = 0; t < width; ++t) *dst++ = src[t];
-            }
-        {
-            std::lock_guard<std::mutex> lk(vmu);
-            if (--p->writers == 0 && p->state == V_SEALED) vcv.notify_all();
-        }
-        return true;
-    };
-    auto launch_pack = [&](VPack &p) -> cudaError_t {
-        const size_t nt = p.tasks.size(), nch = p.chunks.size();
-        const size_t tk_bytes = nt * sizeof(VTask), ch_bytes = nch * sizeof(int2);
-        cudaStream_t vs = vr->s;
-        // pinned buffers grow in steps of at least a pack (cudaHostAlloc /
-        // FreeHost cost milliseconds and FreeHost synchronises)
-        cudaError_t r = p.htk.reserve(std::max<size_t>(tk_bytes + ch_bytes, size_t(256) << 10));
-        if (r == cudaSuccess) r = p.hout.reserve(std::max((size_t)VS_PACK_BYTES, (size_t)p.out_len * 8));
-        if (r == cudaSuccess) r = p.haux.reserve(std::max<size_t>(nt * sizeof(VAux), 64 << 10));
-        if (r == cudaSuccess) r = pool_reserve(p.din, (size_t)p.in_len, vs);
-        if (r == cudaSuccess) r = pool_reserve(p.dout, (size_t)p.out_len, vs);
-        if (r == cudaSuccess) r = pool_reserve(p.dscr, (size_t)p.scr_len, vs);
-        if (r == cudaSuccess) r = pool_reserve(p.daux, nt, vs);
-        if (r == cudaSuccess) r = pool_reserve(p.dtk, nt, vs);
-        if (r == cudaSuccess) r = pool_reserve(p.dch, nch, vs);
-        if (r != cudaSuccess) return r;
-        char *hb = static_cast<char *>(p.htk.p);
-        std::copy(p.tasks.begin(), p.tasks.end(), reinterpret_cast<VTask *>(hb));
-        std::copy(p.chunks.begin(), p.chunks.end(), reinterpret_cast<int2 *>(hb + tk_bytes));
-        r = cudaMemcpyAsync(p.dtk.p, hb, tk_bytes, cudaMemcpyHostToDevice, vs);
-        if (r == cudaSuccess)
-            r = cudaMemcpyAsync(p.dch.p, hb + tk_bytes, ch_bytes, cudaMemcpyHostToDevice, vs);
-        if (r == cudaSuccess)
-            r = cudaMemcpyAsync(p.din.p, p.hin.p, (size_t)p.in_len * 8, cudaMemcpyHostToDevice, vs);
-        if (r == cudaSuccess)
-            r = launch_vsolve(equation == 1, p.dtk.p, (int)nt, p.dch.p, (int)nch, p.kmax, p.din.p,
-                              p.dout.p, p.dscr.p, p.daux.p, vs);
-        if (r == cudaSuccess)
-            r = cudaMemcpyAsync(p.hout.p, p.dout.p, (size_t)p.out_len * 8, cudaMemcpyDeviceToHost, vs);
-        if (r == cudaSuccess)
-            r = cudaMemcpyAsync(p.haux.p, p.daux.p, nt * sizeof(VAux), cudaMemcpyDeviceToHost, vs);
-        if (r == cudaSuccess) r = cudaEventRecord(p.ev, vs);
-        return r;
-    };
-    auto harvest_pack = [&](VPack &p) {
-        const VAux *ax = static_cast<const VAux *>(p.haux.p);
-        const double *o = static_cast<const double *>(p.hout.p);
-        std::vector<int64_t> back;
-        for (size_t i = 0; i < p.items.size(); ++i) {
-            VItem &it = p.items[i];
-            if (ax[i].status == 0 && !force_retry) {
-                G->rows[it.c] = std::move(it.rows);
-                G->V[it.c].assign(o + it.out_off, o + it.out_off + it.nr * it.k * width);
-                n_dev.fetch_add(1);
-            } else {
-                back.push_back(it.c);
-            }
-        }
-        std::lock_guard<std::mutex> lk(vmu);
-        retry.insert(retry.end(), back.begin(), back.end());
-        p.reset();
-        p.state = V_FREE;
-        vcv.notify_all();  // workers waiting for a pack
-    };
-    // launcher: sealed packs (all writers done) to the device, oldest first;
-    // finished packs harvested; at the end the partial pack too
-    double launcher_busy = 0.0;
-    auto launcher = [&]() {
-        cudaSetDevice(mesh->device);
-        for (;;) {
-            VPack *todo = nullptr;
-            bool inflight = false, pending = false;
-            {
-                std::unique_lock<std::mutex> lk(vmu);
-                if (workers_done && vcur && vcur->writers == 0) {
-                    if (vcur->items.empty()) vcur->state = V_FREE;
-                    else vcur->state = V_SEALED;
-                    vcur = nullptr;
-                }
-                for (auto &p : vr->pack) {
-                    if (p.state == V_SEALED && p.writers == 0 && (!todo || p.seq < todo->seq))
-                        todo = &p;
-                    inflight = inflight || p.state == V_INFLIGHT;
-                    pending = pending || p.state == V_SEALED || p.state == V_FILLING;
-                }
-                if (todo) todo->state = V_INFLIGHT;
-                if (!todo && !inflight) {
-                    if (workers_done && !pending) return;
-                    vcv.wait_for(lk, std::chrono::microseconds(500));
-                    continue;
-                }
-            }
-            const auto tl = clk::now();
-            if (todo) {
-                const cudaError_t r = vs_err.load() ? cudaSuccess : launch_pack(*todo);
-                if (r != cudaSuccess) vs_err = (int)r;
-            }
-            bool harvested = false;
-            for (auto &p : vr->pack) {
-                bool ready = false;
-                {
-                    std::lock_guard<std::mutex> lk(vmu);
-                    ready = p.state == V_INFLIGHT;
-                }
-                if (!ready) continue;
-                const cudaError_t q = cudaEventQuery(p.ev);
-                if (q == cudaErrorNotReady) continue;
-                if (q != cudaSuccess) vs_err = (int)q;
-                harvest_pack(p);
-                harvested = true;
-            }
-            launcher_busy += since(tl);
-            if (!todo && !harvested) std::this_thread::sleep_for(std::chrono::microseconds(100));
-        }
     };
     auto worker = [&](int tid) {
         std::vector<double> &Aown = st.aown[tid];  // grow-only across calls: no page faults
@@ -605,7 +332,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
             }
             const int64_t nr = cl_size[c];
             int rc = 0;
-            if (vr) {
+            if (vq) {
                 prow.resize(std::min(nr, nsrc));
                 pcol.resize(prow.size());
                 const int64_t k = gca_aca(equation == 1, Aown.data(), nr, nsrc, epsilon,
@@ -613,7 +340,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                 // k = 0 is the zero-matrix error; ranks above VS_KMAX and a
                 // full pack ring stay on the host (no second ACA)
                 if (k == 0 || k > VS_KMAX ||
-                    !offload(c, Aown.data(), nr, k, prow.data(), pcol.data())) {
+                    !vq->offload(c, Aown.data(), nr, k, prow.data(), pcol.data())) {
                     rc = gca_operator(equation == 1, Aown.data(), nr, nsrc, epsilon, G->rows[c],
                                       G->V[c], k, prow.data(), pcol.data());
                     n_host.fetch_add(1);
@@ -634,7 +361,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     std::thread launch_thread;
     if (e == cudaSuccess) {
         for (int t = 0; t < nthreads; ++t) th.emplace_back(worker, t);
-        if (vr) launch_thread = std::thread(launcher);
+        if (vq) launch_thread = std::thread([&] { vq->run(); });
     }
     int64_t issued = 0, completed = 0;
     while (e == cudaSuccess && completed < nb) {
@@ -682,14 +409,11 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     }
     for (auto &t : th) t.join();
     if (launch_thread.joinable()) {
-        {
-            std::lock_guard<std::mutex> lk(vmu);
-            workers_done = true;
-            vcv.notify_all();
-        }
+        vq->workers_finished();
         launch_thread.join();
     }
-    if (e == cudaSuccess && vs_err.load() != 0) e = (cudaError_t)vs_err.load();
+    if (e == cudaSuccess && vq && vq->error() != cudaSuccess) e = vq->error();
+    std::vector<int64_t> none, &retry = vq ? vq->handed_back() : none;
     tr.mark("pipeline");
     // clusters the device solve handed back (pivot block singular or in the
     // condition bracket's ambiguous window): the Green matrix once more, then
@@ -724,8 +448,8 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     if (tr.on)
         std::fprintf(stderr, "[gca] V solves: %lld device, %lld host, %lld handed back (%.1f ms); "
                      "launcher busy %.1f ms\n",
-                     (long long)n_dev.load(), (long long)n_host.load(), (long long)retry.size(),
-                     1e3 * t_retry_s, 1e3 * launcher_busy);
+                     (long long)(vq ? vq->device_solves() : 0), (long long)n_host.load(),
+                     (long long)retry.size(), 1e3 * t_retry_s, 1e3 * (vq ? vq->busy_s() : 0.0));
     if (tr.on && nthreads > 0)
         std::fprintf(stderr, "[gca] workers: first cluster %.1f-%.1f ms, last done %.1f-%.1f ms, "
                      "waiting for Green batches %.1f ms (all threads)\n",
