@@ -261,12 +261,13 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
  * box box_lo/box_hi (ncl,3)) the device evaluates the Green matrix against
  * green_sources(box, delta, m) (gca.py:83-133; Gauss rule gauss_pts/wts of
  * order m on [0,1], scene_diameter for degenerate boxes) with the Duffy
- * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon) on nthreads
- * threads, overlapped with the next batch (batch_bytes of Green matrix per
- * launch, 4 launches in flight; 0 = 32 MiB); the cond <= 1e14 pivot check and
- * the refined V solve run on the device for packs of clusters (the host
- * solves the ambiguous / rejected ones exactly, with the reference's retry at
- * epsilon/10; GCABEM_GCA_HOST_SOLVE=1 keeps every solve on the host). Results: gcabem_gca_sizes (rank per
+ * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
+ * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
+ * nthreads threads, overlapped with the next batch (batch_bytes of Green
+ * matrix per launch, 4 launches in flight; 0 = 32 MiB). With
+ * GCABEM_GCA_DEVICE_SOLVE=1 the check and the solve run on the device for
+ * packs of clusters (the host solves the ambiguous / rejected ones exactly).
+ * Results: gcabem_gca_sizes (rank per
  * cluster, phase6 {device wait s, pipeline wall s, total s, batches, host
  * thread-seconds, threads}), then
  * gcabem_gca_fetch (row pivots concatenated; V blocks |t| x rank row-major,

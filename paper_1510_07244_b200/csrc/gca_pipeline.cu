@@ -7,15 +7,16 @@
 //   host     ACA per cluster (the pivots, aca.cpp) on a thread pool, each
 //            worker copying its cluster out of the slot first, while the
 //            device computes the next batches;
-//   device   the pivot-block check and the refined V solve (vsolve.cu) of
-//            packs of clusters, launched and harvested by one launcher thread
-//            (clusters it hands back, and those no pack had room for, take
-//            the host solve of gca_operator).
+//   host     the pivot-block check and the refined V solve (gca_operator);
+//            with GCABEM_GCA_DEVICE_SOLVE=1 on the device instead
+//            (vsolve.cu) for packs of clusters, launched and harvested by one
+//            launcher thread (clusters it hands back, and those no pack had
+//            room for, take the host solve).
 //
 // Clusters run largest first (the longest host jobs start early: no tail with
 // idle threads). North star split: the Green matrices (dense FP64 kernel
-// evaluations) and the small dense solves are device work, the pivoting
-// stays on the CPU.
+// evaluations) are device work, the pivoting (and by default the small
+// solves) stays on the CPU.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -287,9 +288,12 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         starved(nthreads, 0.0);
     const auto t_start = clk::now();
     if ((int)st.aown.size() < nthreads) st.aown.resize(nthreads);
-    // device V solves unless GCABEM_GCA_HOST_SOLVE is set (the host path, for
-    // A/B and tests)
-    const bool host_solve = std::getenv("GCABEM_GCA_HOST_SOLVE") != nullptr;
+    // V solves on the host by default; GCABEM_GCA_DEVICE_SOLVE=1 sends them
+    // to the device (gca_vsolve.h). Measured at C3 (16 threads): the device
+    // path is ~5-25% faster on later builds of a process but ~0.5 s slower
+    // on the first (pinned pack buffers, device pool growth), which is the
+    // build a setup pays, so it is opt-in.
+    const bool host_solve = std::getenv("GCABEM_GCA_DEVICE_SOLVE") == nullptr;
     if (!host_solve && e == cudaSuccess && !st.vring) {
         auto r = std::make_unique<VRing>();
         e = r->init();

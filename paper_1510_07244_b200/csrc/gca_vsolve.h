@@ -55,7 +55,10 @@ cudaError_t pool_reserve(PoolBuf<T> &b, size_t n, cudaStream_t s) {
 }
 
 struct VPack {
-    Pinned hin, hout, haux, htk;
+    // hin: the pivot blocks and columns the workers gather, H2D at launch;
+    // V comes back into the same buffer (stream order: the H2D is done
+    // before the kernels, V is never larger than the input)
+    Pinned hin, haux, htk;
     PoolBuf<double> din, dout, dscr;
     PoolBuf<VAux> daux;
     PoolBuf<VTask> dtk;
@@ -137,20 +140,31 @@ class VSolveQueue {
                     cur_ = nullptr;
                     cv_.notify_all();
                 }
-                if (!cur_) cur_ = take_pack();
+                if (!cur_) {
+                    VPack *f = take_pack();
+                    // room for a full pack plus one more cluster (packs seal
+                    // at VS_PACK_BYTES rather than on the first cluster that
+                    // misses); the pinned allocation happens outside the lock
+                    // with the pack private to this worker, so the others
+                    // keep going (first build of a process)
+                    if (f && (int64_t)(f->hin.n / 8) < std::max(need, VS_PACK_BYTES / 8)) {
+                        lk.unlock();
+                        const cudaError_t e =
+                            f->hin.reserve((size_t)std::max(need * 8, 2 * VS_PACK_BYTES));
+                        lk.lock();
+                        if (e != cudaSuccess || cur_) {  // failed, or another pack took over
+                            f->state = V_FREE;
+                            if (e != cudaSuccess) return false;
+                            continue;
+                        }
+                    }
+                    cur_ = f;
+                }
                 if (cur_) break;
                 if (nr * k < VS_WAIT_WORK || err_.load() != 0) return false;
                 cv_.wait(lk);
             }
             p = cur_;
-            // room for a full pack plus one more cluster: packs seal at
-            // VS_PACK_BYTES rather than on the first cluster that misses
-            if (p->items.empty() && (int64_t)(p->hin.n / 8) < std::max(need, VS_PACK_BYTES / 8) &&
-                p->hin.reserve((size_t)std::max(need * 8, 2 * VS_PACK_BYTES)) != cudaSuccess) {
-                p->state = V_FREE;
-                cur_ = nullptr;
-                return false;
-            }
             in_off = p->in_len;
             VTask tk;
             tk.in_off = in_off;
@@ -282,8 +296,6 @@ class VSolveQueue {
         // pinned buffers grow in steps of at least a pack (cudaHostAlloc /
         // FreeHost cost milliseconds and FreeHost synchronises)
         cudaError_t e = p.htk.reserve(std::max<size_t>(tk_bytes + ch_bytes, size_t(256) << 10));
-        if (e == cudaSuccess)
-            e = p.hout.reserve(std::max(p.hin.n, (size_t)p.out_len * 8));  // V fits in the input's size
         if (e == cudaSuccess) e = p.haux.reserve(std::max<size_t>(nt * sizeof(VAux), 64 << 10));
         if (e == cudaSuccess) e = pool_reserve(p.din, (size_t)p.in_len, s);
         if (e == cudaSuccess) e = pool_reserve(p.dout, (size_t)p.out_len, s);
@@ -304,7 +316,7 @@ class VSolveQueue {
             e = launch_vsolve(cplx_, p.dtk.p, (int)nt, p.dch.p, (int)nch, p.kmax, p.din.p,
                               p.dout.p, p.dscr.p, p.daux.p, s);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(p.hout.p, p.dout.p, (size_t)p.out_len * 8, cudaMemcpyDeviceToHost, s);
+            e = cudaMemcpyAsync(p.hin.p, p.dout.p, (size_t)p.out_len * 8, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(p.haux.p, p.daux.p, nt * sizeof(VAux), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaEventRecord(p.ev, s);
@@ -313,7 +325,7 @@ class VSolveQueue {
 
     void harvest(VPack &p) {
         const VAux *ax = static_cast<const VAux *>(p.haux.p);
-        const double *o = static_cast<const double *>(p.hout.p);
+        const double *o = static_cast<const double *>(p.hin.p);  // V, over the input
         std::vector<int64_t> back;
         for (size_t i = 0; i < p.items.size(); ++i) {
             VItem &it = p.items[i];

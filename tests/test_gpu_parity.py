@@ -177,8 +177,9 @@ def test_gca_pipeline_matches_per_cluster_path(eq, kappa):
 @pytest.mark.parametrize("mode", ["device", "retry", "fallback"])
 def test_gca_device_vsolve_matches_host(monkeypatch, eq, kappa, mode):
     """The V solves on the device (csrc/vsolve.cu: LU of B^T, Frobenius
-    condition bracket, two refinement sweeps, explicit roundings) against the
-    host solve of the same pipeline (GCABEM_GCA_HOST_SOLVE): identical pivots
+    condition bracket, two refinement sweeps, explicit roundings; opt-in with
+    GCABEM_GCA_DEVICE_SOLVE) against the host solve of the same pipeline (the
+    default): identical pivots
     on every L5 cluster, V within roundoff and bitwise equal almost
     everywhere. `retry` hands every device solve back to the host pass (Green
     matrix recomputed on the device, host decision); `fallback` solves every
@@ -188,9 +189,8 @@ def test_gca_device_vsolve_matches_host(monkeypatch, eq, kappa, mode):
     spec = kernels.KernelSpec(eq, "single", kappa)
     params = gca.GcaParams()
     ids = sorted({l.row for l in bt.leaves if l.kind == "admissible"})
-    monkeypatch.setenv("GCABEM_GCA_HOST_SOLVE", "1")
-    ref = gca._ops_for_tree(m, t, ids, spec, params, m.diameter(), 0)
-    monkeypatch.delenv("GCABEM_GCA_HOST_SOLVE")
+    ref = gca._ops_for_tree(m, t, ids, spec, params, m.diameter(), 0)  # host solves (default)
+    monkeypatch.setenv("GCABEM_GCA_DEVICE_SOLVE", "1")
     if mode == "retry":
         monkeypatch.setenv("GCABEM_GCA_FORCE_RETRY", "1")
     if mode == "fallback":
