@@ -37,7 +37,7 @@ class DeviceMesh:
 
     def close(self) -> None:
         h, self.handle = getattr(self, "handle", None), None
-        if h and nat._lib is not None:
+        if h and getattr(nat, "_lib", None) is not None:  # nat is None at interpreter teardown
             nat._lib.gcabem_mesh_destroy(h)
 
     def __del__(self):

@@ -215,7 +215,7 @@ class DeviceH2:
     def close(self) -> None:
         from . import _native as nat
         h, self.handle = getattr(self, "handle", None), None
-        if h and nat._lib is not None:
+        if h and getattr(nat, "_lib", None) is not None:  # nat is None at interpreter teardown
             nat._lib.gcabem_h2_free(h)
 
     def __del__(self):

@@ -175,7 +175,7 @@ class NearFieldP1:
 
     def close(self) -> None:
         h, self.handle = getattr(self, "handle", None), None
-        if h and nat._lib is not None:
+        if h and getattr(nat, "_lib", None) is not None:  # nat is None at interpreter teardown
             nat._lib.gcabem_p1_destroy(h)
         lay = getattr(self, "layout", None)
         if lay is not None:

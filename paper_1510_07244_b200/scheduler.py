@@ -346,7 +346,7 @@ class DeviceLayout:
 
     def close(self) -> None:
         h, self.handle = getattr(self, "handle", None), None
-        if h and nat._lib is not None:
+        if h and getattr(nat, "_lib", None) is not None:  # nat is None at interpreter teardown
             nat._lib.gcabem_layout_release(h)
 
     def __del__(self):
@@ -456,7 +456,7 @@ class AssemblyPlan:
 
     def close(self) -> None:
         h, self.handle = getattr(self, "handle", None), None
-        if h and nat._lib is not None:
+        if h and getattr(nat, "_lib", None) is not None:  # nat is None at interpreter teardown
             nat._lib.gcabem_plan_destroy(h)
 
     def __del__(self):
