@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <thread>
 #include <type_traits>
 #include <vector>
@@ -555,8 +556,10 @@ int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, dou
 }  // namespace aca_avx2
 
 namespace {
+// GCABEM_ACA_BASELINE=1 forces the baseline build (tests: both builds agree bitwise)
 bool use_avx2() {
-    static const bool yes = __builtin_cpu_supports("avx2");
+    static const bool yes =
+        __builtin_cpu_supports("avx2") && std::getenv("GCABEM_ACA_BASELINE") == nullptr;
     return yes;
 }
 void aca_dispatch(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps,

@@ -1,5 +1,7 @@
 """Host-side (CPU) parts of the drop-in, bit-exact against the reference."""
 import hashlib
+import os
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -267,6 +269,51 @@ def test_staged_packages_ranges(nstages):
                   "item_tri_y", "item_leaf", "item_offset", "perms", "leaf_base"):
             assert np.array_equal(getattr(pk, f), getattr(ref, f)), (k, f)
         assert sp.offset(k) == full.leaf_base[rng[0]]
+
+
+_ACA_BUILDS_SNIPPET = """
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1510_07244_b200 import gca
+rng = np.random.default_rng(7)
+mats = []
+for nr in (5, 17, 40, 96):
+    for cplx in (False, True):
+        u = rng.standard_normal((nr, 12)) + (1j * rng.standard_normal((nr, 12)) if cplx else 0)
+        v = rng.standard_normal((12, 67)) + (1j * rng.standard_normal((12, 67)) if cplx else 0)
+        a = u @ v + 1e-9 * rng.standard_normal((nr, 67))
+        mats.append(np.ascontiguousarray(a))
+out = {}
+for i, a in enumerate(mats):
+    cplx = np.iscomplexobj(a)
+    flat = a.view(np.float64).ravel() if cplx else a.ravel()
+    r = gca.aca_batch(flat, np.array([0, a.shape[0]]), 67, cplx, 1e-6, nthreads=1)[0]
+    out[f"rows{i}"], out[f"cols{i}"], out[f"res{i}"] = r[0], r[1], np.float64(r[2])
+    op = gca._operator_from_green(i, np.arange(a.shape[0]), a, 1e-6)
+    out[f"V{i}"] = op.V
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_aca_builds_agree_bitwise(tmp_path):
+    """The AVX2 and the baseline x86-64 builds of aca.cpp (GCABEM_ACA_BASELINE
+    forces the latter) give bitwise identical pivots, residuals and V: same
+    IEEE operations in the same order, vector or scalar."""
+    import subprocess
+    import sys
+    script = tmp_path / "aca_builds.py"
+    script.write_text(_ACA_BUILDS_SNIPPET)
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ)
+    subprocess.run([sys.executable, str(script), root, str(tmp_path / "avx2.npz")], check=True,
+                   env=env)
+    env["GCABEM_ACA_BASELINE"] = "1"
+    subprocess.run([sys.executable, str(script), root, str(tmp_path / "base.npz")], check=True,
+                   env=env)
+    a, b = np.load(tmp_path / "avx2.npz"), np.load(tmp_path / "base.npz")
+    assert set(a.files) == set(b.files)
+    for k in a.files:
+        assert a[k].shape == b[k].shape and a[k].tobytes() == b[k].tobytes(), k
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
