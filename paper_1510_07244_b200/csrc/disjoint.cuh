@@ -183,9 +183,10 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // few spilled bytes in the cold full-sincos tier (orders above 7 keep the
 // compiler's choice: they would spill heavily); the fused pair kinds carry two
 // layers of accumulators and get fewer CTAs at the higher orders.
-// pair kinds at orders <= 4: L_PAIR 4 (124 registers; 5 measured 2% slower at
-// C2), H_PAIR 5 (96 registers, +1% at C3 despite a few spilled bytes in the
-// cold full-sincos tier)
+// pair kinds at orders <= 4: L_PAIR 4 (124 registers; 5 measured 1-2% slower at
+// C2), H_PAIR 5 (96 registers, a few spilled bytes in the cold full-sincos
+// tier; 4 and 6 measured 1.6% and 3% slower at C3, re-checked with the v11
+// point kernels)
 constexpr int disjoint_minb(int n, int kind) {
     return n > 7 ? 1                                     // would spill heavily
            : kind == L_SLP ? 7 : kind == L_DLP ? 6 : kind <= H_DLP ? 5
