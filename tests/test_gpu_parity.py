@@ -580,3 +580,33 @@ def test_staged_assembly_equals_unstaged(stages):
     S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops, params)
     assert np.array_equal(S.buffer, refS.buffer) and np.array_equal(D.buffer, refD.buffer)
     scheduler.clear_package_cache()
+
+
+def test_bench_json_contract(tmp_path):
+    """bench.py (our arm, small C1 config) prints one JSON line with the keys
+    the driver reads: metric/value/unit, timing, roofline, e2e with the
+    H2D/D2H byte counts, gpu_launches and the clocks sampled under load."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "bench.py", "--config", "c1", "--steps", "3",
+                          "--warmup", "3", "--e2e-steps", "1", "--no-cpu", "--no-matvec"],
+                         cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert 0.0 < d["roofline"]["frac"] <= 1.0
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["gpu_launches"] > 0
+    assert "workload" in d["config"]
