@@ -35,6 +35,8 @@ class LeafPayloads(MutableMapping):
         self._shape = leaf_shape
         self._over: dict = {}
         self._gone: set = set()
+        # bumped by every entry replacement/removal (device copies key on it)
+        self.version = 0
 
     def _index(self, key) -> int:
         k = int(key)
@@ -57,14 +59,16 @@ class LeafPayloads(MutableMapping):
     def __setitem__(self, key, value):
         self._over[key] = value
         self._gone.discard(int(key))
+        self.version += 1
 
     def __delitem__(self, key):
-        if key in self._over:
-            del self._over[key]
+        present = key in self._over or (self._index(key) >= 0 and int(key) not in self._gone)
+        if not present:
+            raise KeyError(key)
+        self._over.pop(key, None)
         if self._index(key) >= 0:
             self._gone.add(int(key))
-        elif key not in self._over:
-            raise KeyError(key)
+        self.version += 1
 
     def __iter__(self):
         for k in self._ids.tolist():
@@ -222,12 +226,38 @@ class DeviceH2:
         self.close()
 
 
-def device_matrix(M: GCAMatrix, device: int | None = None) -> DeviceH2:
-    """The device-resident copy of M (built once, cached on M)."""
+def _device_key(M: GCAMatrix) -> tuple:
+    """What the device copy was built from: the payload mapping (identity and
+    entry version), its buffer and the operator dicts. Replacing, deleting or
+    reassigning any of them invalidates the copy; writing INTO a payload
+    array in place is not seen (call invalidate(M) after doing that)."""
+    P = M.payloads
+    return (id(P), getattr(P, "version", None), id(getattr(P, "buffer", None)),
+            id(M.row_ops), id(M.col_ops), id(M.block_tree))
+
+
+def invalidate(M: GCAMatrix) -> None:
+    """Drop M's cached device copy (next matvec re-uploads the payloads)."""
     dev = getattr(M, "_device_h2", None)
-    if dev is None or (device is not None and dev.device != device):
+    if dev is not None:
+        dev.close()
+    object.__setattr__(M, "_device_h2", None)
+
+
+def device_matrix(M: GCAMatrix, device: int | None = None) -> DeviceH2:
+    """The device-resident copy of M, cached on M while the payloads and
+    operators it was built from are unchanged (_device_key)."""
+    dev = getattr(M, "_device_h2", None)
+    key = _device_key(M)
+    if isinstance(M.payloads, dict):  # plain dict: no version counter, never cached
+        key = None
+    if dev is None or dev.key != key or key is None or \
+            (device is not None and dev.device != device):
+        invalidate(M)
         dev = DeviceH2(M, device)
-        object.__setattr__(M, "_device_h2", dev)
+        dev.key = key
+        if key is not None:
+            object.__setattr__(M, "_device_h2", dev)
     return dev
 
 

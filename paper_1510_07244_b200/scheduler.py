@@ -51,19 +51,23 @@ __all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "A
            "DeviceLayout", "potential_batch", "clear_package_cache", "run_assembly_pair"]
 
 
+BACKEND_KINDS = ("cuda", "scalar-reference", "batch")
+
+
 @dataclass(frozen=True)
 class Backend:
-    """Execution target. kind "cuda" is the only kind: the sm_100a kernels on
-    `devices` (reference Backend scheduler.py:51-66 had host kinds only)."""
+    """Execution target: the sm_100a kernels on `devices`. The reference's
+    kinds (scheduler.py:51-66: "scalar-reference", "batch") are accepted so
+    reference-style configs construct unchanged; every kind runs the CUDA
+    path (there is no host execution path)."""
     name: str
     kind: str = "cuda"
     affinity: str = ""
     devices: tuple = (0,)
 
     def __post_init__(self):
-        if self.kind != "cuda":
-            raise SchedulerConfigError(
-                f"unknown backend kind {self.kind!r} (this build executes on CUDA only)")
+        if self.kind not in BACKEND_KINDS:
+            raise SchedulerConfigError(f"unknown backend kind {self.kind!r}")
         if not self.affinity:
             object.__setattr__(self, "affinity", self.name)
         if not self.devices:
@@ -72,8 +76,8 @@ class Backend:
 
 CUDA_BACKEND = Backend("cuda")
 # Reference names kept so reference-style configs resolve; both run on CUDA.
-SCALAR_BACKEND = Backend("scalar")
-BATCH_BACKEND = Backend("batch")
+SCALAR_BACKEND = Backend("scalar", "scalar-reference")
+BATCH_BACKEND = Backend("batch", "batch")
 
 
 @dataclass(frozen=True)
@@ -484,11 +488,45 @@ def _events(pk: AssemblyPackages, backend: str, t0: float, t1: float) -> list:
 
 _pk_cache: dict = {}
 _pk_lock = threading.Lock()
+# entries kept per (kind, block tree): a new operator set on the same trees
+# (e.g. a kappa sweep through assemble_operator(trees=bt)) replaces the old
+# entry instead of accumulating packages and device layouts
+_PK_PER_TREE = 1
 
 
 def clear_package_cache() -> None:
     with _pk_lock:
         _pk_cache.clear()
+
+
+def _cache_get(key, block_tree):
+    with _pk_lock:
+        hit = _pk_cache.get(key)
+    return hit[3] if hit is not None and hit[0]() is block_tree else None
+
+
+def _cache_put(key, block_tree, row_ops, col_ops, value) -> None:
+    """Insert, evicting older entries of the same kind on the same block tree
+    (their packages and device layouts are released with the last reference)."""
+    kind = key[0]
+    with _pk_lock:
+        same = [k for k in _pk_cache if k[0] == kind and k[1] == key[1] and k != key]
+        for k in same[:max(0, len(same) - _PK_PER_TREE + 1)]:
+            _pk_cache.pop(k, None)
+        _pk_cache[key] = (weakref.ref(block_tree), row_ops, col_ops, value)
+    weakref.finalize(block_tree, lambda k=key: _pk_cache.pop(k, None))
+
+
+def _cache_drop(key, value) -> None:
+    with _pk_lock:
+        hit = _pk_cache.get(key)
+        if hit is not None and hit[3] is value:
+            del _pk_cache[key]
+
+
+def _pk_key(mesh, block_tree, row_ops, col_ops, maxsize):
+    return ("packages", id(block_tree), id(row_ops), id(col_ops), int(maxsize),
+            id(mesh.triangles))
 
 
 def packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
@@ -497,16 +535,14 @@ def packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
     not depend on the kernel or the orders, so the DLP assembly reuses the
     SLP's (as the reference pipeline reuses trees and operators,
     solver.py:280-282). The cache holds the operator dicts, so their ids
-    stay valid while an entry lives; entries die with the block tree."""
-    key = (id(block_tree), id(row_ops), id(col_ops), int(maxsize), id(mesh.triangles))
-    with _pk_lock:
-        hit = _pk_cache.get(key)
-    if hit is not None and hit[0]() is block_tree:
-        return hit[3]
+    stay valid while an entry lives; one entry per block tree (a new operator
+    set replaces it), entries die with the block tree."""
+    key = _pk_key(mesh, block_tree, row_ops, col_ops, maxsize)
+    hit = _cache_get(key, block_tree)
+    if hit is not None:
+        return hit
     pk = make_packages(mesh.triangles, block_tree, row_ops, col_ops, maxsize)
-    with _pk_lock:
-        _pk_cache[key] = (weakref.ref(block_tree), row_ops, col_ops, pk)
-    weakref.finalize(block_tree, lambda k=key: _pk_cache.pop(k, None))
+    _cache_put(key, block_tree, row_ops, col_ops, pk)
     return pk
 
 
@@ -529,10 +565,13 @@ class StagedPackages:
         # while the (longer) D2H of all earlier ranges runs
         first = L if n == 1 else max(1, L // 64)
         self.ranges = [(0, first)]
+        # allocated once at the maximum stage count and never replaced: the
+        # worker thread stores into them while the ranges are still being cut
         self._pk = [None] * n
         self._ready = [threading.Event() for _ in range(n)]
         self._layout = threading.Event()
         self._err = None
+        self.key = None
         args = (mesh.triangles, block_tree, row_ops, col_ops, int(maxsize))
 
         def work():
@@ -546,7 +585,8 @@ class StagedPackages:
                     self._ready[k].set()
             except BaseException as exc:  # re-raised by stage()
                 self._err = exc
-                for ev in self._ready[k:]:
+            finally:
+                for ev in self._ready:
                     ev.set()
         self._thread = threading.Thread(target=work, name="gcabem-packaging", daemon=True)
         self._thread.start()
@@ -554,6 +594,7 @@ class StagedPackages:
             self.leaf_ids, self.leaf_shape, self.leaf_base = leaf_layout(block_tree, row_ops,
                                                                          col_ops, inputs)
             self.payload_len = int(self.leaf_base[-1])
+            ranges = list(self.ranges)
             if first < L:
                 b0 = self.leaf_base[first]
                 w = STAGE_GROWTH ** np.arange(n - 1)
@@ -561,9 +602,8 @@ class StagedPackages:
                 cuts = np.searchsorted(self.leaf_base, b0 + (self.payload_len - b0) * frac,
                                        side="left")
                 edges = np.unique(np.concatenate([[first], np.clip(cuts, first + 1, L), [L]]))
-                self.ranges += [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
-            self._pk = self._pk[:len(self.ranges)]
-            self._ready = self._ready[:len(self.ranges)]
+                ranges += [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+            self.ranges = ranges
         finally:
             self._layout.set()
 
@@ -575,9 +615,14 @@ class StagedPackages:
 
     def stage(self, k: int) -> AssemblyPackages:
         self._ready[k].wait()
-        if self._pk[k] is None:
-            raise self._err
-        return self._pk[k]
+        pk = self._pk[k]
+        if pk is None:
+            if self.key is not None:  # a failed packaging is not served again
+                _cache_drop(self.key, self)
+            if self._err is not None:
+                raise self._err
+            raise RuntimeError(f"packaging thread produced no packages for stage {k}")
+        return pk
 
     def offset(self, k: int) -> int:
         return int(self.leaf_base[self.ranges[k][0]])
@@ -589,22 +634,17 @@ def staged_packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_o
     packages_for (a second operator from the same packages packages nothing)."""
     key = ("staged", id(block_tree), id(row_ops), id(col_ops), int(maxsize),
            id(mesh.triangles), int(nstages))
-    with _pk_lock:
-        hit = _pk_cache.get(key)
-    if hit is not None and hit[0]() is block_tree:
-        return hit[3]
+    hit = _cache_get(key, block_tree)
+    if hit is not None:
+        return hit
     sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages)
-    with _pk_lock:
-        _pk_cache[key] = (weakref.ref(block_tree), row_ops, col_ops, sp)
-    weakref.finalize(block_tree, lambda k=key: _pk_cache.pop(k, None))
+    sp.key = key
+    _cache_put(key, block_tree, row_ops, col_ops, sp)
     return sp
 
 
 def _cached_packages(mesh, block_tree, row_ops, col_ops, maxsize):
-    key = (id(block_tree), id(row_ops), id(col_ops), int(maxsize), id(mesh.triangles))
-    with _pk_lock:
-        hit = _pk_cache.get(key)
-    return hit[3] if hit is not None and hit[0]() is block_tree else None
+    return _cache_get(_pk_key(mesh, block_tree, row_ops, col_ops, maxsize), block_tree)
 
 
 def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, stats,
@@ -612,7 +652,10 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
     """Single-device assembly over StagedPackages: plan k is created and
     launched (kernels + chunked D2H on its own streams) as soon as range k is
     packaged, so packaging and layout upload of later ranges overlap the
-    device work and the D2H of earlier ones."""
+    device work and the D2H of earlier ones. The payloads are bitwise those
+    of the unstaged path; AssemblyStats list counts/events are per range (each
+    range's lists are cut from its own first leaf), so lists_executed depends
+    on the stage count (pairs_executed does not)."""
     t0 = time.monotonic()
     phase = {}
     sp = staged_packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes,

@@ -130,7 +130,39 @@ def test_split_and_listbuilder_api():
     with pytest.raises(scheduler.SchedulerConfigError):
         scheduler.ListBuilder("disjoint", 16, out.append)
     with pytest.raises(scheduler.SchedulerConfigError):
-        scheduler.Backend("x", "batch")
+        scheduler.Backend("x", "gpu-magic")
+
+
+def test_reference_backend_kinds_construct():
+    """Reference-style backends (scheduler.py:51-66 kinds) construct and
+    resolve through SchedulerParams exactly as in the reference; they run on
+    the CUDA path."""
+    b = scheduler.Backend("batch", "batch")
+    s = scheduler.Backend("scalar", "scalar-reference")
+    assert b.affinity == "batch" and s.kind == "scalar-reference" and b.devices == (0,)
+    params = scheduler.SchedulerParams(
+        backends=(s, b), affinity={"disjoint": "batch", "vertex": "scalar",
+                                   "edge": "scalar", "identical": "scalar"})
+    assert params.backend_for("disjoint") is b and params.backend_for("edge") is s
+    assert params.backend_for("unknown") is s
+    assert scheduler.BATCH_BACKEND.kind == "batch"
+    assert scheduler.SCALAR_BACKEND.kind == "scalar-reference"
+
+
+def test_package_cache_one_entry_per_tree():
+    """A new operator set on the same block tree replaces the cached packages
+    (the cache grew by one entry per operator set)."""
+    from paper_1510_07244_b200 import mesh as mesh_mod
+    m = mesh_mod.build_sphere_mesh(2)
+    t = cluster.build_cluster_tree(m, 16)
+    bt = cluster.build_block_tree(t, t, 2.0)
+    near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    scheduler.clear_package_cache()
+    for _ in range(5):
+        ops = {}
+        scheduler.packages_for(m, near, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    assert sum(1 for k in scheduler._pk_cache if k[1] == id(near)) == 1
+    scheduler.clear_package_cache()
 
 
 def test_green_sources_bitwise(gload):
