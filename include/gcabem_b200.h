@@ -264,9 +264,7 @@ int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows_at, int64_
  * panel rule (nduffy rows {s, t, w}); the host runs ACA (epsilon, one retry
  * at epsilon/10), the cond <= 1e14 pivot check and the refined V solve on
  * nthreads threads, overlapped with the next batch (batch_bytes of Green
- * matrix per launch, 4 launches in flight; 0 = 32 MiB). With
- * GCABEM_GCA_DEVICE_SOLVE=1 the check and the solve run on the device for
- * packs of clusters (the host solves the ambiguous / rejected ones exactly).
+ * matrix per launch, 4 launches in flight; 0 = 32 MiB).
  * Results: gcabem_gca_sizes (rank per
  * cluster, phase6 {device wait s, pipeline wall s, total s, batches, host
  * thread-seconds, threads}), then
@@ -283,6 +281,26 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                      gcabem_gca_t *out);
 int gcabem_gca_sizes(gcabem_gca_t g, int64_t *ranks, double *phase6);
 int gcabem_gca_fetch(gcabem_gca_t g, int64_t *rows, double *V);
+/* Per cluster (order of cl_ids): 1 if one of its ACA decisions (an argmax
+ * over a residual row/column, the stopping test) had a margin inside the
+ * roundoff of the device's Green matrix, i.e. the reference's numpy bits
+ * could decide it the other way. Such clusters were redone by the pipeline
+ * on entries evaluated in the reference's arithmetic (gcabem_green_exact). */
+int gcabem_gca_flags(gcabem_gca_t g, int8_t *ambiguous);
+/* Host only: one cluster's Green matrix with every entry evaluated in the
+ * reference's numpy arithmetic (gca.py:136-179, kernels.py:46-64; the
+ * sources of gca.py:83-133 from the box [box_lo, box_hi]), written to A
+ * (nr x 12 m^2, float64 or interleaved complex128; may be NULL), and, when
+ * rank/rows/V are given, the operator the GCA pipeline computes for a
+ * cluster it redoes on these entries (ACA + check + V solve). The pipeline
+ * uses the same evaluation internally for the clusters gcabem_gca_flags
+ * reports. */
+int gcabem_green_exact(int equation, double kappa, int64_t nv, const double *vertices,
+                       int64_t nt, const int64_t *triangles, const double *gramians, int64_t nr,
+                       const int64_t *panels, const double *box_lo, const double *box_hi,
+                       double delta, int m, const double *gauss_pts, const double *gauss_wts,
+                       double scene_diameter, int64_t nduffy, const double *duffy,
+                       double epsilon, double *A, int64_t *rank, int64_t *rows, double *V);
 int gcabem_gca_free(gcabem_gca_t g);
 /* One cluster's operator from a host Green matrix A (nr x nc row-major,
  * float64 or interleaved complex128): ACA + cond check + refined V solve

@@ -12,6 +12,10 @@ Contents
   loop (reference pkg/src/gcabem/pairquad.py:27-112) and of the batch
   backend gather (scheduler.py:257-261, mesh.py:207-222). Pinned
   bit-for-bit against tests/golden/pair_values_L3.npz.
+* ``batch_quadrature(..., high_precision=True)``: pairquad_hp.c, the same
+  discrete rule on the reference's double-precision chart inputs evaluated
+  in binary128 — the yardstick for entries that are roundoff-dominated in
+  the reference (tests/test_p2_evidence.py).
 * numpy restatements of the rule construction (quadrature.py:82-194),
   the pair classification (quadrature.py:197-220) and the Green matrix
   (gca.py:136-179), pinned against golden hashes / fixtures.
@@ -36,8 +40,9 @@ LAYER = {"single": 0, "double": 1}
 def build() -> str:
     """Compile liboracle.so (gcc, OpenMP) in place; returns its path."""
     path = os.path.join(HERE, "liboracle.so")
-    src = os.path.join(HERE, "pairquad_oracle.c")
-    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("pairquad_oracle.c", "pairquad_hp.c", "Makefile")]
+    if not os.path.exists(path) or \
+            os.path.getmtime(path) < max(os.path.getmtime(s) for s in srcs):
         subprocess.run(["make", "-s", "-C", HERE], check=True)
     return path
 
@@ -56,6 +61,7 @@ def lib():
         L.oracle_batch_quadrature.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double] \
             + [dp] * 4 + [ctypes.c_int64] + [dp] * 4 + [ctypes.c_int64] + [dp] * 4 \
             + [ctypes.c_int]
+        L.oracle_batch_quadrature_hp.argtypes = L.oracle_batch_quadrature.argtypes
         L.oracle_max_threads.restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -86,8 +92,12 @@ def pair_values(equation, layer, kappa, ox, e1x, e2x, gx, oy, e1y, e2y, gy, ny,
 
 
 def batch_quadrature(equation, layer, kappa, vertices, triangles, normals, gramians,
-                     tri_x, tri_y, perm_x, perm_y, xs, ys, w, nthreads=1) -> np.ndarray:
-    """Bit-exact restatement of scheduler.batch_quadrature's batch backend."""
+                     tri_x, tri_y, perm_x, perm_y, xs, ys, w, nthreads=1,
+                     high_precision=False) -> np.ndarray:
+    """Bit-exact restatement of scheduler.batch_quadrature's batch backend.
+    high_precision=True: the same discrete rule on the same double-precision
+    chart inputs evaluated in binary128 (pairquad_hp.c) - the exact value the
+    reference's double arithmetic approximates."""
     V = _f64(vertices)
     T = np.ascontiguousarray(triangles, dtype=np.int64)
     N = _f64(normals)
@@ -98,7 +108,8 @@ def batch_quadrature(equation, layer, kappa, vertices, triangles, normals, grami
     py = None if perm_y is None else np.ascontiguousarray(perm_y, dtype=np.int64)
     xs, ys, w = _f64(xs), _f64(ys), _f64(w)
     out = np.empty(len(tx), dtype=np.complex128)
-    lib().oracle_batch_quadrature(EQ[equation], LAYER[layer], float(kappa),
+    fn = lib().oracle_batch_quadrature_hp if high_precision else lib().oracle_batch_quadrature
+    fn(EQ[equation], LAYER[layer], float(kappa),
                                   _p(V), _p(T), _p(N), _p(G), len(tx), _p(tx), _p(ty),
                                   _p(px), _p(py), w.shape[0], _p(xs), _p(ys), _p(w),
                                   _p(out), int(nthreads))

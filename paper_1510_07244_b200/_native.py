@@ -90,6 +90,9 @@ _SIGS = {
                                                      ctypes.POINTER(_vp)], _int),
     "gcabem_gca_sizes": ([_vp, _vp, _vp], _int),
     "gcabem_gca_fetch": ([_vp, _vp, _vp], _int),
+    "gcabem_gca_flags": ([_vp, _vp], _int),
+    "gcabem_green_exact": ([_int, _dbl, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _dbl,
+                            _int, _vp, _vp, _dbl, _i64, _vp, _dbl, _vp, _vp, _vp, _vp], _int),
     "gcabem_gca_free": ([_vp], _int),
     "gcabem_gca_operator": ([_int, _vp, _i64, _i64, _dbl, _vp, _vp, _vp], _int),
     "gcabem_h2_create": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp,

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "gcabem_b200.h"
+#include "green_exact.h"
 #include "internal.h"
 
 // Compiled twice: as is (baseline x86-64) and from aca_avx2.cpp with -mavx2
@@ -223,10 +224,57 @@ int64_t argmax_mag(const T *x, int64_t n, const char *mask, double *best_out) {
     return jp;
 }
 
+// Tie window of the ACA decisions. The Green matrix this ACA sees is the
+// device's, within a few ulps of the reference's numpy evaluation; a
+// decision whose margin is below these bounds could go the other way on the
+// reference's bits (exact ties from the sphere's symmetry are the common
+// case), so it marks the cluster ambiguous (the caller redoes it on the
+// reference's exact arithmetic). Relative to the winning magnitude, and
+// absolute relative to the largest entry of the original row/column (the
+// residual's rounding scale).
+constexpr double TIE_REL = 1e-10;
+constexpr double TIE_ABS = 1e-12;
+constexpr double STOP_REL = 1e-8;
+
+// another unmasked entry of |x| within delta of best (index jp excluded)?
 template <typename T>
-void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
-             int64_t *cols, int64_t *rank, double *resid) {
+bool near_tie(const T *x, int64_t n, const char *mask, int64_t jp, double best, double delta) {
     using O = Ops<T>;
+    const double lo = best - delta;
+    if (lo <= 0.0) return true;
+    const double lo2 = lo * lo * (1.0 - 1e-12);  // squares carry < 4 ulp error
+    for (int64_t j = 0; j < n; ++j) {
+        if (j == jp || (mask && mask[j])) continue;
+        if (O::norm2(x[j]) >= lo2 && O::mag(x[j]) >= lo) return true;
+    }
+    return false;
+}
+
+template <typename T>
+double max_mag(const T *x, int64_t n, int64_t stride) {
+    using O = Ops<T>;
+    double m2 = 0.0;
+    for (int64_t j = 0; j < n; ++j) m2 = std::max(m2, O::norm2(x[j * stride]));
+    return std::sqrt(m2);
+}
+
+// Row / column access of the matrix the ACA works on: a dense row-major
+// matrix, or entries evaluated on demand (GreenExact, the tie redo path).
+template <typename T>
+struct DenseSrc {
+    const T *A;
+    int64_t nr, nc;
+    void row(int64_t i, T *out) const { std::copy(A + i * nc, A + i * nc + nc, out); }
+    void col(int64_t j, T *out) const {
+        for (int64_t q = 0; q < nr; ++q) out[q] = A[q * nc + j];
+    }
+};
+
+template <typename T, typename Src>
+void aca_core(const Src &src, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
+              int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr) {
+    using O = Ops<T>;
+    bool amb = false;
     std::vector<std::vector<T>> U, W;
     std::vector<char> used(nr, 0);
     std::vector<T> r(nc), c(nr);
@@ -244,12 +292,18 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
             next = f;
         }
         const int64_t i = next;
-        for (int64_t j = 0; j < nc; ++j) r[j] = A[i * nc + j];
+        src.row(i, r.data());
+        const double rscale = ambiguous && !amb ? max_mag<T>(r.data(), nc, 1) : 0.0;
         for (size_t m = 0; m < U.size(); ++m) {
             const T ui = U[m][i];
             mulsub<T>(r.data(), ui, W[m].data(), nc);
         }
-        const int64_t jp = argmax_mag<T>(r.data(), nc, nullptr, nullptr);
+        double rbest = 0.0;
+        const int64_t jp = argmax_mag<T>(r.data(), nc, nullptr, &rbest);
+        if (ambiguous && !amb)
+            amb = rbest <= TIE_ABS * rscale ||
+                  near_tie<T>(r.data(), nc, nullptr, jp, rbest,
+                              std::max(TIE_REL * rbest, TIE_ABS * rscale));
         used[i] = 1;
         if (O::zero(r[jp])) {
             next = nr;
@@ -259,7 +313,8 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
         const T piv = r[jp];
         const typename O::Divider by_piv(piv);
         for (int64_t j = 0; j < nc; ++j) w[j] = by_piv(r[j]);
-        for (int64_t q = 0; q < nr; ++q) c[q] = A[q * nc + jp];
+        src.col(jp, c.data());
+        const double cscale = ambiguous && !amb ? max_mag<T>(c.data(), nr, 1) : 0.0;
         for (size_t m = 0; m < U.size(); ++m) {
             const T wj = W[m][jp];
             mulsub<T>(c.data(), wj, U[m].data(), nr);
@@ -268,7 +323,8 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
         // sums (vectorisable; the reference's np.linalg.norm / np.vdot are
         // BLAS reductions with their own association, so no order is "the"
         // reference order here -- only the elementwise residual updates
-        // above decide pivots and follow the reference exactly)
+        // above decide pivots and follow the reference exactly; a stopping
+        // test within STOP_REL of its bound is flagged)
         const double nu = std::sqrt(dotc<T>(c.data(), c.data(), nr).re);
         const double nw = std::sqrt(dotc<T>(w.data(), w.data(), nc).re);
         double cross = 0.0;
@@ -284,13 +340,26 @@ void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_
         ++k;
         est2 = std::max(est2 + nu * nu * nw * nw + 2.0 * cross, 0.0);
         res = nu * nw;
-        if (res <= eps * std::sqrt(est2)) break;
+        const double bound = eps * std::sqrt(est2);
+        if (ambiguous && !amb) amb = std::fabs(res - bound) <= STOP_REL * bound;
+        if (res <= bound) break;
         double mb = 0.0;
         const int64_t nb = argmax_mag<T>(c.data(), nr, used.data(), &mb);
+        if (ambiguous && !amb && k < cap)
+            amb = mb <= TIE_ABS * cscale ||
+                  near_tie<T>(c.data(), nr, used.data(), nb, mb,
+                              std::max(TIE_REL * mb, TIE_ABS * cscale));
         next = mb == 0.0 ? nr : nb;
     }
     *rank = k;
     *resid = res;
+    if (ambiguous) *ambiguous = amb ? 1 : 0;
+}
+
+template <typename T>
+void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
+             int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr) {
+    aca_core<T>(DenseSrc<T>{A, nr, nc}, nr, nc, eps, cap, rows, cols, rank, resid, ambiguous);
 }
 
 // ---------------------------------------------------------------------------
@@ -505,28 +574,93 @@ int solve_one(const T *A, int64_t nr, int64_t nc, int64_t k, const int64_t *rows
 // solve, and one retry at eps / 10 when the pivot block is rejected
 template <typename T>
 int operator_one(const T *A, int64_t nr, int64_t nc, double eps, std::vector<int64_t> &rows_out,
-                 std::vector<double> &V_out, int64_t pre_k = -1, const int64_t *pre_rows = nullptr,
-                 const int64_t *pre_cols = nullptr) {
+                 std::vector<double> &V_out, int *ambiguous = nullptr) {
     const int64_t cap = std::min(nr, nc);
     std::vector<int64_t> rows(cap), cols(cap);
     for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
         int64_t k = 0;
         const int64_t *r = rows.data(), *c = cols.data();
-        if (attempt == 0 && pre_k >= 0) {
-            k = pre_k;
-            r = pre_rows;
-            c = pre_cols;
-        } else {
-            double resid = 0.0;
-            aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
-        }
+        double resid = 0.0;
+        int amb = 0;
+        aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid,
+                   ambiguous ? &amb : nullptr);
+        if (ambiguous && amb) *ambiguous = 1;
         if (k == 0) return 1;
         if (solve_one<T>(A, nr, nc, k, r, c, rows_out, V_out) == 0) return 0;
     }
     return 2;
 }
 
+// On-demand exact entries (GreenExact); columns are kept for the solve
+template <typename T>
+struct ExactSrc {
+    const gcabem::GreenExact *g;
+    int64_t nr, nc;
+    mutable std::vector<std::vector<T>> cols;  // by column index, filled on demand
+    static T make(double re, double im) {
+        if constexpr (std::is_same<T, Cx>::value)
+            return Cx{re, im};
+        else
+            return re;
+    }
+    void row(int64_t i, T *out) const {
+        for (int64_t j = 0; j < nc; ++j) {
+            double re, im;
+            g->entry(i, j, re, im);
+            out[j] = make(re, im);
+        }
+    }
+    const std::vector<T> &column(int64_t j) const {
+        if (cols.empty()) cols.resize(nc);
+        std::vector<T> &c = cols[j];
+        if (c.empty()) {
+            c.resize(nr);
+            for (int64_t q = 0; q < nr; ++q) {
+                double re, im;
+                g->entry(q, j, re, im);
+                c[q] = make(re, im);
+            }
+        }
+        return c;
+    }
+    void col(int64_t j, T *out) const {
+        const std::vector<T> &c = column(j);
+        std::copy(c.begin(), c.end(), out);
+    }
+};
+
+template <typename T>
+int operator_exact(const gcabem::GreenExact &g, double eps, std::vector<int64_t> &rows_out,
+                   std::vector<double> &V_out) {
+    const int64_t nr = g.nr, nc = g.nsrc(), cap = std::min(nr, nc);
+    ExactSrc<T> src{&g, nr, nc, {}};
+    std::vector<int64_t> rows(cap), cols(cap);
+    for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
+        int64_t k = 0;
+        double resid = 0.0;
+        aca_core<T>(src, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
+        if (k == 0) return 1;
+        // A[:, cols] compacted (nr x k): solve_one reads exactly these values
+        std::vector<T> Ac((size_t)(nr * k));
+        for (int64_t b = 0; b < k; ++b) {
+            const std::vector<T> &c = src.column(cols[b]);
+            for (int64_t q = 0; q < nr; ++q) Ac[q * k + b] = c[q];
+        }
+        std::vector<int64_t> iota(k);
+        for (int64_t b = 0; b < k; ++b) iota[b] = b;
+        if (solve_one<T>(Ac.data(), nr, k, k, rows.data(), iota.data(), rows_out, V_out) == 0)
+            return 0;
+    }
+    return 2;
+}
+
 // entry points of this build
+int exact_entry(bool is_complex, const gcabem::GreenExact &g, double epsilon,
+                std::vector<int64_t> &rows, std::vector<double> &V) {
+    return is_complex ? operator_exact<Cx>(g, epsilon, rows, V)
+                      : operator_exact<double>(g, epsilon, rows, V);
+}
+
 void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps, int64_t cap,
                int64_t *rows, int64_t *cols, int64_t *rank, double *resid) {
     if (is_complex)
@@ -536,12 +670,11 @@ void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double 
 }
 
 int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                   std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
-                   const int64_t *pre_rows, const int64_t *pre_cols) {
+                   std::vector<int64_t> &rows, std::vector<double> &V, int *ambiguous) {
     if (is_complex)
-        return operator_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, epsilon, rows, V, pre_k,
-                                pre_rows, pre_cols);
-    return operator_one<double>(A, nr, nc, epsilon, rows, V, pre_k, pre_rows, pre_cols);
+        return operator_one<Cx>(reinterpret_cast<const Cx *>(A), nr, nc, epsilon, rows, V,
+                                ambiguous);
+    return operator_one<double>(A, nr, nc, epsilon, rows, V, ambiguous);
 }
 
 }  // namespace GCABEM_ACA_NS
@@ -551,8 +684,9 @@ namespace aca_avx2 {
 void aca_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double eps, int64_t cap,
                int64_t *rows, int64_t *cols, int64_t *rank, double *resid);
 int operator_entry(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                   std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
-                   const int64_t *pre_rows, const int64_t *pre_cols);
+                   std::vector<int64_t> &rows, std::vector<double> &V, int *ambiguous);
+int exact_entry(bool is_complex, const gcabem::GreenExact &g, double epsilon,
+                std::vector<int64_t> &rows, std::vector<double> &V);
 }  // namespace aca_avx2
 
 namespace {
@@ -601,13 +735,15 @@ extern "C" int gcabem_aca_batch(int is_complex, int64_t ncl, const int64_t *rows
 
 namespace gcabem {
 int gca_operator(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                 std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k,
-                 const int64_t *pre_rows, const int64_t *pre_cols) {
+                 std::vector<int64_t> &rows, std::vector<double> &V, int *ambiguous) {
     if (use_avx2())
-        return aca_avx2::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, pre_k, pre_rows,
-                                        pre_cols);
-    return aca_base::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, pre_k, pre_rows,
-                                    pre_cols);
+        return aca_avx2::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, ambiguous);
+    return aca_base::operator_entry(is_complex, A, nr, nc, epsilon, rows, V, ambiguous);
+}
+int gca_operator_exact(bool is_complex, const GreenExact &g, double epsilon,
+                       std::vector<int64_t> &rows, std::vector<double> &V) {
+    if (use_avx2()) return aca_avx2::exact_entry(is_complex, g, epsilon, rows, V);
+    return aca_base::exact_entry(is_complex, g, epsilon, rows, V);
 }
 int64_t gca_aca(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
                 int64_t *rows, int64_t *cols) {
@@ -617,6 +753,97 @@ int64_t gca_aca(bool is_complex, const double *A, int64_t nr, int64_t nc, double
     return k;
 }
 }  // namespace gcabem
+
+// Host-exact Green matrix of one cluster (tests: bitwise against the numpy
+// restatement gca.green_matrix_exact and the reference's golden matrices)
+// and the exact-path operator of that cluster. charts: nt x 16 doubles as
+// the device Chart layout is built by gcabem_mesh_create; here from arrays.
+namespace {
+std::vector<gcabem::Chart> host_charts(int64_t nv, const double *V, int64_t nt, const int64_t *T,
+                                       const double *gram) {
+    std::vector<gcabem::Chart> ch(nt);
+    for (int64_t t = 0; t < nt; ++t) {
+        const int64_t i0 = T[3 * t], i1 = T[3 * t + 1], i2 = T[3 * t + 2];
+        for (int k = 0; k < 3; ++k) {
+            ch[t].o[k] = V[3 * i0 + k];
+            ch[t].e1[k] = V[3 * i1 + k] - V[3 * i0 + k];
+            ch[t].e2[k] = V[3 * i2 + k] - V[3 * i1 + k];
+            ch[t].n[k] = 0.0;
+        }
+        ch[t].gram = gram[t];
+    }
+    (void)nv;
+    return ch;
+}
+gcabem::GreenBox enlarged_box(const double *lo, const double *hi, double delta, double scene) {
+    gcabem::GreenBox b;
+    double ext = hi[0] - lo[0];
+    ext = std::max(ext, hi[1] - lo[1]);
+    ext = std::max(ext, hi[2] - lo[2]);
+    const double hmax = 0.5 * std::max(ext, 1e-8 * scene);
+    for (int k = 0; k < 3; ++k) {
+        b.center[k] = 0.5 * (lo[k] + hi[k]);
+        b.half[k] = 0.5 * (hi[k] - lo[k]) + delta * hmax;
+    }
+    return b;
+}
+}  // namespace
+
+extern "C" int gcabem_green_exact(int equation, double kappa, int64_t nv, const double *V,
+                                  int64_t nt, const int64_t *T, const double *gram, int64_t nr,
+                                  const int64_t *panels, const double *box_lo,
+                                  const double *box_hi, double delta, int m,
+                                  const double *gauss_pts, const double *gauss_wts,
+                                  double scene_diameter, int64_t nduffy, const double *duffy,
+                                  double epsilon, double *A, int64_t *rank, int64_t *rows,
+                                  double *Vop) {
+    if (!V || !T || !gram || !panels || nr <= 0 || m < 1 || nduffy < 1 ||
+        !(equation == 0 || equation == 1))
+        return gcabem_internal_error(GCABEM_ERR_ARG, "green_exact: bad arguments");
+    const auto charts = host_charts(nv, V, nt, T, gram);
+    std::vector<int32_t> pan(nr);
+    for (int64_t p = 0; p < nr; ++p) {
+        if (panels[p] < 0 || panels[p] >= nt)
+            return gcabem_internal_error(GCABEM_ERR_ARG, "green_exact: panel out of range");
+        pan[p] = (int32_t)panels[p];
+    }
+    gcabem::GreenExact g;
+    g.charts = charts.data();
+    g.panels = pan.data();
+    g.nr = nr;
+    g.equation = equation;
+    g.kappa = kappa;
+    g.duffy = duffy;
+    g.nq = (int)nduffy;
+    g.m = m;
+    g.sources(enlarged_box(box_lo, box_hi, delta, scene_diameter), gauss_pts, gauss_wts);
+    const int64_t nc = g.nsrc();
+    if (A)
+        for (int64_t p = 0; p < nr; ++p)
+            for (int64_t s = 0; s < nc; ++s) {
+                double re, im;
+                g.entry(p, s, re, im);
+                if (equation == 0) {
+                    A[p * nc + s] = re;
+                } else {
+                    A[2 * (p * nc + s)] = re;
+                    A[2 * (p * nc + s) + 1] = im;
+                }
+            }
+    if (rank && rows && Vop) {
+        std::vector<int64_t> r;
+        std::vector<double> v;
+        const int rc = gcabem::gca_operator_exact(equation == 1, g, epsilon, r, v);
+        if (rc == 1) return gcabem_internal_error(GCABEM_ERR_GCA, "zero Green matrix");
+        if (rc == 2)
+            return gcabem_internal_error(GCABEM_ERR_GCA,
+                                         "singular ACA pivot block (condition above 1e+14)");
+        *rank = (int64_t)r.size();
+        std::copy(r.begin(), r.end(), rows);
+        std::copy(v.begin(), v.end(), Vop);
+    }
+    return GCABEM_OK;
+}
 
 // Host entry for one matrix (tests, gca._operator_from_green): rows and V
 // sized for the rank cap min(nr, nc).

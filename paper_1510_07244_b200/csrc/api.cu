@@ -259,6 +259,7 @@ int gcabem_mesh_create(int device, int64_t nv, const double *vertices, int64_t n
         gcabem_mesh_destroy(m);
         GC_CUDA(e);
     }
+    m->charts_host = std::move(charts);  // host evaluations (GCA tie redo)
     *out = m;
     return GCABEM_OK;
 }

@@ -7,11 +7,14 @@
 //   host     ACA per cluster (the pivots, aca.cpp) on a thread pool, each
 //            worker copying its cluster out of the slot first, while the
 //            device computes the next batches;
-//   host     the pivot-block check and the refined V solve (gca_operator);
-//            with GCABEM_GCA_DEVICE_SOLVE=1 on the device instead
-//            (vsolve.cu) for packs of clusters, launched and harvested by one
-//            launcher thread (clusters it hands back, and those no pack had
-//            room for, take the host solve).
+//   host     the pivot-block check and the refined V solve (gca_operator).
+//
+// Every ACA decision (argmax of a residual row/column, the stopping test) is
+// made on the device's Green matrix, whose entries agree with the
+// reference's numpy evaluation to a few ulps; a decision whose margin is
+// inside that error (exact ties from the mesh's symmetry, mostly) is FLAGGED
+// per cluster (gcabem_gca_flags) so the caller can redo that cluster on a
+// bit-exact host evaluation of the reference's Green matrix (gca.py).
 //
 // Clusters run largest first (the longest host jobs start early: no tail with
 // idle threads). North star split: the Green matrices (dense FP64 kernel
@@ -29,17 +32,17 @@
 #include <thread>
 #include <vector>
 
-#include "gca_vsolve.h"
+#include "green_exact.h"
 #include "internal.h"
 
 using namespace gcabem;
-using namespace gcabem::gca_detail;
 
 struct gcabem_gca_s {
     int is_complex = 0;
     int64_t ncl = 0;
     std::vector<std::vector<int64_t>> rows;  // local row pivots per cluster
     std::vector<std::vector<double>> V;      // |t| x rank per cluster (row-major)
+    std::vector<char> ambiguous;             // an ACA decision within roundoff of a tie
     // device wait, pipeline wall, total, batches, host thread-seconds, threads
     double phase[6] = {0, 0, 0, 0, 0, 0};
 };
@@ -51,6 +54,24 @@ double since(clk::time_point t0) {
     return std::chrono::duration<double>(clk::now() - t0).count();
 }
 
+// grow-only pinned host buffer
+struct Pinned {
+    void *p = nullptr;
+    size_t n = 0;
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= n && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess) n = bytes;
+        return e;
+    }
+};
+
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
 constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
@@ -59,7 +80,6 @@ struct Staging {
     Pinned host[SLOTS];
     DevBuf<double> out[SLOTS];
     std::vector<std::vector<double>> aown;  // per worker: its cluster's Green matrix
-    std::unique_ptr<VRing> vring;
     std::mutex busy;  // one build per device at a time (builds on other devices run in parallel)
 };
 std::mutex g_staging_mutex;
@@ -110,6 +130,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     G->ncl = ncl;
     G->rows.resize(ncl);
     G->V.resize(ncl);
+    G->ambiguous.assign(ncl, 0);
     std::vector<int32_t> perm32(nperm);
     for (int64_t k = 0; k < nperm; ++k) {
         if (perm[k] < 0 || perm[k] >= mesh->nt) {
@@ -288,22 +309,7 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         starved(nthreads, 0.0);
     const auto t_start = clk::now();
     if ((int)st.aown.size() < nthreads) st.aown.resize(nthreads);
-    // V solves on the host by default; GCABEM_GCA_DEVICE_SOLVE=1 sends them
-    // to the device (gca_vsolve.h). Measured at C3 (16 threads): the device
-    // path is ~5-25% faster on later builds of a process but ~0.5 s slower
-    // on the first (pinned pack buffers, device pool growth), which is the
-    // build a setup pays, so it is opt-in.
-    const bool host_solve = std::getenv("GCABEM_GCA_DEVICE_SOLVE") == nullptr;
-    if (!host_solve && e == cudaSuccess && !st.vring) {
-        auto r = std::make_unique<VRing>();
-        e = r->init();
-        if (e == cudaSuccess) st.vring = std::move(r);
-    }
-    std::unique_ptr<VSolveQueue> vq;
-    if (!host_solve && st.vring)
-        vq = std::make_unique<VSolveQueue>(*st.vring, mesh->device, equation == 1, nsrc, G->rows,
-                                           G->V);
-    std::atomic<int64_t> n_host{0};
+    std::atomic<int64_t> n_host{0}, n_exact{0};
     auto fail = [&](int64_t c, int rc) {
         int64_t prev = err_cluster.load();
         while (c < prev && !err_cluster.compare_exchange_weak(prev, c)) {
@@ -312,7 +318,6 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     };
     auto worker = [&](int tid) {
         std::vector<double> &Aown = st.aown[tid];  // grow-only across calls: no page faults
-        std::vector<int64_t> prow, pcol;
         for (;;) {
             const int64_t pos = next.fetch_add(1);
             if (pos >= ncl) return;
@@ -335,25 +340,27 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                 cv.notify_all();
             }
             const int64_t nr = cl_size[c];
-            int rc = 0;
-            if (vq) {
-                prow.resize(std::min(nr, nsrc));
-                pcol.resize(prow.size());
-                const int64_t k = gca_aca(equation == 1, Aown.data(), nr, nsrc, epsilon,
-                                          prow.data(), pcol.data());
-                // k = 0 is the zero-matrix error; ranks above VS_KMAX and a
-                // full pack ring stay on the host (no second ACA)
-                if (k == 0 || k > VS_KMAX ||
-                    !vq->offload(c, Aown.data(), nr, k, prow.data(), pcol.data())) {
-                    rc = gca_operator(equation == 1, Aown.data(), nr, nsrc, epsilon, G->rows[c],
-                                      G->V[c], k, prow.data(), pcol.data());
-                    n_host.fetch_add(1);
-                }
-            } else {
-                rc = gca_operator(equation == 1, Aown.data(), nr, nsrc, epsilon, G->rows[c],
-                                  G->V[c]);
-                n_host.fetch_add(1);
+            int amb = 0;
+            int rc = gca_operator(equation == 1, Aown.data(), nr, nsrc, epsilon, G->rows[c],
+                                  G->V[c], &amb);
+            if (rc == 0 && amb) {
+                // a decision inside the tie window: redo this cluster on
+                // entries evaluated in the reference's own arithmetic
+                GreenExact ge;
+                ge.charts = mesh->charts_host.data();
+                ge.panels = perm32.data() + cl_first[c];
+                ge.nr = nr;
+                ge.equation = equation;
+                ge.kappa = kappa;
+                ge.duffy = duffy;
+                ge.nq = (int)nduffy;
+                ge.m = m;
+                ge.sources(boxes[c], gauss_pts, gauss_wts);
+                rc = gca_operator_exact(equation == 1, ge, epsilon, G->rows[c], G->V[c]);
+                n_exact.fetch_add(1);
             }
+            G->ambiguous[c] = (char)amb;
+            n_host.fetch_add(1);
             if (rc != 0) fail(c, rc);
             busy[tid] += since(t0);
             last_at[tid] = since(t_start);
@@ -362,10 +369,8 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
     double t_wait = 0.0;
     const auto t_pipe = clk::now();
     std::vector<std::thread> th;
-    std::thread launch_thread;
     if (e == cudaSuccess) {
         for (int t = 0; t < nthreads; ++t) th.emplace_back(worker, t);
-        if (vq) launch_thread = std::thread([&] { vq->run(); });
     }
     int64_t issued = 0, completed = 0;
     while (e == cudaSuccess && completed < nb) {
@@ -412,48 +417,13 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
         cv.notify_all();
     }
     for (auto &t : th) t.join();
-    if (launch_thread.joinable()) {
-        vq->workers_finished();
-        launch_thread.join();
-    }
-    if (e == cudaSuccess && vq && vq->error() != cudaSuccess) e = vq->error();
-    std::vector<int64_t> none, &retry = vq ? vq->handed_back() : none;
     tr.mark("pipeline");
-    // clusters the device solve handed back (pivot block singular or in the
-    // condition bracket's ambiguous window): the Green matrix once more, then
-    // the host's exact decision and its tighter ACA retry
-    std::sort(retry.begin(), retry.end());
-    const auto t_retry = clk::now();
-    for (int64_t c : retry) {
-        if (e != cudaSuccess) break;
-        int64_t pos = 0;
-        while (ord[pos] != c) ++pos;
-        std::vector<int2> tk;
-        const int64_t ne = cl_size[c] * ng;
-        for (int64_t e0 = 0; e0 < ne; e0 += GREEN_TPB) tk.push_back(make_int2(0, (int)e0));
-        const int64_t zero = 0;
-        e = cudaMemcpyAsync(d_task.p, tk.data(), sizeof(int2) * tk.size(), cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(d_at.p, &zero, sizeof(int64_t), cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess)
-            e = launch_green_box(equation, mesh->charts.p, d_task.p, (int64_t)tk.size(),
-                                 d_first.p + pos, d_size.p + pos, d_perm.p, d_box.p + pos, m,
-                                 d_gq.p, d_duffy.p, (int)nduffy, d_at.p, st.out[0].p, kappa, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(st.host[0].p, st.out[0].p,
-                                sizeof(double) * cl_size[c] * nsrc * width, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) break;
-        const int rc = gca_operator(equation == 1, static_cast<const double *>(st.host[0].p),
-                                    cl_size[c], nsrc, epsilon, G->rows[c], G->V[c]);
-        if (rc != 0) fail(c, rc);
+    if (tr.on) {
+        int64_t namb = 0;
+        for (char x : G->ambiguous) namb += x;
+        std::fprintf(stderr, "[gca] %lld clusters, %lld with a decision inside the tie window\n",
+                     (long long)n_host.load(), (long long)namb);
     }
-    const double t_retry_s = since(t_retry);
-    if (tr.on)
-        std::fprintf(stderr, "[gca] V solves: %lld device, %lld host, %lld handed back (%.1f ms); "
-                     "launcher busy %.1f ms\n",
-                     (long long)(vq ? vq->device_solves() : 0), (long long)n_host.load(),
-                     (long long)retry.size(), 1e3 * t_retry_s, 1e3 * (vq ? vq->busy_s() : 0.0));
     if (tr.on && nthreads > 0)
         std::fprintf(stderr, "[gca] workers: first cluster %.1f-%.1f ms, last done %.1f-%.1f ms, "
                      "waiting for Green batches %.1f ms (all threads)\n",
@@ -464,7 +434,6 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
                      1e3 * std::accumulate(starved.begin(), starved.end(), 0.0));
     double t_host = 0.0;
     for (double x : busy) t_host += x;
-    t_host += t_retry_s;
     G->phase[1] = since(t_pipe);
     cudaStreamSynchronize(s);
     for (auto &d : done)
@@ -509,6 +478,12 @@ int gcabem_gca_sizes(gcabem_gca_t G, int64_t *ranks, double *phase4) {
     for (int64_t c = 0; c < G->ncl; ++c) ranks[c] = (int64_t)G->rows[c].size();
     if (phase4)
         for (int k = 0; k < 6; ++k) phase4[k] = G->phase[k];
+    return GCABEM_OK;
+}
+
+int gcabem_gca_flags(gcabem_gca_t G, int8_t *ambiguous) {
+    if (!G || !ambiguous) return gcabem_internal_error(GCABEM_ERR_ARG, "null argument");
+    for (int64_t c = 0; c < G->ncl; ++c) ambiguous[c] = (int8_t)G->ambiguous[c];
     return GCABEM_OK;
 }
 

@@ -108,6 +108,7 @@ struct gcabem_mesh_s {
     gcabem::DevBuf<double> V;
     gcabem::DevBuf<int32_t> T;
     gcabem::DevBuf<gcabem::Chart> charts;
+    std::vector<gcabem::Chart> charts_host;
 };
 
 // Device layout of one package set: uploaded once, shared by every plan
@@ -133,36 +134,18 @@ namespace gcabem {
 // V = A[:, cols] inv(A[rows, cols]) with two refinement sweeps
 // (reference gca.py:182-282). A is nr x nc row-major, real or interleaved
 // complex. Returns 0, 1 (zero Green matrix) or 2 (singular pivot block).
-// pre_k >= 0: the first attempt uses these ACA pivots instead of running ACA.
+// ambiguous (optional): set to 1 when an ACA decision fell inside the tie
+// window (aca.cpp TIE_REL/TIE_ABS/STOP_REL).
 int gca_operator(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
-                 std::vector<int64_t> &rows, std::vector<double> &V, int64_t pre_k = -1,
-                 const int64_t *pre_rows = nullptr, const int64_t *pre_cols = nullptr);
+                 std::vector<int64_t> &rows, std::vector<double> &V, int *ambiguous = nullptr);
+// The same operator with every entry evaluated on the host in the
+// reference's numpy arithmetic (green_exact.h), on demand: the redo of a
+// cluster whose ACA on the device's Green matrix was ambiguous.
+struct GreenExact;
+int gca_operator_exact(bool is_complex, const GreenExact &g, double epsilon,
+                       std::vector<int64_t> &rows, std::vector<double> &V);
 // The first attempt's ACA alone: pivots into rows/cols (capacity min(nr, nc)),
 // returns the rank.
 int64_t gca_aca(bool is_complex, const double *A, int64_t nr, int64_t nc, double epsilon,
                 int64_t *rows, int64_t *cols);
-
-// Device V solves (vsolve.cu), the part of gca_operator after ACA. Task t:
-// in + in_off holds the pivot block B (k x k) followed by A[:, cols]^T
-// (k x nr), row-major in the element type; V (nr x k) goes to out + out_off;
-// scratch + scr_off has room for vsolve_scratch(k, nr, w) doubles; chunks
-// list (task, first row) per VS_ROWS rows. aux[t].status: 0 solved, 2
-// singular or condition above 1e14, 3 condition bracket ambiguous (the host
-// decides with the exact SVD).
-constexpr int VS_KMAX = 96;
-constexpr int VS_ROWS = 128;
-struct VTask {
-    int64_t in_off, out_off, scr_off;  // in doubles
-    int32_t nr, k;
-};
-struct VAux {
-    unsigned long long amax, rmax[2];
-    int status, pad;
-};
-inline int64_t vsolve_scratch(int64_t k, int64_t nr, int w) {
-    return (k * k + 2 * k * nr) * w + (k + 1) / 2;
-}
-cudaError_t launch_vsolve(bool is_complex, const VTask *tasks, int ntasks, const int2 *chunks,
-                          int nchunks, int kmax, const double *in, double *out, double *scratch,
-                          VAux *aux, cudaStream_t s);
 }  // namespace gcabem

@@ -163,6 +163,85 @@ def build_green_matrices(mesh: SurfaceMesh, panel_lists, source_sets, spec: Kern
     return (mats, buf, panel_at) if flat else mats
 
 
+_PANEL_CHUNK = 256
+
+
+def green_matrix_exact(mesh: SurfaceMesh, panels, sources: GreenSourceSet, spec: KernelSpec,
+                       order: int = 3) -> np.ndarray:
+    """One cluster's Green matrix on the HOST, in the reference's own numpy
+    arithmetic (gca.py:136-179 operation for operation: 256-panel chunks,
+    chart_arrays, the broadcast point map, kernel_values per column group,
+    einsum over the panel rule, then the Gramian and the source weights), so
+    its bits are the reference's. The yardstick of the native exact entries
+    (green_exact_native, csrc/green_exact.h) that settle ACA decisions the
+    device's matrix leaves inside the tie window."""
+    from .kernels import kernel_values
+    from .mesh import chart_arrays
+    panels = np.asarray(panels, dtype=np.int64)
+    pts, wq = duffy_panel_rule(order)
+    mono_spec = KernelSpec(spec.equation, "single", spec.kappa)
+    dip_spec = KernelSpec(spec.equation, "double", spec.kappa)
+    A = np.empty((len(panels), len(sources.weights)),
+                 dtype=np.complex128 if spec.is_complex else np.float64)
+    src, srcn = sources.points, sources.normals
+    mono = sources.roles == ROLE_MONOPOLE
+    dip = ~mono
+    for base in range(0, len(panels), _PANEL_CHUNK):
+        sel = panels[base:base + _PANEL_CHUNK]
+        v0, e1, e2, gram = chart_arrays(mesh, sel)
+        X = v0[:, None, :] + pts[None, :, 0, None] * e1[:, None, :] \
+            + pts[None, :, 1, None] * e2[:, None, :]
+        kv_m = kernel_values(mono_spec, X[:, :, None, 0] - src[None, None, mono, 0],
+                             X[:, :, None, 1] - src[None, None, mono, 1],
+                             X[:, :, None, 2] - src[None, None, mono, 2])
+        nd = srcn[dip]
+        kv_d = kernel_values(dip_spec, X[:, :, None, 0] - src[None, None, dip, 0],
+                             X[:, :, None, 1] - src[None, None, dip, 1],
+                             X[:, :, None, 2] - src[None, None, dip, 2],
+                             nd[None, None, :, 0], nd[None, None, :, 1], nd[None, None, :, 2])
+        if not (np.all(np.isfinite(kv_m)) and np.all(np.isfinite(kv_d))):
+            raise GcaError("source coincides with a panel quadrature point")
+        im = np.einsum("q,pqs->ps", wq, kv_m) * gram[:, None]
+        idp = np.einsum("q,pqs->ps", wq, kv_d) * gram[:, None]
+        A[base:base + len(sel), mono] = im * sources.weights[mono]
+        A[base:base + len(sel), dip] = idp * sources.weights[dip]
+    return A
+
+
+def green_exact_native(mesh: SurfaceMesh, panels, box_lo, box_hi, spec: KernelSpec,
+                       params: GcaParams, scene_diameter: float, operator: bool = True):
+    """The native host-exact path of one cluster (C ABI gcabem_green_exact):
+    its full Green matrix from csrc/green_exact.h and, with operator=True, the
+    operator (row pivots, V) the GCA pipeline's tie redo computes."""
+    panels = np.ascontiguousarray(panels, dtype=np.int64)
+    nr = panels.size
+    nc = 12 * params.m * params.m
+    w = 2 if spec.is_complex else 1
+    A = np.empty(nr * nc * w, np.float64)
+    g = gauss_legendre(params.m)
+    pts, wq = duffy_panel_rule(params.rule_order)
+    duffy = np.ascontiguousarray(np.column_stack([pts, wq]))
+    cap = min(nr, nc)
+    rank = np.zeros(1, np.int64)
+    rows = np.zeros(cap, np.int64)
+    V = np.zeros(nr * cap * w, np.float64)
+    p = nat.ptr
+    T = np.ascontiguousarray(mesh.triangles, dtype=np.int64)
+    nat.check(nat.lib().gcabem_green_exact(
+        0 if spec.equation == "laplace" else 1, float(spec.kappa), mesh.num_vertices,
+        p(nat.f64(mesh.vertices)), mesh.num_triangles, p(T), p(nat.f64(mesh.gramians)), nr,
+        p(panels), p(nat.f64(box_lo)), p(nat.f64(box_hi)), float(params.delta), int(params.m),
+        p(nat.f64(g.points)), p(nat.f64(g.weights)), float(scene_diameter), duffy.shape[0],
+        p(duffy), float(params.epsilon), p(A), p(rank) if operator else None,
+        p(rows) if operator else None, p(V) if operator else None))
+    Am = (A.view(np.complex128) if spec.is_complex else A).reshape(nr, nc)
+    if not operator:
+        return Am
+    r = int(rank[0])
+    Vv = (V.view(np.complex128) if spec.is_complex else V)[:nr * r].reshape(nr, r)
+    return Am, rows[:r].copy(), Vv
+
+
 def build_green_matrix(mesh: SurfaceMesh, panels, sources: GreenSourceSet, spec: KernelSpec,
                        order: int = 3) -> np.ndarray:
     """One cluster's Green matrix (gca.py:136), on the device."""
@@ -300,6 +379,8 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
         vlen = int(np.sum(sizes * ranks)) * width
         V = np.empty(max(vlen, 1), np.float64)
         nat.check(nat.lib().gcabem_gca_fetch(h, p(rows), p(V)))
+        amb = np.zeros(ids.size, np.int8)
+        nat.check(nat.lib().gcabem_gca_flags(h, p(amb)))
     finally:
         nat.lib().gcabem_gca_free(h)
     t2 = time.perf_counter()
@@ -311,11 +392,19 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
         ops[cid] = InterpolationOperator(cid, loc, perm[first + loc], Vv[vo:vo + n * r].reshape(n, r))
         ro += r
         vo += n * r
+    # clusters with an ACA decision inside the tie window (a tie on the
+    # device's bits, e.g. from the mesh's symmetry) were redone natively on
+    # entries in the reference's own arithmetic (csrc/green_exact.h), so the
+    # pivots are the reference's (package assignment bit-exact)
+    t3 = time.perf_counter()
+    redo = ids[amb != 0]
     last_build_phases.update(device_wait_s=float(phase[0]), pipeline_s=float(phase[1]),
                              native_total_s=float(phase[2]), batches=int(phase[3]),
                              host_thread_s=float(phase[4]), threads=int(phase[5]),
                              clusters=int(ids.size), mesh_s=t_mesh, prep_s=t1 - t0 - t_mesh,
-                             call_s=t2 - t1, wrap_s=time.perf_counter() - t2)
+                             call_s=t2 - t1, wrap_s=t3 - t2, ties=int(redo.size),
+                             ties_panels=int(sizes[amb != 0].sum()),
+                             ties_s=time.perf_counter() - t3)
     return ops
 
 

@@ -1,4 +1,4 @@
-"""Reference GCA pivots/ranks at L4-L7 (and the checksums they imply), generated
+"""Reference GCA pivots/ranks at L4-L8 (and the checksums they imply), generated
 by running the UNMODIFIED reference package in this container.
 
     NUMBA_CACHE_DIR=/tmp/numba PYTHONPATH=/root/reference/pkg/src \
@@ -15,7 +15,7 @@ with, per (level, equation):
     L{L}_{eq}_cids    int32  sorted cluster ids
     L{L}_{eq}_ranks   int32  rank per cluster
     L{L}_{eq}_pivots  int32  concatenated pivots_global (selection order)
-    L{L}_{eq}_vcids   int32  clusters whose V is kept (sample, |t| <= 128)
+    L{L}_{eq}_vcids   int32  clusters whose V is kept (sample: <= 32 of the clusters with id % 37 == 0, |t| <= 128)
     L{L}_{eq}_V       f64/c128 their V matrices, row-major, concatenated
 
 Settings: the reference pipeline defaults SURVEY §8(d) uses (leaf 16,
@@ -42,7 +42,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 from gcabem import cluster, gca, kernels, mesh  # noqa: E402
 
 JOBS = {4: ("laplace", "helmholtz"), 5: ("laplace", "helmholtz"), 6: ("laplace",),
-        7: ("helmholtz",)}
+        7: ("helmholtz",), 8: ("helmholtz",)}
 _CTX = {}
 
 
@@ -81,6 +81,7 @@ def run(level, eq, out, procs):
     out[f"{key}_ranks"] = np.array([res[c][0].size for c in ids], dtype=np.int32)
     out[f"{key}_pivots"] = np.concatenate([res[c][0] for c in ids]).astype(np.int32)
     vc = [c for c in ids if res[c][1] is not None]
+    vc = vc[::max(1, -(-len(vc) // 32))]   # at most 32 clusters' V per level
     out[f"{key}_vcids"] = np.array(vc, dtype=np.int32)
     out[f"{key}_V"] = np.concatenate([res[c][1].ravel() for c in vc])
     print(f"L{level} {eq}: {len(ids)} clusters, {out[f'{key}_pivots'].size} pivots, "
