@@ -1,30 +1,39 @@
 #!/usr/bin/env python
 """Benchmark: FP64 BEM setup hot path on B200 (metric of BASELINE.json).
 
-Workload (BASELINE.json configs[1], "C2"): Laplace SLP + DLP full GCA
-H2-matrix setup of the unit sphere with 32,768 triangles (octahedral
-level 6), quadrature orders 4 (disjoint) / 5 (singular), leaf 16,
-eta 2.0, GCA delta 1, m 6, eps 1e-4, Green rule order 3, 8 MiB lists.
+Workload (default, BASELINE.json configs[2], "C3" -- the config north_star's
+target is quoted on; it fits one GPU): Helmholtz kappa=4 SLP + DLP full H2
+setup of the unit sphere with 131,072 triangles (octahedral level 7),
+quadrature orders 3 (disjoint) / 5 (singular), leaf 16, eta 2.0, GCA delta 1,
+m 6, eps 1e-4, Green rule order 3, 8 MiB lists. --config c2 (L6 Laplace 4/5),
+c5 (L8, --order n) and c4 (P1 crankshaft) are the other configs.
 
-* value      pair-integrals/s of the device hot path with all inputs resident
-             in HBM: one step = every disjoint-rule pair (near field + GCA
-             coupling blocks) and every singular corrective pair of BOTH
-             operators, written into the device payload. Kernel time from CUDA
-             events recorded on the launching stream; L2 flushed between steps.
-* e2e        the same metric through the public API scheduler.run_assembly
-             (host packaging, H2D of the packages, kernels, D2H of all
-             payloads into pinned host memory), wall clock with syncs.
+* value      pair integrals/s of the device hot path with all inputs resident
+             in HBM: one step = every payload entry of BOTH operators (each is
+             one pair integral: the disjoint rule, or the singular rule for a
+             pair sharing a vertex), near field + GCA coupling blocks. Kernel
+             time from CUDA events on the launching stream; L2 flushed
+             between steps.
+* e2e        the same metric through the public API scheduler.run_assembly_pair
+             (host packaging, H2D of the packages, kernels, D2H of all payloads
+             into pinned host memory), wall clock with syncs.
 * roofline   dominant kernel (disjoint pair quadrature) against the measured
              FP64 DFMA peak of the device (no FP64 figure exists in
              MEASURED_PEAKS.json; the probe runs in this process).
+* h2_setup   trees + GCA operators + both assemblies, seconds.
 * cpu_baseline  the bit-exact C oracle (oracle/, kind "port") with OpenMP on
              the host cores, on a deterministic sample of the same packages.
 
-`--impl reference` times only that CPU port (the reference's own algorithm,
-pinned bit-for-bit) on the same workload and prints its line.
-Multi-GPU (torchrun): weak scaling — every rank assembles its own operator
-pair (independent objects, no exchange); --mode strong shards one job's
-leaves across ranks instead.
+`--impl reference` runs the reference's setup path restated in oracle/ on the
+host cores without the product (no libgcabem_b200.so, no GPU): trees in full,
+the GCA on a sample of clusters, the packaging in full, the assembly sampled
+per step; it prints the same metric plus its h2_setup seconds.
+
+Multi-GPU (torchrun, N ranks): by default ONE job split over the ranks
+(--mode strong): each rank builds its part of the GCA clusters, the pivots
+are all-gathered (the only exchange), and each rank packages and assembles
+its leaf window on its GPU. --mode weak: every rank its own job. Without
+torchrun, --gpus N splits the job over N devices of one process.
 """
 from __future__ import annotations
 
@@ -72,7 +81,7 @@ UNIT = "pair-integrals/s"
 # distributed plumbing (one process per GPU, torch.distributed for barrier/max)
 
 class Dist:
-    def __init__(self):
+    def __init__(self, cpu_only: bool = False):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -84,7 +93,8 @@ class Dist:
             # NCCL needs one GPU per rank; fewer GPUs than ranks (a smoke test
             # of the launch on one device) falls back to gloo for the barrier
             # and the max -- neither is on the data path
-            ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+            ngpu = 0 if cpu_only else \
+                (torch.cuda.device_count() if torch.cuda.is_available() else 0)
             backend = "nccl" if ngpu >= self.world else "gloo"
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
@@ -95,13 +105,17 @@ class Dist:
         if self.world > 1:
             self.dist.barrier()
 
-    def max(self, x: float) -> float:
-        if self.world == 1:
-            return x
+    def _reduce(self, x: float, op) -> float:
         t = self.torch.tensor([x], dtype=self.torch.float64,
                               device="cuda" if self.backend == "nccl" else "cpu")
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        self.dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max(self, x: float) -> float:
+        return x if self.world == 1 else self._reduce(x, self.dist.ReduceOp.MAX)
+
+    def sum(self, x):
+        return x if self.world == 1 else type(x)(self._reduce(x, self.dist.ReduceOp.SUM))
 
     def close(self):
         if self.world > 1:
@@ -167,8 +181,11 @@ def l2_flush(buf):
 
 # ---------------------------------------------------------------------------
 
-def build_workload(cfg, device, log):
-    from paper_1510_07244_b200 import cluster, gca, kernels, mesh, packaging, scheduler
+def build_workload(cfg, devices, shard, log, warm_gca=True):
+    """Mesh, trees and GCA operators of the config (the setup before
+    packaging). `shard` = (rank, world): this process builds its part of the
+    GCA clusters and the pivots are all-gathered (gca.exchange_pivots)."""
+    from paper_1510_07244_b200 import cluster, gca, kernels, mesh
     t = {}
     t0 = time.perf_counter()
     m = mesh.build_sphere_mesh(cfg["level"])
@@ -183,25 +200,23 @@ def build_workload(cfg, device, log):
         ops = {}
         t["gca_s"] = 0.0
     else:
+        spec = kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"])
+        dev = tuple(devices) if len(devices) > 1 else devices[0]
         t1 = time.perf_counter()
-        ops, _ = gca.build_interpolation_operators(
-            m, bt, kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"]), gca.GcaParams(),
-            device=device)
+        ops, _ = gca.build_interpolation_operators(m, bt, spec, gca.GcaParams(), device=dev,
+                                                   shard=shard)
         t["gca_s"] = time.perf_counter() - t1
         t["gca_phases"] = dict(gca.last_build_phases)
-        # the same build again: the first call of a process also pays its
-        # pinned staging, pack buffers and worker buffers (kept for later calls)
-        t1 = time.perf_counter()
-        gca.build_interpolation_operators(
-            m, bt, kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"]), gca.GcaParams(),
-            device=device)
-        t["gca_warm_s"] = time.perf_counter() - t1
-    t2 = time.perf_counter()
-    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
-    t["packaging_s"] = time.perf_counter() - t2
-    log(f"workload: nt={m.num_triangles} leaves={pk.leaf_ids.size} blocks={pk.num_blocks} "
-        f"pairs={pk.block_pairs()} singular={pk.num_items} clusters={len(ops)} {t}")
-    return m, bt, ops, pk, t
+        if warm_gca:
+            # the same build again: the first call of a process also pays its
+            # pinned staging and worker buffers (kept for later calls)
+            t1 = time.perf_counter()
+            gca.build_interpolation_operators(m, bt, spec, gca.GcaParams(), device=dev,
+                                              shard=shard)
+            t["gca_warm_s"] = time.perf_counter() - t1
+    log(f"workload: nt={m.num_triangles} leaves={len(bt.leaves)} clusters={len(ops)} "
+        f"{ {k: v for k, v in t.items() if k != 'gca_phases'} }")
+    return m, bt, ops, t
 
 
 def cpu_sample(pk, m, cfg, target_s, nthreads, log):
@@ -251,12 +266,12 @@ def cpu_sample(pk, m, cfg, target_s, nthreads, log):
                                         its[sel, 2], pms[sel, :3].astype(np.int64),
                                         pms[sel, 3:].astype(np.int64),
                                         *oracle.rule(case, cfg["orders"][1]), nthreads=nthreads)
-                pairs += int(np.count_nonzero(sel))
+                # counted above: a corrective item overwrites an entry of a sampled block
     dt = time.perf_counter() - t0
     desc = (f"every {stride}-th disjoint block ({tx.size} pairs) and singular item "
             f"({len(its)}) of the workload packages, {'+'.join(cfg['layers'])} layers")
     log(f"cpu sample: {pairs} pair integrals in {dt:.2f} s on {nthreads} threads ({desc})")
-    return pairs, dt, desc
+    return pairs, dt, desc, stride
 
 
 def host_threads() -> int:
@@ -267,46 +282,104 @@ def host_threads() -> int:
 
 
 def run_reference(args, cfg, dist, log):
-    """--impl reference: the reference algorithm (bit-exact C port) on the
-    host cores; rank 0 only."""
+    """--impl reference: the reference's CPU setup path restated in oracle/
+    (the reference is Python + numba: nothing to compile into oracle/_ref),
+    on the host cores, rank 0 only, WITHOUT the product (no
+    libgcabem_b200.so, no GPU): the sphere and both trees in full
+    (oracle.setup_cpu restating mesh.py / cluster.py), the GCA on a
+    deterministic sample of clusters (every k-th, green matrix + ACA + pivot
+    solve restating gca.py, one worker process per core; the pivots of the
+    sample are checked against the reference's own), the packaging in full
+    (scheduler.py restated) on the reference's pivots
+    (tests/golden/gca_levels.npz, produced by running the reference), and
+    each timed step a sample of the assembly (bit-exact C restatement of
+    pairquad.py with OpenMP on all cores). Sampled phases are extrapolated
+    by panel count / pair count and labelled."""
     if dist.rank != 0:
         return None
     if cfg.get("p1"):
         return {"impl": "reference", "unavailable": "the reference assembles P0 only (P1 exists "
                 "per pair via integrate_pair bases, no matrix assembly)"}
     import oracle
+    from oracle import setup_cpu as sc
     oracle.build()
     nth = host_threads()
-    from paper_1510_07244_b200 import cluster, mesh, packaging, scheduler
-    # GCA pivots come from the device in our arm; the CPU arm needs the same
-    # packages without a GPU dependency, so it uses the near-field + coupling
-    # structure produced by the oracle-side Green matrices only when a device
-    # is absent. Simplest faithful choice: build packages with our host code
-    # (bit-exact with the reference's packaging) and device GCA if available.
-    try:
-        m, bt, ops, pk, _ = build_workload(cfg, 0, log)
-    except Exception as exc:  # no device: near field only, stated in the line
-        log(f"reference arm: device GCA unavailable ({exc}); near-field packages only")
-        m = mesh.build_sphere_mesh(cfg["level"])
-        t = cluster.build_cluster_tree(m, 16)
-        bt = cluster.build_block_tree(t, t, 2.0)
-        bt = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
-        pk = packaging.make_packages(m.triangles, bt, {}, {}, scheduler.DEFAULT_MAXSIZE)
-    vals = []
+    t0 = time.perf_counter()
+    m = sc.sphere_mesh(cfg["level"])
+    mesh_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tree = sc.build_cluster_tree(m, 16)
+    bt = sc.build_block_tree(tree, tree, 2.0)
+    trees_s = time.perf_counter() - t0
+    log(f"reference: mesh {mesh_s:.2f} s, trees {trees_s:.2f} s, {len(bt.leaves)} leaves")
+    setup = {"mesh_s (input, not counted)": round(mesh_s, 3), "trees_s": round(trees_s, 3)}
+    if cfg["near_only"]:
+        bt = sc.BlockTree(bt.nodes, tree, tree, bt.eta,
+                          [l for l in bt.leaves if l.kind == "dense"])
+        ops = {}
+        gca_s = 0.0
+    else:
+        cids = sc.admissible_clusters(bt)
+        g = np.load(os.path.join(ROOT, "tests", "golden", "gca_levels.npz"))
+        key = f"L{cfg['level']}_{cfg['equation']}"
+        # calibrate on a few clusters, then a sample of about gca_seconds
+        probe = cids[::max(1, len(cids) // 64)][:64]
+        tc = time.perf_counter()
+        sc.build_operators(m, tree, probe, cfg["equation"], cfg["kappa"], workers=nth)
+        rate = sum(tree.nodes[c].size for c in probe) / max(time.perf_counter() - tc, 1e-6)
+        total_panels = sum(tree.nodes[c].size for c in cids)
+        gstride = max(1, int(np.ceil(total_panels / (rate * args.gca_seconds))))
+        sample = cids[::gstride]
+        tc = time.perf_counter()
+        sops = sc.build_operators(m, tree, sample, cfg["equation"], cfg["kappa"], workers=nth)
+        gdt = time.perf_counter() - tc
+        gca_s = gdt * total_panels / sum(tree.nodes[c].size for c in sample)
+        if f"{key}_cids" in g.files:
+            ops = sc.pivot_operators(g[f"{key}_cids"], g[f"{key}_ranks"], g[f"{key}_pivots"])
+            pivots_from = "the reference's own (tests/golden/gca_levels.npz)"
+        else:   # no fixture: the restatement builds every cluster
+            ops = sc.build_operators(m, tree, cids, cfg["equation"], cfg["kappa"], workers=nth)
+            pivots_from = "oracle restatement, every cluster"
+        match = sum(np.array_equal(sops[c].pivots_global, ops[c].pivots_global) for c in sample)
+        setup.update({
+            "gca_s": round(gca_s, 3),
+            "gca_sample": f"every {gstride}-th of {len(cids)} clusters ({len(sample)}, "
+                          f"{gdt:.2f} s on {nth} processes), extrapolated by panel count",
+            "gca_sample_pivots_equal_reference": f"{match}/{len(sample)}",
+            "packaging_pivots": pivots_from})
+        log(f"reference GCA: {setup['gca_sample']} -> {gca_s:.1f} s; pivots {match}/{len(sample)}")
+    t0 = time.perf_counter()
+    pk = sc.make_packages(m.triangles, bt, ops, ops, 8 << 20)
+    pack_s = time.perf_counter() - t0
+    log(f"reference packaging {pack_s:.2f} s: {pk.block_pairs()} entries, {pk.num_items} items")
+    vals, asm = [], []
     desc = ""
     for _ in range(args.warmup + args.steps):
-        pairs, dt, desc = cpu_sample(pk, m, cfg, args.cpu_seconds / max(args.steps, 1), nth, log)
+        pairs, dt, desc, stride = cpu_sample(pk, m, cfg, args.cpu_seconds / max(args.steps, 1),
+                                             nth, log)
         vals.append(pairs / dt)
+        asm.append(dt * stride)
     v = statistics.median(vals[args.warmup:]) if len(vals) > args.warmup else vals[-1]
+    asm_s = statistics.median(asm[args.warmup:]) if len(asm) > args.warmup else asm[-1]
+    setup.update({"packaging_s": round(pack_s, 3),
+                  "assembly_slp_dlp_s": round(asm_s, 3),
+                  "assembly_sample": "each step's sampled blocks/items x the stride",
+                  "total_s": round(trees_s + gca_s + pack_s + asm_s, 3)})
     return {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.mode, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic octahedral sphere)",
-        "config": {"workload": cfg["workload"]},
+        "config": {"workload": cfg["workload"], "pairs_per_step": int(pk.block_pairs()) *
+                   len(cfg["layers"]),
+                   "same_config": True},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": nth, "kind": "port",
                          "sample": desc},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "h2_setup": setup,
+        "native_libraries": ["oracle/liboracle.so"],
+        "path": "oracle/ (C restatement of pairquad.py, numpy restatements of mesh, cluster, "
+                "gca and scheduler packaging); the product package is not imported",
     }
 
 
@@ -405,91 +478,126 @@ def run_ours_p1(args, cfg, dist, log):
 
 
 def run_ours(args, cfg, dist, log):
+    """The device path. Under torchrun (N ranks) the default is ONE job split
+    over the ranks (--mode strong): each rank builds its part of the GCA
+    clusters (pivots all-gathered: the only exchange), packages its leaf
+    window (scheduler.shard_window) and assembles it on its GPU. Without
+    torchrun, --gpus N splits the job over N devices of this process."""
     import torch
 
     from paper_1510_07244_b200 import device as devmod
-    from paper_1510_07244_b200 import kernels, scheduler
+    from paper_1510_07244_b200 import kernels, packaging, scheduler
     from paper_1510_07244_b200._native import require_device
 
-    device = dist.local % max(torch.cuda.device_count(), 1)
-    require_device(device)
-    torch.cuda.set_device(device)
-    info = devmod.device_info(device)
-    m, bt, ops, pk, setup_t = build_workload(cfg, device, log)
+    ndev = max(torch.cuda.device_count(), 1)
+    if dist.world > 1:
+        devices = [dist.local % ndev]
+    else:
+        if args.gpus > ndev:
+            raise SystemExit(f"--gpus {args.gpus}: only {ndev} devices visible")
+        devices = list(range(args.gpus))
+    for d in devices:
+        require_device(d)
+    torch.cuda.set_device(devices[0])
+    info = devmod.device_info(devices[0])
+    strong = args.mode == "strong"
+    shard = (dist.rank, dist.world) if (strong and dist.world > 1) else None
+    m, bt, ops, setup_t = build_workload(cfg, devices, shard, log)
     specs = [kernels.KernelSpec(cfg["equation"], layer, cfg["kappa"]) for layer in cfg["layers"]]
-    dm = devmod.device_mesh(m, device)
-    shard = None
-    if args.mode == "strong" and dist.world > 1:
-        from paper_1510_07244_b200.packaging import shard_leaves
-        from paper_1510_07244_b200.quadrature import build_rule
-        shard = shard_leaves(pk, dist.world, cfg["orders"][0] ** 4,
-                             [build_rule(c, cfg["orders"][1]).num_points
-                              for c in ("vertex", "edge", "identical")])[dist.rank]
     fused = len(specs) == 2 and {s.layer for s in specs} == {"single", "double"} and \
         not args.separate
-    tp = time.perf_counter()
-    sep_plans = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], shard) for s in specs]
-    pair_plan = scheduler.AssemblyPlan(dm, specs[0], pk, cfg["orders"], shard, pair=True) \
-        if fused else None
-    plan_s = time.perf_counter() - tp
-    # pair integrals per step: both operators' pairs (block pairs + corrective items)
-    pairs_step = sum(p.disjoint_pairs + sum(p.singular_counts) for p in sep_plans)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
-    stream = torch.cuda.Stream(device=device)
-    for p in sep_plans + ([pair_plan] if pair_plan else []):
-        p.set_stream(stream.cuda_stream)  # one timeline on one stream
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    # this process's leaves: its window of the job (strong) or everything
+    t2 = time.perf_counter()
+    window = scheduler.shard_window(m, bt, ops, ops, shard, cfg["orders"][0] ** 4) \
+        if shard else None
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE,
+                                 leaf_range=window)
+    setup_t["packaging_s"] = time.perf_counter() - t2
+    L = pk.leaf_ids.size
+    sq = [scheduler.build_rule(c, cfg["orders"][1]).num_points
+          for c in ("vertex", "edge", "identical")]
+    dev_ranges = scheduler._split_range(pk, (0, L), len(devices), cfg["orders"][0] ** 4, sq)
+    log(f"rank {dist.rank}: window {window} leaves={L} entries={pk.payload_len} "
+        f"blocks={pk.num_blocks} singular={pk.num_items} devices={devices} {dev_ranges}")
 
-    def time_plans(plans, steps, warmup, clk_sampler=None):
+    tp = time.perf_counter()
+    per_dev = []   # (device, stream, flush buffer, [plans], [separate plans])
+    for d, rng in zip(devices, dev_ranges):
+        dm = devmod.device_mesh(m, d)
+        sep = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], rng) for s in specs]
+        main = [scheduler.AssemblyPlan(dm, specs[0], pk, cfg["orders"], rng, pair=True)] \
+            if fused else sep
+        st = torch.cuda.Stream(device=d)
+        for p in sep + main:
+            p.set_stream(st.cuda_stream)   # one timeline per device
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{d}")
+        per_dev.append((d, st, flush, main, sep))
+    plan_s = time.perf_counter() - tp
+    # pair integrals per step: every payload entry of every operator is one
+    # evaluated pair integral (the disjoint launch skips the entries of
+    # pairs sharing a vertex, the singular pass computes exactly those)
+    entries = sum(p.payload_len for dv in per_dev for p in dv[4][:1])
+    pairs_local = entries * len(specs)
+    pairs_job = dist.sum(pairs_local) if shard else pairs_local * (dist.world if not strong
+                                                                   else 1)
+
+    def time_plans(which, steps, warmup):
+        evs = {d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for d, *_ in per_dev}
+
         def step():
-            with torch.cuda.stream(stream):
-                l2_flush(flush)
-                ev0.record(stream)
-                for p in plans:
-                    p.execute()
-                ev1.record(stream)
-            stream.synchronize()
-            return ev0.elapsed_time(ev1), [p.timing_ms() for p in plans]
+            for d, st, flush, main, sep in per_dev:
+                with torch.cuda.device(d), torch.cuda.stream(st):
+                    l2_flush(flush)
+                    evs[d][0].record(st)
+                    for p in (main if which == "main" else sep):
+                        p.execute()
+                    evs[d][1].record(st)
+            for d, st, *_ in per_dev:
+                st.synchronize()
+            t = max(evs[d][0].elapsed_time(evs[d][1]) for d, *_ in per_dev)
+            # disjoint-launch ms of each plan on the first device (the roofline's kernel)
+            main, sep = per_dev[0][3], per_dev[0][4]
+            return t, [p.timing_ms()["disjoint"] for p in (main if which == "main" else sep)]
         for _ in range(warmup):
             step()
         dist.barrier()
-        torch.cuda.synchronize(device)
-        per, dis = [], []
+        for d, *_ in per_dev:
+            torch.cuda.synchronize(d)
+        per, dk = [], []
         w0 = time.perf_counter()
         for _ in range(steps):
-            total, tm = step()
-            per.append(total)
-            dis.append([t["disjoint"] for t in tm])
-        torch.cuda.synchronize(device)
+            t, k = step()
+            per.append(t)
+            dk.append(k)
+        for d, *_ in per_dev:
+            torch.cuda.synchronize(d)
         wall_ = time.perf_counter() - w0
         dist.barrier()
-        return statistics.mean(per), np.mean(np.array(dis), axis=0), wall_
+        return statistics.mean(per), np.mean(np.array(dk), axis=0), wall_
 
-    peak = devmod.fp64_peak_tflops(device)
-    main_plans = [pair_plan] if fused else sep_plans
-    with ClockSampler(device) as clk:
-        ms, dk, wall = time_plans(main_plans, args.steps, args.warmup)
+    peak = devmod.fp64_peak_tflops(devices[0])
+    with ClockSampler(devices[0]) as clk:
+        ms, dk, wall = time_plans("main", args.steps, args.warmup)
     ms_max = dist.max(ms)
-    # weak: every rank did pairs_step; strong: the ranks split one job
-    total_pairs = pairs_step * dist.world if args.mode == "weak" else \
-        pk_total_pairs(pk, len(sep_plans))
-    value = total_pairs / (ms_max * 1e-3)
+    value = pairs_job / (ms_max * 1e-3)
+    single_device = dist.world == 1 and len(devices) == 1
     separate = None
-    if fused:  # the same workload as two single-layer plans, for reference
-        ms_sep, dk_sep, _ = time_plans(sep_plans, args.steps, 3)
-        ms_sep = dist.max(ms_sep)
-        fl_sep = [p.flops() for p in sep_plans]
+    if fused and single_device:  # the same workload as two single-layer plans
+        ms_sep, dk_sep, _ = time_plans("sep", args.steps, 3)
+        fl_sep = [p.flops() for p in per_dev[0][4]]
         kd = int(np.argmax(dk_sep))
-        separate = {"value": total_pairs / (ms_sep * 1e-3), "ms_per_step": ms_sep,
+        separate = {"value": pairs_job / (ms_sep * 1e-3), "ms_per_step": ms_sep,
                     "dominant_kernel": f"disjoint_kernel<{cfg['orders'][0]},{specs[kd].layer}>",
                     "dominant_frac": fl_sep[kd]["disjoint"] / (dk_sep[kd] * 1e-3) / 1e12 / peak}
 
-    # roofline of the dominant kernel: the disjoint quadrature launch
-    fl = [p.flops() for p in main_plans]
+    # roofline of the dominant kernel (the disjoint quadrature launch) on the
+    # first device of this process: its algorithmic flops / its event time
+    main0 = per_dev[0][3]
+    fl = [p.flops() for p in main0]
     k_dom = int(np.argmax(dk))
     achieved = fl[k_dom]["disjoint"] / (dk[k_dom] * 1e-3) / 1e12
-    share = float(np.sum(dk) / ms)
+    share = float(np.sum(dk) / ms)   # of the step on the first device
     dom_name = "pair" if fused else specs[k_dom].layer
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -498,34 +606,37 @@ def run_ours(args, cfg, dist, log):
             traffic = json.load(open(prof)).get(f"{args.config}/{dom_name}")
         except (OSError, ValueError):
             traffic = None
+    h2d = sum(p.h2d_bytes for dv in per_dev for p in dv[3])
+    launches = args.steps * sum(1 + sum(1 for c in p.singular_counts if c)
+                                for dv in per_dev for p in dv[3])
+    for dv in per_dev:
+        for p in dv[3] + dv[4]:
+            p.close()
+    del per_dev, pk
 
-    # e2e through the public API, host buffers, H2D + D2H inside
-    e2e_t = []
-    params = scheduler.SchedulerParams(backends=(scheduler.Backend("cuda", devices=(device,)),))
-    plans = sep_plans
-    h2d = sum(p.h2d_bytes for p in main_plans)
-    d2h = sum(p.payload_len * 16 for p in sep_plans)
+    # e2e through the public API, host buffers, H2D + D2H inside the step
+    backend = scheduler.Backend("cuda", devices=tuple(devices))
+    params = scheduler.SchedulerParams(backends=(backend,), shard=shard)
+    e2e_t, e2e_phases, d2h = [], [], 0
 
-    def assemble_both(stats_list):
+    def assemble_all(stats_list):
         if fused:
-            st_ = stats_list[0]
             return list(scheduler.run_assembly_pair(m, bt, cfg["equation"], cfg["kappa"], ops,
-                                                    ops, params, cfg["orders"], st_))
+                                                    ops, params, cfg["orders"], stats_list[0]))
         return [scheduler.run_assembly(m, bt, s, ops, ops, params, cfg["orders"], st_)
                 for s, st_ in zip(specs, stats_list)]
     setup_first = None
-    e2e_phases = []
     if args.e2e_steps > 0:
         scheduler.clear_package_cache()
-        warm = assemble_both([scheduler.AssemblyStats() for _ in specs])  # path + pinned pool
+        warm = assemble_all([scheduler.AssemblyStats() for _ in specs])  # path + pinned pool
+        d2h = sum(M.buffer.nbytes for M in warm)
         del warm
     for k in range(args.e2e_steps):
         dist.barrier()
         scheduler.clear_package_cache()  # every step packages once
         t0 = time.perf_counter()
         st = [scheduler.AssemblyStats() for _ in specs]
-        mats = assemble_both(st)
-        torch.cuda.synchronize(device)
+        mats = assemble_all(st)
         dt = time.perf_counter() - t0
         e2e_phases = [dict(x.phase_s) for x in st if x.phase_s]
         e2e_t.append(dt)
@@ -534,16 +645,17 @@ def run_ours(args, cfg, dist, log):
         if setup_first is None:
             setup_first = dt
     e2e_dt = dist.max(statistics.median(e2e_t)) if e2e_t else None
-    e2e_pairs = (pk_total_pairs(pk, len(specs))) * dist.world
-    e2e_value = e2e_pairs / e2e_dt if e2e_dt else None
+    e2e_value = pairs_job / e2e_dt if e2e_dt else None
+    d2h_job = dist.sum(d2h) if shard else d2h * (dist.world if not strong else 1)
+    h2d_job = dist.sum(h2d) if shard else h2d * (dist.world if not strong else 1)
 
     # solve-phase product on the device-resident operator (h2.matvec, SURVEY
     # 8(f)2): HBM-bound, reported against the measured copy bandwidth
     matvec_line = None
-    if not args.no_matvec:
+    if not args.no_matvec and single_device:
         from paper_1510_07244_b200 import h2
         M = scheduler.run_assembly(m, bt, specs[0], ops, ops, params, cfg["orders"])
-        D = h2.DeviceH2(M, device)
+        D = h2.DeviceH2(M, devices[0])
         rng = np.random.default_rng(0)
         x = rng.standard_normal(M.shape[1]) + 1j * rng.standard_normal(M.shape[1])
         for _ in range(3):
@@ -565,40 +677,56 @@ def run_ours(args, cfg, dist, log):
         import oracle
         oracle.build()
         nth = host_threads()
-        pairs, dt, desc = cpu_sample(pk, m, cfg, args.cpu_seconds, nth, log)
+        cpk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+        pairs, dt, desc, _ = cpu_sample(cpk, m, cfg, args.cpu_seconds, nth, log)
         cpu = {"value": pairs / dt, "unit": UNIT, "cores": nth, "kind": "port", "sample": desc}
+        del cpk
 
-    launches = sum(1 + sum(1 for c in p.singular_counts if c) for p in main_plans) * args.steps
+    gca_s = dist.max(setup_t["gca_s"])
+    gca_warm = dist.max(setup_t.get("gca_warm_s", 0.0))
+    trees_s = dist.max(setup_t["trees_s"])
+    asm_first = dist.max(setup_first) if setup_first else None
     h2_setup = {"mesh_s (input, not counted)": round(setup_t["mesh_s"], 3),
-                "trees_s": round(setup_t["trees_s"], 3), "gca_s": round(setup_t["gca_s"], 3),
-                "gca_warm_s (second call)": round(setup_t.get("gca_warm_s", 0.0), 3),
-                "gca_phases_s": {k: round(v, 4) if isinstance(v, float) else v
-                                 for k, v in setup_t.get("gca_phases", {}).items()},
-                "assembly_slp_dlp_s": round(setup_first, 4) if setup_first else None,
-                "total_s": round(setup_t["trees_s"] + setup_t["gca_s"] + setup_first, 3)
-                if setup_first else None,
-                "total_warm_s": round(setup_t["trees_s"] + setup_t.get("gca_warm_s", 0.0)
-                                      + min(e2e_t), 3) if e2e_t else None}
+                "trees_s": round(trees_s, 3), "gca_s": round(gca_s, 3),
+                "gca_warm_s (second call)": round(gca_warm, 3),
+                "gca_phases_s (rank 0)": {k: round(v, 4) if isinstance(v, float) else v
+                                          for k, v in setup_t.get("gca_phases", {}).items()},
+                "assembly_slp_dlp_s": round(asm_first, 4) if asm_first else None,
+                "total_s": round(trees_s + gca_s + asm_first, 3) if asm_first else None,
+                "total_warm_s": round(trees_s + gca_warm + e2e_dt, 3) if e2e_t else None,
+                "timing": "max over ranks of each phase; GCA first call of the process "
+                          "(total_s) and a second call (total_warm_s)"}
+    par = (f"strong x{dist.world * len(devices)}: one job, GCA clusters and leaf windows "
+           f"split over {'ranks' if dist.world > 1 else 'devices'} (pivot all-gather the only "
+           f"exchange)") if strong and (dist.world > 1 or len(devices) > 1) else \
+        (f"weak x{dist.world}, every rank its own job, no collectives" if dist.world > 1
+         else "1 GPU")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world * len(devices),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": args.mode, "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (deterministic octahedral sphere level {cfg['level']})",
-        "config": {"workload": cfg["workload"], "pairs_per_step": int(pairs_step),
+        "config": {"workload": cfg["workload"], "pairs_per_step": int(pairs_job),
+                   "pair_count": "payload entries of both operators (each one pair integral "
+                                 "evaluated once: disjoint rule, or the singular rule for "
+                                 "pairs sharing a vertex)",
                    "operators": list(cfg["layers"]), "orders": list(cfg["orders"]),
                    "plan": "one fused SLP+DLP plan (scheduler.run_assembly_pair)" if fused
                    else "one plan per operator (scheduler.run_assembly)",
                    "l2": "flushed between steps (512 MiB device write)",
-                   "parallelism": f"{args.mode} x{dist.world}, no collectives"},
+                   "parallelism": par},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"disjoint_kernel<{cfg['orders'][0]},{dom_name}>"
                                + (" (fused single+double layer: r, 1/r, phase once per point; "
                                   "flops = roofline.F_DISJOINT_PAIR)" if fused else ""),
                      "peak_source": "measured DFMA probe (gcabem_fp64_probe), this device",
+                     "traffic_source": "ncu dram__bytes_read+write of this kernel and config "
+                                       "(profiles/ncu_traffic.json)",
                      "kernel_share_of_step": share},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_dt,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_job),
+                "d2h_bytes_per_step": int(d2h_job), "seconds_per_step": e2e_dt,
                 "phases_s": [{k: round(v, 4) for k, v in ph.items()} for ph in e2e_phases]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -623,20 +751,18 @@ def _hbm_peak():
         return 6550.0
 
 
-def pk_total_pairs(pk, n_ops: int) -> int:
-    return (pk.block_pairs() + pk.num_items) * n_ops
-
-
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
-    ap.add_argument("--mode", choices=("weak", "strong"), default="weak")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c3")
+    ap.add_argument("--mode", choices=("weak", "strong"), default="strong")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--gca-seconds", type=float, default=20.0,
+                    help="reference arm: wall seconds of the sampled GCA clusters")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
     ap.add_argument("--separate", action="store_true",
@@ -649,7 +775,7 @@ def main(argv=None):
     if args.order is not None:
         cfg["orders"] = (args.order, args.order)
         cfg["workload"] += f", orders {args.order}/{args.order}"
-    dist = Dist()
+    dist = Dist(cpu_only=args.impl == "reference")
 
     def log(msg):
         if dist.rank == 0:

@@ -408,6 +408,63 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
     return ops
 
 
+def partition_clusters(tree: ClusterTree, ids, nparts: int) -> list:
+    """Sorted cluster ids split into `nparts` contiguous ranges balanced by
+    panel count (the Green matrix rows and most of the ACA work scale with
+    |t|). Deterministic: every process computes the same parts."""
+    ids = np.array(sorted(ids), dtype=np.int64)
+    if nparts <= 1:
+        return [ids]
+    w = np.cumsum([tree.nodes[int(c)].size for c in ids]).astype(np.float64)
+    cuts = np.searchsorted(w, w[-1] * np.arange(1, nparts) / nparts) + 1 if ids.size else \
+        np.zeros(nparts - 1, np.int64)
+    return np.split(ids, np.minimum(cuts, ids.size))
+
+
+def exchange_pivots(local_ops: dict, is_complex: bool, group=None) -> dict:
+    """All-gather of the pivots of each process's clusters (torch.distributed,
+    the job's process group: NCCL over NVLink, or gloo): the one exchange
+    step of a GCA split over processes, since packaging a leaf window needs
+    the pivots (rows/cols) of every cluster its coupling leaves touch. A few
+    MB at C3 (sum of ranks x 2 int64). Remote clusters come back as
+    InterpolationOperators whose V has zero rows (V stays with the process
+    that built it; assembly uses pivots only)."""
+    import torch
+    import torch.distributed as dist
+    cids = sorted(local_ops)
+    meta = np.array([[c, local_ops[c].pivots_global.size] for c in cids],
+                    dtype=np.int64).reshape(-1, 2)
+    flat = np.concatenate([np.array([meta.shape[0]], np.int64), meta.ravel()] +
+                          [np.asarray(local_ops[c].pivots_global, np.int64) for c in cids] +
+                          [np.asarray(local_ops[c].pivots_local, np.int64) for c in cids])
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    n = torch.tensor([flat.size], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    nmax = int(max(int(x.item()) for x in sizes))
+    buf = torch.zeros(nmax, dtype=torch.int64, device=dev)
+    buf[:flat.size] = torch.from_numpy(flat).to(dev)
+    got = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(got, buf, group=group)
+    vt = np.complex128 if is_complex else np.float64
+    ops = {}
+    for g, sz in zip(got, sizes):
+        a = g[:int(sz.item())].cpu().numpy()
+        k = int(a[0])
+        m = a[1:1 + 2 * k].reshape(k, 2)
+        tot = int(m[:, 1].sum())
+        pg = a[1 + 2 * k:1 + 2 * k + tot]
+        pl = a[1 + 2 * k + tot:1 + 2 * k + 2 * tot]
+        at = 0
+        for c, r in m.tolist():
+            ops[c] = local_ops[c] if c in local_ops else InterpolationOperator(
+                c, pl[at:at + r].copy(), pg[at:at + r].copy(), np.zeros((0, r), vt))
+            at += r
+    return dict(sorted(ops.items()))
+
+
 def _ops_multi(mesh, tree, ids, spec, params, scene, devices) -> dict:
     """Clusters split into contiguous id ranges balanced by panel count, one
     native pipeline per device running concurrently (the ctypes call releases
@@ -416,9 +473,7 @@ def _ops_multi(mesh, tree, ids, spec, params, scene, devices) -> dict:
     ids = sorted(ids)
     if len(devices) == 1 or len(ids) < 2 * len(devices):
         return _ops_for_tree(mesh, tree, ids, spec, params, scene, devices[0])
-    w = np.cumsum([tree.nodes[c].size for c in ids]).astype(np.float64)
-    cuts = np.searchsorted(w, w[-1] * np.arange(1, len(devices)) / len(devices)) + 1
-    parts = np.split(np.array(ids, dtype=np.int64), np.minimum(cuts, len(ids)))
+    parts = partition_clusters(tree, ids, len(devices))
     share = max(1, _host_threads() // len(devices))
     out, errs = [None] * len(parts), []
 
@@ -444,11 +499,31 @@ def _ops_multi(mesh, tree, ids, spec, params, scene, devices) -> dict:
 
 
 def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
-                                  params: GcaParams, device=None):
+                                  params: GcaParams, device=None, shard=None, group=None):
     """Operators for every cluster in an admissible block (gca.py:285-310);
     (row_ops, col_ops) — the same dict for a shared cluster tree. `device`
     may be a sequence of devices: the clusters are then partitioned across
-    them (balanced by panel count) and built concurrently."""
+    them (balanced by panel count) and built concurrently.
+
+    shard = (rank, world): one job split over processes (torch.distributed
+    initialised, `group` or the default group): this process builds only its
+    part of the clusters (partition_clusters) and exchange_pivots gathers the
+    others' pivots, so every process can package any leaf window; V is kept
+    only for the own clusters."""
+    if shard is not None and int(shard[1]) > 1:
+        rank, world = int(shard[0]), int(shard[1])
+        if not 0 <= rank < world:
+            raise GcaError(f"shard {shard}: need 0 <= rank < world")
+        full_r, full_c = _build_ops(mesh, block_tree, spec, params, device, (rank, world))
+        t0 = time.perf_counter()
+        row = exchange_pivots(full_r, spec.is_complex, group)
+        col = row if full_c is full_r else exchange_pivots(full_c, spec.is_complex, group)
+        last_build_phases["exchange_s"] = time.perf_counter() - t0
+        return row, col
+    return _build_ops(mesh, block_tree, spec, params, device, None)
+
+
+def _build_ops(mesh, block_tree, spec, params, device, part):
     devices = tuple(device) if isinstance(device, (tuple, list)) else \
         (default_device() if device is None else device,)
     t0 = time.perf_counter()
@@ -464,10 +539,17 @@ def build_interpolation_operators(mesh: SurfaceMesh, block_tree: BlockTree, spec
         col_ids = {b.col for b in block_tree.leaves if b.kind == "admissible"}
     last_build_phases.clear()
     last_build_phases["ids_s"] = time.perf_counter() - t0
+
+    def mine(tree, ids):   # this process's part of a job split over processes
+        if part is None:
+            return ids
+        return partition_clusters(tree, ids, part[1])[part[0]].tolist()
     if block_tree.row_tree is block_tree.col_tree:
-        ops = _ops_multi(mesh, block_tree.row_tree, row_ids | col_ids, spec, params, scene,
-                         devices)
+        ops = _ops_multi(mesh, block_tree.row_tree, mine(block_tree.row_tree, row_ids | col_ids),
+                         spec, params, scene, devices)
         return ops, ops
-    return (_ops_multi(mesh, block_tree.row_tree, row_ids, spec, params, scene, devices),
-            _ops_multi(mesh, block_tree.col_tree, col_ids, spec, params, scene, devices))
+    return (_ops_multi(mesh, block_tree.row_tree, mine(block_tree.row_tree, row_ids), spec,
+                       params, scene, devices),
+            _ops_multi(mesh, block_tree.col_tree, mine(block_tree.col_tree, col_ids), spec,
+                       params, scene, devices))
 

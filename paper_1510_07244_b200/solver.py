@@ -50,7 +50,12 @@ def assemble_operator(mesh: SurfaceMesh, spec: KernelSpec, config: PipelineConfi
                       trees=None, ops=None) -> AssembledOperator:
     """Trees, GCA operators (built with the SLP of spec's equation), scheduled
     assembly (solver.py:211-231). Pass trees/ops to reuse them (the DLP
-    operator reuses the SLP's, solver.py:280-282)."""
+    operator reuses the SLP's, solver.py:280-282).
+
+    config.scheduler.shard = (rank, world) splits the job over processes
+    (torch.distributed initialised): each builds its part of the GCA
+    clusters, the pivots are all-gathered, and each assembles its leaf
+    window (the returned matrix holds only those leaves)."""
     block_tree = build_trees(mesh, config) if trees is None else trees
     t0 = time.monotonic()
     if ops is None:
@@ -59,7 +64,7 @@ def assemble_operator(mesh: SurfaceMesh, spec: KernelSpec, config: PipelineConfi
         devices = config.scheduler.backend_for("disjoint").devices
         row_ops, col_ops = build_interpolation_operators(
             mesh, block_tree, KernelSpec(spec.equation, "single", spec.kappa), config.gca,
-            device=tuple(devices))
+            device=tuple(devices), shard=config.scheduler.shard)
     else:
         row_ops, col_ops = ops
     t1 = time.monotonic()
@@ -85,7 +90,7 @@ def assemble_operator_pair(mesh: SurfaceMesh, equation: str, kappa: float,
         devices = config.scheduler.backend_for("disjoint").devices
         row_ops, col_ops = build_interpolation_operators(
             mesh, block_tree, KernelSpec(equation, "single", kappa), config.gca,
-            device=tuple(devices))
+            device=tuple(devices), shard=config.scheduler.shard)
     else:
         row_ops, col_ops = ops
     t1 = time.monotonic()

@@ -474,12 +474,23 @@ def test_pair_plan_shards_equal_single(gload):
     S3, D3 = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
                                          scheduler.SchedulerParams(backends=(be,)), (3, 5))
     assert np.array_equal(S.buffer, S3.buffer) and np.array_equal(D.buffer, D3.buffer)
-    parts = [scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
-                                         scheduler.SchedulerParams(shard=(r, 2)), (3, 5))
-             for r in range(2)]
-    # each shard fills its own leaf range and leaves the rest zero
-    assert np.array_equal(parts[0][0].buffer + parts[1][0].buffer, S.buffer)
-    assert np.array_equal(parts[0][1].buffer + parts[1][1].buffer, D.buffer)
+    L = S.payloads._ids.size
+    for stages in (1, 4):   # unstaged and staged shard paths
+        for world in (2, 3):
+            scheduler.clear_package_cache()
+            parts = [scheduler.run_assembly_pair(
+                m, bt, "helmholtz", 4.0, ops, ops,
+                scheduler.SchedulerParams(shard=(r, world), stages=stages), (3, 5))
+                for r in range(world)]
+            # each shard holds exactly its leaf window; the windows tile the preorder
+            wins = [p[0].leaf_window or (0, L) for p in parts]
+            assert wins[0][0] == 0 and wins[-1][1] == L
+            assert all(a[1] == b[0] for a, b in zip(wins[:-1], wins[1:]))
+            assert np.array_equal(np.concatenate([p[0].buffer for p in parts]), S.buffer)
+            assert np.array_equal(np.concatenate([p[1].buffer for p in parts]), D.buffer)
+            lo, hi = wins[-1]
+            leaf = int(S.payloads._ids[lo])
+            assert np.array_equal(parts[-1][1].payloads[leaf], D.payloads[leaf])
 
 
 @pytest.mark.parametrize("stages", [2, 5])

@@ -6,7 +6,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-import pk_numpy
+import oracle.setup_cpu as pk_numpy
 from helpers import golden_ops, sphere_setup
 from paper_1510_07244_b200 import cluster, gca, kernels, mesh, packaging, quadrature, scheduler
 
@@ -352,7 +352,7 @@ def test_aca_builds_agree_bitwise(tmp_path):
 def test_native_aca_matches_numpy_restatement(eq, kappa):
     """csrc/aca.cpp (threaded batch) vs the numpy ACA on every admissible
     cluster of the L4 sphere, Green matrices from the oracle (CPU)."""
-    import aca_numpy
+    import oracle.setup_cpu as aca_numpy
     import oracle
     m, t, bt = sphere_setup(4)
     ids = sorted({l.row for l in bt.leaves if l.kind == "admissible"})
@@ -377,7 +377,7 @@ def test_native_gca_operator_matches_numpy_restatement(eq, kappa):
     two refinement sweeps) vs numpy/LAPACK on L4 clusters: identical pivots,
     V within roundoff x cond of the pivot block; and V reproduces the pivot
     rows (V[rows] = I), the defining property of the interpolation."""
-    import aca_numpy
+    import oracle.setup_cpu as aca_numpy
     import oracle
     m, t, bt = sphere_setup(4)
     ids = sorted({l.row for l in bt.leaves if l.kind == "admissible"})
@@ -387,7 +387,7 @@ def test_native_gca_operator_matches_numpy_restatement(eq, kappa):
         A = oracle.green_matrix(m.vertices, m.triangles, m.gramians, t.panels(node), src.points,
                                 src.weights, src.normals, src.roles, eq, kappa, 3)
         op = gca._operator_from_green(cid, t.panels(node), A, 1e-4)
-        rows, V = aca_numpy.operator(A, 1e-4)
+        rows, V = aca_numpy.solve_operator(A, 1e-4)
         assert np.array_equal(op.pivots_local, rows)
         assert np.array_equal(op.pivots_global, t.panels(node)[rows])
         assert op.V.dtype == V.dtype and op.V.shape == V.shape

@@ -10,6 +10,7 @@ import sys
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -102,3 +103,52 @@ def test_bench_reference_arm_under_torchrun():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 2
     assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _pivot_rank_main(rank, world, port, out_path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import level_ops, sphere_setup
+    from paper_1510_07244_b200 import gca, scheduler
+    g = np.load(os.path.join(ROOT, "tests", "golden", "gca_levels.npz"))
+    m, t, bt = sphere_setup(4)
+    ops_all = level_ops(lambda name: g, 4, "helmholtz")
+    parts = gca.partition_clusters(t, list(ops_all), world)
+    local = {int(c): ops_all[int(c)] for c in parts[rank]}
+    got = gca.exchange_pivots(local, True)
+    ok = sorted(got) == sorted(ops_all)
+    for c, op in got.items():
+        ok &= np.array_equal(op.pivots_global, ops_all[c].pivots_global)
+        ok &= np.array_equal(op.pivots_local, ops_all[c].pivots_local)
+        ok &= op.rank == ops_all[c].rank
+        ok &= (op is local[c]) if c in local else op.V.shape == (0, ops_all[c].rank)
+    win = scheduler.shard_window(m, bt, got, got, (rank, world), 81)
+    res = torch.tensor([int(ok), win[0], win[1], len(local)], dtype=torch.int64)
+    allres = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allres, res)
+    if rank == 0:
+        np.save(out_path, np.stack([r.numpy() for r in allres]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gca_shard_pivot_exchange(tmp_path, world):
+    """GCA split over processes (build_interpolation_operators(shard=...)):
+    the cluster parts tile the admissible clusters, exchange_pivots gives
+    every rank every cluster's pivots (the reference's, here from the
+    fixture) with V only for its own, and the ranks' leaf windows
+    (scheduler.shard_window, computed independently per rank) tile the
+    preorder."""
+    out = str(tmp_path / "res.npy")
+    mp.spawn(_pivot_rank_main, args=(world, _free_port(), out), nprocs=world, join=True)
+    res = np.load(out)
+    assert np.all(res[:, 0] == 1)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import sphere_setup
+    m, t, bt = sphere_setup(4)
+    assert res[0, 1] == 0 and res[-1, 2] == len(bt.leaves)
+    assert np.all(res[1:, 1] == res[:-1, 2])
+    assert np.all(res[:, 3] > 0)

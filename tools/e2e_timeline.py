@@ -11,7 +11,9 @@ from paper_1510_07244_b200 import scheduler  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 cfg = bench.CONFIGS[cfg_name]
-m, bt, ops, pk, _ = bench.build_workload(cfg, 0, lambda s: None)
+m, bt, ops, _ = bench.build_workload(cfg, [0], None, lambda s: None, warm_gca=False)
+from paper_1510_07244_b200 import packaging as _pkg  # noqa: E402
+pk = _pkg.make_packages(m.triangles, bt, ops, ops, 8 << 20)
 for rep in range(4):
     scheduler.clear_package_cache()
     st = scheduler.AssemblyStats()

@@ -1,4 +1,4 @@
-"""One bench step (C2 by default) for ncu: builds the workload, then executes
+"""One bench step (C3 by default) for ncu: builds the workload, then executes
 every plan `--reps` times. Run under ncu on ONE GPU, e.g.
 
   ncu --set full --clock-control none --import-source on \
@@ -18,12 +18,15 @@ from paper_1510_07244_b200 import kernels, scheduler  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="c2", choices=tuple(bench.CONFIGS))
+    ap.add_argument("--config", default="c3", choices=tuple(bench.CONFIGS))
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--separate", action="store_true", help="one plan per operator")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
-    m, bt, ops, pk, _ = bench.build_workload(cfg, 0, lambda s: print(s, file=sys.stderr))
+    m, bt, ops, _ = bench.build_workload(cfg, [0], None, lambda s: print(s, file=sys.stderr),
+                                         warm_gca=False)
+    from paper_1510_07244_b200 import packaging
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
     dm = devmod.device_mesh(m, 0)
     if len(cfg["layers"]) == 2 and not args.separate:  # the bench's fused SLP+DLP plan
         plans = [scheduler.AssemblyPlan(dm, kernels.KernelSpec(cfg["equation"], "single",
