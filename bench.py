@@ -583,7 +583,7 @@ def run_ours(args, cfg, dist, log):
     value = pairs_job / (ms_max * 1e-3)
     single_device = dist.world == 1 and len(devices) == 1
     separate = None
-    if fused and single_device:  # the same workload as two single-layer plans
+    if fused and single_device and not args.no_separate:  # the same work as two single-layer plans
         ms_sep, dk_sep, _ = time_plans("sep", args.steps, 3)
         fl_sep = [p.flops() for p in per_dev[0][4]]
         kd = int(np.argmax(dk_sep))
@@ -765,6 +765,8 @@ def main(argv=None):
                     help="reference arm: wall seconds of the sampled GCA clusters")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--no-separate", action="store_true",
+                    help="skip timing the single-layer plans next to the fused one")
     ap.add_argument("--separate", action="store_true",
                     help="time SLP and DLP as two single-layer plans (default: one fused plan)")
     ap.add_argument("--order", type=int, default=None,

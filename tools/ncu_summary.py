@@ -82,8 +82,45 @@ def full(path):
     print()
 
 
+
+
+def metrics(path, title, last=None):
+    """Per-kernel table of a multi-metric launch list (--metrics a,b,c --csv):
+    one row per launch with every metric; `last` keeps only the last N
+    launches (e.g. one product of a repeated step)."""
+    rows = _rows(open(path).read())
+    hdr = rows[0]
+    ki, ii, mi, vi, ui = (hdr.index("Kernel Name"), hdr.index("ID"), hdr.index("Metric Name"),
+                          hdr.index("Metric Value"), hdr.index("Metric Unit"))
+    launches = OrderedDict()
+    for r in rows[1:]:
+        d = launches.setdefault(r[ii], {"name": r[ki].split("(")[0]})
+        d[r[mi]] = (float(r[vi].replace(",", "")), r[ui])
+    items = list(launches.values())
+    if last:
+        items = items[-int(last):]
+    print(f"# {title}: ncu --metrics (cold-cache, serialised launches)")
+    print("#   time_ms  dram_read_MB  dram_write_MB  fp64_pipe_%  kernel")
+    for d in items:
+        t, tu = d.get("gpu__time_duration.sum", (0.0, "ns"))
+        t *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+              "msecond": 1.0}.get(tu, 1.0)
+
+        def mb(key):
+            v, u = d.get(key, (0.0, "byte"))
+            return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
+        fp = d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", (0.0, ""))[0]
+        print(f"{t:10.4f} {mb('dram__bytes_read.sum'):12.2f} {mb('dram__bytes_write.sum'):13.2f}"
+              f" {fp:11.1f}  {d['name']}")
+    tot = sum(1 for _ in items)
+    print(f"# {tot} launches")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "launch list")
+    elif sys.argv[1] == "metrics":
+        metrics(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "launch list",
+                sys.argv[4] if len(sys.argv) > 4 else None)
     else:
         full(sys.argv[2])
