@@ -121,7 +121,14 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
                          gcabem_layout_t *out);
 /* The same from the flat package arrays of packaging.make_packages (leaves
  * [leaf_lo, leaf_hi) only; payload indices relative to leaf_lo): the block
- * and item gathers run natively instead of in numpy. */
+ * and item gathers run natively instead of in numpy.
+ * leaf_mirror (nullable, nleaves entries): for each leaf the index of the leaf
+ * of the transposed cluster pair (same cluster tree and operators on both
+ * sides), or -1. Leaves whose mirror lies in [leaf_lo, leaf_hi) are evaluated
+ * together with it (symmetric evaluation: the reference scheduler.py:425-439
+ * assembles leaf (t, s) and leaf (s, t) separately; their panel pairs are the
+ * same with x and y swapped under the symmetric disjoint rule,
+ * quadrature.py:108). */
 int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t leaf_hi,
                                 int64_t nleaves, const int64_t *leaf_shape,
                                 const int64_t *leaf_base, const int64_t *leaf_rows_at,
@@ -132,11 +139,20 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                                 const int8_t *item_case, const int64_t *item_tri_x,
                                 const int64_t *item_tri_y, const int64_t *item_leaf,
                                 const int64_t *item_offset, const uint8_t *perms,
-                                gcabem_layout_t *out);
+                                const int64_t *leaf_mirror, gcabem_layout_t *out);
 /* {payload_len, blocks, tasks, disjoint pairs, vertex, edge, identical items,
  * uploaded bytes} */
 int gcabem_layout_info(gcabem_layout_t layout, int64_t *info8);
+/* {disjoint evaluations of the mirrored kernel (each gives a pair and its
+ * transpose), of the plain kernel, pairs of mirrored (PRIMARY/SELF upper)
+ * blocks, pairs of blocks written by their mirror} */
+int gcabem_layout_mirror_info(gcabem_layout_t layout, int64_t *info4);
 int gcabem_layout_release(gcabem_layout_t layout);
+/* Mirrored evaluation of the layout's mirrored leaves (default: on when the
+ * layout has any and the disjoint order is <= 8); 0 evaluates every block on
+ * its own (the reference's one-pair-at-a-time order). */
+int gcabem_plan_set_mirror(gcabem_plan_t plan, int enable);
+int gcabem_plan_mirrored(gcabem_plan_t plan, int *out);
 int gcabem_plan_create_on(gcabem_layout_t layout, int equation, int layer, double kappa,
                           int disjoint_n, const double *gauss_pts, const double *gauss_wts,
                           const int64_t *sq, const double *const *srule, gcabem_plan_t *out);

@@ -53,8 +53,11 @@ _SIGS = {
     "gcabem_layout_release": ([_vp], _int),
     "gcabem_layout_info": ([_vp, _vp], _int),
     "gcabem_layout_from_packages": ([_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64]
-                                    + [_vp] * 5 + [_i64] + [_vp] * 6 + [ctypes.POINTER(_vp)],
+                                    + [_vp] * 5 + [_i64] + [_vp] * 7 + [ctypes.POINTER(_vp)],
                                     _int),
+    "gcabem_layout_mirror_info": ([_vp, _vp], _int),
+    "gcabem_plan_set_mirror": ([_vp, _int], _int),
+    "gcabem_plan_mirrored": ([_vp, ctypes.POINTER(_int)], _int),
     "gcabem_plan_create_on": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp,
                                ctypes.POINTER(_vp)], _int),
     "gcabem_plan_download": ([_vp, _vp], _int),

@@ -117,6 +117,9 @@ struct gcabem_plan_s {
     cudaStream_t own_stream = nullptr;
     cudaStream_t copy = nullptr;    // D2H, overlapping later chunks' kernels
     bool executed = false;
+    // the layout's mirrored blocks run on the mirrored kernel (orders up to
+    // MAX_MIRROR_ORDER; gcabem_plan_set_mirror can turn it off)
+    bool mirrored = false;
 };
 
 extern "C" {
@@ -350,7 +353,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
             !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= payload_len)) ||
             (b > 0 && r[6] < blocks[7 * (b - 1) + 6]))
             return fail("block descriptor out of bounds or out of order");
-        bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
+        bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, ROLE_NORMAL, 0, 0, 0};
         L->block_task_at[b] = ntasks;
         L->block_leaf[b] = r[6];
         L->block_base[b] = base;
@@ -476,7 +479,7 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                                 const int8_t *item_case, const int64_t *item_tri_x,
                                 const int64_t *item_tri_y, const int64_t *item_leaf,
                                 const int64_t *item_offset, const uint8_t *perms,
-                                gcabem_layout_t *out) {
+                                const int64_t *leaf_mirror, gcabem_layout_t *out) {
     GC_ARG(mesh && out, "null argument");
     *out = nullptr;
     GC_ARG(0 <= leaf_lo && leaf_lo <= leaf_hi && leaf_hi <= nleaves, "bad leaf range");
@@ -499,14 +502,54 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     L->block_leaf.resize(B);
     L->block_base.resize(B);
     L->block_pairs.resize(B);
-    int64_t ntasks = 0;
+    // leaf roles of the mirrored evaluation: a leaf whose mirror (the leaf of
+    // the transposed cluster pair) lies in this range is PRIMARY if it comes
+    // first in the preorder, SKIP if it comes second (its entries are written
+    // by the primary: chunked execution in leaf order sees the primary first),
+    // SELF if it is its own mirror; every other leaf is NORMAL
+    std::vector<int8_t> leaf_role;
+    bool any_mirror = false;
+    if (leaf_mirror) {
+        leaf_role.assign(leaf_hi - leaf_lo, ROLE_NORMAL);
+        for (int64_t lf = leaf_lo; lf < leaf_hi; ++lf) {
+            const int64_t m = leaf_mirror[lf];
+            if (m < leaf_lo || m >= leaf_hi) continue;
+            if (leaf_mirror[m] != lf || leaf_shape[2 * m] != leaf_shape[2 * lf + 1] ||
+                leaf_shape[2 * m + 1] != leaf_shape[2 * lf]) {
+                delete L;
+                return set_error(GCABEM_ERR_ARG, "leaf mirror is not a transposed leaf");
+            }
+            leaf_role[lf - leaf_lo] = m == lf ? ROLE_SELF : m > lf ? ROLE_PRIMARY : ROLE_SKIP;
+            any_mirror = true;
+        }
+    }
+    auto role_of = [&](int64_t lf) -> int {
+        return any_mirror ? leaf_role[lf - leaf_lo] : ROLE_NORMAL;
+    };
+    int64_t ntasks = 0, nmt = 0, nrt = 0;
+    if (any_mirror) {
+        L->block_mtask_at.resize(B + 1);
+        L->block_rtask_at.resize(B + 1);
+    }
     for (int64_t b = 0; b < B; ++b) {
         const int64_t np = blk_nr[b0 + b] * blk_nc[b0 + b];
         L->block_task_at[b] = ntasks;
         L->block_pairs[b] = np;
-        ntasks += (np + DISJOINT_TPB - 1) / DISJOINT_TPB;
+        const int64_t nt = (np + DISJOINT_TPB - 1) / DISJOINT_TPB;
+        ntasks += nt;
+        if (any_mirror) {
+            const int r = role_of(blk_leaf[b0 + b]);
+            L->block_mtask_at[b] = nmt;
+            L->block_rtask_at[b] = nrt;
+            if (r == ROLE_PRIMARY || r == ROLE_SELF) nmt += nt;
+            if (r == ROLE_NORMAL) nrt += nt;
+        }
     }
     L->block_task_at[B] = ntasks;
+    if (any_mirror) {
+        L->block_mtask_at[B] = nmt;
+        L->block_rtask_at[B] = nrt;
+    }
     // singular items of the range: per-chunk case counts (stable counting sort)
     constexpr int MAXT = 8;
     int64_t cnt[MAXT][4] = {};
@@ -547,9 +590,13 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     const int64_t S = L->case_at[3];
     L->item_out.resize(S);
     tr.mark("counts");
-    // one pinned arena: [BlockDesc B | int2 ntasks | int32 npanels | SingItem S]
+    // one pinned arena: [BlockDesc B | int2 ntasks | int2 nmt | int2 nrt | int32 npanels |
+    // SingItem S]
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t off_t = align(sizeof(BlockDesc) * B), off_p = off_t + align(sizeof(int2) * ntasks),
+    const size_t off_t = align(sizeof(BlockDesc) * B),
+                 off_mt = off_t + align(sizeof(int2) * ntasks),
+                 off_rt = off_mt + align(sizeof(int2) * nmt),
+                 off_p = off_rt + align(sizeof(int2) * nrt),
                  off_s = off_p + align(sizeof(int32_t) * npanels),
                  total = off_s + align(sizeof(SingItem) * S);
     std::lock_guard<std::mutex> arena_lock(g_arena_mutex);
@@ -568,6 +615,8 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     char *arena = static_cast<char *>(g_arena);
     BlockDesc *bd = reinterpret_cast<BlockDesc *>(arena);
     int2 *tasks = reinterpret_cast<int2 *>(arena + off_t);
+    int2 *mtasks = reinterpret_cast<int2 *>(arena + off_mt);
+    int2 *rtasks = reinterpret_cast<int2 *>(arena + off_rt);
     int32_t *pan = reinterpret_cast<int32_t *>(arena + off_p);
     SingItem *si = reinterpret_cast<SingItem *>(arena + off_s);
     par_for(B, 1 << 14, [&](int64_t lo, int64_t hi, int) {
@@ -580,12 +629,34 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                 !(ra >= 0 && ra + nr <= npanels && ca >= 0 && ca + nc <= npanels) ||
                 !(nr == 0 || nc == 0 || (base >= 0 && base + (nr - 1) * ld + nc <= plen)))
                 bad = true;
-            bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, 0};
+            const int role = role_of(lf);
+            int64_t mbase = 0, mld = 0, dr = 0;
+            if (role == ROLE_PRIMARY || role == ROLE_SELF) {
+                // entry (i, j) of this block is leaf entry (r0 + i, c0 + j); the
+                // transposed pair is entry (c0 + j, r0 + i) of the mirror leaf
+                const int64_t m = leaf_mirror[lf];
+                mld = leaf_shape[2 * m + 1];
+                mbase = leaf_base[m] - base0 + blk_c0[g] * mld + blk_r0[g];
+                dr = blk_r0[g] - blk_c0[g];
+                if (!(nr == 0 || nc == 0 || (mbase >= 0 && mbase + (nc - 1) * mld + nr <= plen)))
+                    bad = true;
+            }
+            bd[b] = BlockDesc{base, ra, ca, (int32_t)ld, (int32_t)nr, (int32_t)nc, role, mbase,
+                              (int32_t)mld, (int32_t)dr};
             L->block_leaf[b] = lf;
             L->block_base[b] = base;
             int64_t t = L->block_task_at[b];
             for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
                 tasks[t++] = make_int2((int)b, (int)k0);
+            if (any_mirror && (role == ROLE_PRIMARY || role == ROLE_SELF)) {
+                int64_t q = L->block_mtask_at[b];
+                for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
+                    mtasks[q++] = make_int2((int)b, (int)k0);
+            } else if (any_mirror && role == ROLE_NORMAL) {
+                int64_t q = L->block_rtask_at[b];
+                for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
+                    rtasks[q++] = make_int2((int)b, (int)k0);
+            }
         }
     });
     par_for(npanels, 1 << 16, [&](int64_t lo, int64_t hi, int) {
@@ -638,14 +709,55 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     }
     tr.mark("fill");
     L->ntasks = ntasks;
+    L->nmtasks = nmt;
+    L->nrtasks = nrt;
+    if (any_mirror) {
+        // evaluation counts for the roofline: pairs of PRIMARY/SELF(upper)
+        // blocks minus their vertex-sharing pairs (one mirrored evaluation
+        // each), NORMAL pairs minus theirs
+        int64_t mp = 0, sp = 0, np_ = 0, up = 0;
+        for (int64_t b = 0; b < B; ++b) {
+            const int64_t g = b0 + b, lf = blk_leaf[g], nr = blk_nr[g], nc = blk_nc[g];
+            const int r = role_of(lf);
+            if (r == ROLE_PRIMARY) mp += nr * nc;
+            else if (r == ROLE_SKIP) sp += nr * nc;
+            else if (r == ROLE_NORMAL) np_ += nr * nc;
+            else {  // SELF: leaf entries (r0 + i, c0 + j) with r0 + i < c0 + j
+                const int64_t dr = blk_r0[g] - blk_c0[g];
+                for (int64_t i = 0; i < nr; ++i)
+                    up += std::max<int64_t>(0, nc - std::max<int64_t>(0, i + dr + 1));
+            }
+        }
+        int64_t sh_m = 0, sh_n = 0;
+        for (int64_t k = 0; k < nitems; ++k) {
+            const int64_t lf = item_leaf[k];
+            if (lf < leaf_lo || lf >= leaf_hi) continue;
+            const int r = role_of(lf);
+            if (r == ROLE_PRIMARY) ++sh_m;
+            else if (r == ROLE_NORMAL) ++sh_n;
+            else if (r == ROLE_SELF) {
+                const int64_t ncol = leaf_shape[2 * lf + 1];
+                const int64_t i = item_offset[k] / ncol, j = item_offset[k] % ncol;
+                if (i < j) ++sh_m;
+            }
+        }
+        L->mirror_info[0] = mp + up - sh_m;
+        L->mirror_info[1] = np_ - sh_n;
+        L->mirror_info[2] = mp + up;
+        L->mirror_info[3] = sp;
+    }
     cudaStream_t s = mesh->stream;
     cudaError_t e = pool_init(mesh->device);
     if (e == cudaSuccess) e = L->blocks.alloc(B, s);
     if (e == cudaSuccess) e = L->tasks.alloc(ntasks, s);
+    if (e == cudaSuccess && nmt) e = L->mtasks.alloc(nmt, s);
+    if (e == cudaSuccess && nrt) e = L->rtasks.alloc(nrt, s);
     if (e == cudaSuccess) e = L->panels.alloc(npanels, s);
     if (e == cudaSuccess) e = L->items.alloc(S, s);
     if (e == cudaSuccess && B) e = cudaMemcpyAsync(L->blocks.p, bd, sizeof(BlockDesc) * B, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && ntasks) e = cudaMemcpyAsync(L->tasks.p, tasks, sizeof(int2) * ntasks, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && nmt) e = cudaMemcpyAsync(L->mtasks.p, mtasks, sizeof(int2) * nmt, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && nrt) e = cudaMemcpyAsync(L->rtasks.p, rtasks, sizeof(int2) * nrt, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && npanels) e = cudaMemcpyAsync(L->panels.p, pan, sizeof(int32_t) * npanels, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && S) e = cudaMemcpyAsync(L->items.p, si, sizeof(SingItem) * S, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the arena is reused after this
@@ -667,8 +779,15 @@ int gcabem_layout_info(gcabem_layout_t L, int64_t *info8) {
     info8[2] = L->ntasks;
     info8[3] = pairs;
     for (int c = 0; c < 3; ++c) info8[4 + c] = L->case_at[c + 1] - L->case_at[c];
-    info8[7] = (int64_t)(L->blocks.n * sizeof(BlockDesc) + L->tasks.n * sizeof(int2) +
+    info8[7] = (int64_t)(L->blocks.n * sizeof(BlockDesc) +
+                         (L->tasks.n + L->mtasks.n + L->rtasks.n) * sizeof(int2) +
                          L->panels.n * sizeof(int32_t) + L->items.n * sizeof(SingItem));
+    return GCABEM_OK;
+}
+
+int gcabem_layout_mirror_info(gcabem_layout_t L, int64_t *info4) {
+    GC_ARG(L && info4, "null argument");
+    for (int k = 0; k < 4; ++k) info4[k] = L->mirror_info[k];
     return GCABEM_OK;
 }
 
@@ -731,6 +850,7 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
     p->kind = kind;
     p->order = disjoint_n;
     p->kappa = kappa;
+    p->mirrored = L->nmtasks > 0 && disjoint_n <= MAX_MIRROR_ORDER;
     p->payload_len = L->payload_len;
     cudaError_t e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking);
@@ -780,12 +900,35 @@ namespace {
 
 // Launch the kernels of blocks [b0, b1) and of the singular items whose
 // payload index lies in [p0, p1) on the plan stream.
+// Disjoint kernels of blocks [b0, b1): the plain kernel over every task, or
+// (mirrored plan) the plain kernel over the NORMAL blocks' tasks and the
+// mirrored kernel over the PRIMARY/SELF blocks' tasks (SKIP blocks: none).
+int enqueue_disjoint(gcabem_plan_t p, int64_t b0, int64_t b1) {
+    gcabem_mesh_t m = p->mesh;
+    gcabem_layout_t L = p->L;
+    cudaStream_t s = p->stream;
+    if (!p->mirrored) {
+        const int64_t t0 = L->block_task_at[b0], t1 = L->block_task_at[b1];
+        GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p,
+                                L->tasks.p + t0, t1 - t0, L->panels.p, p->payload.p,
+                                p->payload2.p, p->kappa, s));
+        return GCABEM_OK;
+    }
+    const int64_t r0 = L->block_rtask_at[b0], r1 = L->block_rtask_at[b1];
+    const int64_t q0 = L->block_mtask_at[b0], q1 = L->block_mtask_at[b1];
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p,
+                            L->rtasks.p + r0, r1 - r0, L->panels.p, p->payload.p, p->payload2.p,
+                            p->kappa, s));
+    GC_CUDA(launch_disjoint(p->kind + MIRRORED, p->order, m->charts.p, m->T.p, L->blocks.p,
+                            L->mtasks.p + q0, q1 - q0, L->panels.p, p->payload.p, p->payload2.p,
+                            p->kappa, s));
+    return GCABEM_OK;
+}
+
 int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p1) {
     gcabem_mesh_t m = p->mesh;
     cudaStream_t s = p->stream;
-    const int64_t t0 = p->L->block_task_at[b0], t1 = p->L->block_task_at[b1];
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p + t0, t1 - t0,
-                            p->L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
+    if (int rc = enqueue_disjoint(p, b0, b1)) return rc;
     for (int c = 0; c < 3; ++c) {
         const auto first = p->L->item_out.begin() + p->L->case_at[c];
         const auto last = p->L->item_out.begin() + p->L->case_at[c + 1];
@@ -806,14 +949,10 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     gcabem_mesh_t m = p->mesh;
     GC_CUDA(cudaSetDevice(m->device));
     cudaStream_t s = p->stream;
-    if (p->payload_len > 0) {
-        GC_CUDA(cudaMemsetAsync(p->payload.p, 0, sizeof(double2) * p->payload_len, s));
-        if (kind_pair(p->kind))
-            GC_CUDA(cudaMemsetAsync(p->payload2.p, 0, sizeof(double2) * p->payload_len, s));
-    }
+    // no memset: the blocks tile every leaf and the disjoint kernels write
+    // every entry (pairs sharing a vertex as 0, SKIP blocks by their primary)
     GC_CUDA(cudaEventRecord(p->ev[0], s));
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, p->L->blocks.p, p->L->tasks.p, p->L->ntasks,
-                            p->L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
+    if (int rc = enqueue_disjoint(p, 0, (int64_t)p->L->block_leaf.size())) return rc;
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     for (int c = 0; c < 3; ++c) {
         const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
@@ -824,6 +963,18 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_set_mirror(gcabem_plan_t p, int enable) {
+    GC_ARG(p, "null plan");
+    p->mirrored = enable && p->L->nmtasks > 0 && p->order <= MAX_MIRROR_ORDER;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_mirrored(gcabem_plan_t p, int *out) {
+    GC_ARG(p && out, "null argument");
+    *out = p->mirrored ? 1 : 0;
     return GCABEM_OK;
 }
 
@@ -863,11 +1014,8 @@ int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, 
         const int64_t b0 = cut[k], b1 = cut[k + 1];
         const int64_t p0 = b0 < B ? p->L->block_base[b0] : p->payload_len;
         const int64_t p1 = b1 < B ? p->L->block_base[b1] : p->payload_len;
-        if (p1 > p0) {
-            GC_CUDA(cudaMemsetAsync(p->payload.p + p0, 0, sizeof(double2) * (p1 - p0), s));
-            if (kind_pair(p->kind))
-                GC_CUDA(cudaMemsetAsync(p->payload2.p + p0, 0, sizeof(double2) * (p1 - p0), s));
-        }
+        // chunks run in leaf order, so every SKIP entry of this chunk was
+        // written by its PRIMARY in this or an earlier chunk before this D2H
         if (int rc = enqueue_range(p, b0, b1, p0, p1)) return rc;
         GC_CUDA(cudaEventRecord(p->chunk_ev[k], s));
         if (p1 > p0) {

@@ -52,14 +52,49 @@ static cudaError_t upload_tables(int n, const double *g, const double *gw) {
 #endif
 constexpr double EXPANDED_MAX_RATIO = GCABEM_EXPANDED_MAX_RATIO;
 
+// accumulator slots a kind uses (in[] / acc[] of 6): {re, im} of the single
+// layer or of a single kind's operator, then the pair kinds' double layer,
+// then (MIR) the transposed pair's double layer (see accumulate_mirror)
+__host__ __device__ constexpr bool slot_used(int kind, bool mir, int k) {
+    return k == 0 ? true
+         : k == 1 ? kind_helm(kind)
+         : k == 2 ? (kind_pair(kind) || (mir && (kind == L_DLP || kind == H_DLP)))
+         : k == 3 ? (kind == H_PAIR || (mir && kind == H_DLP))
+         : k == 4 ? (mir && kind_pair(kind))
+         : k == 5 ? (mir && kind == H_PAIR) : false;
+}
 
-template <int N, int KIND, int PH>
+template <int KIND, bool MIR, int PH>
+__device__ __forceinline__ void accumulate_any(double r2, double dn, double dnm, double w,
+                                               double kappa, double phi0, double in[6]) {
+    if constexpr (MIR)
+        accumulate_mirror<KIND, PH>(r2, dn, dnm, w, kappa, phi0, in);
+    else
+        accumulate<KIND, PH>(r2, dn, w, kappa, phi0, in);
+}
+
+
+// x-side polynomial coefficients (below) parked in shared memory instead of
+// registers: per thread 15 doubles at stride DISJOINT_TPB (conflict-free),
+// read back once per x point; frees ~30 registers of the hot loop for more
+// independent quadrature points in flight
+#ifndef GCABEM_XSMEM
+#define GCABEM_XSMEM 0
+#endif
+
+// MIR: also the transposed pair (j, i) (ROLE_PRIMARY / ROLE_SELF blocks): its
+// double layer needs d . n_x, n_x the x panel's normal (nx); dnm = -d . n_x =
+// gc u_d . n_x - xo . n_x, formed like dn from per-y (unm) and per-x (xonm) parts
+template <int N, int KIND, int PH, bool MIR = false>
 __device__ __forceinline__ void disjoint_expanded(const double dO[3], const double e1x[3],
                                                   const double e2x[3], const double e1y[3],
                                                   const double e2y[3], const double n[3],
-                                                  double kappa, double phi0, double acc[4]) {
+                                                  double kappa, double phi0, double acc[6],
+                                                  double *xc = nullptr,
+                                                  const double *nx = nullptr) {
     constexpr bool DL = kind_normal(KIND);
-    double uu[N], un[N];
+    constexpr bool DM = MIR && DL;   // the transposed pair's double layer
+    double uu[N], un[N], unm[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) {
         const double gd = c_gauss[N][d];
@@ -68,6 +103,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
         const double uz = fma(gd, e2y[2], e1y[2]);
         uu[d] = fma(ux, ux, fma(uy, uy, uz * uz));
         un[d] = DL ? fma(ux, n[0], fma(uy, n[1], uz * n[2])) : 0.0;
+        unm[d] = DM ? fma(ux, nx[0], fma(uy, nx[1], uz * nx[2])) : 0.0;
     }
     // x-side quantities as polynomials in the x point (s, t) = (a, a b):
     //   |xo|^2     = Q0 + s (2 P1 + s Q11) + t (2 P2 + 2 s Q12 + t Q22)
@@ -81,24 +117,42 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
     const double B0 = -2.0 * dot(dO, e2y), B1 = -2.0 * dot(e1x, e2y), B2 = -2.0 * dot(e2x, e2y);
     const double N0 = DL ? dot(dO, n) : 0.0, N1 = DL ? dot(e1x, n) : 0.0,
                  N2 = DL ? dot(e2x, n) : 0.0;
+    // xo . n_x (MIR): dO . n_x + s e1x . n_x + t e2x . n_x
+    const double M0 = DM ? dot(dO, nx) : 0.0, M1 = DM ? dot(e1x, nx) : 0.0,
+                 M2 = DM ? dot(e2x, nx) : 0.0;
+#if GCABEM_XSMEM
+    constexpr int S_ = DISJOINT_TPB;
+    {
+        const double v[15] = {Q0, P1, P2, Q11, Q12, Q22, A0, A1, A2, B0, B1, B2, N0, N1, N2};
+#pragma unroll
+        for (int k = 0; k < 15; ++k) xc[k * S_] = v[k];
+    }
+#define XC(k) (*(volatile double *)&xc[(k) * S_])
+#else
+#define XC(k) (k == 0 ? Q0 : k == 1 ? P1 : k == 2 ? P2 : k == 3 ? Q11 : k == 4 ? Q12 : \
+               k == 5 ? Q22 : k == 6 ? A0 : k == 7 ? A1 : k == 8 ? A2 : k == 9 ? B0 : \
+               k == 10 ? B1 : k == 11 ? B2 : k == 12 ? N0 : k == 13 ? N1 : N2)
+#endif
 #pragma unroll 1
     for (int ia = 0; ia < N; ++ia) {
         const double s = c_gauss[N][ia];
-        const double xs = fma(s, fma(s, Q11, P1), Q0);
-        const double vs = fma(s, Q12, P2);
-        const double as = fma(s, A1, A0);
-        const double bs = fma(s, B1, B0);
-        const double ns = DL ? fma(s, N1, N0) : 0.0;
+        const double xs = fma(s, fma(s, XC(3), XC(1)), XC(0));
+        const double vs = fma(s, XC(4), XC(2));
+        const double as = fma(s, XC(7), XC(6));
+        const double bs = fma(s, XC(10), XC(9));
+        const double ns = DL ? fma(s, XC(13), XC(12)) : 0.0;
+        const double ms = DM ? fma(s, M1, M0) : 0.0;
 #pragma unroll 1
         for (int ib = 0; ib < N; ++ib) {
             const int p = ia * N + ib;
             const double t = c_duffy_t[duffy_offset(N) + p];
             const double wx = c_duffy_w[duffy_offset(N) + p];
-            const double xx = fma(t, fma(t, Q22, vs), xs);
-            const double xon = DL ? fma(t, N2, ns) : 0.0;
-            const double a2 = fma(t, A2, as);
-            const double b2 = fma(t, B2, bs);
-            double in[4] = {0.0, 0.0, 0.0, 0.0};
+            const double xx = fma(t, fma(t, XC(5), vs), xs);
+            const double xon = DL ? fma(t, XC(14), ns) : 0.0;
+            const double xonm = DM ? fma(t, M2, ms) : 0.0;
+            const double a2 = fma(t, XC(8), as);
+            const double b2 = fma(t, XC(11), bs);
+            double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             // fused pair kinds at orders >= 6 roll the outer y loop (the fully
             // unrolled N^2 body spills their two layers of state)
             constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
@@ -111,24 +165,27 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
                     const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
                     const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
                     const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                    accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
+                    const double dnm = DM ? fma(gc, unm[d], -xonm) : 0.0;
+                    accumulate_any<KIND, MIR, PH>(r2, dn, dnm, wy, kappa, phi0, in);
                 }
             }
-            acc[0] = fma(wx, in[0], acc[0]);
-            if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
-            if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
-            if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
         }
     }
+#undef XC
 }
 
-template <int N, int KIND, int PH>
+template <int N, int KIND, int PH, bool MIR = false>
 __device__ __forceinline__ void disjoint_direct(const double dO[3], const double e1x[3],
                                                 const double e2x[3], const double e1y[3],
                                                 const double e2y[3], const double n[3],
-                                                double kappa, double phi0, double acc[4]) {
+                                                double kappa, double phi0, double acc[6],
+                                                const double *nx = nullptr) {
     constexpr bool DL = kind_normal(KIND);
-    double ux[N], uy[N], uz[N], un[N];
+    constexpr bool DM = MIR && DL;
+    double ux[N], uy[N], uz[N], un[N], unm[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) {
         const double gd = c_gauss[N][d];
@@ -136,6 +193,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         uy[d] = fma(gd, e2y[1], e1y[1]);
         uz[d] = fma(gd, e2y[2], e1y[2]);
         un[d] = DL ? fma(ux[d], n[0], fma(uy[d], n[1], uz[d] * n[2])) : 0.0;
+        unm[d] = DM ? fma(ux[d], nx[0], fma(uy[d], nx[1], uz[d] * nx[2])) : 0.0;
     }
 #pragma unroll 1
     for (int p = 0; p < N * N; ++p) {
@@ -146,7 +204,8 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xo1 = fma(t, e2x[1], fma(s, e1x[1], dO[1]));
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
-        double in[4] = {0.0, 0.0, 0.0, 0.0};
+        const double xonm = DM ? fma(xo0, nx[0], fma(xo1, nx[1], xo2 * nx[2])) : 0.0;
+        double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;  // see disjoint_expanded
 #pragma unroll OUTER
         for (int c = 0; c < N; ++c) {
@@ -159,13 +218,13 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
                 const double dz = fma(-gc, uz[d], xo2);
                 const double r2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
-                accumulate<KIND, PH>(r2, dn, wy, kappa, phi0, in);
+                const double dnm = DM ? fma(gc, unm[d], -xonm) : 0.0;
+                accumulate_any<KIND, MIR, PH>(r2, dn, dnm, wy, kappa, phi0, in);
             }
         }
-        acc[0] = fma(wx, in[0], acc[0]);
-        if (kind_helm(KIND)) acc[1] = fma(wx, in[1], acc[1]);
-        if (kind_pair(KIND)) acc[2] = fma(wx, in[2], acc[2]);
-        if (KIND == H_PAIR) acc[3] = fma(wx, in[3], acc[3]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
     }
 }
 
@@ -187,31 +246,56 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // C2), H_PAIR 5 (96 registers, a few spilled bytes in the cold full-sincos
 // tier; 4 and 6 measured 1.6% and 3% slower at C3, re-checked with the v11
 // point kernels)
+#ifndef GCABEM_HPAIR_MINB
+#define GCABEM_HPAIR_MINB 5
+#endif
 constexpr int disjoint_minb(int n, int kind) {
     return n > 7 ? 1                                     // would spill heavily
            : kind == L_SLP ? 7 : kind == L_DLP ? 6 : kind <= H_DLP ? 5
-           : n <= 4 ? (kind == L_PAIR ? 4 : 5)
+           : n <= 4 ? (kind == L_PAIR ? 4 : GCABEM_HPAIR_MINB)
            : n <= 6 ? 3 : 2;                             // pair kinds: 2 layers of state
 }
 
-template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB, disjoint_minb(N, KIND))
+// mirrored kernels (MIR) carry a third accumulator pair (the transposed
+// double layer): one CTA fewer per SM than the plain kernel of the kind
+constexpr int disjoint_minb_mir(int n, int kind) {
+    return n > 7 ? 1 : kind == L_SLP ? 7 : kind == H_SLP ? 5
+           : kind == L_DLP ? 5 : kind == H_DLP ? 4
+           : n <= 4 ? (kind == L_PAIR ? 4 : 4) : n <= 6 ? 3 : 2;
+}
+
+template <int N, int KIND, bool MIR>
+__global__ void __launch_bounds__(DISJOINT_TPB, MIR ? disjoint_minb_mir(N, KIND)
+                                                    : disjoint_minb(N, KIND))
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,
                 double2 *__restrict__ payload2, double kappa) {
+#if GCABEM_XSMEM
+    __shared__ double xcoef[15 * DISJOINT_TPB];
+    double *xc = xcoef + threadIdx.x;
+#else
+    double *xc = nullptr;
+#endif
     const int2 task = tasks[blockIdx.x];
     const BlockDesc b = blocks[task.x];
     const int k = task.y + threadIdx.x;
     // no early exit before the warp votes below: every lane of the CTA's
     // four full warps reaches them
-    const bool inb = k < b.nr * b.nc;
+    bool inb = k < b.nr * b.nc;
     const int i = inb ? k / b.nc : 0;
     const int j = inb ? k - i * b.nc : 0;
+    // ROLE_SELF (diagonal leaf): the strict lower triangle is written by the
+    // upper one (the diagonal holds identical pairs: shared, written 0)
+    if (MIR && b.role == ROLE_SELF && i + b.dr > j) inb = false;
     const int tx = panels[b.rows_at + i], ty = panels[b.cols_at + j];
     const int64_t pos = b.base + (int64_t)i * b.ld + j;
     double2 *dst = payload + pos;
     double2 *dst2 = kind_pair(KIND) ? payload2 + pos : nullptr;
+    // the transposed pair's entry (MIR): mirror leaf, row j, column i
+    const int64_t mpos = MIR ? b.mbase + (int64_t)j * b.mld + i : 0;
+    double2 *mdst = MIR ? payload + mpos : nullptr;
+    double2 *mdst2 = MIR && kind_pair(KIND) ? payload2 + mpos : nullptr;
     bool shared;
     {
         const int a0 = T[3 * tx], a1 = T[3 * tx + 1], a2 = T[3 * tx + 2];
@@ -222,7 +306,8 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const bool active = inb && !shared;
     const Chart *cx = charts + tx;
     const Chart *cy = charts + ty;
-    double dO[3], e1x[3], e2x[3], e1y[3], e2y[3], n[3] = {0.0, 0.0, 0.0};
+    double dO[3], e1x[3], e2x[3], e1y[3], e2y[3], n[3] = {0.0, 0.0, 0.0},
+           nx[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         dO[c] = cx->o[c] - cy->o[c];
@@ -231,6 +316,7 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
         e1y[c] = cy->e1[c];
         e2y[c] = cy->e2[c];
         if (kind_normal(KIND)) n[c] = cy->n[c];
+        if (MIR && kind_normal(KIND)) nx[c] = cx->n[c];
     }
     const double gx = cx->gram, gy = cy->gram;
     const double rx = cx->radius, ry = cy->radius;
@@ -242,7 +328,7 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
     const double dcen = norm3(dc[0], dc[1], dc[2]);
     const double rmin = dcen - rx - ry;
     const double S = norm3(dO[0], dO[1], dO[2]) + cx->enorm + cy->enorm;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     // evaluation form and phase tier are chosen per WARP (votes over the
     // active lanes): a lane that needs the direct form or a longer phase
     // polynomial takes its whole warp along instead of splitting it into
@@ -260,6 +346,10 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
         if (inb) {
             *dst = make_double2(0.0, 0.0);
             if (kind_pair(KIND)) *dst2 = make_double2(0.0, 0.0);
+            if (MIR) {
+                *mdst = make_double2(0.0, 0.0);
+                if (kind_pair(KIND)) *mdst2 = make_double2(0.0, 0.0);
+            }
         }
         return;
     }
@@ -278,47 +368,67 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
             }
             if (tiny) {
                 if (expanded)
-                    disjoint_expanded<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                    disjoint_expanded<N, KIND, 2, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, xc, nx);
                 else
-                    disjoint_direct<N, KIND, 2>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                    disjoint_direct<N, KIND, 2, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
             } else {
                 if (expanded)
-                    disjoint_expanded<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                    disjoint_expanded<N, KIND, 1, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, xc, nx);
                 else
-                    disjoint_direct<N, KIND, 1>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc);
+                    disjoint_direct<N, KIND, 1, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
             }
-            rotate_acc<KIND>(phi0, acc);
-            unscale_acc<KIND>(kappa, acc);
+            rotate_acc<KIND, MIR>(phi0, acc);
+            unscale_acc<KIND, MIR>(kappa, acc);
         } else {
             if (expanded)
-                disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+                disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, xc, nx);
             else
-                disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+                disjoint_direct<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
         }
     } else {
         if (expanded)
-            disjoint_expanded<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+            disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, xc, nx);
         else
-            disjoint_direct<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
+            disjoint_direct<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
     }
-    finish_acc<KIND>(acc, gx, gy, dst, dst2);
+    if constexpr (MIR)
+        finish_acc_mirror<KIND>(acc, gx, gy, dst, dst2, mdst, mdst2);
+    else
+        finish_acc<KIND>(acc, gx, gy, dst, dst2);
 }
 
+template <int N, bool MIR>
+static cudaError_t launch_disjoint_nm(int kind, const Chart *charts, const int32_t *T,
+                                      const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                      const int32_t *panels, double2 *payload, double2 *payload2,
+                                      double kappa, cudaStream_t s) {
+    const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
+    switch (kind) {
+        case L_SLP: disjoint_kernel<N, L_SLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case L_DLP: disjoint_kernel<N, L_DLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case H_SLP: disjoint_kernel<N, H_SLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case H_DLP: disjoint_kernel<N, H_DLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case L_PAIR: disjoint_kernel<N, L_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        default:    disjoint_kernel<N, H_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+    }
+    return cudaGetLastError();
+}
+
+// kind >= MIRRORED: the mirrored kernel (orders <= MAX_MIRROR_ORDER)
 template <int N>
 static cudaError_t launch_disjoint_n(int kind, const Chart *charts, const int32_t *T,
                                      const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
                                      const int32_t *panels, double2 *payload, double2 *payload2,
                                      double kappa, cudaStream_t s) {
-    const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
-    switch (kind) {
-        case L_SLP: disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case L_DLP: disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case H_SLP: disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case H_DLP: disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case L_PAIR: disjoint_kernel<N, L_PAIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        default:    disjoint_kernel<N, H_PAIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+    if (kind >= MIRRORED) {
+        if constexpr (N <= MAX_MIRROR_ORDER)
+            return launch_disjoint_nm<N, true>(kind - MIRRORED, charts, T, blocks, tasks, ntasks,
+                                               panels, payload, payload2, kappa, s);
+        else
+            return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
+    return launch_disjoint_nm<N, false>(kind, charts, T, blocks, tasks, ntasks, panels, payload,
+                                        payload2, kappa, s);
 }
 
 }  // namespace gcabem

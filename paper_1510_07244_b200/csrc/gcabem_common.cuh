@@ -22,14 +22,31 @@ struct __align__(16) Chart {
 };
 static_assert(sizeof(Chart) == 128, "Chart must be one 128 B line");
 
+// Mirror roles of a block (symmetric evaluation): on a shared
+// cluster tree with shared operators, leaf (t, s) and leaf (s, t) hold the
+// integrals of the same panel pairs with the roles of x and y swapped (the
+// disjoint rule is a symmetric tensor product), so one thread evaluates pair
+// (i, j) and its transpose (j, i) together: the single layer is the same
+// value, the double layer of (j, i) shares r, 1/r and the phase and differs
+// only in d . n (the normal of panel i instead of j).
+enum BlockRole { ROLE_NORMAL = 0,   // no mirror in this layout: evaluated alone
+                 ROLE_PRIMARY = 1,  // writes its entries and the mirror leaf's
+                 ROLE_SELF = 2,     // diagonal leaf (t, t): the upper triangle
+                                    // writes both (i, j) and (j, i)
+                 ROLE_SKIP = 3 };   // written by its (earlier) primary
+
 struct BlockDesc {
     int64_t base;     // payload index of entry (0,0)
     int64_t rows_at;  // offset of the row panels in the panel array
     int64_t cols_at;  // offset of the column panels
     int32_t ld;       // payload row stride (leaf ncols)
     int32_t nr, nc;
-    int32_t pad;
+    int32_t role;     // BlockRole
+    int64_t mbase;    // PRIMARY/SELF: payload index of the transposed entry (0,0)
+    int32_t mld;      //   its row stride: entry (i, j) mirrors to mbase + j mld + i
+    int32_t dr;       // SELF: r0 - c0 (leaf row minus leaf column of entry (0,0))
 };
+static_assert(sizeof(BlockDesc) == 56, "BlockDesc layout");
 
 struct SingItem {
     int64_t out;          // payload index (leaf base + WorkItem.offset)
@@ -61,7 +78,10 @@ inline int kind_of(int equation, int layer) { return equation * 2 + layer; }
 // ---- launchers (kernels.cu) ------------------------------------------------
 cudaError_t upload_disjoint_rule(int order, const double *gauss_pts, const double *gauss_wts);
 // kind L_PAIR / H_PAIR: payload gets the single layer, payload2 the double
-// layer (payload2 unused otherwise)
+// layer (payload2 unused otherwise). kind + MIRRORED: the mirrored kernel over
+// ROLE_PRIMARY / ROLE_SELF tasks (orders <= MAX_MIRROR_ORDER).
+constexpr int MIRRORED = 8;
+constexpr int MAX_MIRROR_ORDER = 8;
 cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
                             const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
                             const int32_t *panels, double2 *payload, double2 *payload2,

@@ -120,6 +120,15 @@ struct gcabem_layout_s {
     gcabem::PoolBuf<gcabem::BlockDesc> blocks;
     gcabem::PoolBuf<int2> tasks;
     int64_t ntasks = 0;
+    // mirrored evaluation (gcabem::BlockRole): tasks of ROLE_PRIMARY/SELF
+    // blocks (mirrored kernel) and of ROLE_NORMAL blocks (plain kernel);
+    // ROLE_SKIP blocks have none. Empty when no leaf has a mirror.
+    gcabem::PoolBuf<int2> mtasks, rtasks;
+    int64_t nmtasks = 0, nrtasks = 0;
+    std::vector<int64_t> block_mtask_at, block_rtask_at;
+    // {evaluations by the mirrored kernel, by the plain kernel (pairs sharing
+    // a vertex excluded), pairs of PRIMARY/SELF blocks, pairs of SKIP blocks}
+    int64_t mirror_info[4] = {0, 0, 0, 0};
     gcabem::PoolBuf<int32_t> panels;
     gcabem::PoolBuf<gcabem::SingItem> items;
     int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])

@@ -126,7 +126,7 @@ class NearFieldP1:
         nf = near_field_tree(block_tree)
         self.packages = make_packages(mesh.triangles, nf, {}, {}, maxsize)
         dm = device_mesh(mesh, self.device)
-        self.layout = DeviceLayout(dm, self.packages)
+        self.layout = DeviceLayout(dm, self.packages, mirror=False)
         dn, sn = self.orders
         g = gauss_legendre(dn)
         gp, gw = nat.f64(g.points), nat.f64(g.weights)

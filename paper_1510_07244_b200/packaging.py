@@ -64,6 +64,10 @@ class AssemblyPackages:
     item_src_block: np.ndarray  # (S,) block whose scan generated the item
     perms: np.ndarray           # (S, 6) uint8 perm_x, perm_y
     extra: dict = field(default_factory=dict)
+    # (L,) position of the leaf of the transposed cluster pair in these
+    # packages, -1 if none (or outside a leaf range); None when the two sides
+    # differ (different trees or operators): see leaf_mirrors()
+    leaf_mirror: np.ndarray | None = None
 
     @property
     def payload_len(self) -> int:
@@ -260,6 +264,36 @@ def leaf_layout(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs |
     return x.leaf_ids, shape, base
 
 
+def leaf_mirrors(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs | None = None,
+                 leaf_range=None):
+    """Position of each leaf's mirror, the leaf (s, t) of leaf (t, s), or
+    None when the block tree's two sides differ. With one cluster tree and
+    one operator set on both sides (the reference's pipelines:
+    build_block_tree(tree, tree), gca.py:303-306 returning the same dict
+    twice), leaf (s, t) holds the transposed panel pairs of leaf (t, s):
+    dense leaves the same panels, admissible leaves the same pivots. The
+    admissibility test and the subdivision are symmetric, so every leaf has
+    its mirror (a diagonal leaf (t, t) is its own)."""
+    if block_tree.row_tree is not block_tree.col_tree or row_ops is not col_ops:
+        return None
+    x = inputs or package_inputs(np.zeros((0, 3), np.int64), block_tree, row_ops, col_ops)
+    leaves = x.leaves
+    lo, hi = (0, leaves.shape[0]) if leaf_range is None else leaf_range
+    n = np.int64(len(block_tree.row_tree.nodes))
+    key = leaves[:, 0] * n + leaves[:, 1]
+    order = np.argsort(key, kind="stable")
+    want = leaves[lo:hi, 1] * n + leaves[lo:hi, 0]
+    pos = np.searchsorted(key[order], want)
+    pos = np.minimum(pos, key.size - 1)
+    hit = key[order][pos] == want
+    m = np.where(hit, order[pos], -1)
+    if not np.all(hit) or not np.array_equal(leaves[m, 2], leaves[lo:hi, 2]):
+        return None          # not a symmetric block tree: no mirrored evaluation
+    m = m - lo
+    m[(m < 0) | (m >= hi - lo)] = -1
+    return np.ascontiguousarray(m, dtype=np.int64)
+
+
 def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops,
                   maxsize: int, nthreads: int = 0, leaf_range=None,
                   inputs: PackageInputs | None = None) -> AssemblyPackages:
@@ -312,7 +346,8 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         blk_nr=blocks[2], blk_c0=blocks[3], blk_nc=blocks[4], blk_list=blk_list,
         n_disjoint_lists=nlists, item_case=items[0].astype(np.int8), item_tri_x=items[1],
         item_tri_y=items[2], item_leaf=items[3], item_offset=items[4],
-        item_src_block=items[5], perms=perms)
+        item_src_block=items[5], perms=perms,
+        leaf_mirror=leaf_mirrors(block_tree, row_ops, col_ops, x, leaf_range))
 
 
 def shard_leaves(pk: AssemblyPackages, nshards: int, disjoint_q: int, singular_q=None):

@@ -17,6 +17,12 @@ F_SINGULAR = {k: v + 24 for k, v in F_DISJOINT.items()}
 # (its own 1/r, weight product and accumulation: 3 flops Laplace, 7 Helmholtz)
 F_DISJOINT_PAIR = {"laplace": 19 + 3, "helmholtz": 31 + 7}
 F_SINGULAR_PAIR = {k: v + 24 for k, v in F_DISJOINT_PAIR.items()}
+# mirrored evaluation (a pair and its transpose from one point evaluation,
+# DESIGN.md §4): the single layer is symmetric (one value for both entries);
+# the transposed double layer adds its own d . n (5), and the product of the
+# shared kernel factor with it and the weight plus the accumulation: Laplace 3,
+# Helmholtz 6 (complex x real, twice) + 2 (complex add) -> +8 / +11 per point
+F_MIRROR_EXTRA = {"laplace": 5 + 3, "helmholtz": 5 + 6}
 PAIR_OVERHEAD = 4
 # Green-matrix entry: n^2 panel points x disjoint F (monopole SLP, dipole DLP) + 2
 GREEN_ENTRY_OVERHEAD = 2
@@ -33,6 +39,16 @@ def point_flops(spec, family: str, pair: bool = False) -> int:
 def pair_flops(spec, family: str, q: int, pair: bool = False) -> int:
     """Flops of one pair integral with a Q-point rule (pair: both layers)."""
     return q * point_flops(spec, family, pair) + (2 if pair else 1) * PAIR_OVERHEAD
+
+
+def mirror_pair_flops(spec, q: int, pair: bool = False) -> int:
+    """Flops of one mirrored disjoint evaluation: pair (i, j) and its
+    transpose (j, i) with a Q-point rule (pair: both layers of each)."""
+    if spec.layer == "single" and not pair:
+        f = point_flops(spec, "disjoint")            # symmetric: the value is shared
+    else:
+        f = point_flops(spec, "disjoint", pair) + F_MIRROR_EXTRA[spec.equation]
+    return q * f + (4 if pair else 2) * PAIR_OVERHEAD
 
 
 def p1_pair_flops(spec, family: str, q: int, order: int) -> int:

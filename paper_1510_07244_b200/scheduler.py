@@ -98,6 +98,11 @@ class SchedulerParams:
     # cached yet: stage k+1 is packaged on a host thread while stage k's
     # kernels and D2H run (1 = package everything first)
     stages: int = 6
+    # symmetric evaluation: leaf (t, s) and its mirror (s, t) in the same plan
+    # from one point evaluation per pair; False evaluates each
+    # pair on its own (results then bitwise independent of how leaves are
+    # split into stages / devices / shards)
+    mirror: bool = True
 
     def backend_for(self, case: str) -> Backend:
         wanted = self.affinity.get(case)
@@ -308,7 +313,8 @@ class DeviceLayout:
     block descriptors, tasks, panel indices, singular items. Shared by every
     operator assembled from the same packages; cached on the packages."""
 
-    def __init__(self, dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None):
+    def __init__(self, dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None,
+                 mirror: bool = True):
         t0 = time.monotonic()
         lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
         self.leaf_range = (lo, hi)
@@ -329,9 +335,16 @@ class DeviceLayout:
             pk.blk_leaf.size, p(pk.blk_leaf), p(pk.blk_r0), p(pk.blk_nr), p(pk.blk_c0),
             p(pk.blk_nc), pk.item_case.size, p(pk.item_case), p(pk.item_tri_x),
             p(pk.item_tri_y), p(pk.item_leaf), p(pk.item_offset), p(pk.perms),
+            p(pk.leaf_mirror) if (mirror and pk.leaf_mirror is not None) else None,
             ctypes.byref(h)))
         info = np.zeros(8, np.int64)
         nat.check(nat.lib().gcabem_layout_info(h, p(info)))
+        mi = np.zeros(4, np.int64)
+        nat.check(nat.lib().gcabem_layout_mirror_info(h, p(mi)))
+        # disjoint-kernel evaluations: mirrored (a pair and its transpose) and
+        # plain; 0/0 without mirrors (then every non-sharing pair is plain)
+        self.mirror_info = {"evals_mirrored": int(mi[0]), "evals_plain": int(mi[1]),
+                            "pairs_mirrored": int(mi[2]), "pairs_skipped": int(mi[3])}
         self.disjoint_pairs = int(info[3])
         self.singular_counts = [int(x) for x in info[4:7]]
         self.h2d_bytes = int(info[7])
@@ -339,12 +352,13 @@ class DeviceLayout:
         self.handle = h.value
 
     @staticmethod
-    def cached(dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None) -> "DeviceLayout":
+    def cached(dm: DeviceMesh, pk: AssemblyPackages, leaf_range=None,
+               mirror: bool = True) -> "DeviceLayout":
         lo, hi = leaf_range if leaf_range is not None else (0, pk.leaf_ids.size)
-        key = ("layout", dm.device, id(dm), lo, hi)
+        key = ("layout", dm.device, id(dm), lo, hi, bool(mirror))
         lay = pk.extra.get(key)
         if lay is None:
-            lay = DeviceLayout(dm, pk, (lo, hi))
+            lay = DeviceLayout(dm, pk, (lo, hi), mirror)
             pk.extra[key] = lay
         return lay
 
@@ -368,9 +382,9 @@ class AssemblyPlan:
     execute_download() fill two host buffers."""
 
     def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
-                 leaf_range=None, pair: bool = False):
+                 leaf_range=None, pair: bool = False, mirror: bool = True):
         t_prep = time.monotonic()
-        self.layout = DeviceLayout.cached(dm, pk, leaf_range)
+        self.layout = DeviceLayout.cached(dm, pk, leaf_range, mirror)
         lay = self.layout
         self.leaf_range = lay.leaf_range
         self.payload_offset = lay.payload_offset
@@ -401,6 +415,9 @@ class AssemblyPlan:
                 nat.ptr(sq), ctypes.cast(rptr, ctypes.c_void_p), ctypes.byref(h)))
         self.handle = h.value
         self._keep = rules
+        m = ctypes.c_int()
+        nat.check(nat.lib().gcabem_plan_mirrored(self.handle, ctypes.byref(m)))
+        self.mirrored = bool(m.value)
 
     def execute(self) -> None:
         nat.check(nat.lib().gcabem_plan_execute(self.handle))
@@ -450,10 +467,15 @@ class AssemblyPlan:
         """Algorithmic FP64 flops of one execute (SURVEY §8(d) convention). The
         disjoint launch skips the pairs that share a vertex (it writes 0 and the
         singular pass overwrites them), so they are not credited to it."""
-        from .roofline import pair_flops
+        from .roofline import mirror_pair_flops, pair_flops
         dq = self.orders[0] ** 4
-        computed = self.disjoint_pairs - sum(self.singular_counts)
-        dis = pair_flops(self.spec, "disjoint", dq, self.pair) * computed
+        if self.mirrored:
+            mi = self.layout.mirror_info
+            dis = pair_flops(self.spec, "disjoint", dq, self.pair) * mi["evals_plain"] + \
+                mirror_pair_flops(self.spec, dq, self.pair) * mi["evals_mirrored"]
+        else:
+            computed = self.disjoint_pairs - sum(self.singular_counts)
+            dis = pair_flops(self.spec, "disjoint", dq, self.pair) * computed
         sing = sum(pair_flops(self.spec, "singular", q, self.pair) * n
                    for q, n in zip(self.singular_q, self.singular_counts))
         return {"disjoint": dis, "singular": sing}
@@ -719,7 +741,7 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
             pk = sp.stage(k)
             tr = time.monotonic()
             wait += tr - tw
-            p = AssemblyPlan(dm, spec, pk, orders, pair=pair)
+            p = AssemblyPlan(dm, spec, pk, orders, pair=pair, mirror=params.mirror)
             plans.append(p)
             tp = time.monotonic()
             if p.payload_len:
@@ -806,7 +828,8 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
     try:
         ta = time.monotonic()
         for dev, rng in zip(devices, ranges):
-            plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng, pair=pair))
+            plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng, pair=pair,
+                                      mirror=params.mirror))
         phase["plan_create"] = time.monotonic() - ta
         phase["plan_host_prep"] = sum(p.prep_s for p in plans)
         ta = time.monotonic()

@@ -1,0 +1,125 @@
+"""Mirrored (symmetric) evaluation on the device: leaf (t, s) and its mirror
+(s, t) of a shared cluster tree hold the same panel pairs with x and y
+swapped, and the disjoint rule is a symmetric tensor product (reference
+quadrature.py:108), so one thread evaluates pair (i, j) and (j, i) together
+(SchedulerParams.mirror, default on). Checked here:
+
+* every kind (L/H x SLP/DLP, both fused pair kinds) and several orders: the
+  mirrored payload against the bit-exact oracle (P2, 1e-12) and against the
+  per-pair evaluation (mirror=False) within roundoff (1e-13);
+* the chunked D2H path (leaf-ordered chunks: a SKIP leaf's entries are
+  written by its earlier PRIMARY before that chunk's copy) equals the
+  one-shot execute + download bit for bit;
+* the evaluation accounting of the layout (roofline flops): every pair of a
+  mirrored leaf pair is evaluated once.
+"""
+import numpy as np
+import pytest
+
+from helpers import golden_ops, oracle_assemble, p2_check, sphere_setup
+from paper_1510_07244_b200 import device as devmod
+from paper_1510_07244_b200 import kernels, packaging, scheduler
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [("laplace", "single", 0.0), ("laplace", "double", 0.0), ("helmholtz", "single", 4.0),
+         ("helmholtz", "double", 4.0)]
+
+
+@pytest.mark.parametrize("eq,layer,kappa", KINDS)
+@pytest.mark.parametrize("orders", [(3, 5), (4, 5), (6, 5)])
+def test_mirrored_single_kinds_vs_oracle_and_plain(gload, eq, layer, kappa, orders):
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), eq)
+    spec = kernels.KernelSpec(eq, layer, kappa)
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    assert pk.leaf_mirror is not None and np.all(pk.leaf_mirror >= 0)
+    p = scheduler.SchedulerParams(stages=1)
+    M = scheduler.run_assembly(m, bt, spec, ops, ops, p, orders)
+    P = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(stages=1,
+                                                                                mirror=False),
+                               orders)
+    ref = oracle_assemble(m, pk, eq, layer, kappa, orders)
+    ok, worst, _ = p2_check(pk, M.buffer, ref, 1e-12, m, (eq, layer, kappa), orders)
+    assert ok, ("oracle", worst)
+    ok, worst, _ = p2_check(pk, M.buffer, P.buffer, 1e-13, m, (eq, layer, kappa), orders,
+                            ref_is_device=True)
+    assert ok, ("plain", worst)
+    if layer == "single":   # the mirror of an SLP entry is the same value
+        for l in bt.leaves[::7]:
+            if l.kind == "dense" and l.row != l.col:
+                mir = next(x for x in bt.leaves if x.row == l.col and x.col == l.row)
+                assert np.array_equal(M.payloads[l.index], M.payloads[mir.index].T)
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+@pytest.mark.parametrize("orders", [(3, 5), (4, 5), (7, 7)])
+def test_mirrored_pair_plan_vs_oracle(gload, eq, kappa, orders):
+    m, t, bt = sphere_setup(3)
+    ops = golden_ops(gload("gca_L3.npz"), eq)
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    S, D = scheduler.run_assembly_pair(m, bt, eq, kappa, ops, ops,
+                                       scheduler.SchedulerParams(stages=1), orders)
+    for layer, M in (("single", S), ("double", D)):
+        ref = oracle_assemble(m, pk, eq, layer, kappa, orders)
+        ok, worst, _ = p2_check(pk, M.buffer, ref, 1e-12, m, (eq, layer, kappa), orders)
+        assert ok, (layer, worst)
+
+
+@pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
+def test_mirrored_chunked_download_equals_one_shot(gload, eq, kappa):
+    m, t, bt = sphere_setup(4)
+    from paper_1510_07244_b200 import gca
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec(eq, "single", kappa),
+                                               gca.GcaParams())
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    dm = devmod.device_mesh(m, 0)
+    plan = scheduler.AssemblyPlan(dm, kernels.KernelSpec(eq, "single", kappa), pk, (3, 5),
+                                  pair=True)
+    assert plan.mirrored
+    from paper_1510_07244_b200 import _native as nat
+    a1 = nat.pinned_empty(pk.payload_len, np.complex128)
+    a2 = nat.pinned_empty(pk.payload_len, np.complex128)
+    plan.execute()
+    plan.download(a1, a2)
+    plan.synchronize()
+    one = (np.array(a1), np.array(a2))
+    for nchunks in (3, 17):
+        a1[:] = np.nan
+        a2[:] = np.nan
+        plan.execute_download(a1, nchunks, a2)
+        plan.synchronize()
+        assert np.array_equal(a1, one[0]) and np.array_equal(a2, one[1]), nchunks
+    plan.close()
+
+
+def test_mirror_evaluation_accounting(gload):
+    """Layout counts: the PRIMARY leaves' pairs equal their mirrors' (written
+    by them), every non-sharing pair of the matrix is covered by exactly one
+    evaluation, and the flops credit the mirrored evaluations."""
+    m, t, bt = sphere_setup(4)
+    from paper_1510_07244_b200 import gca
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    dm = devmod.device_mesh(m, 0)
+    spec = kernels.KernelSpec("helmholtz", "single", 4.0)
+    mp = scheduler.AssemblyPlan(dm, spec, pk, (3, 5), pair=True)
+    pp = scheduler.AssemblyPlan(dm, spec, pk, (3, 5), pair=True, mirror=False)
+    mi = mp.layout.mirror_info
+    diag = [k for k, l in enumerate(pk.leaf_mirror) if l == k]
+    diag_pairs = int(sum(pk.leaf_shape[k, 0] * pk.leaf_shape[k, 1] for k in diag))
+    diag_upper = int(sum(pk.leaf_shape[k, 0] * (pk.leaf_shape[k, 0] - 1) // 2 for k in diag))
+    assert mi["pairs_mirrored"] - diag_upper == mi["pairs_skipped"]
+    total = pk.block_pairs()
+    plain_pairs = total - 2 * mi["pairs_skipped"] - diag_pairs
+    items = pk.num_items
+    # every item is a pair sharing a vertex: the diagonal's (identical) and
+    # lower-triangle items, and the SKIP leaves' items, have no evaluation
+    computed = 2 * mi["evals_mirrored"] + mi["evals_plain"]
+    assert computed == total - items
+    assert mi["evals_plain"] <= plain_pairs
+    fm, fp = mp.flops()["disjoint"], pp.flops()["disjoint"]
+    assert fm < fp and fm > 0.5 * fp
+    mp.close()
+    pp.close()

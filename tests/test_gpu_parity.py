@@ -115,11 +115,22 @@ def test_multi_device_shards_equal_single(gload):
     m, t, bt = sphere_setup(3)
     ops = golden_ops(gload("gca_L3.npz"), "laplace")
     spec = kernels.KernelSpec("laplace", "double")
-    one = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(), (3, 5))
+    # bitwise with per-pair evaluation (mirror=False): the split of the leaves
+    # does not change any entry's arithmetic
+    one = scheduler.run_assembly(m, bt, spec, ops, ops,
+                                 scheduler.SchedulerParams(mirror=False), (3, 5))
     be = scheduler.Backend("cuda", devices=(0, 0, 0))
     three = scheduler.run_assembly(m, bt, spec, ops, ops,
-                                   scheduler.SchedulerParams(backends=(be,)), (3, 5))
+                                   scheduler.SchedulerParams(backends=(be,), mirror=False), (3, 5))
     assert np.array_equal(one.buffer, three.buffer)
+    # mirrored (default): mirrors inside one device's range are evaluated
+    # together, the rest alone -- equal to the plain values within roundoff
+    three_m = scheduler.run_assembly(m, bt, spec, ops, ops,
+                                     scheduler.SchedulerParams(backends=(be,)), (3, 5))
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    ok, worst, _ = p2_check(pk, three_m.buffer, one.buffer, 1e-13, m, ("laplace", "double", 0.0),
+                            (3, 5), ref_is_device=True)
+    assert ok, worst
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
@@ -251,8 +262,10 @@ def test_slp_block_symmetry_L5():
     dense leaves (t,s) and (s,t) are transposes on uncorrected entries."""
     m, t, bt = sphere_setup(5)
     near = cluster.BlockTree(bt.nodes, t, t, bt.eta, [l for l in bt.leaves if l.kind == "dense"])
+    # per-pair evaluation: with the mirrored default the transposes are equal
+    # by construction
     M = scheduler.run_assembly(m, near, kernels.KernelSpec("laplace", "single"), {}, {},
-                               scheduler.SchedulerParams(), (4, 5))
+                               scheduler.SchedulerParams(mirror=False), (4, 5))
     leaf = {(l.row, l.col): l.index for l in near.leaves}
     worst = 0.0
     for (r, c), idx in leaf.items():
@@ -469,10 +482,11 @@ def test_pair_plan_shards_equal_single(gload):
     m, t, bt = sphere_setup(3)
     ops = golden_ops(gload("gca_L3.npz"), "helmholtz")
     S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
-                                       scheduler.SchedulerParams(), (3, 5))
+                                       scheduler.SchedulerParams(mirror=False), (3, 5))
     be = scheduler.Backend("cuda", devices=(0, 0, 0))
     S3, D3 = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
-                                         scheduler.SchedulerParams(backends=(be,)), (3, 5))
+                                         scheduler.SchedulerParams(backends=(be,), mirror=False),
+                                         (3, 5))
     assert np.array_equal(S.buffer, S3.buffer) and np.array_equal(D.buffer, D3.buffer)
     L = S.payloads._ids.size
     for stages in (1, 4):   # unstaged and staged shard paths
@@ -480,7 +494,8 @@ def test_pair_plan_shards_equal_single(gload):
             scheduler.clear_package_cache()
             parts = [scheduler.run_assembly_pair(
                 m, bt, "helmholtz", 4.0, ops, ops,
-                scheduler.SchedulerParams(shard=(r, world), stages=stages), (3, 5))
+                scheduler.SchedulerParams(shard=(r, world), stages=stages, mirror=False),
+                (3, 5))
                 for r in range(world)]
             # each shard holds exactly its leaf window; the windows tile the preorder
             wins = [p[0].leaf_window or (0, L) for p in parts]
@@ -504,11 +519,12 @@ def test_staged_assembly_equals_unstaged(stages):
                                                                          4.0), gca.GcaParams())
     spec = kernels.KernelSpec("helmholtz", "double", 4.0)
     scheduler.clear_package_cache()
-    ref = scheduler.run_assembly(m, bt, spec, ops, ops, scheduler.SchedulerParams(stages=1))
+    ref = scheduler.run_assembly(m, bt, spec, ops, ops,
+                                 scheduler.SchedulerParams(stages=1, mirror=False))
     refS, refD = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
-                                             scheduler.SchedulerParams(stages=1))
+                                             scheduler.SchedulerParams(stages=1, mirror=False))
     scheduler.clear_package_cache()
-    params = scheduler.SchedulerParams(stages=stages)
+    params = scheduler.SchedulerParams(stages=stages, mirror=False)
     st = scheduler.AssemblyStats()
     got = scheduler.run_assembly(m, bt, spec, ops, ops, params, stats=st)
     assert "packaging_wait" in st.phase_s
