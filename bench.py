@@ -524,9 +524,10 @@ def run_ours(args, cfg, dist, log):
     per_dev = []   # (device, stream, flush buffer, [plans], [separate plans])
     for d, rng in zip(devices, dev_ranges):
         dm = devmod.device_mesh(m, d)
-        sep = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], rng) for s in specs]
-        main = [scheduler.AssemblyPlan(dm, specs[0], pk, cfg["orders"], rng, pair=True)] \
-            if fused else sep
+        mir = not args.no_mirror
+        sep = [scheduler.AssemblyPlan(dm, s, pk, cfg["orders"], rng, mirror=mir) for s in specs]
+        main = [scheduler.AssemblyPlan(dm, specs[0], pk, cfg["orders"], rng, pair=True,
+                                       mirror=mir)] if fused else sep
         st = torch.cuda.Stream(device=d)
         for p in sep + main:
             p.set_stream(st.cuda_stream)   # one timeline per device
@@ -607,6 +608,7 @@ def run_ours(args, cfg, dist, log):
         except (OSError, ValueError):
             traffic = None
     h2d = sum(p.h2d_bytes for dv in per_dev for p in dv[3])
+    mirrored_info = per_dev[0][3][0].layout.mirror_info if per_dev[0][3][0].mirrored else {}
     launches = args.steps * sum(1 + sum(1 for c in p.singular_counts if c)
                                 for dv in per_dev for p in dv[3])
     for dv in per_dev:
@@ -616,7 +618,8 @@ def run_ours(args, cfg, dist, log):
 
     # e2e through the public API, host buffers, H2D + D2H inside the step
     backend = scheduler.Backend("cuda", devices=tuple(devices))
-    params = scheduler.SchedulerParams(backends=(backend,), shard=shard)
+    params = scheduler.SchedulerParams(backends=(backend,), shard=shard,
+                                       mirror=not args.no_mirror)
     e2e_t, e2e_phases, d2h = [], [], 0
 
     def assemble_all(stats_list):
@@ -714,6 +717,8 @@ def run_ours(args, cfg, dist, log):
                    "operators": list(cfg["layers"]), "orders": list(cfg["orders"]),
                    "plan": "one fused SLP+DLP plan (scheduler.run_assembly_pair)" if fused
                    else "one plan per operator (scheduler.run_assembly)",
+                   "mirrored_evaluation": bool(mirrored_info) and not args.no_mirror,
+                   "mirror_counts": mirrored_info,
                    "l2": "flushed between steps (512 MiB device write)",
                    "parallelism": par},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -765,6 +770,9 @@ def main(argv=None):
                     help="reference arm: wall seconds of the sampled GCA clusters")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--no-mirror", action="store_true",
+                    help="evaluate every pair on its own (no symmetric evaluation of mirror "
+                         "leaves)")
     ap.add_argument("--no-separate", action="store_true",
                     help="skip timing the single-layer plans next to the fused one")
     ap.add_argument("--separate", action="store_true",

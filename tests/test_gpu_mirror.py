@@ -45,11 +45,18 @@ def test_mirrored_single_kinds_vs_oracle_and_plain(gload, eq, layer, kappa, orde
     ok, worst, _ = p2_check(pk, M.buffer, P.buffer, 1e-13, m, (eq, layer, kappa), orders,
                             ref_is_device=True)
     assert ok, ("plain", worst)
-    if layer == "single":   # the mirror of an SLP entry is the same value
+    if layer == "single":
+        # the mirror of a disjoint-rule SLP entry is the same value (entries of
+        # pairs sharing a vertex come from the singular rules of (i, j) and
+        # (j, i), which agree only to the rules' accuracy, as in the reference)
         for l in bt.leaves[::7]:
             if l.kind == "dense" and l.row != l.col:
                 mir = next(x for x in bt.leaves if x.row == l.col and x.col == l.row)
-                assert np.array_equal(M.payloads[l.index], M.payloads[mir.index].T)
+                ta = m.triangles[t.panels(t.nodes[l.row])]
+                tb = m.triangles[t.panels(t.nodes[l.col])]
+                touch = (ta[:, None, :, None] == tb[None, :, None, :]).any(axis=(2, 3))
+                A, B = M.payloads[l.index], M.payloads[mir.index].T
+                assert np.array_equal(A[~touch], B[~touch])
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
