@@ -258,10 +258,17 @@ constexpr int disjoint_minb(int n, int kind) {
 
 // mirrored kernels (MIR) carry a third accumulator pair (the transposed
 // double layer): one CTA fewer per SM than the plain kernel of the kind
+#ifndef GCABEM_MIR_MINB_LPAIR
+#define GCABEM_MIR_MINB_LPAIR 3
+#endif
+#ifndef GCABEM_MIR_MINB_HPAIR
+#define GCABEM_MIR_MINB_HPAIR 4
+#endif
 constexpr int disjoint_minb_mir(int n, int kind) {
     return n > 7 ? 1 : kind == L_SLP ? 7 : kind == H_SLP ? 5
            : kind == L_DLP ? 5 : kind == H_DLP ? 4
-           : n <= 4 ? (kind == L_PAIR ? 4 : 4) : n <= 6 ? 3 : 2;
+           : n <= 4 ? (kind == L_PAIR ? GCABEM_MIR_MINB_LPAIR : GCABEM_MIR_MINB_HPAIR)
+           : n <= 6 ? 3 : 2;
 }
 
 template <int N, int KIND, bool MIR>

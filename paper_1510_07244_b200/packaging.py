@@ -135,6 +135,7 @@ class AssemblyPackages:
 
 _tree_cache: dict = {}
 _leaf_cache: dict = {}
+_mirror_cache: dict = {}
 _cache_lock = threading.Lock()
 
 
@@ -277,19 +278,24 @@ def leaf_mirrors(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs 
     if block_tree.row_tree is not block_tree.col_tree or row_ops is not col_ops:
         return None
     x = inputs or package_inputs(np.zeros((0, 3), np.int64), block_tree, row_ops, col_ops)
-    leaves = x.leaves
-    lo, hi = (0, leaves.shape[0]) if leaf_range is None else leaf_range
-    n = np.int64(len(block_tree.row_tree.nodes))
-    key = leaves[:, 0] * n + leaves[:, 1]
-    order = np.argsort(key, kind="stable")
-    want = leaves[lo:hi, 1] * n + leaves[lo:hi, 0]
-    pos = np.searchsorted(key[order], want)
-    pos = np.minimum(pos, key.size - 1)
-    hit = key[order][pos] == want
-    m = np.where(hit, order[pos], -1)
-    if not np.all(hit) or not np.array_equal(leaves[m, 2], leaves[lo:hi, 2]):
-        return None          # not a symmetric block tree: no mirrored evaluation
-    m = m - lo
+
+    def build(bt):   # whole-tree map, once per block tree (it does not depend on ops)
+        leaves = x.leaves
+        n = np.int64(len(bt.row_tree.nodes))
+        key = leaves[:, 0] * n + leaves[:, 1]
+        order = np.argsort(key, kind="stable")
+        want = leaves[:, 1] * n + leaves[:, 0]
+        pos = np.minimum(np.searchsorted(key[order], want), max(key.size - 1, 0))
+        hit = key[order][pos] == want if key.size else np.zeros(0, bool)
+        m = np.where(hit, order[pos], -1)
+        if not np.all(hit) or not np.array_equal(leaves[m, 2], leaves[:, 2]):
+            return None      # not a symmetric block tree: no mirrored evaluation
+        return m.astype(np.int64)
+    full = _cached(_mirror_cache, block_tree, build)
+    if full is None:
+        return None
+    lo, hi = (0, full.size) if leaf_range is None else leaf_range
+    m = full[lo:hi] - lo
     m[(m < 0) | (m >= hi - lo)] = -1
     return np.ascontiguousarray(m, dtype=np.int64)
 
