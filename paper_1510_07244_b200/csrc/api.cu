@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -111,6 +112,10 @@ struct gcabem_plan_s {
     PoolBuf<double2> payload2;  // pair kinds: the double layer
     PoolBuf<double> srule[3];
     int64_t sq[3] = {0, 0, 0};
+    // x-grouped vertex and edge rules (kernels.cu generic_pair_grouped)
+    PoolBuf<double> grows[3], ggroups[3];
+    PoolBuf<int4> gchunks[3];
+    int gn[3] = {0, 0, 0};
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> chunk_ev;
     cudaStream_t stream = nullptr;  // kernels (own_stream, or the caller's)
@@ -803,6 +808,53 @@ int gcabem_layout_release(gcabem_layout_t L) {
 }  // extern "C"
 
 namespace {
+// Group the points of a staged singular rule (rows {xs, xt, ys, yt, w}) by
+// their x point, in first-appearance order, packed into chunks of at most
+// RULE_CHUNK rows and groups (a group larger than a chunk is split into
+// groups with the same x point).
+void group_rule(const double *r5, int64_t q, std::vector<double> &rows,
+                std::vector<double> &groups, std::vector<int4> &chunks) {
+    std::vector<std::pair<std::pair<double, double>, std::vector<int64_t>>> order;
+    std::map<std::pair<uint64_t, uint64_t>, size_t> at;
+    for (int64_t k = 0; k < q; ++k) {
+        uint64_t a, b;
+        std::memcpy(&a, r5 + 5 * k, 8);
+        std::memcpy(&b, r5 + 5 * k + 1, 8);
+        auto it = at.find({a, b});
+        if (it == at.end()) {
+            at.emplace(std::make_pair(a, b), order.size());
+            order.push_back({{r5[5 * k], r5[5 * k + 1]}, {k}});
+        } else {
+            order[it->second].second.push_back(k);
+        }
+    }
+    rows.clear();
+    groups.clear();
+    chunks.clear();
+    int r0 = 0, g0 = 0, nr = 0, ng = 0;
+    for (auto &grp : order) {
+        const auto &idx = grp.second;
+        for (size_t p0 = 0; p0 < idx.size(); p0 += RULE_CHUNK) {
+            const int piece = (int)std::min<size_t>(RULE_CHUNK, idx.size() - p0);
+            if (nr + piece > RULE_CHUNK || ng + 1 > RULE_CHUNK) {
+                chunks.push_back(make_int4(r0, r0 + nr, g0, g0 + ng));
+                r0 += nr;
+                g0 += ng;
+                nr = ng = 0;
+            }
+            groups.insert(groups.end(), {grp.first.first, grp.first.second,
+                                         (double)(r0 + nr), (double)piece});
+            for (int j = 0; j < piece; ++j) {
+                const double *r = r5 + 5 * idx[p0 + j];
+                rows.insert(rows.end(), {r[2], r[3], r[4]});
+            }
+            nr += piece;
+            ++ng;
+        }
+    }
+    if (nr > 0) chunks.push_back(make_int4(r0, r0 + nr, g0, g0 + ng));
+}
+
 int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
                      const double *gauss_pts, const double *gauss_wts, const int64_t *sq,
                      const double *const *srule, gcabem_plan_t *out);
@@ -863,6 +915,19 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
         p->sq[c] = sq ? sq[c] : 0;
         if (p->sq[c] > 0 && L->case_at[c + 1] > L->case_at[c])
             e = p->srule[c].upload(srule[c], 5 * p->sq[c], p->stream);
+        // vertex and edge items: the x-grouped rule (the identical case keeps
+        // its exact-difference form); GCABEM_NO_GROUPED=1 turns it off
+        static const bool no_grouped = std::getenv("GCABEM_NO_GROUPED") != nullptr;
+        if (e == cudaSuccess && c < 2 && !no_grouped && p->sq[c] > 0 &&
+            L->case_at[c + 1] > L->case_at[c]) {
+            std::vector<double> rows, groups;
+            std::vector<int4> chunks;
+            group_rule(srule[c], p->sq[c], rows, groups, chunks);
+            e = p->grows[c].upload(rows.data(), rows.size(), p->stream);
+            if (e == cudaSuccess) e = p->ggroups[c].upload(groups.data(), groups.size(), p->stream);
+            if (e == cudaSuccess) e = p->gchunks[c].upload(chunks.data(), chunks.size(), p->stream);
+            p->gn[c] = (int)chunks.size();
+        }
     }
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
@@ -900,6 +965,17 @@ namespace {
 
 // Launch the kernels of blocks [b0, b1) and of the singular items whose
 // payload index lies in [p0, p1) on the plan stream.
+GroupedRule grouped_of(gcabem_plan_t p, int c) {
+    GroupedRule g;
+    if (p->gn[c] > 0) {
+        g.rows = p->grows[c].p;
+        g.groups = p->ggroups[c].p;
+        g.chunks = p->gchunks[c].p;
+        g.nchunks = p->gn[c];
+    }
+    return g;
+}
+
 // Disjoint kernels of blocks [b0, b1): the plain kernel over every task, or
 // (mirrored plan) the plain kernel over the NORMAL blocks' tasks and the
 // mirrored kernel over the PRIMARY/SELF blocks' tasks (SKIP blocks: none).
@@ -937,7 +1013,7 @@ int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p
         if (i1 <= i0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->L->items.p + i0,
                                i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->payload2.p,
-                               p->kappa, s));
+                               p->kappa, s, grouped_of(p, c)));
     }
     return GCABEM_OK;
 }
@@ -959,7 +1035,7 @@ int gcabem_plan_execute(gcabem_plan_t p) {
         if (n == 0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
                                p->L->items.p + p->L->case_at[c], n, p->srule[c].p, p->sq[c],
-                               p->payload.p, p->payload2.p, p->kappa, s));
+                               p->payload.p, p->payload2.p, p->kappa, s, grouped_of(p, c)));
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
@@ -1099,6 +1175,9 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
     p->payload2.release();
     tr.mark("free");
     for (auto &r : p->srule) r.release();
+    for (auto &r : p->grows) r.release();
+    for (auto &r : p->ggroups) r.release();
+    for (auto &r : p->gchunks) r.release();
     cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
     if (mine) cudaStreamDestroy(mine);
     if (p->copy) cudaStreamDestroy(p->copy);

@@ -89,10 +89,19 @@ cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int3
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
 // same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).
+// x-grouped form of a singular rule (kernels.cu generic_pair_grouped): rows
+// {ys, yt, w}, groups {xs, xt, first row, row count} (doubles), chunks
+// {row0, row1, group0, group1} of at most RULE_CHUNK rows / groups each.
+struct GroupedRule {
+    const double *rows = nullptr;
+    const double *groups = nullptr;
+    const int4 *chunks = nullptr;
+    int nchunks = 0;
+};
 cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int32_t *T,
                            const Chart *charts, const SingItem *items, int64_t n,
                            const double *rule, int64_t q, double2 *payload, double2 *payload2,
-                           double kappa, cudaStream_t s);
+                           double kappa, cudaStream_t s, GroupedRule grouped = GroupedRule());
 // Raw charts (gcabem_pair_values): per pair 22 doubles
 // {ox,e1x,e2x, oy,e1y,e2y, ny} (21) + gx, gy packed as 24 doubles.
 cudaError_t launch_raw(int kind, const double *pairs, int64_t n, const double *rule, int64_t q,
