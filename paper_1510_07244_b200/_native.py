@@ -57,6 +57,7 @@ _SIGS = {
                                     _int),
     "gcabem_layout_mirror_info": ([_vp, _vp], _int),
     "gcabem_plan_set_mirror": ([_vp, _int], _int),
+    "gcabem_plan_singular_evals": ([_vp, _vp], _int),
     "gcabem_plan_mirrored": ([_vp, ctypes.POINTER(_int)], _int),
     "gcabem_plan_create_on": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _vp,
                                ctypes.POINTER(_vp)], _int),

@@ -716,6 +716,36 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     L->ntasks = ntasks;
     L->nmtasks = nmt;
     L->nrtasks = nrt;
+    std::vector<SingItem> vm, vp;
+    std::vector<int64_t> vm_mout;
+    if (any_mirror) {
+        // vertex items (case slot 0, sorted by payload index) -> mirrored /
+        // plain / written-by-partner, from their leaf's role
+        int64_t dropped = 0;
+        for (int64_t q = L->case_at[0]; q < L->case_at[1]; ++q) {
+            const SingItem &it = si[q];
+            const int64_t g = it.out + base0;
+            const int64_t lf = std::upper_bound(leaf_base + leaf_lo, leaf_base + leaf_hi + 1, g) -
+                               leaf_base - 1;
+            const int r = role_of(lf);
+            const int64_t ncol = leaf_shape[2 * lf + 1], off = g - leaf_base[lf];
+            const int64_t i = off / ncol, j = off % ncol;
+            if (r == ROLE_PRIMARY || (r == ROLE_SELF && i < j)) {
+                const int64_t m = leaf_mirror[lf];
+                vm.push_back(it);
+                vm_mout.push_back(leaf_base[m] - base0 + j * leaf_shape[2 * m + 1] + i);
+            } else if (r == ROLE_NORMAL) {
+                vp.push_back(it);
+            } else {
+                ++dropped;
+            }
+        }
+        L->vertex_mirror = dropped == (int64_t)vm.size();
+        if (L->vertex_mirror) {
+            for (const auto &it : vm) L->vm_out.push_back(it.out);
+            for (const auto &it : vp) L->vp_out.push_back(it.out);
+        }
+    }
     if (any_mirror) {
         // evaluation counts for the roofline: pairs of PRIMARY/SELF(upper)
         // blocks minus their vertex-sharing pairs (one mirrored evaluation
@@ -765,6 +795,11 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     if (e == cudaSuccess && nrt) e = cudaMemcpyAsync(L->rtasks.p, rtasks, sizeof(int2) * nrt, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && npanels) e = cudaMemcpyAsync(L->panels.p, pan, sizeof(int32_t) * npanels, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && S) e = cudaMemcpyAsync(L->items.p, si, sizeof(SingItem) * S, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && L->vertex_mirror) {
+        e = L->vm_items.upload(vm.data(), vm.size(), s);
+        if (e == cudaSuccess) e = L->vm_mout.upload(vm_mout.data(), vm_mout.size(), s);
+        if (e == cudaSuccess) e = L->vp_items.upload(vp.data(), vp.size(), s);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the arena is reused after this
     tr.mark("upload");
     if (e != cudaSuccess) {
@@ -976,6 +1011,12 @@ GroupedRule grouped_of(gcabem_plan_t p, int c) {
     return g;
 }
 
+// vertex items on the mirrored path: a mirrored plan whose layout split the
+// vertex items and whose vertex rule is x-grouped
+bool vertex_mirrored(gcabem_plan_t p) {
+    return p->mirrored && p->L->vertex_mirror && p->gn[0] > 0;
+}
+
 // Disjoint kernels of blocks [b0, b1): the plain kernel over every task, or
 // (mirrored plan) the plain kernel over the NORMAL blocks' tasks and the
 // mirrored kernel over the PRIMARY/SELF blocks' tasks (SKIP blocks: none).
@@ -1006,6 +1047,20 @@ int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p
     cudaStream_t s = p->stream;
     if (int rc = enqueue_disjoint(p, b0, b1)) return rc;
     for (int c = 0; c < 3; ++c) {
+        if (c == 0 && vertex_mirrored(p)) {
+            gcabem_layout_t L = p->L;
+            const int64_t a0 = std::lower_bound(L->vm_out.begin(), L->vm_out.end(), p0) - L->vm_out.begin();
+            const int64_t a1 = std::lower_bound(L->vm_out.begin(), L->vm_out.end(), p1) - L->vm_out.begin();
+            GC_CUDA(launch_generic_mirror(p->kind, m->V.p, m->T.p, m->charts.p, L->vm_items.p + a0,
+                                          L->vm_mout.p + a0, a1 - a0, p->payload.p, p->payload2.p,
+                                          p->kappa, s, grouped_of(p, 0)));
+            const int64_t q0 = std::lower_bound(L->vp_out.begin(), L->vp_out.end(), p0) - L->vp_out.begin();
+            const int64_t q1 = std::lower_bound(L->vp_out.begin(), L->vp_out.end(), p1) - L->vp_out.begin();
+            GC_CUDA(launch_generic(p->kind, false, m->V.p, m->T.p, m->charts.p, L->vp_items.p + q0,
+                                   q1 - q0, p->srule[0].p, p->sq[0], p->payload.p, p->payload2.p,
+                                   p->kappa, s, grouped_of(p, 0)));
+            continue;
+        }
         const auto first = p->L->item_out.begin() + p->L->case_at[c];
         const auto last = p->L->item_out.begin() + p->L->case_at[c + 1];
         const int64_t i0 = std::lower_bound(first, last, p0) - p->L->item_out.begin();
@@ -1031,6 +1086,16 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     if (int rc = enqueue_disjoint(p, 0, (int64_t)p->L->block_leaf.size())) return rc;
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     for (int c = 0; c < 3; ++c) {
+        if (c == 0 && vertex_mirrored(p)) {
+            gcabem_layout_t L = p->L;
+            GC_CUDA(launch_generic_mirror(p->kind, m->V.p, m->T.p, m->charts.p, L->vm_items.p,
+                                          L->vm_mout.p, (int64_t)L->vm_out.size(), p->payload.p,
+                                          p->payload2.p, p->kappa, s, grouped_of(p, 0)));
+            GC_CUDA(launch_generic(p->kind, false, m->V.p, m->T.p, m->charts.p, L->vp_items.p,
+                                   (int64_t)L->vp_out.size(), p->srule[0].p, p->sq[0],
+                                   p->payload.p, p->payload2.p, p->kappa, s, grouped_of(p, 0)));
+            continue;
+        }
         const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
         if (n == 0) continue;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
@@ -1039,6 +1104,17 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
+    return GCABEM_OK;
+}
+
+int gcabem_plan_singular_evals(gcabem_plan_t p, int64_t *out4) {
+    GC_ARG(p && out4, "null argument");
+    gcabem_layout_t L = p->L;
+    const bool vm = vertex_mirrored(p);
+    out4[0] = vm ? (int64_t)L->vm_out.size() : 0;
+    out4[1] = vm ? (int64_t)L->vp_out.size() : L->case_at[1] - L->case_at[0];
+    out4[2] = L->case_at[2] - L->case_at[1];
+    out4[3] = L->case_at[3] - L->case_at[2];
     return GCABEM_OK;
 }
 

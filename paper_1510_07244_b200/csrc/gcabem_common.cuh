@@ -102,6 +102,12 @@ cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int
                            const Chart *charts, const SingItem *items, int64_t n,
                            const double *rule, int64_t q, double2 *payload, double2 *payload2,
                            double kappa, cudaStream_t s, GroupedRule grouped = GroupedRule());
+// mirrored vertex items: item idx also writes the transposed pair at mout[idx]
+cudaError_t launch_generic_mirror(int kind, const double *V, const int32_t *T,
+                                  const Chart *charts, const SingItem *items,
+                                  const int64_t *mout, int64_t n, double2 *payload,
+                                  double2 *payload2, double kappa, cudaStream_t s,
+                                  GroupedRule grouped);
 // Raw charts (gcabem_pair_values): per pair 22 doubles
 // {ox,e1x,e2x, oy,e1y,e2y, ny} (21) + gx, gy packed as 24 doubles.
 cudaError_t launch_raw(int kind, const double *pairs, int64_t n, const double *rule, int64_t q,

@@ -129,6 +129,15 @@ struct gcabem_layout_s {
     // {evaluations by the mirrored kernel, by the plain kernel (pairs sharing
     // a vertex excluded), pairs of PRIMARY/SELF blocks, pairs of SKIP blocks}
     int64_t mirror_info[4] = {0, 0, 0, 0};
+    // vertex items split for mirrored execution (the vertex rule is symmetric):
+    // vm = items of PRIMARY / SELF-upper positions, each also writing its
+    // transpose at vm_mout; vp = items of NORMAL leaves (alone); the items of
+    // SKIP / SELF-lower positions are written by their partners. Empty unless
+    // every partner was found.
+    gcabem::PoolBuf<gcabem::SingItem> vm_items, vp_items;
+    gcabem::PoolBuf<int64_t> vm_mout;
+    std::vector<int64_t> vm_out, vp_out;
+    bool vertex_mirror = false;
     gcabem::PoolBuf<int32_t> panels;
     gcabem::PoolBuf<gcabem::SingItem> items;
     int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])

@@ -41,13 +41,14 @@ def pair_flops(spec, family: str, q: int, pair: bool = False) -> int:
     return q * point_flops(spec, family, pair) + (2 if pair else 1) * PAIR_OVERHEAD
 
 
-def mirror_pair_flops(spec, q: int, pair: bool = False) -> int:
-    """Flops of one mirrored disjoint evaluation: pair (i, j) and its
-    transpose (j, i) with a Q-point rule (pair: both layers of each)."""
+def mirror_pair_flops(spec, q: int, pair: bool = False, family: str = "disjoint") -> int:
+    """Flops of one mirrored evaluation: pair (i, j) and its transpose (j, i)
+    with a Q-point rule (pair: both layers of each); family "singular" for
+    the symmetric vertex rule (mapping included)."""
     if spec.layer == "single" and not pair:
-        f = point_flops(spec, "disjoint")            # symmetric: the value is shared
+        f = point_flops(spec, family)                # symmetric: the value is shared
     else:
-        f = point_flops(spec, "disjoint", pair) + F_MIRROR_EXTRA[spec.equation]
+        f = point_flops(spec, family, pair) + F_MIRROR_EXTRA[spec.equation]
     return q * f + (4 if pair else 2) * PAIR_OVERHEAD
 
 

@@ -476,8 +476,13 @@ class AssemblyPlan:
         else:
             computed = self.disjoint_pairs - sum(self.singular_counts)
             dis = pair_flops(self.spec, "disjoint", dq, self.pair) * computed
-        sing = sum(pair_flops(self.spec, "singular", q, self.pair) * n
-                   for q, n in zip(self.singular_q, self.singular_counts))
+        ev = np.zeros(4, np.int64)
+        nat.check(nat.lib().gcabem_plan_singular_evals(self.handle, nat.ptr(ev)))
+        sing = sum(pair_flops(self.spec, "singular", q, self.pair) * int(n)
+                   for q, n in zip(self.singular_q, ev[1:]))
+        # vertex items evaluated with their transpose (symmetric vertex rule)
+        sing += mirror_pair_flops(self.spec, self.singular_q[0], self.pair, "singular") * \
+            int(ev[0])
         return {"disjoint": dis, "singular": sing}
 
     def close(self) -> None:

@@ -11,7 +11,8 @@ quadrature.py:108), so one thread evaluates pair (i, j) and (j, i) together
   written by its earlier PRIMARY before that chunk's copy) equals the
   one-shot execute + download bit for bit;
 * the evaluation accounting of the layout (roofline flops): every pair of a
-  mirrored leaf pair is evaluated once.
+  mirrored leaf pair is evaluated once, and so is every vertex item pair (the
+  vertex rule, quadrature.py:112-117, is symmetric under x <-> y).
 """
 import numpy as np
 import pytest
@@ -128,5 +129,17 @@ def test_mirror_evaluation_accounting(gload):
     assert mi["evals_plain"] <= plain_pairs
     fm, fp = mp.flops()["disjoint"], pp.flops()["disjoint"]
     assert fm < fp and fm > 0.5 * fp
+    # vertex items: the symmetric vertex rule evaluates (i, j) and (j, i)
+    # together; the partners are not evaluated again
+    import ctypes
+    from paper_1510_07244_b200 import _native as nat
+    ev = np.zeros(4, np.int64)
+    nat.check(nat.lib().gcabem_plan_singular_evals(mp.handle, nat.ptr(ev)))
+    nv = int(np.count_nonzero(pk.item_case == 1))
+    assert ev[0] > 0 and 2 * ev[0] + ev[1] == nv
+    assert ev[2] == np.count_nonzero(pk.item_case == 2)
+    nat.check(nat.lib().gcabem_plan_singular_evals(pp.handle, nat.ptr(ev)))
+    assert ev[0] == 0 and ev[1] == nv
+    assert mp.flops()["singular"] < pp.flops()["singular"]
     mp.close()
     pp.close()
