@@ -81,6 +81,12 @@ __device__ __forceinline__ void accumulate_any(double r2, double dn, double dnm,
 #ifndef GCABEM_XSMEM
 #define GCABEM_XSMEM 0
 #endif
+// accumulate every point straight into the pair's sums with weight wx wy
+// (no per-x-point partial sums: 12 fewer live registers, one product more
+// per point)
+#ifndef GCABEM_DIRECT_ACC
+#define GCABEM_DIRECT_ACC 0
+#endif
 
 // MIR: also the transposed pair (j, i) (ROLE_PRIMARY / ROLE_SELF blocks): its
 // double layer needs d . n_x, n_x the x panel's normal (nx); dnm = -d . n_x =
@@ -152,7 +158,15 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
             const double xonm = DM ? fma(t, M2, ms) : 0.0;
             const double a2 = fma(t, XC(8), as);
             const double b2 = fma(t, XC(11), bs);
-            double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#if GCABEM_DIRECT_ACC
+            double *in = acc;   // the point weight carries wx (one product per point)
+#else
+    #if GCABEM_DIRECT_ACC
+        double *in = acc;
+#else
+        double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#endif
+#endif
             // fused pair kinds at orders >= 6 roll the outer y loop (the fully
             // unrolled N^2 body spills their two layers of state)
             constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
@@ -162,7 +176,15 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
                     const double gc = c_gauss[N][c];
-                    const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+#if GCABEM_DIRECT_ACC
+                    const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
+#else
+    #if GCABEM_DIRECT_ACC
+                const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
+#else
+                const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+#endif
+#endif
                     const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
                     const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
                     const double dnm = DM ? fma(gc, unm[d], -xonm) : 0.0;
@@ -171,7 +193,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
             }
 #pragma unroll
             for (int k = 0; k < 6; ++k)
-                if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
+                if (!GCABEM_DIRECT_ACC && slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
         }
     }
 #undef XC
@@ -205,14 +227,22 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         const double xonm = DM ? fma(xo0, nx[0], fma(xo1, nx[1], xo2 * nx[2])) : 0.0;
+#if GCABEM_DIRECT_ACC
+        double *in = acc;
+#else
         double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#endif
         constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;  // see disjoint_expanded
 #pragma unroll OUTER
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
 #pragma unroll
             for (int d = 0; d < N; ++d) {
+#if GCABEM_DIRECT_ACC
+                const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
+#else
                 const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
+#endif
                 const double dx = fma(-gc, ux[d], xo0);
                 const double dy = fma(-gc, uy[d], xo1);
                 const double dz = fma(-gc, uz[d], xo2);
@@ -224,7 +254,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k)
-            if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
+            if (!GCABEM_DIRECT_ACC && slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
     }
 }
 
