@@ -744,7 +744,52 @@ def run_ours(args, cfg, dist, log):
         line["matvec"] = matvec_line
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if single_device and not args.no_secondary and args.config == "c3":
+        line["secondary"] = {"c5_order3": secondary_c5(devices[0], peak, log)}
     return line if dist.rank == 0 else None
+
+
+def secondary_c5(device, peak, log):
+    """C5 at n = 3 (BASELINE configs[4]: L8 sphere, 524,288 triangles,
+    Helmholtz kappa=4 SLP+DLP, disjoint = singular order 3): the device step
+    of the fused mirrored pair plan only (value and roofline, no e2e)."""
+    import torch
+
+    from paper_1510_07244_b200 import device as devmod
+    from paper_1510_07244_b200 import kernels, packaging, scheduler
+    cfg = dict(CONFIGS["c5"])
+    t0 = time.perf_counter()
+    m, bt, ops, st = build_workload(cfg, [device], None, log, warm_gca=False)
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    spec = kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"])
+    plan = scheduler.AssemblyPlan(devmod.device_mesh(m, device), spec, pk, cfg["orders"],
+                                  pair=True)
+    stream = torch.cuda.Stream(device=device)
+    plan.set_stream(stream.cuda_stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms, dk = [], []
+    for k in range(5):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            ev0.record(stream)
+            plan.execute()
+            ev1.record(stream)
+        stream.synchronize()
+        if k >= 2:   # 2 warm-up steps
+            ms.append(ev0.elapsed_time(ev1))
+            dk.append(plan.timing_ms()["disjoint"])
+    fl = plan.flops()
+    res = {"workload": cfg["workload"] + ", orders 3/3", "pairs_per_step": 2 * pk.payload_len,
+           "ms_per_step": statistics.mean(ms),
+           "value": 2 * pk.payload_len / (statistics.mean(ms) * 1e-3), "unit": UNIT,
+           "roofline_frac": fl["disjoint"] / (statistics.mean(dk) * 1e-3) / 1e12 / peak,
+           "gca_s": round(st["gca_s"], 3), "build_s": round(time.perf_counter() - t0, 1)}
+    plan.close()
+    del plan, pk
+    devmod.release_cached(device)
+    log(f"secondary C5 n=3: {res}")
+    return res
 
 
 def _hbm_peak():
@@ -773,6 +818,8 @@ def main(argv=None):
     ap.add_argument("--no-mirror", action="store_true",
                     help="evaluate every pair on its own (no symmetric evaluation of mirror "
                          "leaves)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C5 (order 3) device-step key of the default C3 line")
     ap.add_argument("--no-separate", action="store_true",
                     help="skip timing the single-layer plans next to the fused one")
     ap.add_argument("--separate", action="store_true",
