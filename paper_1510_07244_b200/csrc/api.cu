@@ -722,11 +722,11 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
         // vertex items (case slot 0, sorted by payload index) -> mirrored /
         // plain / written-by-partner, from their leaf's role
         int64_t dropped = 0;
+        int64_t lf = leaf_lo;   // items are in payload order: walk the leaves alongside
         for (int64_t q = L->case_at[0]; q < L->case_at[1]; ++q) {
             const SingItem &it = si[q];
             const int64_t g = it.out + base0;
-            const int64_t lf = std::upper_bound(leaf_base + leaf_lo, leaf_base + leaf_hi + 1, g) -
-                               leaf_base - 1;
+            while (lf + 1 < leaf_hi && leaf_base[lf + 1] <= g) ++lf;
             const int r = role_of(lf);
             const int64_t ncol = leaf_shape[2 * lf + 1], off = g - leaf_base[lf];
             const int64_t i = off / ncol, j = off % ncol;
@@ -745,6 +745,7 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
             for (const auto &it : vm) L->vm_out.push_back(it.out);
             for (const auto &it : vp) L->vp_out.push_back(it.out);
         }
+        tr.mark("mirror-split");
     }
     if (any_mirror) {
         // evaluation counts for the roofline: pairs of PRIMARY/SELF(upper)

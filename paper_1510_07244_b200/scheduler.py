@@ -18,6 +18,7 @@ library or device raises BackendError.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 import time
 import weakref
@@ -40,7 +41,7 @@ from .quadrature import QuadRule4D, build_rule, classify_pair, gauss_legendre
 DEFAULT_MAXSIZE = 8 * 2 ** 20
 # payload growth between consecutive ranges of a staged assembly (measured at
 # C3: 1.5 with 6 ranges beats 2 with 5 by ~5% e2e)
-STAGE_GROWTH = 1.5
+STAGE_GROWTH = float(os.environ.get("GCABEM_STAGE_GROWTH", "1.5"))
 _CASE_OF_SHARED = {1: "vertex", 2: "edge", 3: "identical"}
 
 __all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "AssemblyStats",
