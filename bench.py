@@ -481,7 +481,8 @@ def run_ours(args, cfg, dist, log):
     """The device path. Under torchrun (N ranks) the default is ONE job split
     over the ranks (--mode strong): each rank builds its part of the GCA
     clusters (pivots all-gathered: the only exchange), packages its leaf
-    window (scheduler.shard_window) and assembles it on its GPU. Without
+    leaf set (packaging.shard_leaf_set: every leaf with its mirror, so the
+    mirrored evaluation stays inside the rank) and assembles it on its GPU. Without
     torchrun, --gpus N splits the job over N devices of this process."""
     import torch
 
@@ -508,16 +509,17 @@ def run_ours(args, cfg, dist, log):
         not args.separate
     # this process's leaves: its window of the job (strong) or everything
     t2 = time.perf_counter()
-    window = scheduler.shard_window(m, bt, ops, ops, shard, cfg["orders"][0] ** 4) \
+    leaf_set = scheduler.shard_leaves_of(m, bt, ops, ops, shard, cfg["orders"][0] ** 4) \
         if shard else None
     pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE,
-                                 leaf_range=window)
+                                 leaf_index=leaf_set)
     setup_t["packaging_s"] = time.perf_counter() - t2
     L = pk.leaf_ids.size
     sq = [scheduler.build_rule(c, cfg["orders"][1]).num_points
           for c in ("vertex", "edge", "identical")]
     dev_ranges = scheduler._split_range(pk, (0, L), len(devices), cfg["orders"][0] ** 4, sq)
-    log(f"rank {dist.rank}: window {window} leaves={L} entries={pk.payload_len} "
+    log(f"rank {dist.rank}: {'all' if leaf_set is None else 'a set of'} leaves={L} "
+        f"entries={pk.payload_len} "
         f"blocks={pk.num_blocks} singular={pk.num_items} devices={devices} {dev_ranges}")
 
     tp = time.perf_counter()
@@ -699,7 +701,7 @@ def run_ours(args, cfg, dist, log):
                 "total_warm_s": round(trees_s + gca_warm + e2e_dt, 3) if e2e_t else None,
                 "timing": "max over ranks of each phase; GCA first call of the process "
                           "(total_s) and a second call (total_warm_s)"}
-    par = (f"strong x{dist.world * len(devices)}: one job, GCA clusters and leaf windows "
+    par = (f"strong x{dist.world * len(devices)}: one job, GCA clusters and leaf sets "
            f"split over {'ranks' if dist.world > 1 else 'devices'} (pivot all-gather the only "
            f"exchange)") if strong and (dist.world > 1 or len(devices) > 1) else \
         (f"weak x{dist.world}, every rank its own job, no collectives" if dist.world > 1

@@ -95,10 +95,10 @@ class GCAMatrix:
     col_ops: dict
     payloads: dict
     buffer: np.ndarray | None = field(default=None, repr=False)
-    # (lo, hi): this matrix holds only the block-tree leaves [lo, hi) of the
-    # preorder (one process's shard of a job split over processes,
+    # sorted preorder positions of the block-tree leaves this matrix holds
+    # (one process's shard of a job split over processes,
     # SchedulerParams.shard); None = every leaf
-    leaf_window: tuple | None = None
+    shard_leaves: np.ndarray | None = field(default=None, repr=False)
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -107,8 +107,9 @@ class GCAMatrix:
 
     def checksum(self) -> str:
         """sha256 over all leaf payloads in block-tree preorder (h2.py:40-46)."""
-        if self.leaf_window is not None:
-            raise ValueError(f"a shard (leaves {self.leaf_window}) has no whole-matrix checksum")
+        if self.shard_leaves is not None:
+            raise ValueError(f"a shard ({self.shard_leaves.size} of {len(self.block_tree.leaves)} "
+                             "leaves) has no whole-matrix checksum")
         h = hashlib.sha256()
         for leaf in self.block_tree.leaves:
             h.update(np.ascontiguousarray(self.payloads[leaf.index]).tobytes())
@@ -190,9 +191,9 @@ class DeviceH2:
         import ctypes
         from . import _native as nat
         from .pairquad import default_device
-        if M.leaf_window is not None:
+        if M.shard_leaves is not None:
             raise ValueError("DeviceH2 needs the whole matrix, not a process shard "
-                             f"(leaves {M.leaf_window})")
+                             f"({M.shard_leaves.size} leaves)")
         self.device = default_device() if device is None else device
         nat.require_device(self.device)
         desc, base, buf, (rdesc, nro), (cdesc, nco), V = _leaf_arrays(M)

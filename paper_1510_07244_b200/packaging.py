@@ -266,7 +266,7 @@ def leaf_layout(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs |
 
 
 def leaf_mirrors(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs | None = None,
-                 leaf_range=None):
+                 leaf_range=None, leaf_index=None):
     """Position of each leaf's mirror, the leaf (s, t) of leaf (t, s), or
     None when the block tree's two sides differ. With one cluster tree and
     one operator set on both sides (the reference's pipelines:
@@ -294,25 +294,75 @@ def leaf_mirrors(block_tree: BlockTree, row_ops, col_ops, inputs: PackageInputs 
     full = _cached(_mirror_cache, block_tree, build)
     if full is None:
         return None
+    if leaf_index is not None:   # a leaf set (sorted positions): mirrors inside it
+        idx = np.asarray(leaf_index, dtype=np.int64)
+        pos = np.full(full.size, -1, np.int64)
+        pos[idx] = np.arange(idx.size)
+        return np.ascontiguousarray(pos[full[idx]], dtype=np.int64)
     lo, hi = (0, full.size) if leaf_range is None else leaf_range
     m = full[lo:hi] - lo
     m[(m < 0) | (m >= hi - lo)] = -1
     return np.ascontiguousarray(m, dtype=np.int64)
 
 
+def full_leaf_mirrors(block_tree: BlockTree, row_ops, col_ops, inputs=None):
+    """Whole-tree mirror positions (leaf_mirrors without a range), or None."""
+    return leaf_mirrors(block_tree, row_ops, col_ops, inputs)
+
+
+def shard_leaf_set(block_tree: BlockTree, row_ops, col_ops, shard, disjoint_q: int,
+                   inputs: PackageInputs | None = None) -> np.ndarray:
+    """Leaves of process `rank` of `world` when one assembly is split over
+    processes: sorted preorder positions. Each leaf travels with its mirror
+    (leaf (s, t) of leaf (t, s)), so the mirrored evaluation stays inside a
+    process: the leaf pairs, keyed by their first leaf in the preorder, are
+    cut into `world` contiguous runs balanced by disjoint-rule points (one
+    evaluation per mirrored pair). Without mirrors (different trees or
+    operators) the sets are contiguous preorder ranges. Every process
+    computes the same sets from the payload layout alone."""
+    rank, world = int(shard[0]), int(shard[1])
+    if not 0 <= rank < world:
+        raise SchedulerConfigError(f"shard {shard}: need 0 <= rank < world")
+    x = inputs or package_inputs(np.zeros((0, 3), np.int64), block_tree, row_ops, col_ops)
+    _, shape, _ = leaf_layout(block_tree, row_ops, col_ops, x)
+    L = shape.shape[0]
+    if world == 1 or L == 0:
+        return np.arange(L, dtype=np.int64)
+    m = leaf_mirrors(block_tree, row_ops, col_ops, x)
+    work = (shape[:, 0] * shape[:, 1]).astype(np.float64) * disjoint_q
+    if m is None:
+        first = np.arange(L, dtype=np.int64)
+    else:
+        first = np.flatnonzero(m >= np.arange(L))     # primaries and diagonal leaves
+    cum = np.cumsum(work[first])
+    cuts = np.searchsorted(cum, cum[-1] * np.arange(1, world) / world, side="left") + 1
+    edges = np.maximum.accumulate(np.concatenate([[0], np.minimum(cuts, first.size),
+                                                  [first.size]]))
+    mine = first[edges[rank]:edges[rank + 1]]
+    if m is not None:
+        mine = np.union1d(mine, m[mine])
+    return np.ascontiguousarray(mine, dtype=np.int64)
+
+
 def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops,
                   maxsize: int, nthreads: int = 0, leaf_range=None,
-                  inputs: PackageInputs | None = None) -> AssemblyPackages:
+                  inputs: PackageInputs | None = None, leaf_index=None) -> AssemblyPackages:
     """Packages of the block tree's leaves (or of the leaves [lo, hi) of
     leaf_range, payload offsets then relative to leaf lo: the same blocks and
     corrective items those leaves get in the whole-tree packages, list ids
-    counted from 0). `inputs`: package_inputs() of the same arguments."""
+    counted from 0; or of the leaf set `leaf_index`, sorted preorder
+    positions, payload laid out leaf after leaf in that order).
+    `inputs`: package_inputs() of the same arguments."""
     if maxsize < BYTES_PER_PAIR:
         raise SchedulerConfigError(
             f"maxsize {maxsize} smaller than one pair record ({BYTES_PER_PAIR} B)")
     x = inputs or package_inputs(triangles, block_tree, row_ops, col_ops)
     T, leaves, leaf_ids = x.T, x.leaves, x.leaf_ids
-    if leaf_range is not None:
+    if leaf_index is not None:
+        leaf_index = np.asarray(leaf_index, dtype=np.int64)
+        leaves = np.ascontiguousarray(leaves[leaf_index])
+        leaf_ids = leaf_ids[leaf_index]
+    elif leaf_range is not None:
         lo, hi = leaf_range
         leaves, leaf_ids = leaves[lo:hi], leaf_ids[lo:hi]
     rs, rz, rlo, rhi, rperm = x.row
@@ -353,7 +403,7 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         n_disjoint_lists=nlists, item_case=items[0].astype(np.int8), item_tri_x=items[1],
         item_tri_y=items[2], item_leaf=items[3], item_offset=items[4],
         item_src_block=items[5], perms=perms,
-        leaf_mirror=leaf_mirrors(block_tree, row_ops, col_ops, x, leaf_range))
+        leaf_mirror=leaf_mirrors(block_tree, row_ops, col_ops, x, leaf_range, leaf_index))
 
 
 def shard_leaves(pk: AssemblyPackages, nshards: int, disjoint_q: int, singular_q=None):

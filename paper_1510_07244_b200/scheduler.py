@@ -35,7 +35,7 @@ from .kernels import KernelSpec
 from .mesh import SurfaceMesh
 from .packaging import (BYTES_PER_PAIR, PAIR_RECORD_BYTES, SINGULAR_CASES, VALUE_BYTES,
                         AssemblyPackages, SchedulerConfigError, leaf_layout, make_packages,
-                        package_inputs, shard_leaves)
+                        package_inputs, shard_leaf_set, shard_leaves)
 from .quadrature import QuadRule4D, build_rule, classify_pair, gauss_legendre
 
 DEFAULT_MAXSIZE = 8 * 2 ** 20
@@ -581,28 +581,30 @@ class StagedPackages:
     the whole-tree packages restricted to its leaves (payload offsets relative
     to the range's first leaf).
 
-    window = (lo, hi): only the leaves [lo, hi) of the block tree (this
-    process's shard of a job split over processes, SchedulerParams.shard);
-    leaf_ids / leaf_shape / leaf_base / payload_len / offset() then describe
-    the window, offsets relative to its first leaf."""
+    leaf_set: only those leaves (sorted preorder positions: this process's
+    shard of a job split over processes, SchedulerParams.shard); the ranges
+    cut the set, and leaf_ids / leaf_shape / leaf_base / payload_len /
+    offset() describe the set's payload, its leaves back to back."""
 
     def __init__(self, mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
-                 maxsize: int, nstages: int, window=None, inputs=None):
+                 maxsize: int, nstages: int, leaf_set=None, inputs=None):
         inputs = inputs or package_inputs(mesh.triangles, block_tree, row_ops, col_ops)
         L_all = inputs.leaves.shape[0]
-        wlo, whi = (0, L_all) if window is None else (int(window[0]), int(window[1]))
-        if not 0 <= wlo <= whi <= L_all:
-            raise SchedulerConfigError(f"leaf window {window} outside 0..{L_all}")
-        self.window = (wlo, whi)
-        L = whi - wlo
+        sel = np.arange(L_all, dtype=np.int64) if leaf_set is None else \
+            np.asarray(leaf_set, dtype=np.int64)
+        if sel.size and (sel[0] < 0 or sel[-1] >= L_all or np.any(np.diff(sel) <= 0)):
+            raise SchedulerConfigError("leaf set must be sorted positions of the block tree")
+        contiguous = sel.size == 0 or sel[-1] - sel[0] + 1 == sel.size
+        self.leaf_set = sel
+        L = sel.size
         n = max(1, min(int(nstages), max(L, 1)))
         # range 0 = the first L/64 leaves, packaged at once (before the layout
         # is known: the device and the PCIe link start within milliseconds);
         # the rest is cut leaf-aligned into ranges growing geometrically
         # (payload weights 1, g, g^2, ... with g = STAGE_GROWTH), each packaged
-        # while the (longer) D2H of all earlier ranges runs
-        first = wlo + (L if n == 1 else max(1, L // 64))
-        self.ranges = [(wlo, first)]
+        # while the (longer) D2H of all earlier ranges runs. Ranges index the set.
+        first = L if n == 1 else max(1, L // 64)
+        self.ranges = [(0, first)]
         # allocated once at the maximum stage count and never replaced: the
         # worker thread stores into them while the ranges are still being cut
         self._pk = [None] * n
@@ -612,14 +614,19 @@ class StagedPackages:
         self.key = None
         args = (mesh.triangles, block_tree, row_ops, col_ops, int(maxsize))
 
+        def package(a, b):
+            if contiguous:
+                return make_packages(*args, leaf_range=(int(sel[0]) + a, int(sel[0]) + b),
+                                     inputs=inputs)
+            return make_packages(*args, leaf_index=sel[a:b], inputs=inputs)
+
         def work():
-            k = 0
             try:
-                self._pk[0] = make_packages(*args, leaf_range=self.ranges[0], inputs=inputs)
+                self._pk[0] = package(*self.ranges[0])
                 self._ready[0].set()
                 self._layout.wait()
                 for k in range(1, len(self.ranges)):
-                    self._pk[k] = make_packages(*args, leaf_range=self.ranges[k], inputs=inputs)
+                    self._pk[k] = package(*self.ranges[k])
                     self._ready[k].set()
             except BaseException as exc:  # re-raised by stage()
                 self._err = exc
@@ -629,20 +636,20 @@ class StagedPackages:
         self._thread = threading.Thread(target=work, name="gcabem-packaging", daemon=True)
         self._thread.start()
         try:
-            ids, shape, base = leaf_layout(block_tree, row_ops, col_ops, inputs)
-            self._base_all = base
-            self.leaf_ids = ids[wlo:whi]
-            self.leaf_shape = shape[wlo:whi]
-            self.leaf_base = base[wlo:whi + 1] - base[wlo]
-            self.payload_len = int(base[whi] - base[wlo])
+            ids, shape, _ = leaf_layout(block_tree, row_ops, col_ops, inputs)
+            self.leaf_ids = ids[sel]
+            self.leaf_shape = shape[sel]
+            base = np.zeros(L + 1, np.int64)
+            np.cumsum(self.leaf_shape[:, 0] * self.leaf_shape[:, 1], out=base[1:])
+            self.leaf_base = base
+            self.payload_len = int(base[-1])
             ranges = list(self.ranges)
-            if first < whi:
+            if first < L:
                 b0 = base[first]
                 w = STAGE_GROWTH ** np.arange(n - 1)
                 frac = np.cumsum(w)[:-1] / w.sum()
-                cuts = np.searchsorted(base, b0 + (base[whi] - b0) * frac, side="left")
-                edges = np.unique(np.concatenate([[first], np.clip(cuts, first + 1, whi),
-                                                  [whi]]))
+                cuts = np.searchsorted(base, b0 + (base[L] - b0) * frac, side="left")
+                edges = np.unique(np.concatenate([[first], np.clip(cuts, first + 1, L), [L]]))
                 ranges += [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
             self.ranges = ranges
         finally:
@@ -651,7 +658,7 @@ class StagedPackages:
     def chunks(self, k: int, total: int) -> int:
         """D2H chunks of range k: about `total` over all ranges, by size."""
         lo, hi = self.ranges[k]
-        share = (self._base_all[hi] - self._base_all[lo]) / max(self.payload_len, 1)
+        share = (self.leaf_base[hi] - self.leaf_base[lo]) / max(self.payload_len, 1)
         return max(2, int(round(total * share)))
 
     def stage(self, k: int) -> AssemblyPackages:
@@ -666,43 +673,32 @@ class StagedPackages:
         return pk
 
     def offset(self, k: int) -> int:
-        """Payload offset of range k, relative to the window's first leaf."""
-        return int(self._base_all[self.ranges[k][0]] - self._base_all[self.window[0]])
+        """Payload offset of range k in the set's payload."""
+        return int(self.leaf_base[self.ranges[k][0]])
 
 
-def shard_window(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops, shard,
-                 disjoint_q: int, inputs=None):
-    """Leaf window [lo, hi) of process `rank` of `world` when one assembly is
-    split over processes: contiguous leaf ranges balanced by disjoint-rule
-    quadrature points, cut from the payload layout alone (no packaging of the
-    whole tree; every rank computes the same cuts). The singular items are
-    not weighed (~15% of the points at C3, spread evenly over the preorder:
-    measured imbalance <= 1.7% at 8 shards)."""
-    rank, world = int(shard[0]), int(shard[1])
-    if not 0 <= rank < world:
-        raise SchedulerConfigError(f"shard {shard}: need 0 <= rank < world")
+def shard_leaves_of(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops, shard,
+                    disjoint_q: int, inputs=None) -> np.ndarray:
+    """This process's leaves (sorted preorder positions) of a job split over
+    processes: packaging.shard_leaf_set (each leaf with its mirror, the
+    leaf pairs cut into contiguous runs balanced by disjoint-rule points)."""
     inputs = inputs or package_inputs(mesh.triangles, block_tree, row_ops, col_ops)
-    _, shape, _ = leaf_layout(block_tree, row_ops, col_ops, inputs)
-    L = shape.shape[0]
-    if world == 1 or L == 0:
-        return (0, L)
-    cum = np.cumsum((shape[:, 0] * shape[:, 1]).astype(np.float64) * disjoint_q)
-    cuts = np.searchsorted(cum, cum[-1] * np.arange(1, world) / world, side="left") + 1
-    edges = np.maximum.accumulate(np.concatenate([[0], np.minimum(cuts, L), [L]]))
-    return int(edges[rank]), int(edges[rank + 1])
+    return shard_leaf_set(block_tree, row_ops, col_ops, shard, disjoint_q, inputs)
 
 
 def staged_packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
-                        maxsize: int, nstages: int, window=None) -> StagedPackages:
-    """StagedPackages of (block tree, operators, budget, stages[, leaf
-    window]), cached like packages_for (a second operator from the same
-    packages packages nothing)."""
+                        maxsize: int, nstages: int, leaf_set=None,
+                        inputs=None) -> StagedPackages:
+    """StagedPackages of (block tree, operators, budget, stages[, leaf set]),
+    cached like packages_for (a second operator from the same packages
+    packages nothing)."""
     key = ("staged", id(block_tree), id(row_ops), id(col_ops), int(maxsize),
-           id(mesh.triangles), int(nstages), None if window is None else tuple(window))
+           id(mesh.triangles), int(nstages),
+           None if leaf_set is None else (int(leaf_set.size), hash(leaf_set.tobytes())))
     hit = _cache_get(key, block_tree)
     if hit is not None:
         return hit
-    sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages, window)
+    sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages, leaf_set, inputs)
     sp.key = key
     _cache_put(key, block_tree, row_ops, col_ops, sp)
     return sp
@@ -712,28 +708,28 @@ def _cached_packages(mesh, block_tree, row_ops, col_ops, maxsize):
     return _cache_get(_pk_key(mesh, block_tree, row_ops, col_ops, maxsize), block_tree)
 
 
-def _matrices(block_tree, row_ops, col_ops, bufs, leaf_ids, leaf_base, leaf_shape, window,
+def _matrices(block_tree, row_ops, col_ops, bufs, leaf_ids, leaf_base, leaf_shape, leaf_set,
               nleaves):
-    win = None if window is None or tuple(window) == (0, nleaves) else tuple(window)
+    part = None if leaf_set is None or leaf_set.size == nleaves else leaf_set
     return tuple(GCAMatrix(block_tree, row_ops, col_ops,
                            LeafPayloads(buf, leaf_ids, leaf_base, leaf_shape), buffer=buf,
-                           leaf_window=win) for buf in bufs)
+                           shard_leaves=part) for buf in bufs)
 
 
 def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, stats,
-                     device, window=None, inputs=None):
+                     device, leaf_set=None, inputs=None):
     """Single-device assembly over StagedPackages: plan k is created and
     launched (kernels + chunked D2H on its own streams) as soon as range k is
     packaged, so packaging and layout upload of later ranges overlap the
     device work and the D2H of earlier ones. The payloads are bitwise those
     of the unstaged path; AssemblyStats list counts/events are per range (each
     range's lists are cut from its own first leaf), so lists_executed depends
-    on the stage count (pairs_executed does not). `window`: only those leaves
-    (a process shard)."""
+    on the stage count (pairs_executed does not). `leaf_set`: only those
+    leaves (a process shard)."""
     t0 = time.monotonic()
     phase = {}
     sp = staged_packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes,
-                             params.stages, window)
+                             params.stages, leaf_set, inputs)
     ta = time.monotonic()
     outs = [nat.pinned_empty(sp.payload_len, np.complex128) for _ in range(2 if pair else 1)]
     phase["pinned_alloc"] = time.monotonic() - ta
@@ -783,8 +779,9 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
     stats.pairs_executed += mult * sum(r["pairs"] for r in ev)
     phase["total"] = time.monotonic() - t0
     stats.phase_s = phase
+    nleaves = len(block_tree.leaves)
     return _matrices(block_tree, row_ops, col_ops, outs, sp.leaf_ids, sp.leaf_base,
-                     sp.leaf_shape, sp.window, int(sp._base_all.size - 1))
+                     sp.leaf_shape, sp.leaf_set, nleaves)
 
 
 def _use_staged(mesh, block_tree, row_ops, col_ops, params) -> bool:
@@ -796,39 +793,36 @@ def _use_staged(mesh, block_tree, row_ops, col_ops, params) -> bool:
 def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, stats):
     """run_assembly / run_assembly_pair. Leaves are split into contiguous
     ranges, one per device of the backend; with params.shard = (rank, world)
-    this process assembles only its leaf window (shard_window) and the
-    returned matrices hold only those leaves (GCAMatrix.leaf_window)."""
+    this process assembles only its leaf set (packaging.shard_leaf_set: each
+    leaf with its mirror) and the returned matrices hold only those leaves
+    (GCAMatrix.shard_leaves)."""
     params = params or SchedulerParams()
     stats = stats if stats is not None else AssemblyStats()
     if not params.backends:
         raise SchedulerConfigError("at least one backend required")
     backend = params.backend_for("disjoint")
-    window = None
+    leaf_set = None
     inputs = None
     if params.shard is not None:
         inputs = package_inputs(mesh.triangles, block_tree, row_ops, col_ops)
-        window = shard_window(mesh, block_tree, row_ops, col_ops, params.shard, orders[0] ** 4,
-                              inputs)
+        leaf_set = shard_leaves_of(mesh, block_tree, row_ops, col_ops, params.shard,
+                                   orders[0] ** 4, inputs)
     if _use_staged(mesh, block_tree, row_ops, col_ops, params):
         return _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders,
-                                stats, backend.devices[0], window, inputs)
+                                stats, backend.devices[0], leaf_set, inputs)
     t0 = time.monotonic()
     phase = {}
-    pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
+    if leaf_set is None:
+        pk = packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes)
+    else:   # this process's leaves only
+        pk = make_packages(mesh.triangles, block_tree, row_ops, col_ops, params.maxsize_bytes,
+                           leaf_index=leaf_set, inputs=inputs)
     phase["packaging"] = time.monotonic() - t0
     devices = list(backend.devices)
     sq = [build_rule(c, orders[1]).num_points for c in SINGULAR_CASES]
-    L = pk.leaf_ids.size
-    wlo, whi = window if window is not None else (0, L)
-    if window is not None:
-        ranges = [(wlo + a, wlo + b) for a, b in
-                  _split_range(pk, (wlo, whi), len(devices), orders[0] ** 4, sq)]
-    else:
-        ranges = shard_leaves(pk, len(devices), orders[0] ** 4, sq)
-    base0 = int(pk.leaf_base[wlo])
-    plen = int(pk.leaf_base[whi]) - base0
+    ranges = shard_leaves(pk, len(devices), orders[0] ** 4, sq)
     ta = time.monotonic()
-    outs = [nat.pinned_empty(plen, np.complex128) for _ in range(2 if pair else 1)]
+    outs = [nat.pinned_empty(pk.payload_len, np.complex128) for _ in range(2 if pair else 1)]
     phase["pinned_alloc"] = time.monotonic() - ta
     plans = []
     try:
@@ -841,7 +835,7 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
         ta = time.monotonic()
         for p in plans:
             if p.payload_len:
-                sl = slice(p.payload_offset - base0, p.payload_offset - base0 + p.payload_len)
+                sl = slice(p.payload_offset, p.payload_offset + p.payload_len)
                 p.execute_download(outs[0][sl], params.chunks, outs[1][sl] if pair else None)
         for p in plans:
             p.synchronize()
@@ -855,23 +849,15 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
     t1 = time.monotonic()
     stats.phase_s = phase
     mult = 2 if pair else 1
-    if window is None:
-        bp, ni = pk.block_pairs(), pk.num_items
-    else:
-        bp = sum(p.disjoint_pairs for p in plans)
-        ni = sum(sum(p.singular_counts) for p in plans)
-    stats.block_pairs += mult * bp
-    stats.corrective_items += mult * ni
-    if window is None:
-        ev = _events(pk, backend.name, t0, t1)
-        stats.events.extend(ev * mult)
-        stats.lists_executed += mult * len(ev)
-        stats.pairs_executed += mult * sum(r["pairs"] for r in ev)
-    else:  # the whole-tree lists straddle the window: count its pairs only
-        stats.pairs_executed += mult * (bp + ni)
+    stats.block_pairs += mult * pk.block_pairs()
+    stats.corrective_items += mult * pk.num_items
+    ev = _events(pk, backend.name, t0, t1)
+    stats.events.extend(ev * mult)
+    stats.lists_executed += mult * len(ev)
+    stats.pairs_executed += mult * sum(r["pairs"] for r in ev)
     phase["total"] = time.monotonic() - t0
-    return _matrices(block_tree, row_ops, col_ops, outs, pk.leaf_ids[wlo:whi],
-                     pk.leaf_base[wlo:whi + 1] - base0, pk.leaf_shape[wlo:whi], window, L)
+    return _matrices(block_tree, row_ops, col_ops, outs, pk.leaf_ids, pk.leaf_base,
+                     pk.leaf_shape, leaf_set, len(block_tree.leaves))
 
 
 def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
@@ -882,7 +868,7 @@ def run_assembly(mesh: SurfaceMesh, block_tree: BlockTree, spec: KernelSpec,
     Leaves are split into contiguous ranges, one per device of the backend;
     each device streams its payload range into one pinned host buffer while
     it computes. With params.shard = (rank, world) (one job split over
-    processes) only this process's leaf window is assembled and returned."""
+    processes) only this process's leaf set is assembled and returned."""
     return _assemble(mesh, block_tree, spec, False, row_ops, col_ops, params, orders, stats)[0]
 
 

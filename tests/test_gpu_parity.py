@@ -497,15 +497,26 @@ def test_pair_plan_shards_equal_single(gload):
                 scheduler.SchedulerParams(shard=(r, world), stages=stages, mirror=False),
                 (3, 5))
                 for r in range(world)]
-            # each shard holds exactly its leaf window; the windows tile the preorder
-            wins = [p[0].leaf_window or (0, L) for p in parts]
-            assert wins[0][0] == 0 and wins[-1][1] == L
-            assert all(a[1] == b[0] for a, b in zip(wins[:-1], wins[1:]))
-            assert np.array_equal(np.concatenate([p[0].buffer for p in parts]), S.buffer)
-            assert np.array_equal(np.concatenate([p[1].buffer for p in parts]), D.buffer)
-            lo, hi = wins[-1]
-            leaf = int(S.payloads._ids[lo])
-            assert np.array_equal(parts[-1][1].payloads[leaf], D.payloads[leaf])
+            # each shard holds exactly its leaf set (every leaf with its
+            # mirror); the sets partition the leaves, and every leaf's payload
+            # is the single-process one bit for bit
+            sets = [p[0].shard_leaves for p in parts]
+            assert np.array_equal(np.sort(np.concatenate(sets)), np.arange(L))
+            for part in parts:
+                for lid in list(part[0].payloads)[::5]:
+                    assert np.array_equal(part[0].payloads[lid], S.payloads[lid])
+                    assert np.array_equal(part[1].payloads[lid], D.payloads[lid])
+                assert part[0].buffer.size == sum(v.size for v in part[0].payloads.values())
+    # mirrored (default): a shard evaluates each of its leaves with its mirror
+    # (both are in the set) -- equal to the per-pair values within roundoff
+    parts = [scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops,
+                                         scheduler.SchedulerParams(shard=(r, 2)), (3, 5))
+             for r in range(2)]
+    for part in parts:
+        for M, R in ((part[0], S), (part[1], D)):
+            for lid in M.payloads:
+                a, b = M.payloads[lid], R.payloads[lid]
+                assert np.all(np.abs(a - b) <= 1e-13 * np.maximum(np.abs(b), np.abs(b).max()))
 
 
 @pytest.mark.parametrize("stages", [2, 5])

@@ -124,12 +124,21 @@ def _pivot_rank_main(rank, world, port, out_path):
         ok &= np.array_equal(op.pivots_local, ops_all[c].pivots_local)
         ok &= op.rank == ops_all[c].rank
         ok &= (op is local[c]) if c in local else op.V.shape == (0, ops_all[c].rank)
-    win = scheduler.shard_window(m, bt, got, got, (rank, world), 81)
-    res = torch.tensor([int(ok), win[0], win[1], len(local)], dtype=torch.int64)
-    allres = [torch.zeros(4, dtype=torch.int64) for _ in range(world)]
+    from paper_1510_07244_b200 import packaging
+    mine = scheduler.shard_leaves_of(m, bt, got, got, (rank, world), 81)
+    # every leaf travels with its mirror
+    mir = packaging.leaf_mirrors(bt, got, got)
+    ok &= bool(np.all(np.isin(mir[mine], mine)))
+    res = torch.tensor([int(ok), mine.size, len(local)], dtype=torch.int64)
+    allres = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(allres, res)
+    L = len(bt.leaves)
+    mask = torch.zeros(L, dtype=torch.int64)
+    mask[torch.from_numpy(mine)] = 1
+    dist.all_reduce(mask)
     if rank == 0:
         np.save(out_path, np.stack([r.numpy() for r in allres]))
+        np.save(out_path + ".mask.npy", mask.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -139,16 +148,13 @@ def test_gca_shard_pivot_exchange(tmp_path, world):
     """GCA split over processes (build_interpolation_operators(shard=...)):
     the cluster parts tile the admissible clusters, exchange_pivots gives
     every rank every cluster's pivots (the reference's, here from the
-    fixture) with V only for its own, and the ranks' leaf windows
-    (scheduler.shard_window, computed independently per rank) tile the
-    preorder."""
+    fixture) with V only for its own, and the ranks' leaf sets
+    (scheduler.shard_leaves_of, computed independently per rank) partition
+    the leaves, each leaf in the set of its mirror."""
     out = str(tmp_path / "res.npy")
     mp.spawn(_pivot_rank_main, args=(world, _free_port(), out), nprocs=world, join=True)
     res = np.load(out)
     assert np.all(res[:, 0] == 1)
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from helpers import sphere_setup
-    m, t, bt = sphere_setup(4)
-    assert res[0, 1] == 0 and res[-1, 2] == len(bt.leaves)
-    assert np.all(res[1:, 1] == res[:-1, 2])
-    assert np.all(res[:, 3] > 0)
+    mask = np.load(out + ".mask.npy")
+    assert np.all(mask == 1)                       # every leaf in exactly one set
+    assert np.all(res[:, 1] > 0) and np.all(res[:, 2] > 0)
