@@ -274,6 +274,65 @@ def cpu_sample(pk, m, cfg, target_s, nthreads, log):
     return pairs, dt, desc, stride
 
 
+def cpu_sample_p1(plan, m, cfg, target_s, log):
+    """C4 CPU baseline: the oracle's numpy restatement of the reference's P1
+    pair integral (integrate_pair with P1 bases, oracle/p1_cpu.py) on a
+    deterministic sample of the plan's near-field pairs (every k-th disjoint
+    pair and singular item), one process-wide numpy thread pool."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import p1_cpu
+    pk = plan.packages
+    all_blocks = pk.device_blocks()
+    items, perms = pk.device_items()
+    eq, layer, kappa = cfg["equation"], cfg["layers"][0], cfg["kappa"]
+    nth = host_threads()
+
+    def block_pairs(blocks):
+        cnt = blocks[:, 2] * blocks[:, 3]
+        own = np.repeat(np.arange(len(blocks)), cnt)
+        k = np.arange(own.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        i, j = k // blocks[own, 3], k % blocks[own, 3]
+        tx, ty = pk.panels[blocks[own, 4] + i], pk.panels[blocks[own, 5] + j]
+        sh = (m.triangles[tx][:, :, None] == m.triangles[ty][:, None, :]).any(axis=(1, 2))
+        return tx[~sh], ty[~sh]
+    # the near field is ~68 M pairs: sample blocks (every k-th) before expanding
+    npairs = int(np.sum(all_blocks[:, 2] * all_blocks[:, 3]))
+    bstride = max(1, len(all_blocks) // 16384)
+    tx, ty = block_pairs(all_blocks[::bstride])
+    scale = npairs / max(1, int(np.sum(all_blocks[::bstride, 2] * all_blocks[::bstride, 3])))
+
+    def run(sel_tx, sel_ty, case, order, px=None, py=None):
+        parts = np.array_split(np.arange(sel_tx.size), nth)
+        with ThreadPoolExecutor(nth) as ex:
+            list(ex.map(lambda ix: p1_cpu.local_matrices(
+                m.vertices, m.triangles, m.normals, m.gramians, eq, layer, kappa, case, order,
+                sel_tx[ix], sel_ty[ix], None if px is None else px[ix],
+                None if py is None else py[ix]), parts))
+    probe = slice(0, 4096)
+    tc = time.perf_counter()
+    run(tx[probe], ty[probe], "disjoint", cfg["orders"][0])
+    rate = min(4096, tx.size) / max(time.perf_counter() - tc, 1e-6)
+    total = tx.size + items.shape[0] * 20 / scale   # singular items ~20x the points
+    stride = max(1, int(np.ceil(total / (rate * target_s))))
+    t0 = time.perf_counter()
+    run(tx[::stride], ty[::stride], "disjoint", cfg["orders"][0])
+    n = tx[::stride].size
+    for code, case in ((1, "vertex"), (2, "edge"), (3, "identical")):
+        sel = np.flatnonzero(items[:, 0] == code)[::max(1, int(stride * scale))]
+        if sel.size:
+            run(items[sel, 1], items[sel, 2], case, cfg["orders"][1],
+                perms[sel, :3].astype(np.int64), perms[sel, 3:].astype(np.int64))
+            n += sel.size
+    dt = time.perf_counter() - t0
+    desc = (f"every {bstride}-th near-field block, every {stride}-th of its pairs "
+            f"({tx[::stride].size} disjoint) and a matching share of the singular items "
+            f"({n - tx[::stride].size}) of the C4 packages, oracle/p1_cpu.py (numpy), "
+            f"{nth} threads")
+    log(f"cpu sample (P1): {n} pairs in {dt:.2f} s ({desc})")
+    return {"value": n / dt, "unit": UNIT, "cores": nth, "kind": "port", "sample": desc}
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -449,6 +508,15 @@ def run_ours_p1(args, cfg, dist, log):
         e2e_t.append(time.perf_counter() - t0)
     e2e_dt = dist.max(statistics.median(e2e_t))
     d2h = int((plan.num_vertices + 1) * 8 + plan.nnz * 20)
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        cpu = cpu_sample_p1(plan, m, cfg, args.cpu_seconds, log)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(
+            "c4/p1_disjoint")
+    except (OSError, ValueError):
+        traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -459,7 +527,9 @@ def run_ours_p1(args, cfg, dist, log):
                    "nnz": int(plan.nnz), "l2": "flushed between steps (512 MiB device write)",
                    "parallelism": f"weak x{dist.world}, no collectives"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "ncu dram bytes of p1_disjoint_kernel<3,H_DLP> per launch "
+                                       "(profiles/r2/ncu_p1_c4.txt)",
                      "kernel": "p1 local matrices (disjoint + singular launches; flops per "
                                "roofline.p1_pair_flops: P0 point work + the basis weighting)",
                      "peak_source": "measured DFMA probe (gcabem_fp64_probe), this device"},
@@ -473,6 +543,8 @@ def run_ours_p1(args, cfg, dist, log):
         "timing_ms": {"local": local_ms,
                       "scatter": statistics.mean(t["scatter"] for t in per)},
     }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
     plan.close()
     return line if dist.rank == 0 else None
 

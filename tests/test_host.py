@@ -496,3 +496,22 @@ def test_p1_numpy_restatement_matches_reference_golden(gload):
                 got = p1_numpy.local_matrix(m, spec, rule, tx, ty, perms[k, :3], perms[k, 3:])
                 scale = np.max(np.abs(ref[k]))
                 assert np.max(np.abs(got - ref[k])) <= 1e-12 * scale, (case, name, k)
+
+
+def test_oracle_p1_batch_matches_reference_golden(gload):
+    """oracle/p1_cpu.py (the C4 cpu_baseline of bench.py) reproduces the
+    reference's integrate_pair with P1 bases on the golden pairs."""
+    from oracle import p1_cpu
+    g = gload("p1_crank.npz")
+    m = mesh.make_surface_mesh(g["vertices"], g["triangles"])
+    kinds = {"L-SLP": ("laplace", "single", 0.0), "L-DLP": ("laplace", "double", 0.0),
+             "H-SLP": ("helmholtz", "single", 4.0), "H-DLP": ("helmholtz", "double", 4.0)}
+    for case in ("disjoint", "vertex", "edge", "identical"):
+        pairs, perms = g[f"pairs_{case}"], g[f"perms_{case}"]
+        for name, (eq, layer, kappa) in kinds.items():
+            ref = g[f"p1_{case}_{name}"]
+            got = p1_cpu.local_matrices(m.vertices, m.triangles, m.normals, m.gramians, eq,
+                                        layer, kappa, case, 3 if case == "disjoint" else 5,
+                                        pairs[:, 0], pairs[:, 1], perms[:, :3], perms[:, 3:])
+            scale = np.max(np.abs(ref), axis=(1, 2))
+            assert np.all(np.max(np.abs(got - ref), axis=(1, 2)) <= 1e-12 * scale), (case, name)
