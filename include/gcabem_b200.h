@@ -250,6 +250,10 @@ int gcabem_green_matrices(gcabem_mesh_t mesh, int equation, double kappa, int64_
 typedef struct gcabem_tree_s *gcabem_tree_t;
 int gcabem_cluster_tree(int64_t nt, const double *tri_lo, const double *tri_hi,
                         const double *mid, int64_t leaf_size, gcabem_tree_t *out);
+/* The same from the mesh: triangles (nt x 3, int64) and vertices (nv x 3);
+ * the bounds and midpoints are formed natively (mesh.py:65-73). */
+int gcabem_cluster_tree_mesh(int64_t nt, const int64_t *triangles, const double *vertices,
+                             int64_t leaf_size, gcabem_tree_t *out);
 int gcabem_block_tree(int64_t nrow, const int64_t *row_c0, const int64_t *row_c1,
                       const double *row_lo, const double *row_hi, const double *row_diam,
                       int64_t ncol, const int64_t *col_c0, const int64_t *col_c1,

@@ -82,6 +82,7 @@ _SIGS = {
     "gcabem_packages_fetch": ([_vp] * 11, _int),
     "gcabem_packages_free": ([_vp], _int),
     "gcabem_leaf_layout": ([_i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp], _int),
+    "gcabem_cluster_tree_mesh": ([_i64, _vp, _vp, _i64, ctypes.POINTER(_vp)], _int),
     "gcabem_cluster_tree": ([_i64, _vp, _vp, _vp, _i64, ctypes.POINTER(_vp)], _int),
     "gcabem_block_tree": ([_i64] + [_vp] * 5 + [_i64] + [_vp] * 5 + [_dbl, _int,
                                                                      ctypes.POINTER(_vp)], _int),

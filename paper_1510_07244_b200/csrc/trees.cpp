@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <map>
+#include <thread>
 #include <vector>
 
 #include "gcabem_b200.h"
@@ -20,19 +22,45 @@ int gcabem_internal_error(int code, const char *msg);  // api.cu
 
 namespace {
 
+// Preorder bisection tree. The node count of a subtree depends only on its
+// panel count, so every subtree's node and panel offsets are known before it
+// is built: the two halves of a large node are built concurrently into
+// preallocated arrays. A node only needs its halves as SETS (each child
+// re-sorts by its own axis), so the split is an nth_element on the
+// reference's key (midpoint coordinate, panel index); a half that becomes a
+// leaf keeps the parent's sorted order (the leaf's panel order), so it is
+// fully sorted.
 struct CTree {
     const double *tlo, *thi, *mid;
     int64_t leaf;
-    std::vector<int64_t> start, size, c0, c1, perm;
+    std::vector<int64_t> start, size, c0, c1, perm, idx;
     std::vector<double> lo, hi;
-    int64_t cursor = 0;
+    std::map<int64_t, int64_t> memo;
 
-    int64_t build(std::vector<int64_t> &idx, int64_t a, int64_t b) {
-        const int64_t me = (int64_t)start.size();
-        start.push_back(cursor);
-        size.push_back(b - a);
-        c0.push_back(-1);
-        c1.push_back(-1);
+    int64_t count(int64_t n) {
+        if (n <= leaf) return 1;
+        auto it = memo.find(n);
+        if (it != memo.end()) return it->second;
+        const int64_t c = 1 + count(n / 2) + count(n - n / 2);
+        memo[n] = c;
+        return c;
+    }
+    // node ids: the counts of every size that occurs, computed up front
+    // (the concurrent builds only read the memo)
+    void prime(int64_t n) {
+        if (n <= leaf || memo.count(n)) return;
+        prime(n / 2);
+        prime(n - n / 2);
+        count(n);
+    }
+    int64_t cnt(int64_t n) const {
+        if (n <= leaf) return 1;
+        return memo.at(n);
+    }
+
+    void build(int64_t me, int64_t a, int64_t b, int depth) {
+        start[me] = a;
+        size[me] = b - a;
         double l[3] = {tlo[3 * idx[a]], tlo[3 * idx[a] + 1], tlo[3 * idx[a] + 2]};
         double h[3] = {thi[3 * idx[a]], thi[3 * idx[a] + 1], thi[3 * idx[a] + 2]};
         for (int64_t k = a + 1; k < b; ++k)
@@ -40,11 +68,13 @@ struct CTree {
                 l[q] = std::min(l[q], tlo[3 * idx[k] + q]);
                 h[q] = std::max(h[q], thi[3 * idx[k] + q]);
             }
-        lo.insert(lo.end(), l, l + 3);
-        hi.insert(hi.end(), h, h + 3);
+        for (int q = 0; q < 3; ++q) {
+            lo[3 * me + q] = l[q];
+            hi[3 * me + q] = h[q];
+        }
         if (b - a <= leaf) {
-            for (int64_t k = a; k < b; ++k) perm[cursor++] = idx[k];
-            return me;
+            for (int64_t k = a; k < b; ++k) perm[k] = idx[k];
+            return;
         }
         int axis = 0;
         double ext = h[0] - l[0];
@@ -53,16 +83,25 @@ struct CTree {
                 ext = h[q] - l[q];
                 axis = q;
             }
-        std::sort(idx.begin() + a, idx.begin() + b, [&](int64_t u, int64_t v) {
+        auto less = [&](int64_t u, int64_t v) {
             const double mu = mid[3 * u + axis], mv = mid[3 * v + axis];
             return mu < mv || (mu == mv && u < v);
-        });
+        };
         const int64_t half = (b - a) / 2;
-        const int64_t left = build(idx, a, a + half);
-        const int64_t right = build(idx, a + half, b);
+        std::nth_element(idx.begin() + a, idx.begin() + a + half, idx.begin() + b, less);
+        if (half <= leaf) std::sort(idx.begin() + a, idx.begin() + a + half, less);
+        if (b - a - half <= leaf) std::sort(idx.begin() + a + half, idx.begin() + b, less);
+        const int64_t left = me + 1, right = me + 1 + cnt(half);
         c0[me] = left;
         c1[me] = right;
-        return me;
+        if (depth < 3 && b - a > 4096) {
+            std::thread th([&, left, a, half, depth] { build(left, a, a + half, depth + 1); });
+            build(right, a + half, b, depth + 1);
+            th.join();
+        } else {
+            build(left, a, a + half, depth + 1);
+            build(right, a + half, b, depth + 1);
+        }
     }
 };
 
@@ -115,12 +154,13 @@ struct BTree {
             int nt = 0, ns = 0;
             if (tleaf) tk[nt++] = t; else { tk[nt++] = rc0[t]; tk[nt++] = rc1[t]; }
             if (sleaf) sk[ns++] = s; else { sk[ns++] = cc0[s]; sk[ns++] = cc1[s]; }
-            std::vector<int64_t> mine;
+            int64_t mine[4];
+            int nm = 0;
             for (int a = 0; a < nt; ++a)
-                for (int b = 0; b < ns; ++b) mine.push_back(build(tk[a], sk[b]));
+                for (int b = 0; b < ns; ++b) mine[nm++] = build(tk[a], sk[b]);
             first[me] = (int64_t)kids.size();
-            nkids[me] = (int64_t)mine.size();
-            kids.insert(kids.end(), mine.begin(), mine.end());
+            nkids[me] = nm;
+            kids.insert(kids.end(), mine, mine + nm);
         }
         return me;
     }
@@ -148,10 +188,18 @@ int gcabem_cluster_tree(int64_t nt, const double *tri_lo, const double *tri_hi,
     t.thi = tri_hi;
     t.mid = mid;
     t.leaf = leaf_size;
+    t.prime(nt);
+    const int64_t nn = t.cnt(nt);
+    t.start.assign(nn, 0);
+    t.size.assign(nn, 0);
+    t.c0.assign(nn, -1);
+    t.c1.assign(nn, -1);
+    t.lo.assign(3 * nn, 0.0);
+    t.hi.assign(3 * nn, 0.0);
     t.perm.assign(nt, 0);
-    std::vector<int64_t> idx(nt);
-    for (int64_t k = 0; k < nt; ++k) idx[k] = k;
-    t.build(idx, 0, nt);
+    t.idx.resize(nt);
+    for (int64_t k = 0; k < nt; ++k) t.idx[k] = k;
+    t.build(0, 0, nt, 0);
     auto *r = new gcabem_tree_s();
     r->a = std::move(t.start);
     r->b = std::move(t.size);
@@ -162,6 +210,25 @@ int gcabem_cluster_tree(int64_t nt, const double *tri_lo, const double *tri_hi,
     r->hi = std::move(t.hi);
     *out = r;
     return GCABEM_OK;
+}
+
+// The same from the mesh arrays: per-triangle bounds (min/max of the
+// corners, mesh.py:70-73) and midpoints ((v0 + v1 + v2) / 3, mesh.py:65-68,
+// the same IEEE operations) formed here.
+int gcabem_cluster_tree_mesh(int64_t nt, const int64_t *T, const double *V, int64_t leaf_size,
+                             gcabem_tree_t *out) {
+    if (!T || !V || nt <= 0)
+        return gcabem_internal_error(GCABEM_ERR_ARG, "cluster tree: bad arguments");
+    std::vector<double> lo(3 * nt), hi(3 * nt), mid(3 * nt);
+    for (int64_t k = 0; k < nt; ++k) {
+        const double *a = V + 3 * T[3 * k], *b = V + 3 * T[3 * k + 1], *c = V + 3 * T[3 * k + 2];
+        for (int q = 0; q < 3; ++q) {
+            lo[3 * k + q] = std::min(std::min(a[q], b[q]), c[q]);
+            hi[3 * k + q] = std::max(std::max(a[q], b[q]), c[q]);
+            mid[3 * k + q] = ((a[q] + b[q]) + c[q]) / 3.0;
+        }
+    }
+    return gcabem_cluster_tree(nt, lo.data(), hi.data(), mid.data(), leaf_size, out);
 }
 
 // Block tree over (row tree, col tree). Output arrays:
@@ -176,6 +243,8 @@ int gcabem_block_tree(int64_t nrow, const int64_t *row_c0, const int64_t *row_c1
         return gcabem_internal_error(GCABEM_ERR_ARG, "block tree: bad arguments");
     BTree t{row_c0, row_c1, col_c0, col_c1, row_lo, row_hi, col_lo, col_hi, row_diam, col_diam,
             eta, norm_variant, {}, {}, {}, {}, {}, {}};
+    const size_t guess = (size_t)(64 * std::max(nrow, ncol));
+    for (auto *v : {&t.row, &t.col, &t.kind, &t.first, &t.nkids, &t.kids}) v->reserve(guess);
     t.build(0, 0);
     auto *r = new gcabem_tree_s();
     r->a = std::move(t.row);
