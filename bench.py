@@ -683,8 +683,7 @@ def run_ours(args, cfg, dist, log):
             traffic = None
     h2d = sum(p.h2d_bytes for dv in per_dev for p in dv[3])
     mirrored_info = per_dev[0][3][0].layout.mirror_info if per_dev[0][3][0].mirrored else {}
-    launches = args.steps * sum(1 + sum(1 for c in p.singular_counts if c)
-                                for dv in per_dev for p in dv[3])
+    launches = args.steps * sum(p.launches_per_execute() for dv in per_dev for p in dv[3])
     for dv in per_dev:
         for p in dv[3] + dv[4]:
             p.close()

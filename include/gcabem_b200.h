@@ -145,8 +145,9 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
 int gcabem_layout_info(gcabem_layout_t layout, int64_t *info8);
 /* {disjoint evaluations of the mirrored kernel (each gives a pair and its
  * transpose), of the plain kernel, pairs of mirrored (PRIMARY/SELF upper)
- * blocks, pairs of blocks written by their mirror} */
-int gcabem_layout_mirror_info(gcabem_layout_t layout, int64_t *info4);
+ * blocks, pairs of blocks written by their mirror, tasks of the mirrored
+ * kernel, tasks of the plain kernel on a mirrored plan} */
+int gcabem_layout_mirror_info(gcabem_layout_t layout, int64_t *info6);
 int gcabem_layout_release(gcabem_layout_t layout);
 /* Mirrored evaluation of the layout's mirrored leaves (default: on when the
  * layout has any and the disjoint order is <= 8); 0 evaluates every block on

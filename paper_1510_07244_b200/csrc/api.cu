@@ -826,9 +826,11 @@ int gcabem_layout_info(gcabem_layout_t L, int64_t *info8) {
     return GCABEM_OK;
 }
 
-int gcabem_layout_mirror_info(gcabem_layout_t L, int64_t *info4) {
-    GC_ARG(L && info4, "null argument");
-    for (int k = 0; k < 4; ++k) info4[k] = L->mirror_info[k];
+int gcabem_layout_mirror_info(gcabem_layout_t L, int64_t *info6) {
+    GC_ARG(L && info6, "null argument");
+    for (int k = 0; k < 4; ++k) info6[k] = L->mirror_info[k];
+    info6[4] = L->nmtasks;
+    info6[5] = L->nrtasks;
     return GCABEM_OK;
 }
 

@@ -340,12 +340,13 @@ class DeviceLayout:
             ctypes.byref(h)))
         info = np.zeros(8, np.int64)
         nat.check(nat.lib().gcabem_layout_info(h, p(info)))
-        mi = np.zeros(4, np.int64)
+        mi = np.zeros(6, np.int64)
         nat.check(nat.lib().gcabem_layout_mirror_info(h, p(mi)))
         # disjoint-kernel evaluations: mirrored (a pair and its transpose) and
         # plain; 0/0 without mirrors (then every non-sharing pair is plain)
         self.mirror_info = {"evals_mirrored": int(mi[0]), "evals_plain": int(mi[1]),
-                            "pairs_mirrored": int(mi[2]), "pairs_skipped": int(mi[3])}
+                            "pairs_mirrored": int(mi[2]), "pairs_skipped": int(mi[3]),
+                            "tasks_mirrored": int(mi[4]), "tasks_plain": int(mi[5])}
         self.disjoint_pairs = int(info[3])
         self.singular_counts = [int(x) for x in info[4:7]]
         self.h2d_bytes = int(info[7])
@@ -419,6 +420,19 @@ class AssemblyPlan:
         m = ctypes.c_int()
         nat.check(nat.lib().gcabem_plan_mirrored(self.handle, ctypes.byref(m)))
         self.mirrored = bool(m.value)
+
+    def launches_per_execute(self) -> int:
+        """Kernel launches of one execute(): the disjoint launch(es) -- plain
+        and mirrored when both kinds of blocks exist -- and one per non-empty
+        singular list (vertex mirrored / alone, edge, identical)."""
+        ev = np.zeros(4, np.int64)
+        nat.check(nat.lib().gcabem_plan_singular_evals(self.handle, nat.ptr(ev)))
+        if self.mirrored:
+            mi = self.layout.mirror_info
+            dis = int(mi["tasks_plain"] > 0) + int(mi["tasks_mirrored"] > 0)
+        else:
+            dis = int(self.disjoint_pairs > 0)
+        return dis + int(np.count_nonzero(ev))
 
     def execute(self) -> None:
         nat.check(nat.lib().gcabem_plan_execute(self.handle))
