@@ -154,8 +154,10 @@ int gcabem_layout_release(gcabem_layout_t layout);
  * its own (the reference's one-pair-at-a-time order). */
 int gcabem_plan_set_mirror(gcabem_plan_t plan, int enable);
 /* {vertex items evaluated with their transpose (the vertex rule is symmetric),
- * vertex items alone, edge items, identical items} of one execute */
-int gcabem_plan_singular_evals(gcabem_plan_t plan, int64_t *out4);
+ * vertex items alone, edge items, identical items, rule points evaluated per
+ * identical item (half the rule: its terms come in x <-> y swapped pairs)} of
+ * one execute */
+int gcabem_plan_singular_evals(gcabem_plan_t plan, int64_t *out5);
 int gcabem_plan_mirrored(gcabem_plan_t plan, int *out);
 int gcabem_plan_create_on(gcabem_layout_t layout, int equation, int layer, double kappa,
                           int disjoint_n, const double *gauss_pts, const double *gauss_wts,

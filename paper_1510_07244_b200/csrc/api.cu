@@ -116,6 +116,9 @@ struct gcabem_plan_s {
     PoolBuf<double> grows[3], ggroups[3];
     PoolBuf<int4> gchunks[3];
     int gn[3] = {0, 0, 0};
+    // identical rule: its base half when the terms come in swapped pairs
+    PoolBuf<double> hrule;
+    int64_t hq = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> chunk_ev;
     cudaStream_t stream = nullptr;  // kernels (own_stream, or the caller's)
@@ -956,7 +959,9 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
         // vertex and edge items: the x-grouped rule (the identical case keeps
         // its exact-difference form); GCABEM_NO_GROUPED=1 turns it off
         static const bool no_grouped = std::getenv("GCABEM_NO_GROUPED") != nullptr;
-        if (e == cudaSuccess && c < 2 && !no_grouped && p->sq[c] > 0 &&
+        static const bool no_grouped_edge = std::getenv("GCABEM_NO_GROUPED_EDGE") != nullptr;
+        if (e == cudaSuccess && c < 2 && !no_grouped && !(c == 1 && no_grouped_edge) &&
+            p->sq[c] > 0 &&
             L->case_at[c + 1] > L->case_at[c]) {
             std::vector<double> rows, groups;
             std::vector<int4> chunks;
@@ -965,6 +970,30 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
             if (e == cudaSuccess) e = p->ggroups[c].upload(groups.data(), groups.size(), p->stream);
             if (e == cudaSuccess) e = p->gchunks[c].upload(chunks.data(), chunks.size(), p->stream);
             p->gn[c] = (int)chunks.size();
+        }
+        // identical items: the 6 terms of the rule are 3 base terms each
+        // followed by its x <-> y swap with the same weights (quadrature.py:
+        // 132-143); verified point by point, the base half is kept
+        static const bool no_half = std::getenv("GCABEM_NO_SYM_HALF") != nullptr;
+        if (e == cudaSuccess && c == 2 && !no_half && p->sq[2] > 0 && p->sq[2] % 6 == 0 &&
+            L->case_at[3] > L->case_at[2]) {
+            const double *r = srule[2];
+            const int64_t n4 = p->sq[2] / 6;
+            bool ok = true;
+            for (int m = 0; m < 3 && ok; ++m)
+                for (int64_t k = 2 * m * n4; k < (2 * m + 1) * n4 && ok; ++k) {
+                    const double *a = r + 5 * k, *b = r + 5 * (k + n4);
+                    ok = a[0] == b[2] && a[1] == b[3] && a[2] == b[0] && a[3] == b[1] &&
+                         a[4] == b[4];
+                }
+            if (ok) {
+                std::vector<double> half;
+                half.reserve(15 * n4);
+                for (int m = 0; m < 3; ++m)
+                    half.insert(half.end(), r + 5 * (2 * m * n4), r + 5 * ((2 * m + 1) * n4));
+                e = p->hrule.upload(half.data(), half.size(), p->stream);
+                p->hq = 3 * n4;
+            }
         }
     }
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreate(&p->ev[k]);
@@ -1005,6 +1034,7 @@ namespace {
 // payload index lies in [p0, p1) on the plan stream.
 GroupedRule grouped_of(gcabem_plan_t p, int c) {
     GroupedRule g;
+    if (c == 2 && p->hq > 0) g.sym_half = 1;
     if (p->gn[c] > 0) {
         g.rows = p->grows[c].p;
         g.groups = p->ggroups[c].p;
@@ -1069,8 +1099,10 @@ int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p
         const int64_t i0 = std::lower_bound(first, last, p0) - p->L->item_out.begin();
         const int64_t i1 = std::lower_bound(first, last, p1) - p->L->item_out.begin();
         if (i1 <= i0) continue;
+        const bool half = c == 2 && p->hq > 0;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->L->items.p + i0,
-                               i1 - i0, p->srule[c].p, p->sq[c], p->payload.p, p->payload2.p,
+                               i1 - i0, half ? p->hrule.p : p->srule[c].p,
+                               half ? p->hq : p->sq[c], p->payload.p, p->payload2.p,
                                p->kappa, s, grouped_of(p, c)));
     }
     return GCABEM_OK;
@@ -1101,8 +1133,10 @@ int gcabem_plan_execute(gcabem_plan_t p) {
         }
         const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
         if (n == 0) continue;
+        const bool half = c == 2 && p->hq > 0;
         GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
-                               p->L->items.p + p->L->case_at[c], n, p->srule[c].p, p->sq[c],
+                               p->L->items.p + p->L->case_at[c], n,
+                               half ? p->hrule.p : p->srule[c].p, half ? p->hq : p->sq[c],
                                p->payload.p, p->payload2.p, p->kappa, s, grouped_of(p, c)));
     }
     GC_CUDA(cudaEventRecord(p->ev[2], s));
@@ -1110,14 +1144,15 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     return GCABEM_OK;
 }
 
-int gcabem_plan_singular_evals(gcabem_plan_t p, int64_t *out4) {
-    GC_ARG(p && out4, "null argument");
+int gcabem_plan_singular_evals(gcabem_plan_t p, int64_t *out5) {
+    GC_ARG(p && out5, "null argument");
     gcabem_layout_t L = p->L;
     const bool vm = vertex_mirrored(p);
-    out4[0] = vm ? (int64_t)L->vm_out.size() : 0;
-    out4[1] = vm ? (int64_t)L->vp_out.size() : L->case_at[1] - L->case_at[0];
-    out4[2] = L->case_at[2] - L->case_at[1];
-    out4[3] = L->case_at[3] - L->case_at[2];
+    out5[0] = vm ? (int64_t)L->vm_out.size() : 0;
+    out5[1] = vm ? (int64_t)L->vp_out.size() : L->case_at[1] - L->case_at[0];
+    out5[2] = L->case_at[2] - L->case_at[1];
+    out5[3] = L->case_at[3] - L->case_at[2];
+    out5[4] = p->hq > 0 ? p->hq : p->sq[2];   // rule points per identical item evaluated
     return GCABEM_OK;
 }
 
@@ -1257,6 +1292,7 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
     for (auto &r : p->grows) r.release();
     for (auto &r : p->ggroups) r.release();
     for (auto &r : p->gchunks) r.release();
+    p->hrule.release();
     cudaStream_t mine = p->own_stream ? p->own_stream : p->stream;
     if (mine) cudaStreamDestroy(mine);
     if (p->copy) cudaStreamDestroy(p->copy);

@@ -97,6 +97,10 @@ struct GroupedRule {
     const double *groups = nullptr;
     const int4 *chunks = nullptr;
     int nchunks = 0;
+    // identical case (SAME): the rule passed is the base half of a rule whose
+    // terms come in swapped pairs (quadrature.py:132-143): single layer x 2,
+    // double layer 0 (exactly cancelling pairs; see generic_kernel)
+    int sym_half = 0;
 };
 cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int32_t *T,
                            const Chart *charts, const SingItem *items, int64_t n,

@@ -425,8 +425,9 @@ class AssemblyPlan:
         """Kernel launches of one execute(): the disjoint launch(es) -- plain
         and mirrored when both kinds of blocks exist -- and one per non-empty
         singular list (vertex mirrored / alone, edge, identical)."""
-        ev = np.zeros(4, np.int64)
+        ev = np.zeros(5, np.int64)
         nat.check(nat.lib().gcabem_plan_singular_evals(self.handle, nat.ptr(ev)))
+        ev = ev[:4]
         if self.mirrored:
             mi = self.layout.mirror_info
             dis = int(mi["tasks_plain"] > 0) + int(mi["tasks_mirrored"] > 0)
@@ -491,10 +492,13 @@ class AssemblyPlan:
         else:
             computed = self.disjoint_pairs - sum(self.singular_counts)
             dis = pair_flops(self.spec, "disjoint", dq, self.pair) * computed
-        ev = np.zeros(4, np.int64)
+        ev = np.zeros(5, np.int64)
         nat.check(nat.lib().gcabem_plan_singular_evals(self.handle, nat.ptr(ev)))
+        # identical items: the points actually evaluated (the base half of a
+        # symmetric rule: the minimal algorithm's work)
+        qs = [self.singular_q[0], self.singular_q[1], int(ev[4])]
         sing = sum(pair_flops(self.spec, "singular", q, self.pair) * int(n)
-                   for q, n in zip(self.singular_q, ev[1:]))
+                   for q, n in zip(qs, ev[1:4]))
         # vertex items evaluated with their transpose (symmetric vertex rule)
         sing += mirror_pair_flops(self.spec, self.singular_q[0], self.pair, "singular") * \
             int(ev[0])

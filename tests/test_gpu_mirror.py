@@ -133,11 +133,14 @@ def test_mirror_evaluation_accounting(gload):
     # together; the partners are not evaluated again
     import ctypes
     from paper_1510_07244_b200 import _native as nat
-    ev = np.zeros(4, np.int64)
+    ev = np.zeros(5, np.int64)
     nat.check(nat.lib().gcabem_plan_singular_evals(mp.handle, nat.ptr(ev)))
     nv = int(np.count_nonzero(pk.item_case == 1))
     assert ev[0] > 0 and 2 * ev[0] + ev[1] == nv
     assert ev[2] == np.count_nonzero(pk.item_case == 2)
+    # identical items evaluate the base half of the rule (its terms come in
+    # x <-> y swapped pairs with equal weights)
+    assert ev[4] * 2 == mp.singular_q[2]
     nat.check(nat.lib().gcabem_plan_singular_evals(pp.handle, nat.ptr(ev)))
     assert ev[0] == 0 and ev[1] == nv
     assert mp.flops()["singular"] < pp.flops()["singular"]
