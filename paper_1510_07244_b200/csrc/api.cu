@@ -850,47 +850,61 @@ int gcabem_layout_release(gcabem_layout_t L) {
 
 namespace {
 // Group the points of a staged singular rule (rows {xs, xt, ys, yt, w}) by
-// their x point, in first-appearance order, packed into chunks of at most
-// RULE_CHUNK rows and groups (a group larger than a chunk is split into
-// groups with the same x point).
-void group_rule(const double *r5, int64_t q, std::vector<double> &rows,
+// the point of one side, term by term (`nterms` terms of equal size, in rule
+// order): per term the side with fewer distinct points is held fixed (a
+// vertex term has 25 distinct x points for 625 points, an edge term as few
+// as 25 on one side and 385 on the other). Groups in first-appearance order,
+// packed into chunks of at most RULE_CHUNK rows and groups (a group larger
+// than a chunk is split). Group record {a, b, first row, rows, side}: side 0
+// = x point (a, b) fixed, rows {ys, yt, w}; side 1 = y point fixed, rows
+// {xs, xt, w}.
+void group_rule(const double *r5, int64_t q, int nterms, std::vector<double> &rows,
                 std::vector<double> &groups, std::vector<int4> &chunks) {
-    std::vector<std::pair<std::pair<double, double>, std::vector<int64_t>>> order;
-    std::map<std::pair<uint64_t, uint64_t>, size_t> at;
-    for (int64_t k = 0; k < q; ++k) {
-        uint64_t a, b;
-        std::memcpy(&a, r5 + 5 * k, 8);
-        std::memcpy(&b, r5 + 5 * k + 1, 8);
-        auto it = at.find({a, b});
-        if (it == at.end()) {
-            at.emplace(std::make_pair(a, b), order.size());
-            order.push_back({{r5[5 * k], r5[5 * k + 1]}, {k}});
-        } else {
-            order[it->second].second.push_back(k);
-        }
-    }
     rows.clear();
     groups.clear();
     chunks.clear();
+    if (nterms < 1 || q % nterms) nterms = 1;
+    const int64_t tq = q / nterms;
     int r0 = 0, g0 = 0, nr = 0, ng = 0;
-    for (auto &grp : order) {
-        const auto &idx = grp.second;
-        for (size_t p0 = 0; p0 < idx.size(); p0 += RULE_CHUNK) {
-            const int piece = (int)std::min<size_t>(RULE_CHUNK, idx.size() - p0);
-            if (nr + piece > RULE_CHUNK || ng + 1 > RULE_CHUNK) {
-                chunks.push_back(make_int4(r0, r0 + nr, g0, g0 + ng));
-                r0 += nr;
-                g0 += ng;
-                nr = ng = 0;
+    for (int term = 0; term < nterms; ++term) {
+        const int64_t k0 = term * tq, k1 = k0 + tq;
+        std::vector<std::pair<std::pair<double, double>, std::vector<int64_t>>> order[2];
+        for (int side = 0; side < 2; ++side) {
+            std::map<std::pair<uint64_t, uint64_t>, size_t> at;
+            for (int64_t k = k0; k < k1; ++k) {
+                uint64_t a, b;
+                std::memcpy(&a, r5 + 5 * k + 2 * side, 8);
+                std::memcpy(&b, r5 + 5 * k + 2 * side + 1, 8);
+                auto it = at.find({a, b});
+                if (it == at.end()) {
+                    at.emplace(std::make_pair(a, b), order[side].size());
+                    order[side].push_back({{r5[5 * k + 2 * side], r5[5 * k + 2 * side + 1]}, {k}});
+                } else {
+                    order[side][it->second].second.push_back(k);
+                }
             }
-            groups.insert(groups.end(), {grp.first.first, grp.first.second,
-                                         (double)(r0 + nr), (double)piece});
-            for (int j = 0; j < piece; ++j) {
-                const double *r = r5 + 5 * idx[p0 + j];
-                rows.insert(rows.end(), {r[2], r[3], r[4]});
+        }
+        const int side = order[1].size() < order[0].size() ? 1 : 0;
+        const int other = 2 - 2 * side;   // column of the varying point
+        for (auto &grp : order[side]) {
+            const auto &idx = grp.second;
+            for (size_t p0 = 0; p0 < idx.size(); p0 += RULE_CHUNK) {
+                const int piece = (int)std::min<size_t>(RULE_CHUNK, idx.size() - p0);
+                if (nr + piece > RULE_CHUNK || ng + 1 > RULE_CHUNK) {
+                    chunks.push_back(make_int4(r0, r0 + nr, g0, g0 + ng));
+                    r0 += nr;
+                    g0 += ng;
+                    nr = ng = 0;
+                }
+                groups.insert(groups.end(), {grp.first.first, grp.first.second,
+                                             (double)(r0 + nr), (double)piece, (double)side});
+                for (int j = 0; j < piece; ++j) {
+                    const double *r = r5 + 5 * idx[p0 + j];
+                    rows.insert(rows.end(), {r[other], r[other + 1], r[4]});
+                }
+                nr += piece;
+                ++ng;
             }
-            nr += piece;
-            ++ng;
         }
     }
     if (nr > 0) chunks.push_back(make_int4(r0, r0 + nr, g0, g0 + ng));
@@ -965,7 +979,7 @@ int plan_create_kind(gcabem_layout_t L, int kind, double kappa, int disjoint_n,
             L->case_at[c + 1] > L->case_at[c]) {
             std::vector<double> rows, groups;
             std::vector<int4> chunks;
-            group_rule(srule[c], p->sq[c], rows, groups, chunks);
+            group_rule(srule[c], p->sq[c], c == 0 ? 2 : 5, rows, groups, chunks);
             e = p->grows[c].upload(rows.data(), rows.size(), p->stream);
             if (e == cudaSuccess) e = p->ggroups[c].upload(groups.data(), groups.size(), p->stream);
             if (e == cudaSuccess) e = p->gchunks[c].upload(chunks.data(), chunks.size(), p->stream);

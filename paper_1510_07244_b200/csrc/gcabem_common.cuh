@@ -89,9 +89,11 @@ cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int3
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
 // same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).
-// x-grouped form of a singular rule (kernels.cu generic_pair_grouped): rows
-// {ys, yt, w}, groups {xs, xt, first row, row count} (doubles), chunks
+// grouped form of a singular rule (kernels.cu generic_pair_grouped): groups
+// {a, b, first row, row count, side} (doubles; side 0: x point (a, b) fixed,
+// rows {ys, yt, w}; side 1: y point fixed, rows {xs, xt, w}), chunks
 // {row0, row1, group0, group1} of at most RULE_CHUNK rows / groups each.
+constexpr int GROUP_REC = 5;
 struct GroupedRule {
     const double *rows = nullptr;
     const double *groups = nullptr;
