@@ -74,19 +74,7 @@ __device__ __forceinline__ void accumulate_any(double r2, double dn, double dnm,
 }
 
 
-// x-side polynomial coefficients (below) parked in shared memory instead of
-// registers: per thread 15 doubles at stride DISJOINT_TPB (conflict-free),
-// read back once per x point; frees ~30 registers of the hot loop for more
-// independent quadrature points in flight
-#ifndef GCABEM_XSMEM
-#define GCABEM_XSMEM 0
-#endif
-// accumulate every point straight into the pair's sums with weight wx wy
-// (no per-x-point partial sums: 12 fewer live registers, one product more
-// per point)
-#ifndef GCABEM_DIRECT_ACC
-#define GCABEM_DIRECT_ACC 0
-#endif
+
 
 // MIR: also the transposed pair (j, i) (ROLE_PRIMARY / ROLE_SELF blocks): its
 // double layer needs d . n_x, n_x the x panel's normal (nx); dnm = -d . n_x =
@@ -96,7 +84,6 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
                                                   const double e2x[3], const double e1y[3],
                                                   const double e2y[3], const double n[3],
                                                   double kappa, double phi0, double acc[6],
-                                                  double *xc = nullptr,
                                                   const double *nx = nullptr) {
     constexpr bool DL = kind_normal(KIND);
     constexpr bool DM = MIR && DL;   // the transposed pair's double layer
@@ -126,47 +113,27 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
     // xo . n_x (MIR): dO . n_x + s e1x . n_x + t e2x . n_x
     const double M0 = DM ? dot(dO, nx) : 0.0, M1 = DM ? dot(e1x, nx) : 0.0,
                  M2 = DM ? dot(e2x, nx) : 0.0;
-#if GCABEM_XSMEM
-    constexpr int S_ = DISJOINT_TPB;
-    {
-        const double v[15] = {Q0, P1, P2, Q11, Q12, Q22, A0, A1, A2, B0, B1, B2, N0, N1, N2};
-#pragma unroll
-        for (int k = 0; k < 15; ++k) xc[k * S_] = v[k];
-    }
-#define XC(k) (*(volatile double *)&xc[(k) * S_])
-#else
-#define XC(k) (k == 0 ? Q0 : k == 1 ? P1 : k == 2 ? P2 : k == 3 ? Q11 : k == 4 ? Q12 : \
-               k == 5 ? Q22 : k == 6 ? A0 : k == 7 ? A1 : k == 8 ? A2 : k == 9 ? B0 : \
-               k == 10 ? B1 : k == 11 ? B2 : k == 12 ? N0 : k == 13 ? N1 : N2)
-#endif
+
 #pragma unroll 1
     for (int ia = 0; ia < N; ++ia) {
         const double s = c_gauss[N][ia];
-        const double xs = fma(s, fma(s, XC(3), XC(1)), XC(0));
-        const double vs = fma(s, XC(4), XC(2));
-        const double as = fma(s, XC(7), XC(6));
-        const double bs = fma(s, XC(10), XC(9));
-        const double ns = DL ? fma(s, XC(13), XC(12)) : 0.0;
+        const double xs = fma(s, fma(s, Q11, P1), Q0);
+        const double vs = fma(s, Q12, P2);
+        const double as = fma(s, A1, A0);
+        const double bs = fma(s, B1, B0);
+        const double ns = DL ? fma(s, N1, N0) : 0.0;
         const double ms = DM ? fma(s, M1, M0) : 0.0;
 #pragma unroll 1
         for (int ib = 0; ib < N; ++ib) {
             const int p = ia * N + ib;
             const double t = c_duffy_t[duffy_offset(N) + p];
             const double wx = c_duffy_w[duffy_offset(N) + p];
-            const double xx = fma(t, fma(t, XC(5), vs), xs);
-            const double xon = DL ? fma(t, XC(14), ns) : 0.0;
+            const double xx = fma(t, fma(t, Q22, vs), xs);
+            const double xon = DL ? fma(t, N2, ns) : 0.0;
             const double xonm = DM ? fma(t, M2, ms) : 0.0;
-            const double a2 = fma(t, XC(8), as);
-            const double b2 = fma(t, XC(11), bs);
-#if GCABEM_DIRECT_ACC
-            double *in = acc;   // the point weight carries wx (one product per point)
-#else
-    #if GCABEM_DIRECT_ACC
-        double *in = acc;
-#else
-        double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#endif
-#endif
+            const double a2 = fma(t, A2, as);
+            const double b2 = fma(t, B2, bs);
+            double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             // fused pair kinds at orders >= 6 roll the outer y loop (the fully
             // unrolled N^2 body spills their two layers of state)
             constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
@@ -176,15 +143,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
 #pragma unroll
                 for (int c = 0; c < N; ++c) {
                     const double gc = c_gauss[N][c];
-#if GCABEM_DIRECT_ACC
-                    const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
-#else
-    #if GCABEM_DIRECT_ACC
-                const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
-#else
-                const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
-#endif
-#endif
+                    const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
                     const double r2 = fma(gc, fma(gc, uu[d], m2b), xx);
                     const double dn = DL ? fma(-gc, un[d], xon) : 0.0;
                     const double dnm = DM ? fma(gc, unm[d], -xonm) : 0.0;
@@ -193,10 +152,9 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
             }
 #pragma unroll
             for (int k = 0; k < 6; ++k)
-                if (!GCABEM_DIRECT_ACC && slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
+                if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
         }
     }
-#undef XC
 }
 
 template <int N, int KIND, int PH, bool MIR = false>
@@ -227,22 +185,14 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xo2 = fma(t, e2x[2], fma(s, e1x[2], dO[2]));
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         const double xonm = DM ? fma(xo0, nx[0], fma(xo1, nx[1], xo2 * nx[2])) : 0.0;
-#if GCABEM_DIRECT_ACC
-        double *in = acc;
-#else
         double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#endif
         constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;  // see disjoint_expanded
 #pragma unroll OUTER
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
 #pragma unroll
             for (int d = 0; d < N; ++d) {
-#if GCABEM_DIRECT_ACC
-                const double wy = wx * c_duffy_w[duffy_offset(N) + c * N + d];
-#else
                 const double wy = c_duffy_w[duffy_offset(N) + c * N + d];
-#endif
                 const double dx = fma(-gc, ux[d], xo0);
                 const double dy = fma(-gc, uy[d], xo1);
                 const double dz = fma(-gc, uz[d], xo2);
@@ -254,7 +204,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k)
-            if (!GCABEM_DIRECT_ACC && slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
+            if (slot_used(KIND, MIR, k)) acc[k] = fma(wx, in[k], acc[k]);
     }
 }
 
@@ -308,12 +258,6 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,
                 double2 *__restrict__ payload2, double kappa) {
-#if GCABEM_XSMEM
-    __shared__ double xcoef[15 * DISJOINT_TPB];
-    double *xc = xcoef + threadIdx.x;
-#else
-    double *xc = nullptr;
-#endif
     const int2 task = tasks[blockIdx.x];
     const BlockDesc b = blocks[task.x];
     const int k = task.y + threadIdx.x;
@@ -405,12 +349,12 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
             }
             if (tiny) {
                 if (expanded)
-                    disjoint_expanded<N, KIND, 2, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, xc, nx);
+                    disjoint_expanded<N, KIND, 2, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
                 else
                     disjoint_direct<N, KIND, 2, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
             } else {
                 if (expanded)
-                    disjoint_expanded<N, KIND, 1, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, xc, nx);
+                    disjoint_expanded<N, KIND, 1, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
                 else
                     disjoint_direct<N, KIND, 1, MIR>(dO, e1x, e2x, e1y, e2y, n, 1.0, phi0, acc, nx);
             }
@@ -418,13 +362,13 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
             unscale_acc<KIND, MIR>(kappa, acc);
         } else {
             if (expanded)
-                disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, xc, nx);
+                disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
             else
                 disjoint_direct<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
         }
     } else {
         if (expanded)
-            disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, xc, nx);
+            disjoint_expanded<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
         else
             disjoint_direct<N, KIND, 0, MIR>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc, nx);
     }
