@@ -61,7 +61,7 @@ def test_mirrored_single_kinds_vs_oracle_and_plain(gload, eq, layer, kappa, orde
 
 
 @pytest.mark.parametrize("eq,kappa", [("laplace", 0.0), ("helmholtz", 4.0)])
-@pytest.mark.parametrize("orders", [(3, 5), (4, 5), (7, 7)])
+@pytest.mark.parametrize("orders", [(3, 5), (4, 5), (7, 7), (8, 5), (9, 5)])
 def test_mirrored_pair_plan_vs_oracle(gload, eq, kappa, orders):
     m, t, bt = sphere_setup(3)
     ops = golden_ops(gload("gca_L3.npz"), eq)
