@@ -15,10 +15,14 @@ Contents
 * ``batch_quadrature(..., high_precision=True)``: pairquad_hp.c, the same
   discrete rule on the reference's double-precision chart inputs evaluated
   in binary128 — the yardstick for entries that are roundoff-dominated in
-  the reference (tests/test_p2_evidence.py).
+  the reference (tests/test_reference_levels.py).
 * numpy restatements of the rule construction (quadrature.py:82-194),
   the pair classification (quadrature.py:197-220) and the Green matrix
   (gca.py:136-179), pinned against golden hashes / fixtures.
+* setup_cpu.py: the reference's setup pipeline restated (sphere mesh,
+  cluster and block trees, GCA operators, work packaging) -- the bench's
+  reference arm, runnable without the product library; p1_cpu.py: the P1
+  pair integrals (C4's cpu_baseline).
 
 Parity is pinned (see tests/test_oracle.py); it is not "unpinned".
 """
