@@ -71,7 +71,10 @@ constexpr int MAX_ORDER = 12;
 constexpr int DISJOINT_TPB = 128;   // pairs (threads) per disjoint task
 constexpr int GENERIC_TPB = 128;
 constexpr int GREEN_TPB = 128;
-constexpr int RULE_CHUNK = 256;     // rule points staged in shared memory at once
+#ifndef GCABEM_RULE_CHUNK
+#define GCABEM_RULE_CHUNK 256
+#endif
+constexpr int RULE_CHUNK = GCABEM_RULE_CHUNK;  // rule points staged in shared memory at once
 
 inline int kind_of(int equation, int layer) { return equation * 2 + layer; }
 
