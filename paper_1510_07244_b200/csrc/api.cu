@@ -723,30 +723,55 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     std::vector<int64_t> vm_mout;
     if (any_mirror) {
         // vertex items (case slot 0, sorted by payload index) -> mirrored /
-        // plain / written-by-partner, from their leaf's role
-        int64_t dropped = 0;
-        int64_t lf = leaf_lo;   // items are in payload order: walk the leaves alongside
-        for (int64_t q = L->case_at[0]; q < L->case_at[1]; ++q) {
-            const SingItem &it = si[q];
-            const int64_t g = it.out + base0;
-            while (lf + 1 < leaf_hi && leaf_base[lf + 1] <= g) ++lf;
-            const int r = role_of(lf);
-            const int64_t ncol = leaf_shape[2 * lf + 1], off = g - leaf_base[lf];
-            const int64_t i = off / ncol, j = off % ncol;
-            if (r == ROLE_PRIMARY || (r == ROLE_SELF && i < j)) {
-                const int64_t m = leaf_mirror[lf];
-                vm.push_back(it);
-                vm_mout.push_back(leaf_base[m] - base0 + j * leaf_shape[2 * m + 1] + i);
-            } else if (r == ROLE_NORMAL) {
-                vp.push_back(it);
-            } else {
-                ++dropped;
+        // plain / written-by-partner, from their leaf's role; in item chunks
+        // on the pool (each chunk finds its first leaf by bisection, then
+        // walks the leaves alongside), concatenated in chunk order
+        const int64_t q0 = L->case_at[0], nv = L->case_at[1] - L->case_at[0];
+        constexpr int VCH = 8;
+        struct Part {
+            std::vector<SingItem> vm, vp;
+            std::vector<int64_t> mout;
+            int64_t dropped = 0;
+        } parts[VCH];
+        par_for(VCH, nv < (1 << 15) ? VCH : 1, [&](int64_t c0, int64_t c1, int) {
+            for (int64_t ch = c0; ch < c1; ++ch) {
+                const int64_t a0 = q0 + ch * nv / VCH, a1 = q0 + (ch + 1) * nv / VCH;
+                Part &P = parts[ch];
+                if (a1 <= a0) continue;
+                int64_t lf = std::upper_bound(leaf_base + leaf_lo, leaf_base + leaf_hi + 1,
+                                              si[a0].out + base0) - leaf_base - 1;
+                for (int64_t q = a0; q < a1; ++q) {
+                    const SingItem &it = si[q];
+                    const int64_t g = it.out + base0;
+                    while (lf + 1 < leaf_hi && leaf_base[lf + 1] <= g) ++lf;
+                    const int r = role_of(lf);
+                    const int64_t ncol = leaf_shape[2 * lf + 1], off = g - leaf_base[lf];
+                    const int64_t i = off / ncol, j = off % ncol;
+                    if (r == ROLE_PRIMARY || (r == ROLE_SELF && i < j)) {
+                        const int64_t m = leaf_mirror[lf];
+                        P.vm.push_back(it);
+                        P.mout.push_back(leaf_base[m] - base0 + j * leaf_shape[2 * m + 1] + i);
+                    } else if (r == ROLE_NORMAL) {
+                        P.vp.push_back(it);
+                    } else {
+                        ++P.dropped;
+                    }
+                }
             }
+        });
+        int64_t dropped = 0;
+        for (const Part &P : parts) {
+            dropped += P.dropped;
+            vm.insert(vm.end(), P.vm.begin(), P.vm.end());
+            vm_mout.insert(vm_mout.end(), P.mout.begin(), P.mout.end());
+            vp.insert(vp.end(), P.vp.begin(), P.vp.end());
         }
         L->vertex_mirror = dropped == (int64_t)vm.size();
         if (L->vertex_mirror) {
-            for (const auto &it : vm) L->vm_out.push_back(it.out);
-            for (const auto &it : vp) L->vp_out.push_back(it.out);
+            L->vm_out.resize(vm.size());
+            L->vp_out.resize(vp.size());
+            for (size_t k = 0; k < vm.size(); ++k) L->vm_out[k] = vm[k].out;
+            for (size_t k = 0; k < vp.size(); ++k) L->vp_out[k] = vp[k].out;
         }
         tr.mark("mirror-split");
     }
