@@ -1,7 +1,7 @@
 """Reference fingerprints beyond L3, on the CPU (no device):
 
-* GCAMatrix.checksum() of the reference at L4 (full GCA), L5 and - with
-  GCABEM_SLOW=1 - L6 (C2) and L7 (C3), as measured independently in
+* GCAMatrix.checksum() of the reference at L4 (full GCA), L5 and - in the
+  box's -m gpu suite or with GCABEM_SLOW=1 - L6 (C2) and L7 (C3), as measured independently in
   SURVEY §8(c), reproduced bit for bit by: the reference's own pivots
   (tests/golden/gca_levels.npz, gen_gca_levels.py) -> this repo's native
   host packaging (bit-exact P1 work) -> the bit-exact oracle values. This
@@ -44,9 +44,10 @@ def _packages(gload, level, eq):
     return m, bt, packaging.make_packages(m.triangles, bt, ops, ops, 8 << 20)
 
 
+# L6 (C2) and L7 (C3): minutes of oracle CPU time -- run in the box's suite
+# (-m gpu: 16+ host cores, ~2 min), or here with GCABEM_SLOW=1
 @pytest.mark.parametrize("key", [k for k in SURVEY_CHECKSUMS if k[0] <= 5] +
-                         [pytest.param(k, marks=pytest.mark.skipif(
-                             not SLOW, reason="GCABEM_SLOW=1 (minutes of CPU)"))
+                         [pytest.param(k, marks=() if SLOW else pytest.mark.gpu)
                           for k in SURVEY_CHECKSUMS if k[0] > 5])
 def test_reference_checksum_reproduced(gload, key):
     level, eq, layer, orders = key
