@@ -1114,37 +1114,65 @@ int enqueue_disjoint(gcabem_plan_t p, int64_t b0, int64_t b1) {
     return GCABEM_OK;
 }
 
-int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p1) {
+// The singular lists of the items whose payload index lies in [p0, p1), as
+// one fused launch (launch_singular_fused): mirrored vertex items, vertex
+// items alone, edge items, identical items (half rule when available).
+int enqueue_singular(gcabem_plan_t p, int64_t p0, int64_t p1) {
     gcabem_mesh_t m = p->mesh;
-    cudaStream_t s = p->stream;
-    if (int rc = enqueue_disjoint(p, b0, b1)) return rc;
-    for (int c = 0; c < 3; ++c) {
-        if (c == 0 && vertex_mirrored(p)) {
-            gcabem_layout_t L = p->L;
-            const int64_t a0 = std::lower_bound(L->vm_out.begin(), L->vm_out.end(), p0) - L->vm_out.begin();
-            const int64_t a1 = std::lower_bound(L->vm_out.begin(), L->vm_out.end(), p1) - L->vm_out.begin();
-            GC_CUDA(launch_generic_mirror(p->kind, m->V.p, m->T.p, m->charts.p, L->vm_items.p + a0,
-                                          L->vm_mout.p + a0, a1 - a0, p->payload.p, p->payload2.p,
-                                          p->kappa, s, grouped_of(p, 0)));
-            const int64_t q0 = std::lower_bound(L->vp_out.begin(), L->vp_out.end(), p0) - L->vp_out.begin();
-            const int64_t q1 = std::lower_bound(L->vp_out.begin(), L->vp_out.end(), p1) - L->vp_out.begin();
-            GC_CUDA(launch_generic(p->kind, false, m->V.p, m->T.p, m->charts.p, L->vp_items.p + q0,
-                                   q1 - q0, p->srule[0].p, p->sq[0], p->payload.p, p->payload2.p,
-                                   p->kappa, s, grouped_of(p, 0)));
-            continue;
-        }
-        const auto first = p->L->item_out.begin() + p->L->case_at[c];
-        const auto last = p->L->item_out.begin() + p->L->case_at[c + 1];
-        const int64_t i0 = std::lower_bound(first, last, p0) - p->L->item_out.begin();
-        const int64_t i1 = std::lower_bound(first, last, p1) - p->L->item_out.begin();
-        if (i1 <= i0) continue;
-        const bool half = c == 2 && p->hq > 0;
-        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p, p->L->items.p + i0,
-                               i1 - i0, half ? p->hrule.p : p->srule[c].p,
-                               half ? p->hq : p->sq[c], p->payload.p, p->payload2.p,
-                               p->kappa, s, grouped_of(p, c)));
+    gcabem_layout_t L = p->L;
+    SingularBatch sb;
+    int k = 0;
+    auto add = [&](const SingItem *items, const int64_t *mout, int64_t n, const double *rule,
+                   int64_t q, int same, GroupedRule g) {
+        if (n <= 0) return;
+        SingularSeg &seg = sb.seg[k];
+        seg.items = items;
+        seg.mout = mout;
+        seg.n = n;
+        seg.rule = rule;
+        seg.q = q;
+        seg.same = same;
+        seg.grouped = g;
+        sb.cta_at[k + 1] = sb.cta_at[k] + (n + GENERIC_TPB - 1) / GENERIC_TPB;
+        ++k;
+    };
+    auto range = [&](const std::vector<int64_t> &v, int64_t a0, int64_t a1) {
+        const int64_t lo = std::lower_bound(v.begin() + a0, v.begin() + a1, p0) - v.begin();
+        const int64_t hi = std::lower_bound(v.begin() + a0, v.begin() + a1, p1) - v.begin();
+        return std::make_pair(lo, hi);
+    };
+    if (vertex_mirrored(p)) {
+        auto r = range(L->vm_out, 0, (int64_t)L->vm_out.size());
+        add(L->vm_items.p + r.first, L->vm_mout.p + r.first, r.second - r.first, nullptr, 0, 0,
+            grouped_of(p, 0));
+        r = range(L->vp_out, 0, (int64_t)L->vp_out.size());
+        add(L->vp_items.p + r.first, nullptr, r.second - r.first, p->srule[0].p, p->sq[0], 0,
+            grouped_of(p, 0));
+    } else {
+        auto r = range(L->item_out, L->case_at[0], L->case_at[1]);
+        add(L->items.p + r.first, nullptr, r.second - r.first, p->srule[0].p, p->sq[0], 0,
+            grouped_of(p, 0));
     }
+    {
+        auto r = range(L->item_out, L->case_at[1], L->case_at[2]);
+        add(L->items.p + r.first, nullptr, r.second - r.first, p->srule[1].p, p->sq[1], 0,
+            grouped_of(p, 1));
+    }
+    {
+        auto r = range(L->item_out, L->case_at[2], L->case_at[3]);
+        const bool half = p->hq > 0;
+        add(L->items.p + r.first, nullptr, r.second - r.first,
+            half ? p->hrule.p : p->srule[2].p, half ? p->hq : p->sq[2], 1, grouped_of(p, 2));
+    }
+    for (int e = k + 1; e <= 4; ++e) sb.cta_at[e] = sb.cta_at[k];
+    GC_CUDA(launch_singular_fused(p->kind, m->V.p, m->T.p, m->charts.p, sb, p->payload.p,
+                                  p->payload2.p, p->kappa, p->stream));
     return GCABEM_OK;
+}
+
+int enqueue_range(gcabem_plan_t p, int64_t b0, int64_t b1, int64_t p0, int64_t p1) {
+    if (int rc = enqueue_disjoint(p, b0, b1)) return rc;
+    return enqueue_singular(p, p0, p1);
 }
 
 }  // namespace
@@ -1159,25 +1187,7 @@ int gcabem_plan_execute(gcabem_plan_t p) {
     GC_CUDA(cudaEventRecord(p->ev[0], s));
     if (int rc = enqueue_disjoint(p, 0, (int64_t)p->L->block_leaf.size())) return rc;
     GC_CUDA(cudaEventRecord(p->ev[1], s));
-    for (int c = 0; c < 3; ++c) {
-        if (c == 0 && vertex_mirrored(p)) {
-            gcabem_layout_t L = p->L;
-            GC_CUDA(launch_generic_mirror(p->kind, m->V.p, m->T.p, m->charts.p, L->vm_items.p,
-                                          L->vm_mout.p, (int64_t)L->vm_out.size(), p->payload.p,
-                                          p->payload2.p, p->kappa, s, grouped_of(p, 0)));
-            GC_CUDA(launch_generic(p->kind, false, m->V.p, m->T.p, m->charts.p, L->vp_items.p,
-                                   (int64_t)L->vp_out.size(), p->srule[0].p, p->sq[0],
-                                   p->payload.p, p->payload2.p, p->kappa, s, grouped_of(p, 0)));
-            continue;
-        }
-        const int64_t n = p->L->case_at[c + 1] - p->L->case_at[c];
-        if (n == 0) continue;
-        const bool half = c == 2 && p->hq > 0;
-        GC_CUDA(launch_generic(p->kind, c == 2, m->V.p, m->T.p, m->charts.p,
-                               p->L->items.p + p->L->case_at[c], n,
-                               half ? p->hrule.p : p->srule[c].p, half ? p->hq : p->sq[c],
-                               p->payload.p, p->payload2.p, p->kappa, s, grouped_of(p, c)));
-    }
+    if (int rc = enqueue_singular(p, 0, p->payload_len)) return rc;
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
     return GCABEM_OK;

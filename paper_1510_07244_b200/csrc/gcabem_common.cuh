@@ -111,6 +111,24 @@ cudaError_t launch_generic(int kind, bool same_chart, const double *V, const int
                            const Chart *charts, const SingItem *items, int64_t n,
                            const double *rule, int64_t q, double2 *payload, double2 *payload2,
                            double kappa, cudaStream_t s, GroupedRule grouped = GroupedRule());
+// one singular list of a fused launch (launch_singular_fused)
+struct SingularSeg {
+    const SingItem *items = nullptr;
+    const int64_t *mout = nullptr;   // mirrored vertex items (else nullptr)
+    int64_t n = 0;
+    const double *rule = nullptr;    // staged rule (ungrouped / identical)
+    int64_t q = 0;
+    int same = 0;                    // identical items (exact-difference form)
+    GroupedRule grouped;
+};
+struct SingularBatch {
+    SingularSeg seg[4];
+    int64_t cta_at[5] = {0, 0, 0, 0, 0};
+};
+cudaError_t launch_singular_fused(int kind, const double *V, const int32_t *T,
+                                  const Chart *charts, const SingularBatch &b,
+                                  double2 *payload, double2 *payload2, double kappa,
+                                  cudaStream_t s);
 // mirrored vertex items: item idx also writes the transposed pair at mout[idx]
 cudaError_t launch_generic_mirror(int kind, const double *V, const int32_t *T,
                                   const Chart *charts, const SingItem *items,

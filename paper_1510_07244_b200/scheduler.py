@@ -423,8 +423,8 @@ class AssemblyPlan:
 
     def launches_per_execute(self) -> int:
         """Kernel launches of one execute(): the disjoint launch(es) -- plain
-        and mirrored when both kinds of blocks exist -- and one per non-empty
-        singular list (vertex mirrored / alone, edge, identical)."""
+        and mirrored when both kinds of blocks exist -- and one fused launch
+        for all singular lists (vertex mirrored / alone, edge, identical)."""
         ev = np.zeros(5, np.int64)
         nat.check(nat.lib().gcabem_plan_singular_evals(self.handle, nat.ptr(ev)))
         ev = ev[:4]
@@ -433,7 +433,7 @@ class AssemblyPlan:
             dis = int(mi["tasks_plain"] > 0) + int(mi["tasks_mirrored"] > 0)
         else:
             dis = int(self.disjoint_pairs > 0)
-        return dis + int(np.count_nonzero(ev))
+        return dis + int(np.count_nonzero(ev) > 0)
 
     def execute(self) -> None:
         nat.check(nat.lib().gcabem_plan_execute(self.handle))
