@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+from collections.abc import MutableMapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -332,6 +333,98 @@ def build_interpolation_operator(mesh: SurfaceMesh, cluster_index: int, panels, 
 last_build_phases: dict = {}
 
 
+class OperatorMap(MutableMapping):
+    """dict[cluster id -> InterpolationOperator] over the flat arrays one GCA
+    build returns (sorted ids, ranks, local pivots, V), materialising an
+    operator on first access (16k clusters at C3: building them all eagerly
+    costs more than packaging needs). pivot_arrays() hands the packaging the
+    flat pivot table directly. Assignment and deletion work as on a dict."""
+
+    def __init__(self, ids, starts, sizes, ranks, rows, perm, V):
+        self._ids = np.asarray(ids, dtype=np.int64)
+        self._starts, self._sizes = np.asarray(starts), np.asarray(sizes)
+        self._ranks = np.asarray(ranks, dtype=np.int64)
+        self._rows, self._perm, self._V = rows, perm, V
+        self._ro = np.concatenate([[0], np.cumsum(self._ranks)])
+        self._vo = np.concatenate([[0], np.cumsum(self._sizes * self._ranks)])
+        self._made: dict = {}
+        self._over: dict = {}
+        self._gone: set = set()
+        self._pivots = None
+
+    def _pos(self, key) -> int:
+        k = int(key)
+        i = int(np.searchsorted(self._ids, k))
+        return i if i < self._ids.size and self._ids[i] == k else -1
+
+    def __getitem__(self, key):
+        k = int(key)
+        if k in self._over:
+            return self._over[k]
+        op = self._made.get(k)
+        if op is not None:
+            return op
+        i = self._pos(k)
+        if i < 0 or k in self._gone:
+            raise KeyError(key)
+        r0, r1 = int(self._ro[i]), int(self._ro[i + 1])
+        loc = self._rows[r0:r1]
+        n, r = int(self._sizes[i]), r1 - r0
+        op = InterpolationOperator(k, loc, self._perm[int(self._starts[i]) + loc],
+                                   self._V[int(self._vo[i]):int(self._vo[i + 1])].reshape(n, r))
+        self._made[k] = op
+        return op
+
+    def __setitem__(self, key, value):
+        self._over[int(key)] = value
+        self._gone.discard(int(key))
+        self._pivots = None
+
+    def __delitem__(self, key):
+        k = int(key)
+        if k not in self:
+            raise KeyError(key)
+        self._over.pop(k, None)
+        self._gone.add(k)
+        self._pivots = None
+
+    def __contains__(self, key):
+        try:
+            k = int(key)
+        except (TypeError, ValueError):
+            return False
+        return k in self._over or (self._pos(k) >= 0 and k not in self._gone)
+
+    def __iter__(self):
+        if not self._over and not self._gone:
+            return iter(self._ids.tolist())
+        keys = set(self._ids.tolist()) - self._gone | set(self._over)
+        return iter(sorted(keys))
+
+    def __len__(self):
+        if not self._over and not self._gone:
+            return int(self._ids.size)
+        return len(set(self._ids.tolist()) - self._gone | set(self._over))
+
+    def pivot_arrays(self, nnodes: int):
+        """(at, pivots) as packaging._op_arrays builds them: at[c+1] - at[c]
+        = rank of cluster c, pivots_global in cluster-id order; None once the
+        map was modified (the generic path then walks the operators)."""
+        if self._over or self._gone:
+            return None
+        if self._pivots is None or self._pivots[0] != nnodes:
+            ok = (self._ids >= 0) & (self._ids < nnodes)
+            at = np.zeros(nnodes + 1, dtype=np.int64)
+            at[self._ids[ok] + 1] = self._ranks[ok]
+            np.cumsum(at, out=at)
+            glob = self._perm[np.repeat(self._starts, self._ranks) + self._rows[:self._ro[-1]]]
+            keep = np.repeat(ok, self._ranks)
+            piv = np.ascontiguousarray(glob[keep].astype(np.int64)) if glob.size else \
+                np.zeros(1, np.int64)
+            self._pivots = (nnodes, (at, piv if piv.size else np.zeros(1, np.int64)))
+        return self._pivots[1]
+
+
 def _host_threads() -> int:
     """Host threads for the ACA pool (packaging.host_threads: this process's
     share of the node's CPU set)."""
@@ -385,13 +478,7 @@ def _ops_for_tree(mesh, tree: ClusterTree, ids, spec, params, scene, device,
         nat.lib().gcabem_gca_free(h)
     t2 = time.perf_counter()
     Vv = V.view(np.complex128) if spec.is_complex else V
-    ops = {}
-    ro = vo = 0
-    for cid, first, n, r in zip(ids.tolist(), starts.tolist(), sizes.tolist(), ranks.tolist()):
-        loc = rows[ro:ro + r]
-        ops[cid] = InterpolationOperator(cid, loc, perm[first + loc], Vv[vo:vo + n * r].reshape(n, r))
-        ro += r
-        vo += n * r
+    ops = OperatorMap(ids, starts, sizes, ranks, rows, perm, Vv)
     # clusters with an ACA decision inside the tie window (a tie on the
     # device's bits, e.g. from the mesh's symmetry) were redone natively on
     # entries in the reference's own arithmetic (csrc/green_exact.h), so the

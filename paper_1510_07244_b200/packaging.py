@@ -187,6 +187,11 @@ def _op_arrays(ops: dict, nnodes: int):
     operator objects (ops dicts cannot be weak-referenced: the entry keeps a
     fingerprint of (cluster, operator identity) pairs and is replaced when it
     no longer matches)."""
+    fast = getattr(ops, "pivot_arrays", None)
+    if fast is not None:   # gca.OperatorMap: the flat table, no per-operator walk
+        arrs = fast(nnodes)
+        if arrs is not None:
+            return arrs
     fp = (nnodes, tuple(ops.keys()), tuple(map(id, ops.values())))
     with _cache_lock:
         hit = _op_cache.get(id(ops))
