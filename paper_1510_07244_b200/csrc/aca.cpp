@@ -177,6 +177,79 @@ inline void mulsub(T *x, T s, const T *y, int64_t n) {
     for (int64_t j = 0; j < n; ++j) x[j] = O::sub(x[j], O::mul(s, y[j]));
 }
 
+constexpr int64_t SOLVE_CHUNK = 64;  // right-hand sides per cache-resident pass
+constexpr int64_t ACA_TILE = 512;    // column entries per L1-resident update pass
+
+// x[q] <- (...((x[q] - s[0] y_0[q]) - s[1] y_1[q]) ...) - s[cnt-1] y_(cnt-1)[q]
+// with y_m = y + m * ys: the updates of cnt mulsub calls in the same order,
+// with x held in registers across them (one load and store of x per element
+// instead of one per update). Every element sees exactly mulsub's operations,
+// so the result is bitwise that of the mulsub sequence in both builds.
+template <typename T>
+void mulsub_rows(T *x, int64_t n, const T *s, int64_t cnt, const T *y, int64_t ys) {
+    using O = Ops<T>;
+    int64_t q = 0;
+#ifdef GCABEM_ACA_AVX2
+    if constexpr (std::is_same<T, Cx>::value) {
+        // 2 complex per register: s y = addsub(re(s) y, im(s) swap(y))
+        auto step = [](__m256d a, __m256d sr, __m256d si, const double *yp) {
+            const __m256d yv = _mm256_loadu_pd(yp);
+            const __m256d p = _mm256_addsub_pd(_mm256_mul_pd(sr, yv),
+                                               _mm256_mul_pd(si, _mm256_permute_pd(yv, 0x5)));
+            return _mm256_sub_pd(a, p);
+        };
+        for (; q + 8 <= n; q += 8) {
+            double *xp = reinterpret_cast<double *>(x + q);
+            __m256d a0 = _mm256_loadu_pd(xp), a1 = _mm256_loadu_pd(xp + 4);
+            __m256d a2 = _mm256_loadu_pd(xp + 8), a3 = _mm256_loadu_pd(xp + 12);
+            for (int64_t m = 0; m < cnt; ++m) {
+                const __m256d sr = _mm256_broadcast_sd(&s[m].re);
+                const __m256d si = _mm256_broadcast_sd(&s[m].im);
+                const double *yp = reinterpret_cast<const double *>(y + m * ys + q);
+                a0 = step(a0, sr, si, yp);
+                a1 = step(a1, sr, si, yp + 4);
+                a2 = step(a2, sr, si, yp + 8);
+                a3 = step(a3, sr, si, yp + 12);
+            }
+            _mm256_storeu_pd(xp, a0);
+            _mm256_storeu_pd(xp + 4, a1);
+            _mm256_storeu_pd(xp + 8, a2);
+            _mm256_storeu_pd(xp + 12, a3);
+        }
+        for (; q + 2 <= n; q += 2) {
+            double *xp = reinterpret_cast<double *>(x + q);
+            __m256d a0 = _mm256_loadu_pd(xp);
+            for (int64_t m = 0; m < cnt; ++m)
+                a0 = step(a0, _mm256_broadcast_sd(&s[m].re), _mm256_broadcast_sd(&s[m].im),
+                          reinterpret_cast<const double *>(y + m * ys + q));
+            _mm256_storeu_pd(xp, a0);
+        }
+    } else {
+        for (; q + 16 <= n; q += 16) {
+            double *xp = reinterpret_cast<double *>(x + q);
+            __m256d a0 = _mm256_loadu_pd(xp), a1 = _mm256_loadu_pd(xp + 4);
+            __m256d a2 = _mm256_loadu_pd(xp + 8), a3 = _mm256_loadu_pd(xp + 12);
+            for (int64_t m = 0; m < cnt; ++m) {
+                const __m256d sv = _mm256_broadcast_sd(reinterpret_cast<const double *>(s + m));
+                const double *yp = reinterpret_cast<const double *>(y + m * ys + q);
+                a0 = _mm256_sub_pd(a0, _mm256_mul_pd(sv, _mm256_loadu_pd(yp)));
+                a1 = _mm256_sub_pd(a1, _mm256_mul_pd(sv, _mm256_loadu_pd(yp + 4)));
+                a2 = _mm256_sub_pd(a2, _mm256_mul_pd(sv, _mm256_loadu_pd(yp + 8)));
+                a3 = _mm256_sub_pd(a3, _mm256_mul_pd(sv, _mm256_loadu_pd(yp + 12)));
+            }
+            _mm256_storeu_pd(xp, a0);
+            _mm256_storeu_pd(xp + 4, a1);
+            _mm256_storeu_pd(xp + 8, a2);
+            _mm256_storeu_pd(xp + 12, a3);
+        }
+    }
+#endif
+    for (; q < n; ++q) {
+        T acc = x[q];
+        for (int64_t m = 0; m < cnt; ++m) acc = O::sub(acc, O::mul(s[m], y[m * ys + q]));
+        x[q] = acc;
+    }
+}
 
 // np.argmax(np.abs(x)) with masked entries read as 0.0 (first index wins
 // ties). Complex magnitudes are hypot as numpy's; a squared-magnitude pass
@@ -272,7 +345,9 @@ struct DenseSrc {
 
 template <typename T, typename Src>
 void aca_core(const Src &src, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
-              int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr) {
+              int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr,
+              std::vector<T> *orig_cols = nullptr) {
+    if (orig_cols) orig_cols->clear();
     using O = Ops<T>;
     bool amb = false;
     std::vector<std::vector<T>> U, W;
@@ -314,6 +389,7 @@ void aca_core(const Src &src, int64_t nr, int64_t nc, double eps, int64_t cap, i
         const typename O::Divider by_piv(piv);
         for (int64_t j = 0; j < nc; ++j) w[j] = by_piv(r[j]);
         src.col(jp, c.data());
+        if (orig_cols) orig_cols->insert(orig_cols->end(), c.begin(), c.end());
         const double cscale = ambiguous && !amb ? max_mag<T>(c.data(), nr, 1) : 0.0;
         for (size_t m = 0; m < U.size(); ++m) {
             const T wj = W[m][jp];
@@ -358,8 +434,10 @@ void aca_core(const Src &src, int64_t nr, int64_t nc, double eps, int64_t cap, i
 
 template <typename T>
 void aca_one(const T *A, int64_t nr, int64_t nc, double eps, int64_t cap, int64_t *rows,
-             int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr) {
-    aca_core<T>(DenseSrc<T>{A, nr, nc}, nr, nc, eps, cap, rows, cols, rank, resid, ambiguous);
+             int64_t *cols, int64_t *rank, double *resid, int *ambiguous = nullptr,
+             std::vector<T> *orig_cols = nullptr) {
+    aca_core<T>(DenseSrc<T>{A, nr, nc}, nr, nc, eps, cap, rows, cols, rank, resid, ambiguous,
+                orig_cols);
 }
 
 // ---------------------------------------------------------------------------
@@ -446,6 +524,7 @@ double cond2(const T *B, int64_t r) {
 
 // LU with partial pivoting of M (r x r, row-major) and multi-RHS solves on
 // row-major (r x n) right-hand sides (inner loops run along n: contiguous).
+
 template <typename T>
 struct LU {
     int64_t r = 0;
@@ -482,19 +561,24 @@ struct LU {
     }
     // X (r x n, row-major) <- M^-1 X
     void solve(T *X, int64_t n) const {
+        for (int64_t q0 = 0; q0 < n; q0 += SOLVE_CHUNK)
+            solve_cols(X, n, q0, std::min(SOLVE_CHUNK, n - q0));
+    }
+    // columns [q0, q0 + nq) of X (row stride ld): every column is an
+    // independent right-hand side, so a chunk small enough to stay in L1/L2
+    // performs exactly the per-column operations of the whole solve
+    void solve_cols(T *X, int64_t ld, int64_t q0, int64_t nq) const {
         using O = Ops<T>;
+        X += q0;
         for (int64_t k = 0; k < r; ++k)
             if (piv[k] != k)
-                for (int64_t q = 0; q < n; ++q) std::swap(X[k * n + q], X[piv[k] * n + q]);
-        for (int64_t i = 1; i < r; ++i) {
-            T *xi = X + i * n;
-            for (int64_t j = 0; j < i; ++j) mulsub<T>(xi, m[i * r + j], X + j * n, n);
-        }
+                for (int64_t q = 0; q < nq; ++q) std::swap(X[k * ld + q], X[piv[k] * ld + q]);
+        for (int64_t i = 1; i < r; ++i) mulsub_rows<T>(X + i * ld, nq, &m[i * r], i, X, ld);
         for (int64_t i = r - 1; i >= 0; --i) {
-            T *xi = X + i * n;
-            for (int64_t j = i + 1; j < r; ++j) mulsub<T>(xi, m[i * r + j], X + j * n, n);
+            T *xi = X + i * ld;
+            mulsub_rows<T>(xi, nq, &m[i * r + i + 1], r - 1 - i, X + (i + 1) * ld, ld);
             const typename O::Divider by_d(m[i * r + i]);
-            for (int64_t q = 0; q < n; ++q) xi[q] = by_d(xi[q]);
+            for (int64_t q = 0; q < nq; ++q) xi[q] = by_d(xi[q]);
         }
     }
 };
@@ -520,53 +604,84 @@ bool cond_ok(const T *B, const LU<T> &luT, int64_t r) {
     return cond2<T>(B, r) <= 1e14;
 }
 
-// V = A[:, cols] B^-1 for ACA pivots (rows, cols, rank k): 0, or 2 when the
-// pivot block is singular or its condition number is above 1e14
+// V = A[:, cols] B^-1 for ACA pivots (rows, rank k) given the pivot columns
+// Acol[b * nr + q] = A[q, cols[b]]: 0, or 2 when the pivot block is singular
+// or its condition number is above 1e14
 template <typename T>
-int solve_one(const T *A, int64_t nr, int64_t nc, int64_t k, const int64_t *rows,
-              const int64_t *cols, std::vector<int64_t> &rows_out, std::vector<double> &V_out) {
+int solve_one(const T *Acol, int64_t nr, int64_t k, const int64_t *rows,
+              std::vector<int64_t> &rows_out, std::vector<double> &V_out) {
     using O = Ops<T>;
     // pivot block B[a][b] = A[rows[a], cols[b]], and M = B^T
     std::vector<T> B((size_t)(k * k)), M((size_t)(k * k));
     for (int64_t a = 0; a < k; ++a)
         for (int64_t b = 0; b < k; ++b) {
-            B[a * k + b] = A[rows[a] * nc + cols[b]];
+            B[a * k + b] = Acol[b * nr + rows[a]];
             M[b * k + a] = B[a * k + b];
         }
     LU<T> lu;
     if (!lu.factor(M.data(), k)) return 2;  // exactly singular: cond = inf
     if (!cond_ok<T>(B.data(), lu, k)) return 2;
-    // X = V^T (k x nr) solves M X = A_cols^T
-    std::vector<T> RHS((size_t)(k * nr)), X, R((size_t)(k * nr));
+    // X = V^T (k x nr) solves M X = A_cols^T, in chunks of SOLVE_CHUNK
+    // columns stored chunk-major (chunk c, row b at (c k + b) SOLVE_CHUNK):
+    // every chunk is a contiguous, cache-resident block, and each column
+    // sees the operations of whole-matrix passes (columns are independent)
+    constexpr int64_t QB = SOLVE_CHUNK;
+    const int64_t nch = (nr + QB - 1) / QB;
+    std::vector<T> RHS((size_t)(nch * k * QB)), X((size_t)(nch * k * QB)),
+        R((size_t)(k * QB));
     double amax = 0.0;
-    for (int64_t q = 0; q < nr; ++q)
-        for (int64_t b = 0; b < k; ++b) {
-            const T v = A[q * nc + cols[b]];
-            RHS[b * nr + q] = v;
+    for (int64_t b = 0; b < k; ++b)
+        for (int64_t q = 0; q < nr; ++q) {
+            const T v = Acol[b * nr + q];
+            RHS[((q / QB) * k + b) * QB + q % QB] = v;
             amax = std::max(amax, O::mag(v));
         }
     X = RHS;
-    lu.solve(X.data(), nr);
     const double lim = 1e-15 * std::max(amax, 1.0);
-    for (int sweep = 0; sweep < 2; ++sweep) {
-        // R^T = A_cols^T - B^T V^T = RHS - M X
-        R = RHS;
-        for (int64_t b = 0; b < k; ++b) {
-            T *rb = R.data() + b * nr;
-            for (int64_t l = 0; l < k; ++l) mulsub<T>(rb, M[b * k + l], X.data() + l * nr, nr);
-        }
+    // R = RHS - M X on one chunk (R^T = A_cols^T - B^T V^T), its max |.|
+    auto residual = [&](int64_t ch, int64_t nq) {
+        const T *xc = X.data() + ch * k * QB, *hc = RHS.data() + ch * k * QB;
         double rmax = 0.0;
-        for (const T &v : R) rmax = std::max(rmax, O::mag(v));
-        if (rmax <= lim) break;
-        lu.solve(R.data(), nr);
-        for (size_t e = 0; e < X.size(); ++e) X[e] = add_(X[e], R[e]);
+        for (int64_t b = 0; b < k; ++b) {
+            T *rb = R.data() + b * QB;
+            std::copy(hc + b * QB, hc + b * QB + nq, rb);
+            mulsub_rows<T>(rb, nq, &M[b * k], k, xc, QB);
+            for (int64_t q = 0; q < nq; ++q) rmax = std::max(rmax, O::mag(rb[q]));
+        }
+        return rmax;
+    };
+    std::vector<double> chmax((size_t)nch);
+    double rmax = 0.0;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t nq = std::min(QB, nr - ch * QB);
+        lu.solve_cols(X.data() + ch * k * QB, QB, 0, nq);
+        rmax = std::max(rmax, residual(ch, nq));
+    }
+    for (int sweep = 0; sweep < 2 && rmax > lim; ++sweep) {
+        // X += M^-1 (RHS - M X), then (first sweep only) the new residual
+        const bool last = sweep == 1;
+        rmax = 0.0;
+        for (int64_t ch = 0; ch < nch; ++ch) {
+            const int64_t nq = std::min(QB, nr - ch * QB);
+            residual(ch, nq);
+            lu.solve_cols(R.data(), QB, 0, nq);
+            T *xc = X.data() + ch * k * QB;
+            for (int64_t b = 0; b < k; ++b)
+                for (int64_t q = 0; q < nq; ++q)
+                    xc[b * QB + q] = add_(xc[b * QB + q], R[b * QB + q]);
+            if (!last) rmax = std::max(rmax, residual(ch, nq));
+        }
     }
     rows_out.assign(rows, rows + k);
     const int w = std::is_same<T, Cx>::value ? 2 : 1;
     V_out.resize((size_t)(nr * k * w));
     T *V = reinterpret_cast<T *>(V_out.data());
-    for (int64_t q = 0; q < nr; ++q)
-        for (int64_t b = 0; b < k; ++b) V[q * k + b] = X[b * nr + q];
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t q0 = ch * QB, nq = std::min(QB, nr - q0);
+        const T *xc = X.data() + ch * k * QB;
+        for (int64_t q = 0; q < nq; ++q)
+            for (int64_t b = 0; b < k; ++b) V[(q0 + q) * k + b] = xc[b * QB + q];
+    }
     return 0;
 }
 
@@ -577,16 +692,17 @@ int operator_one(const T *A, int64_t nr, int64_t nc, double eps, std::vector<int
                  std::vector<double> &V_out, int *ambiguous = nullptr) {
     const int64_t cap = std::min(nr, nc);
     std::vector<int64_t> rows(cap), cols(cap);
+    std::vector<T> acol;  // the pivot columns A[:, cols[b]] the ACA fetched
     for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
         int64_t k = 0;
-        const int64_t *r = rows.data(), *c = cols.data();
+        const int64_t *r = rows.data();
         double resid = 0.0;
         int amb = 0;
         aca_one<T>(A, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid,
-                   ambiguous ? &amb : nullptr);
+                   ambiguous ? &amb : nullptr, &acol);
         if (ambiguous && amb) *ambiguous = 1;
         if (k == 0) return 1;
-        if (solve_one<T>(A, nr, nc, k, r, c, rows_out, V_out) == 0) return 0;
+        if (solve_one<T>(acol.data(), nr, k, r, rows_out, V_out) == 0) return 0;
     }
     return 2;
 }
@@ -635,21 +751,14 @@ int operator_exact(const gcabem::GreenExact &g, double eps, std::vector<int64_t>
     const int64_t nr = g.nr, nc = g.nsrc(), cap = std::min(nr, nc);
     ExactSrc<T> src{&g, nr, nc, {}};
     std::vector<int64_t> rows(cap), cols(cap);
+    std::vector<T> acol;
     for (int attempt = 0; attempt < 2; ++attempt, eps *= 0.1) {
         int64_t k = 0;
         double resid = 0.0;
-        aca_core<T>(src, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid);
+        aca_core<T>(src, nr, nc, eps, cap, rows.data(), cols.data(), &k, &resid, nullptr,
+                    &acol);
         if (k == 0) return 1;
-        // A[:, cols] compacted (nr x k): solve_one reads exactly these values
-        std::vector<T> Ac((size_t)(nr * k));
-        for (int64_t b = 0; b < k; ++b) {
-            const std::vector<T> &c = src.column(cols[b]);
-            for (int64_t q = 0; q < nr; ++q) Ac[q * k + b] = c[q];
-        }
-        std::vector<int64_t> iota(k);
-        for (int64_t b = 0; b < k; ++b) iota[b] = b;
-        if (solve_one<T>(Ac.data(), nr, k, k, rows.data(), iota.data(), rows_out, V_out) == 0)
-            return 0;
+        if (solve_one<T>(acol.data(), nr, k, rows.data(), rows_out, V_out) == 0) return 0;
     }
     return 2;
 }
