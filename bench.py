@@ -692,8 +692,9 @@ def run_ours(args, cfg, dist, log):
     # e2e through the public API, host buffers, H2D + D2H inside the step
     backend = scheduler.Backend("cuda", devices=tuple(devices))
     params = scheduler.SchedulerParams(backends=(backend,), shard=shard,
-                                       mirror=not args.no_mirror)
-    e2e_t, e2e_phases, d2h = [], [], 0
+                                       mirror=not args.no_mirror,
+                                       symmetric_download=not args.no_sym_download)
+    e2e_t, e2e_phases, d2h, payload_bytes = [], [], 0, 0
 
     def assemble_all(stats_list):
         if fused:
@@ -704,8 +705,12 @@ def run_ours(args, cfg, dist, log):
     setup_first = None
     if args.e2e_steps > 0:
         scheduler.clear_package_cache()
-        warm = assemble_all([scheduler.AssemblyStats() for _ in specs])  # path + pinned pool
-        d2h = sum(M.buffer.nbytes for M in warm)
+        st_warm = [scheduler.AssemblyStats() for _ in specs]
+        warm = assemble_all(st_warm)  # path + pinned pool
+        # bytes the download moved (a symmetric download skips the SKIP
+        # leaves of the single layer: less than the payloads' size)
+        d2h = sum(x.d2h_bytes for x in st_warm)
+        payload_bytes = sum(M.buffer.nbytes for M in warm)
         del warm
     for k in range(args.e2e_steps):
         dist.barrier()
@@ -723,6 +728,8 @@ def run_ours(args, cfg, dist, log):
     e2e_dt = dist.max(statistics.median(e2e_t)) if e2e_t else None
     e2e_value = pairs_job / e2e_dt if e2e_dt else None
     d2h_job = dist.sum(d2h) if shard else d2h * (dist.world if not strong else 1)
+    payload_job = dist.sum(payload_bytes) if shard else \
+        payload_bytes * (dist.world if not strong else 1)
     h2d_job = dist.sum(h2d) if shard else h2d * (dist.world if not strong else 1)
 
     # solve-phase product on the device-resident operator (h2.matvec, SURVEY
@@ -805,6 +812,8 @@ def run_ours(args, cfg, dist, log):
                      "kernel_share_of_step": share},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_job),
                 "d2h_bytes_per_step": int(d2h_job), "seconds_per_step": e2e_dt,
+                "payload_bytes_per_step": int(payload_job),
+                "symmetric_download": not args.no_sym_download,
                 "phases_s": [{k: round(v, 4) for k, v in ph.items()} for ph in e2e_phases]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -891,6 +900,9 @@ def main(argv=None):
     ap.add_argument("--no-mirror", action="store_true",
                     help="evaluate every pair on its own (no symmetric evaluation of mirror "
                          "leaves)")
+    ap.add_argument("--no-sym-download", action="store_true",
+                    help="e2e: copy every payload entry (no symmetric download of the single "
+                         "layer's mirror leaves)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the C5 (order 3) device-step key of the default C3 line")
     ap.add_argument("--no-separate", action="store_true",

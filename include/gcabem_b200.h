@@ -179,6 +179,18 @@ int gcabem_plan_execute(gcabem_plan_t plan);
  * gcabem_plan_synchronize before reading `host`. */
 int gcabem_plan_execute_download(gcabem_plan_t plan, double *host, int nchunks);
 int gcabem_plan_execute_download2(gcabem_plan_t plan, double *host, double *host2, int nchunks);
+/* Symmetric download (mirrored plans whose first payload is a single layer:
+ * L/H single layer and the pair kinds): execute_download copies neither the
+ * SKIP leaves of runs of at least 16384 entries nor their value: a host
+ * thread of the plan writes each as the transpose of its PRIMARY leaf (the
+ * mirrored kernels write one value to both entries) plus its singular entries,
+ * gathered on the device (the edge rule is not symmetric). The host buffer
+ * ends up bitwise equal to the device payload; gcabem_plan_synchronize also
+ * waits for the host thread. enable = 0 restores full copies. */
+int gcabem_plan_set_symmetric_download(gcabem_plan_t plan, int enable);
+/* Bytes the last execute_download moved device -> host (both payloads and
+ * the singular patch of a symmetric download). */
+int gcabem_plan_d2h_bytes(gcabem_plan_t plan, int64_t *out);
 /* Copy the payload (payload_len complex128) to host memory and wait. */
 int gcabem_plan_download(gcabem_plan_t plan, double *host);
 int gcabem_plan_download2(gcabem_plan_t plan, double *host, double *host2);

@@ -68,6 +68,8 @@ _SIGS = {
     "gcabem_plan_execute_download2": ([_vp, _vp, _vp, _int], _int),
     "gcabem_plan_execute_download": ([_vp, _vp, _int], _int),
     "gcabem_plan_synchronize": ([_vp], _int),
+    "gcabem_plan_set_symmetric_download": ([_vp, _int], _int),
+    "gcabem_plan_d2h_bytes": ([_vp, ctypes.POINTER(_i64)], _int),
     "gcabem_plan_timing": ([_vp, _vp], _int),
     "gcabem_plan_payload": ([_vp, ctypes.POINTER(_vp)], _int),
     "gcabem_plan_set_stream": ([_vp, _vp], _int),

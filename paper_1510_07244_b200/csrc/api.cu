@@ -1,6 +1,7 @@
 // C ABI of gcabem_b200 (declared in include/gcabem_b200.h). Host-side
 // ownership, uploads, task decomposition and error mapping; no compute here.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <map>
@@ -128,6 +129,19 @@ struct gcabem_plan_s {
     // the layout's mirrored blocks run on the mirrored kernel (orders up to
     // MAX_MIRROR_ORDER; gcabem_plan_set_mirror can turn it off)
     bool mirrored = false;
+    // symmetric download of the single layer (gcabem_layout_s::hf_lo): the
+    // gathered singular entries of the host-filled leaves (device, pinned
+    // host), one event per chunk after its copies, the host thread that
+    // fills the leaves chunk by chunk, and the bytes the last download moved
+    bool sym = false;
+    PoolBuf<double2> patch_vals;
+    double2 *patch_host = nullptr;
+    size_t patch_host_bytes = 0;
+    std::vector<cudaEvent_t> copy_ev;
+    std::thread filler;
+    int fill_rc = 0;
+    std::string fill_msg;
+    int64_t d2h_bytes = 0;
 };
 
 extern "C" {
@@ -451,8 +465,9 @@ namespace {
 
 // split [0, n) over up to `maxt` std::threads (inline below `grain`)
 template <typename F>
-void par_for(int64_t n, int64_t grain, F fn) {
-    const int maxt = (int)std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency()));
+void par_for(int64_t n, int64_t grain, F fn, unsigned max_threads = 8) {
+    const int maxt = (int)std::min<unsigned>(max_threads,
+                                             std::max(1u, std::thread::hardware_concurrency()));
     const int nt = (int)std::min<int64_t>(maxt, std::max<int64_t>(1, n / std::max<int64_t>(grain, 1)));
     if (nt <= 1) {
         fn(0, n, 0);
@@ -468,10 +483,66 @@ void par_for(int64_t n, int64_t grain, F fn) {
     for (auto &x : th) x.join();
 }
 
-// pinned staging for layout uploads (grow-only, one user at a time)
-std::mutex g_arena_mutex;
-void *g_arena = nullptr;
-size_t g_arena_bytes = 0;
+// pinned host blocks reused across plans (cudaHostAlloc costs milliseconds):
+// a free list by size
+std::mutex g_pin_mutex;
+std::multimap<size_t, void *> g_pin_free;
+
+void *pinned_acquire(size_t bytes, size_t *got) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mutex);
+        auto it = g_pin_free.lower_bound(bytes);
+        if (it != g_pin_free.end() && it->first <= 4 * bytes + (1 << 20)) {
+            void *ptr = it->second;
+            *got = it->first;
+            g_pin_free.erase(it);
+            return ptr;
+        }
+    }
+    size_t n = 1 << 16;
+    while (n < bytes) n <<= 1;
+    void *ptr = nullptr;
+    if (cudaHostAlloc(&ptr, n, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    *got = n;
+    return ptr;
+}
+
+void pinned_release(void *ptr, size_t bytes) {
+    if (!ptr) return;
+    std::lock_guard<std::mutex> lk(g_pin_mutex);
+    g_pin_free.emplace(bytes, ptr);
+}
+
+__global__ void gather_entries_kernel(const double2 *__restrict__ src,
+                                      const int64_t *__restrict__ idx, int64_t n,
+                                      double2 *__restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+
+// SKIP leaf s of the host-filled list: its entries as the transpose of its
+// PRIMARY (already in `host`), written with streaming stores (the rows are
+// contiguous; no read-for-ownership of the target lines), then its singular
+// entries from the patch
+void host_fill_leaf(const gcabem_layout_s *L, int64_t s, double2 *host, const double2 *patch) {
+    const int64_t nr = L->hf_nr[s], nc = L->hf_nc[s];
+    double *dst = reinterpret_cast<double *>(host + L->hf_lo[s]);
+    const double *src = reinterpret_cast<const double *>(host + L->hf_m[s]);  // nc x nr
+    constexpr int64_t TB = 16;
+    for (int64_t i0 = 0; i0 < nr; i0 += TB)
+        for (int64_t j0 = 0; j0 < nc; j0 += TB) {
+            const int64_t i1 = std::min(nr, i0 + TB), j1 = std::min(nc, j0 + TB);
+            for (int64_t i = i0; i < i1; ++i)
+                for (int64_t j = j0; j < j1; ++j)
+                    _mm_stream_pd(dst + 2 * (i * nc + j), _mm_loadu_pd(src + 2 * (j * nr + i)));
+        }
+    _mm_sfence();
+    for (int64_t q = L->hf_item_at[s]; q < L->hf_item_at[s + 1]; ++q)
+        host[L->patch_out[q]] = patch[q];
+}
 
 }  // namespace
 
@@ -607,20 +678,19 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                  off_p = off_rt + align(sizeof(int2) * nrt),
                  off_s = off_p + align(sizeof(int32_t) * npanels),
                  total = off_s + align(sizeof(SingItem) * S);
-    std::lock_guard<std::mutex> arena_lock(g_arena_mutex);
-    if (total > g_arena_bytes) {
-        if (g_arena) cudaFreeHost(g_arena);
-        g_arena = nullptr;
-        g_arena_bytes = 0;
-        cudaError_t e = cudaHostAlloc(&g_arena, std::max<size_t>(total, size_t(64) << 20),
-                                      cudaHostAllocPortable);
-        if (e != cudaSuccess) {
-            delete L;
-            GC_CUDA(e);
-        }
-        g_arena_bytes = std::max<size_t>(total, size_t(64) << 20);
+    // from the pinned pool (no lock held while filling: layouts of several
+    // leaf ranges may be built concurrently); returned after the stream sync
+    struct PinnedBlock {
+        void *p = nullptr;
+        size_t n = 0;
+        ~PinnedBlock() { pinned_release(p, n); }
+    } arena_blk;
+    arena_blk.p = pinned_acquire(total, &arena_blk.n);
+    if (!arena_blk.p) {
+        delete L;
+        return set_error(GCABEM_ERR_CUDA, "pinned staging allocation failed");
     }
-    char *arena = static_cast<char *>(g_arena);
+    char *arena = static_cast<char *>(arena_blk.p);
     BlockDesc *bd = reinterpret_cast<BlockDesc *>(arena);
     int2 *tasks = reinterpret_cast<int2 *>(arena + off_t);
     int2 *mtasks = reinterpret_cast<int2 *>(arena + off_mt);
@@ -810,6 +880,66 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
         L->mirror_info[2] = mp + up;
         L->mirror_info[3] = sp;
     }
+    if (any_mirror) {
+        // host-filled SKIP leaves (symmetric download): runs of consecutive
+        // SKIP leaves of at least SYM_MIN_RUN entries (a shorter gap costs
+        // less to copy than one more D2H call; GCABEM_SYM_MIN_RUN overrides)
+        const char *env_run = std::getenv("GCABEM_SYM_MIN_RUN");
+        const int64_t min_run = env_run ? std::max<long long>(1, std::atoll(env_run)) : SYM_MIN_RUN;
+        for (int64_t lf = leaf_lo; lf < leaf_hi;) {
+            if (role_of(lf) != ROLE_SKIP) {
+                ++lf;
+                continue;
+            }
+            int64_t e = lf;
+            while (e < leaf_hi && role_of(e) == ROLE_SKIP) ++e;
+            if (leaf_base[e] - leaf_base[lf] >= min_run)
+                for (int64_t q = lf; q < e; ++q) {
+                    L->hf_lo.push_back(leaf_base[q] - base0);
+                    L->hf_m.push_back(leaf_base[leaf_mirror[q]] - base0);
+                    L->hf_nr.push_back((int32_t)leaf_shape[2 * q]);
+                    L->hf_nc.push_back((int32_t)leaf_shape[2 * q + 1]);
+                }
+            lf = e;
+        }
+        // their singular entries: per case the item payload indices ascend,
+        // so a sweep against the (ascending) leaves finds them; in leaf
+        // chunks on the pool (each chunk bisects to its first item), one
+        // pass counting, one filling
+        const int64_t H = (int64_t)L->hf_lo.size();
+        L->hf_item_at.assign(H + 1, 0);
+        std::vector<int64_t> hf_hi(H);
+        for (int64_t h = 0; h < H; ++h) hf_hi[h] = L->hf_lo[h] + (int64_t)L->hf_nr[h] * L->hf_nc[h];
+        constexpr int64_t NCH = 64;
+        auto sweep = [&](int64_t ch, auto &&visit) {
+            const int64_t h0 = ch * H / NCH, h1 = (ch + 1) * H / NCH;
+            if (h0 >= h1) return;
+            for (int c = 0; c < 3; ++c) {
+                const int64_t *b = L->item_out.data() + L->case_at[c];
+                const int64_t *e = L->item_out.data() + L->case_at[c + 1];
+                int64_t h = h0;
+                for (const int64_t *it = std::lower_bound(b, e, L->hf_lo[h0]);
+                     it != e && *it < hf_hi[h1 - 1]; ++it) {
+                    while (hf_hi[h] <= *it) ++h;
+                    if (*it >= L->hf_lo[h]) visit(h, *it);
+                }
+            }
+        };
+        if (H) {
+            par_for(NCH, 1, [&](int64_t c0, int64_t c1, int) {
+                for (int64_t ch = c0; ch < c1; ++ch)
+                    sweep(ch, [&](int64_t h, int64_t) { ++L->hf_item_at[h + 1]; });
+            });
+            for (int64_t h = 0; h < H; ++h) L->hf_item_at[h + 1] += L->hf_item_at[h];
+            L->patch_out.resize(L->hf_item_at[H]);
+            std::vector<int64_t> cur(L->hf_item_at.begin(), L->hf_item_at.end() - 1);
+            par_for(NCH, 1, [&](int64_t c0, int64_t c1, int) {
+                for (int64_t ch = c0; ch < c1; ++ch)
+                    sweep(ch, [&](int64_t h, int64_t off) { L->patch_out[cur[h]++] = off; });
+            });
+        }
+        tr.mark("sym-leaves");
+    }
     cudaStream_t s = mesh->stream;
     cudaError_t e = pool_init(mesh->device);
     if (e == cudaSuccess) e = L->blocks.alloc(B, s);
@@ -829,6 +959,8 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
         if (e == cudaSuccess) e = L->vm_mout.upload(vm_mout.data(), vm_mout.size(), s);
         if (e == cudaSuccess) e = L->vp_items.upload(vp.data(), vp.size(), s);
     }
+    if (e == cudaSuccess && !L->patch_out.empty())
+        e = L->patch_dev.upload(L->patch_out.data(), L->patch_out.size(), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the arena is reused after this
     tr.mark("upload");
     if (e != cudaSuccess) {
@@ -1222,11 +1354,53 @@ int gcabem_plan_execute_download(gcabem_plan_t p, double *host, int nchunks) {
     return gcabem_plan_execute_download2(p, host, nullptr, nchunks);
 }
 
+namespace {
+int join_filler(gcabem_plan_t p) {
+    if (p->filler.joinable()) p->filler.join();
+    const int rc = p->fill_rc;
+    p->fill_rc = 0;
+    return rc ? set_error(rc, p->fill_msg) : GCABEM_OK;
+}
+}  // namespace
+
+int gcabem_plan_set_symmetric_download(gcabem_plan_t p, int enable) {
+    GC_ARG(p, "null plan");
+    // the first payload is a single layer: symmetric under the mirror
+    p->sym = enable && (p->kind == L_SLP || p->kind == H_SLP || kind_pair(p->kind));
+    return GCABEM_OK;
+}
+
+int gcabem_plan_d2h_bytes(gcabem_plan_t p, int64_t *out) {
+    GC_ARG(p && out, "null argument");
+    *out = p->d2h_bytes;
+    return GCABEM_OK;
+}
+
 int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, int nchunks) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
     GC_ARG(!kind_pair(p->kind) || host2 || p->payload_len == 0,
            "pair plan: the double-layer target is missing");
     GC_CUDA(cudaSetDevice(p->mesh->device));
+    if (int rc = join_filler(p)) return rc;
+    gcabem_layout_t L = p->L;
+    // symmetric download: host-filled SKIP leaves are not copied (see
+    // gcabem_layout_s::hf_lo); needs the mirrored kernels to have written
+    // their values (one value to both entries of a mirrored pair)
+    const bool sym = p->sym && p->mirrored && !L->hf_lo.empty();
+    const int64_t npatch = sym ? (int64_t)L->patch_out.size() : 0;
+    if (npatch > 0) {
+        GC_CUDA(p->patch_vals.alloc(npatch, p->stream));
+        if (p->patch_host_bytes < sizeof(double2) * npatch) {
+            pinned_release(p->patch_host, p->patch_host_bytes);
+            p->patch_host = (double2 *)pinned_acquire(sizeof(double2) * npatch,
+                                                      &p->patch_host_bytes);
+            if (!p->patch_host) {
+                p->patch_host_bytes = 0;
+                return set_error(GCABEM_ERR_CUDA, "pinned patch staging allocation failed");
+            }
+        }
+    }
+    p->d2h_bytes = 0;
     const int64_t B = (int64_t)p->L->block_leaf.size();
     if (nchunks < 1) nchunks = 1;
     // leaf-aligned chunk boundaries balanced by pairs
@@ -1249,27 +1423,90 @@ int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, 
         GC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         p->chunk_ev.push_back(e);
     }
+    if (sym)
+        while (p->copy_ev.size() < p->chunk_ev.size()) {
+            cudaEvent_t e;
+            GC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            p->copy_ev.push_back(e);
+        }
+    double2 *h1 = reinterpret_cast<double2 *>(host);
+    std::vector<std::pair<int64_t, int64_t>> fill;  // host-filled leaves per chunk
+    auto copy = [&](double2 *dst, const double2 *src, int64_t n) -> cudaError_t {
+        p->d2h_bytes += (int64_t)sizeof(double2) * n;
+        return cudaMemcpyAsync(dst, src, sizeof(double2) * n, cudaMemcpyDeviceToHost, p->copy);
+    };
     for (size_t k = 0; k + 1 < cut.size(); ++k) {
         const int64_t b0 = cut[k], b1 = cut[k + 1];
-        const int64_t p0 = b0 < B ? p->L->block_base[b0] : p->payload_len;
-        const int64_t p1 = b1 < B ? p->L->block_base[b1] : p->payload_len;
+        const int64_t p0 = b0 < B ? L->block_base[b0] : p->payload_len;
+        const int64_t p1 = b1 < B ? L->block_base[b1] : p->payload_len;
         // chunks run in leaf order, so every SKIP entry of this chunk was
         // written by its PRIMARY in this or an earlier chunk before this D2H
         if (int rc = enqueue_range(p, b0, b1, p0, p1)) return rc;
+        int64_t s0 = 0, s1 = 0, q0 = 0, q1 = 0;
+        if (sym) {
+            s0 = std::lower_bound(L->hf_lo.begin(), L->hf_lo.end(), p0) - L->hf_lo.begin();
+            s1 = std::lower_bound(L->hf_lo.begin(), L->hf_lo.end(), p1) - L->hf_lo.begin();
+            q0 = L->hf_item_at[s0];
+            q1 = L->hf_item_at[s1];
+            if (q1 > q0)
+                gather_entries_kernel<<<(unsigned)((q1 - q0 + 255) / 256), 256, 0, s>>>(
+                    p->payload.p, L->patch_dev.p + q0, q1 - q0, p->patch_vals.p + q0);
+            GC_CUDA(cudaGetLastError());
+        }
         GC_CUDA(cudaEventRecord(p->chunk_ev[k], s));
         if (p1 > p0) {
             GC_CUDA(cudaStreamWaitEvent(p->copy, p->chunk_ev[k], 0));
-            GC_CUDA(cudaMemcpyAsync(host + 2 * p0, p->payload.p + p0, sizeof(double2) * (p1 - p0),
-                                    cudaMemcpyDeviceToHost, p->copy));
+            if (sym) {  // the chunk's payload minus its host-filled leaves
+                int64_t cur = p0;
+                for (int64_t h = s0; h < s1; ++h) {
+                    if (L->hf_lo[h] > cur)
+                        GC_CUDA(copy(h1 + cur, p->payload.p + cur, L->hf_lo[h] - cur));
+                    cur = L->hf_lo[h] + (int64_t)L->hf_nr[h] * L->hf_nc[h];
+                }
+                if (cur < p1) GC_CUDA(copy(h1 + cur, p->payload.p + cur, p1 - cur));
+                if (q1 > q0)
+                    GC_CUDA(copy(p->patch_host + q0, p->patch_vals.p + q0, q1 - q0));
+            } else {
+                GC_CUDA(copy(h1 + p0, p->payload.p + p0, p1 - p0));
+            }
             if (kind_pair(p->kind))
-                GC_CUDA(cudaMemcpyAsync(host2 + 2 * p0, p->payload2.p + p0,
-                                        sizeof(double2) * (p1 - p0), cudaMemcpyDeviceToHost,
-                                        p->copy));
+                GC_CUDA(copy(reinterpret_cast<double2 *>(host2) + p0, p->payload2.p + p0,
+                             p1 - p0));
+        }
+        if (sym) {
+            GC_CUDA(cudaEventRecord(p->copy_ev[k], p->copy));
+            fill.emplace_back(s0, s1);
         }
     }
     GC_CUDA(cudaEventRecord(p->ev[1], s));
     GC_CUDA(cudaEventRecord(p->ev[2], s));
     p->executed = true;
+    if (sym) {
+        // the host side: chunk by chunk (copies complete in chunk order, so a
+        // leaf's PRIMARY, in this or an earlier chunk, has arrived), the
+        // chunk's host-filled leaves on the pool
+        const int dev = p->mesh->device;
+        std::vector<cudaEvent_t> evs(p->copy_ev.begin(), p->copy_ev.begin() + fill.size());
+        double2 *patch = p->patch_host;
+        p->filler = std::thread([p, L, h1, patch, dev, evs, fill]() {
+            cudaSetDevice(dev);
+            Trace tr("sym-fill");
+            for (size_t k = 0; k < fill.size(); ++k) {
+                if (cudaEventSynchronize(evs[k]) != cudaSuccess) {
+                    p->fill_msg = std::string("symmetric download: ") +
+                                  cudaGetErrorString(cudaGetLastError());
+                    p->fill_rc = GCABEM_ERR_CUDA;
+                    return;
+                }
+                tr.mark("copied");
+                const int64_t s0 = fill[k].first, n = fill[k].second - fill[k].first;
+                par_for(n, 32, [&](int64_t a, int64_t b, int) {
+                    for (int64_t h = a; h < b; ++h) host_fill_leaf(L, s0 + h, h1, patch);
+                }, 16u);
+                tr.mark("filled");
+            }
+        });
+    }
     return GCABEM_OK;
 }
 
@@ -1280,6 +1517,7 @@ int gcabem_plan_download(gcabem_plan_t p, double *host) {
 int gcabem_plan_download2(gcabem_plan_t p, double *host, double *host2) {
     GC_ARG(p && (host || p->payload_len == 0), "null argument");
     GC_CUDA(cudaSetDevice(p->mesh->device));
+    if (int rc = join_filler(p)) return rc;
     if (p->payload_len > 0)
         GC_CUDA(cudaMemcpyAsync(host, p->payload.p, sizeof(double2) * p->payload_len,
                                 cudaMemcpyDeviceToHost, p->stream));
@@ -1295,7 +1533,7 @@ int gcabem_plan_synchronize(gcabem_plan_t p) {
     GC_CUDA(cudaSetDevice(p->mesh->device));
     GC_CUDA(cudaStreamSynchronize(p->stream));
     GC_CUDA(cudaStreamSynchronize(p->copy));
-    return GCABEM_OK;
+    return join_filler(p);
 }
 
 int gcabem_plan_timing(gcabem_plan_t p, float *ms3) {
@@ -1330,9 +1568,13 @@ int gcabem_plan_destroy(gcabem_plan_t p) {
     cudaSetDevice(p->mesh->device);
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->copy) cudaStreamSynchronize(p->copy);
+    join_filler(p);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : p->chunk_ev) cudaEventDestroy(e);
+    for (auto &e : p->copy_ev) cudaEventDestroy(e);
+    pinned_release(p->patch_host, p->patch_host_bytes);
+    p->patch_vals.release();
     tr.mark("sync+events");
     p->payload.release();
     p->payload2.release();
@@ -1428,10 +1670,9 @@ int gcabem_release_cached(int device) {
     GC_CUDA(cudaDeviceSynchronize());
     gca_release_staging(device);
     {
-        std::lock_guard<std::mutex> lock(g_arena_mutex);
-        if (g_arena) cudaFreeHost(g_arena);
-        g_arena = nullptr;
-        g_arena_bytes = 0;
+        std::lock_guard<std::mutex> lock(g_pin_mutex);
+        for (auto &kv : g_pin_free) cudaFreeHost(kv.second);
+        g_pin_free.clear();
     }
     cudaMemPool_t pool;
     GC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

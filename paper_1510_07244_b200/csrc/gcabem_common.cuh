@@ -85,6 +85,12 @@ cudaError_t upload_disjoint_rule(int order, const double *gauss_pts, const doubl
 // ROLE_PRIMARY / ROLE_SELF tasks (orders <= MAX_MIRROR_ORDER).
 constexpr int MIRRORED = 8;
 constexpr int MAX_MIRROR_ORDER = 8;
+// symmetric download: SKIP-leaf runs of at least this many payload entries
+// (256 KB) are written on the host from their PRIMARY instead of copied
+#ifndef GCABEM_SYM_MIN_RUN
+#define GCABEM_SYM_MIN_RUN 16384
+#endif
+constexpr int64_t SYM_MIN_RUN = GCABEM_SYM_MIN_RUN;
 cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
                             const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
                             const int32_t *panels, double2 *payload, double2 *payload2,

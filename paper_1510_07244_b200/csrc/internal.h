@@ -138,6 +138,17 @@ struct gcabem_layout_s {
     gcabem::PoolBuf<int64_t> vm_mout;
     std::vector<int64_t> vm_out, vp_out;
     bool vertex_mirror = false;
+    // symmetric download of a mirrored single layer (gcabem_plan_set_symmetric_
+    // download): the SKIP leaves of runs of at least SYM_MIN_RUN payload
+    // entries are not copied; the host writes each as the transpose of its
+    // PRIMARY (the mirrored kernels write one value to both entries), then its
+    // singular entries (written by their own items: the edge rule is not
+    // symmetric) from a device gather. Per such leaf, in payload order: its
+    // start, shape and its PRIMARY's start; its singular entries are
+    // patch_out[hf_item_at[s], hf_item_at[s + 1]) (payload indices).
+    std::vector<int64_t> hf_lo, hf_m, hf_item_at, patch_out;
+    std::vector<int32_t> hf_nr, hf_nc;
+    gcabem::PoolBuf<int64_t> patch_dev;
     gcabem::PoolBuf<int32_t> panels;
     gcabem::PoolBuf<gcabem::SingItem> items;
     int64_t case_at[4] = {0, 0, 0, 0};  // items of case c at [case_at[c-1], case_at[c])

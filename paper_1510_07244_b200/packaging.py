@@ -19,7 +19,9 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
+import time
 import weakref
 from dataclasses import dataclass, field
 
@@ -349,6 +351,20 @@ def shard_leaf_set(block_tree: BlockTree, row_ops, col_ops, shard, disjoint_q: i
     return np.ascontiguousarray(mine, dtype=np.int64)
 
 
+class _Trace:
+    """GCABEM_TRACE=1: phase times of the host packaging on stderr."""
+
+    def __init__(self, who: str):
+        self.who, self.on = who, bool(os.environ.get("GCABEM_TRACE"))
+        self.t = time.perf_counter()
+
+    def mark(self, what: str) -> None:
+        if self.on:
+            now = time.perf_counter()
+            print(f"[{self.who}] {what:<12} {(now - self.t) * 1e3:8.2f} ms", file=sys.stderr)
+            self.t = now
+
+
 def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops,
                   maxsize: int, nthreads: int = 0, leaf_range=None,
                   inputs: PackageInputs | None = None, leaf_index=None) -> AssemblyPackages:
@@ -377,6 +393,7 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
     nthreads = nthreads or host_threads()
     h = ctypes.c_void_p()
     p = nat.ptr
+    tr = _Trace("make_packages")
     nat.check(nat.lib().gcabem_packages_build(
         T.shape[0], p(T), leaves.shape[0], p(leaves), rs.size, p(rs), p(rz), p(rlo), p(rhi),
         p(rperm), p(rat), p(rpiv), cs.size, p(cs), p(cz), p(clo), p(chi), p(cperm), p(cat),
@@ -395,11 +412,15 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         blk_list = np.empty(nblk, np.int64)
         items = np.empty((6, nit), np.int64)
         perms = np.empty((nit, 6), np.uint8)
+        tr.mark("build+alloc")
         nat.check(nat.lib().gcabem_packages_fetch(
             h, p(panels), p(shape), p(base), p(rows_at), p(cols_at), p(flagged), p(blocks),
             p(blk_list), p(items), p(perms)))
+        tr.mark("fetch")
     finally:
         nat.lib().gcabem_packages_free(h)
+    mirrors = leaf_mirrors(block_tree, row_ops, col_ops, x, leaf_range, leaf_index)
+    tr.mark("mirrors")
     return AssemblyPackages(
         maxsize=int(maxsize), leaf_ids=leaf_ids, leaf_shape=shape, leaf_base=base,
         panels=panels, leaf_rows_at=rows_at, leaf_cols_at=cols_at,
@@ -407,8 +428,7 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         blk_nr=blocks[2], blk_c0=blocks[3], blk_nc=blocks[4], blk_list=blk_list,
         n_disjoint_lists=nlists, item_case=items[0].astype(np.int8), item_tri_x=items[1],
         item_tri_y=items[2], item_leaf=items[3], item_offset=items[4],
-        item_src_block=items[5], perms=perms,
-        leaf_mirror=leaf_mirrors(block_tree, row_ops, col_ops, x, leaf_range, leaf_index))
+        item_src_block=items[5], perms=perms, leaf_mirror=mirrors)
 
 
 def shard_leaves(pk: AssemblyPackages, nshards: int, disjoint_q: int, singular_q=None):

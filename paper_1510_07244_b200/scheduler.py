@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 import time
 import weakref
@@ -42,6 +43,12 @@ DEFAULT_MAXSIZE = 8 * 2 ** 20
 # payload growth between consecutive ranges of a staged assembly (measured at
 # C3: 1.5 with 6 ranges beats 2 with 5 by ~5% e2e)
 STAGE_GROWTH = float(os.environ.get("GCABEM_STAGE_GROWTH", "1.5"))
+# host threads packaging leaf ranges (and building their device layouts) ahead
+# of the device
+PACK_WORKERS = int(os.environ.get("GCABEM_PACK_WORKERS", "2"))
+# the last STAGE_TAPER ranges halve in size one after the other (a small last
+# range shortens the tail: its packaging, layout and D2H follow everything else)
+STAGE_TAPER = int(os.environ.get("GCABEM_STAGE_TAPER", "0"))
 _CASE_OF_SHARED = {1: "vertex", 2: "edge", 3: "identical"}
 
 __all__ = ["Backend", "SchedulerParams", "WorkBlock", "WorkItem", "WorkList", "AssemblyStats",
@@ -104,6 +111,11 @@ class SchedulerParams:
     # pair on its own (results then bitwise independent of how leaves are
     # split into stages / devices / shards)
     mirror: bool = True
+    # symmetric download of a mirrored single layer: SKIP leaves (the
+    # transposes of earlier PRIMARY leaves) are written on the host instead
+    # of copied over PCIe (gcabem_plan_set_symmetric_download); the host
+    # buffer is bitwise the device payload either way
+    symmetric_download: bool = True
 
     def backend_for(self, case: str) -> Backend:
         wanted = self.affinity.get(case)
@@ -177,6 +189,9 @@ class AssemblyStats:
     phase_s: dict = field(default_factory=dict)
     # staged assembly: per range (packaged, plan created, launched, synchronized), s from start
     stage_times: list = field(default_factory=list)
+    # device -> host bytes of the call (both payloads of a pair call; a
+    # symmetric download moves less than the payload)
+    d2h_bytes: int = 0
 
     def event_rows(self):
         return list(self.events)
@@ -384,7 +399,8 @@ class AssemblyPlan:
     execute_download() fill two host buffers."""
 
     def __init__(self, dm: DeviceMesh, spec: KernelSpec, pk: AssemblyPackages, orders,
-                 leaf_range=None, pair: bool = False, mirror: bool = True):
+                 leaf_range=None, pair: bool = False, mirror: bool = True,
+                 symmetric_download: bool = True):
         t_prep = time.monotonic()
         self.layout = DeviceLayout.cached(dm, pk, leaf_range, mirror)
         lay = self.layout
@@ -420,6 +436,15 @@ class AssemblyPlan:
         m = ctypes.c_int()
         nat.check(nat.lib().gcabem_plan_mirrored(self.handle, ctypes.byref(m)))
         self.mirrored = bool(m.value)
+        nat.check(nat.lib().gcabem_plan_set_symmetric_download(self.handle,
+                                                               int(bool(symmetric_download))))
+
+    def d2h_bytes(self) -> int:
+        """Bytes the last execute_download moved device -> host (a symmetric
+        download skips the SKIP leaves of the single layer)."""
+        v = ctypes.c_int64()
+        nat.check(nat.lib().gcabem_plan_d2h_bytes(self.handle, ctypes.byref(v)))
+        return int(v.value)
 
     def launches_per_execute(self) -> int:
         """Kernel launches of one execute(): the disjoint launch(es) -- plain
@@ -605,7 +630,7 @@ class StagedPackages:
     offset() describe the set's payload, its leaves back to back."""
 
     def __init__(self, mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
-                 maxsize: int, nstages: int, leaf_set=None, inputs=None):
+                 maxsize: int, nstages: int, leaf_set=None, inputs=None, prepare=None):
         inputs = inputs or package_inputs(mesh.triangles, block_tree, row_ops, col_ops)
         L_all = inputs.leaves.shape[0]
         sel = np.arange(L_all, dtype=np.int64) if leaf_set is None else \
@@ -638,21 +663,32 @@ class StagedPackages:
                                      inputs=inputs)
             return make_packages(*args, leaf_index=sel[a:b], inputs=inputs)
 
-        def work():
+        def one(k):
+            pk = package(*self.ranges[k])
+            if prepare is not None:   # e.g. the device layout of the range
+                prepare(k, pk)
+            self._pk[k] = pk
+            self._ready[k].set()
+
+        nw = max(1, PACK_WORKERS)
+
+        def work(w):
+            # worker 0 packages range 0 at once; ranges 1, 2, ... go round-robin
+            # to the workers once the cuts are known
             try:
-                self._pk[0] = package(*self.ranges[0])
-                self._ready[0].set()
+                if w == 0:
+                    one(0)
                 self._layout.wait()
-                for k in range(1, len(self.ranges)):
-                    self._pk[k] = package(*self.ranges[k])
-                    self._ready[k].set()
+                for k in range(1 + w, len(self.ranges), nw):
+                    one(k)
             except BaseException as exc:  # re-raised by stage()
                 self._err = exc
-            finally:
                 for ev in self._ready:
                     ev.set()
-        self._thread = threading.Thread(target=work, name="gcabem-packaging", daemon=True)
-        self._thread.start()
+        self._threads = [threading.Thread(target=work, args=(w,), name=f"gcabem-packaging-{w}",
+                                          daemon=True) for w in range(nw)]
+        for t in self._threads:
+            t.start()
         try:
             ids, shape, _ = leaf_layout(block_tree, row_ops, col_ops, inputs)
             self.leaf_ids = ids[sel]
@@ -664,7 +700,9 @@ class StagedPackages:
             ranges = list(self.ranges)
             if first < L:
                 b0 = base[first]
-                w = STAGE_GROWTH ** np.arange(n - 1)
+                k = np.arange(n - 1)
+                peak = max(0, n - 2 - STAGE_TAPER)
+                w = STAGE_GROWTH ** np.minimum(k, peak) * 0.5 ** np.maximum(0, k - peak)
                 frac = np.cumsum(w)[:-1] / w.sum()
                 cuts = np.searchsorted(base, b0 + (base[L] - b0) * frac, side="left")
                 edges = np.unique(np.concatenate([[first], np.clip(cuts, first + 1, L), [L]]))
@@ -706,17 +744,19 @@ def shard_leaves_of(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops, 
 
 def staged_packages_for(mesh: SurfaceMesh, block_tree: BlockTree, row_ops, col_ops,
                         maxsize: int, nstages: int, leaf_set=None,
-                        inputs=None) -> StagedPackages:
+                        inputs=None, prepare=None) -> StagedPackages:
     """StagedPackages of (block tree, operators, budget, stages[, leaf set]),
     cached like packages_for (a second operator from the same packages
-    packages nothing)."""
+    packages nothing). `prepare(k, packages)` runs on the packaging thread
+    after range k is packaged (a new StagedPackages only)."""
     key = ("staged", id(block_tree), id(row_ops), id(col_ops), int(maxsize),
            id(mesh.triangles), int(nstages),
            None if leaf_set is None else (int(leaf_set.size), hash(leaf_set.tobytes())))
     hit = _cache_get(key, block_tree)
     if hit is not None:
         return hit
-    sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages, leaf_set, inputs)
+    sp = StagedPackages(mesh, block_tree, row_ops, col_ops, maxsize, nstages, leaf_set, inputs,
+                        prepare)
     sp.key = key
     _cache_put(key, block_tree, row_ops, col_ops, sp)
     return sp
@@ -746,12 +786,15 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
     leaves (a process shard)."""
     t0 = time.monotonic()
     phase = {}
+    dm = device_mesh(mesh, device)
+    mirror = params.mirror
+    # the packaging threads also build each range's device layout
     sp = staged_packages_for(mesh, block_tree, row_ops, col_ops, params.maxsize_bytes,
-                             params.stages, leaf_set, inputs)
+                             params.stages, leaf_set, inputs,
+                             lambda k, pk: DeviceLayout.cached(dm, pk, None, mirror))
     ta = time.monotonic()
     outs = [nat.pinned_empty(sp.payload_len, np.complex128) for _ in range(2 if pair else 1)]
     phase["pinned_alloc"] = time.monotonic() - ta
-    dm = device_mesh(mesh, device)
     plans, wait = [], 0.0
     try:
         ta = time.monotonic()
@@ -761,9 +804,13 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
             pk = sp.stage(k)
             tr = time.monotonic()
             wait += tr - tw
-            p = AssemblyPlan(dm, spec, pk, orders, pair=pair, mirror=params.mirror)
+            p = AssemblyPlan(dm, spec, pk, orders, pair=pair, mirror=params.mirror,
+                             symmetric_download=params.symmetric_download)
             plans.append(p)
             tp = time.monotonic()
+            if os.environ.get("GCABEM_TRACE"):
+                print(f"[stage {k}] layout {p.layout.prep_s * 1e3:.2f} ms, plan "
+                      f"{(tp - tr) * 1e3:.2f} ms", file=sys.stderr)
             if p.payload_len:
                 sl = slice(sp.offset(k), sp.offset(k) + p.payload_len)
                 p.execute_download(outs[0][sl], sp.chunks(k, 2 * params.chunks),
@@ -774,6 +821,7 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
         for p, tk in zip(plans, times):
             p.synchronize()
             tk.append(time.monotonic() - t0)
+            stats.d2h_bytes += p.d2h_bytes() if p.payload_len else 0
         stats.stage_times = [tuple(round(x, 4) for x in tk) for tk in times]
         phase["execute_download"] = time.monotonic() - ta
         ms = [p.timing_ms() for p in plans if p.payload_len]
@@ -847,7 +895,8 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
         ta = time.monotonic()
         for dev, rng in zip(devices, ranges):
             plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng, pair=pair,
-                                      mirror=params.mirror))
+                                      mirror=params.mirror,
+                                      symmetric_download=params.symmetric_download))
         phase["plan_create"] = time.monotonic() - ta
         phase["plan_host_prep"] = sum(p.prep_s for p in plans)
         ta = time.monotonic()
@@ -857,6 +906,7 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
                 p.execute_download(outs[0][sl], params.chunks, outs[1][sl] if pair else None)
         for p in plans:
             p.synchronize()
+            stats.d2h_bytes += p.d2h_bytes() if p.payload_len else 0
         phase["execute_download"] = time.monotonic() - ta
         stats.device_ms = {f"device{p.device}": p.timing_ms() for p in plans if p.payload_len}
     finally:

@@ -146,3 +146,72 @@ def test_mirror_evaluation_accounting(gload):
     assert mp.flops()["singular"] < pp.flops()["singular"]
     mp.close()
     pp.close()
+
+
+@pytest.mark.parametrize("min_run", ["1", "16384"])
+@pytest.mark.parametrize("kind", ["pair", "single", "double"])
+def test_symmetric_download_bitwise(gload, monkeypatch, min_run, kind):
+    """Symmetric download (the host writes the SKIP leaves of the single layer
+    from their PRIMARY plus a gathered singular patch): the host buffers are
+    bitwise those of the full copy, for one and several chunks, and fewer
+    bytes cross the link (the double layer is copied in full)."""
+    monkeypatch.setenv("GCABEM_SYM_MIN_RUN", min_run)
+    from paper_1510_07244_b200 import gca
+    from paper_1510_07244_b200 import _native as nat
+    m, t, bt = sphere_setup(5)
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    pk = packaging.make_packages(m.triangles, bt, ops, ops, scheduler.DEFAULT_MAXSIZE)
+    dm = devmod.device_mesh(m, 0)
+    layer = "single" if kind == "pair" else kind
+    spec = kernels.KernelSpec("helmholtz", layer, 4.0)
+    pair = kind == "pair"
+    full = scheduler.AssemblyPlan(dm, spec, pk, (3, 5), pair=pair, symmetric_download=False)
+    a = [nat.pinned_empty(pk.payload_len, np.complex128) for _ in range(2)]
+    full.execute_download(a[0], 4, a[1] if pair else None)
+    full.synchronize()
+    ref = [np.array(x) for x in a]
+    bytes_full = full.d2h_bytes()
+    assert bytes_full == pk.payload_len * 16 * (2 if pair else 1)
+    full.close()
+    sym = scheduler.AssemblyPlan(dm, spec, pk, (3, 5), pair=pair)
+    assert sym.mirrored
+    for nchunks in (1, 7):
+        for x in a:
+            x[:] = np.nan
+        sym.execute_download(a[0], nchunks, a[1] if pair else None)
+        sym.synchronize()
+        assert np.array_equal(a[0], ref[0]), nchunks
+        if pair:
+            assert np.array_equal(a[1], ref[1]), nchunks
+        if kind == "double" or min_run != "1":
+            assert sym.d2h_bytes() <= bytes_full
+        else:
+            # every SKIP leaf is host-filled: about a quarter (pair) / half
+            # (single) of the bytes stay on the device
+            saved = 1.0 - sym.d2h_bytes() / bytes_full
+            assert saved > (0.2 if pair else 0.4), saved
+    if kind == "double":
+        assert sym.d2h_bytes() == bytes_full
+    sym.close()
+
+
+def test_symmetric_download_staged_public_api(gload, monkeypatch):
+    """run_assembly_pair through the staged pipeline: symmetric and full
+    downloads give bitwise equal matrices; the stats count the moved bytes."""
+    monkeypatch.setenv("GCABEM_SYM_MIN_RUN", "64")
+    from paper_1510_07244_b200 import gca
+    m, t, bt = sphere_setup(5)
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    out = {}
+    for sym in (False, True):
+        scheduler.clear_package_cache()
+        st = scheduler.AssemblyStats()
+        p = scheduler.SchedulerParams(stages=4, symmetric_download=sym)
+        S, D = scheduler.run_assembly_pair(m, bt, "helmholtz", 4.0, ops, ops, p, (3, 5), st)
+        out[sym] = (np.array(S.buffer), np.array(D.buffer), st.d2h_bytes)
+    assert np.array_equal(out[True][0], out[False][0])
+    assert np.array_equal(out[True][1], out[False][1])
+    assert out[False][2] == out[False][0].nbytes + out[False][1].nbytes
+    assert out[True][2] < out[False][2]

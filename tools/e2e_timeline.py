@@ -14,15 +14,17 @@ cfg = bench.CONFIGS[cfg_name]
 m, bt, ops, _ = bench.build_workload(cfg, [0], None, lambda s: None, warm_gca=False)
 from paper_1510_07244_b200 import packaging as _pkg  # noqa: E402
 pk = _pkg.make_packages(m.triangles, bt, ops, ops, 8 << 20)
-for rep in range(4):
+for rep in range(int(os.environ.get("REPS", "4"))):
     scheduler.clear_package_cache()
     st = scheduler.AssemblyStats()
     t0 = time.perf_counter()
     out = scheduler.run_assembly_pair(m, bt, cfg["equation"], cfg["kappa"], ops, ops,
-                                      scheduler.SchedulerParams(stages=int(os.environ.get("STAGES", "6"))),
+                                      scheduler.SchedulerParams(
+                                          stages=int(os.environ.get("STAGES", "6")),
+                                          symmetric_download=os.environ.get("SYM", "1") == "1"),
                                       cfg["orders"], st)
     dt = time.perf_counter() - t0
-    print(f"{cfg_name} total {dt * 1e3:.1f} ms  phases " +
+    print(f"{cfg_name} total {dt * 1e3:.1f} ms  d2h {st.d2h_bytes / 1e9:.2f} GB  phases " +
           " ".join(f"{k}={v * 1e3:.1f}" for k, v in st.phase_s.items()))
     for k, t in enumerate(st.stage_times):
         print(f"   range {k}: packaged {t[0] * 1e3:6.1f}  plan {t[1] * 1e3:6.1f}  "
