@@ -1,6 +1,7 @@
 // C ABI of gcabem_b200 (declared in include/gcabem_b200.h). Host-side
 // ownership, uploads, task decomposition and error mapping; no compute here.
 #include <cuda_runtime.h>
+#include <sched.h>
 #include <emmintrin.h>
 
 #include <algorithm>
@@ -463,11 +464,24 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
 
 namespace {
 
-// split [0, n) over up to `maxt` std::threads (inline below `grain`)
+// this process's share of the host CPUs: its affinity set divided among the
+// ranks of a node (torchrun LOCAL_WORLD_SIZE), as packaging.host_threads
+unsigned host_cpus() {
+    static const unsigned n = [] {
+        cpu_set_t set;
+        unsigned c = std::max(1u, std::thread::hardware_concurrency());
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) c = (unsigned)CPU_COUNT(&set);
+        const char *lw = std::getenv("LOCAL_WORLD_SIZE");
+        const int ranks = lw ? std::max(1, std::atoi(lw)) : 1;
+        return std::max(1u, c / (unsigned)ranks);
+    }();
+    return n;
+}
+
+// split [0, n) over up to `max_threads` std::threads (inline below `grain`)
 template <typename F>
 void par_for(int64_t n, int64_t grain, F fn, unsigned max_threads = 8) {
-    const int maxt = (int)std::min<unsigned>(max_threads,
-                                             std::max(1u, std::thread::hardware_concurrency()));
+    const int maxt = (int)std::min<unsigned>(max_threads, host_cpus());
     const int nt = (int)std::min<int64_t>(maxt, std::max<int64_t>(1, n / std::max<int64_t>(grain, 1)));
     if (nt <= 1) {
         fn(0, n, 0);
