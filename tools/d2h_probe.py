@@ -1,43 +1,31 @@
-"""Device execute + D2H of one whole C3 pair plan (packages and layout
-prepared beforehand): the link-bound floor of the e2e step, symmetric
-download on and off, and a raw pinned D2H of the same bytes."""
-import os
-import sys
+"""D2H bandwidth of this box: one pinned 2 GiB target, copies of several
+sizes on one and on two streams (the e2e path is D2H-bound)."""
+import json
 import time
 
-sys.path.insert(0, os.getcwd())
-import numpy as np  # noqa: E402
+import torch
 
-import bench  # noqa: E402
-from paper_1510_07244_b200 import _native as nat  # noqa: E402
-from paper_1510_07244_b200 import device as devmod, kernels, packaging, scheduler  # noqa: E402
-
-cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"]
-m, bt, ops, _ = bench.build_workload(cfg, [0], None, lambda s: None, warm_gca=False)
-pk = packaging.make_packages(m.triangles, bt, ops, ops, 8 << 20)
-dm = devmod.device_mesh(m, 0)
-spec = kernels.KernelSpec(cfg["equation"], "single", cfg["kappa"])
-a = [nat.pinned_empty(pk.payload_len, np.complex128) for _ in range(2)]
-for sym in (True, False):
-    p = scheduler.AssemblyPlan(dm, spec, pk, cfg["orders"], pair=True, symmetric_download=sym)
-    for nch in (8, 32):
-        ts = []
-        for rep in range(4):
+dev = torch.device("cuda:0")
+N = 2 << 30
+src = torch.empty(N, dtype=torch.uint8, device=dev).fill_(1)
+dst = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+res = {}
+for chunk in (8 << 20, 64 << 20, 256 << 20, 1 << 30, 2 << 30):
+    for nstreams in (1, 2, 4):
+        ss = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+        for rep in range(3):
+            torch.cuda.synchronize()
             t0 = time.perf_counter()
-            p.execute_download(a[0], nch, a[1])
-            p.synchronize()
-            ts.append(time.perf_counter() - t0)
-        b = p.d2h_bytes()
-        print(f"sym={sym} chunks={nch}: {min(ts) * 1e3:.1f} ms  {b / 1e9:.2f} GB  "
-              f"{b / min(ts) / 1e9:.1f} GB/s", flush=True)
-    p.close()
-import torch  # noqa: E402
-x = torch.empty(pk.payload_len * 2, dtype=torch.float64, device="cuda:0")
-h = torch.from_numpy(a[0].view(np.float64))
-for rep in range(3):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    h.copy_(x, non_blocking=True)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-print(f"raw pinned D2H {h.numel() * 8 / 1e9:.2f} GB: {dt * 1e3:.1f} ms {h.numel() * 8 / dt / 1e9:.1f} GB/s")
+            for k, off in enumerate(range(0, N, chunk)):
+                with torch.cuda.stream(ss[k % nstreams]):
+                    dst[off:off + chunk].copy_(src[off:off + chunk], non_blocking=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        res[f"chunk{chunk >> 20}MB_s{nstreams}"] = round(N / dt / 1e9, 1)
+# H2D for reference
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+src.copy_(dst, non_blocking=True)
+torch.cuda.synchronize()
+res["h2d_2GB"] = round(N / (time.perf_counter() - t0) / 1e9, 1)
+print(json.dumps(res))
