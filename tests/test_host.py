@@ -515,3 +515,80 @@ def test_oracle_p1_batch_matches_reference_golden(gload):
                                         pairs[:, 0], pairs[:, 1], perms[:, :3], perms[:, 3:])
             scale = np.max(np.abs(ref), axis=(1, 2))
             assert np.all(np.max(np.abs(got - ref), axis=(1, 2)) <= 1e-12 * scale), (case, name)
+
+
+def test_staged_packages_prepare_hook_and_errors(monkeypatch):
+    """The packaging threads run prepare(k, packages) before range k is served
+    (the staged assembly builds the device layout there); an exception in it
+    reaches the caller through stage(), whichever worker raised it."""
+    m, t, bt = sphere_setup(4)
+    ids = {l.row for l in bt.leaves if l.kind == "admissible"} | \
+          {l.col for l in bt.leaves if l.kind == "admissible"}
+    ops = {c: gca.InterpolationOperator(c, None, t.panels(t.nodes[c])[::-1][:20], None)
+           for c in ids}
+    for workers in (1, 2, 3):
+        monkeypatch.setattr(scheduler, "PACK_WORKERS", workers)
+        seen = []
+        sp = scheduler.StagedPackages(m, bt, ops, ops, 20000, 6,
+                                      prepare=lambda k, pk: seen.append((k, pk.leaf_ids.size)))
+        for k in range(len(sp.ranges)):
+            pk = sp.stage(k)
+            assert (k, pk.leaf_ids.size) in seen
+        assert sorted(k for k, _ in seen) == list(range(len(sp.ranges)))
+
+        def boom(k, pk):
+            if k == 3:
+                raise RuntimeError("layout failed")
+        sp = scheduler.StagedPackages(m, bt, ops, ops, 20000, 6, prepare=boom)
+        with pytest.raises(RuntimeError, match="layout failed"):
+            for k in range(len(sp.ranges)):
+                sp.stage(k)
+
+
+def test_operator_map_behaves_like_the_dict():
+    """gca.OperatorMap (the GCA build's result: operators materialised on
+    access from the flat arrays) against the plain dict of the same
+    operators: lookups, order, length, membership, mutation, and the flat
+    pivot table packaging reads (the same as the generic walk)."""
+    rng = np.random.default_rng(3)
+    ids = np.array([2, 5, 6, 11, 40], np.int64)
+    sizes = np.array([4, 7, 3, 9, 5], np.int64)
+    ranks = np.array([2, 3, 1, 4, 2], np.int64)
+    starts = np.array([0, 4, 11, 14, 23], np.int64)
+    perm = rng.permutation(28).astype(np.int64)
+    rows = np.concatenate([rng.choice(n, r, replace=False) for n, r in zip(sizes, ranks)])
+    V = rng.standard_normal(int(np.sum(sizes * ranks))) + 1j * rng.standard_normal(
+        int(np.sum(sizes * ranks)))
+    om = gca.OperatorMap(ids, starts, sizes, ranks, rows, perm, V)
+    ref, ro, vo = {}, 0, 0
+    for c, s0, n, r in zip(ids, starts, sizes, ranks):
+        loc = rows[ro:ro + r]
+        ref[int(c)] = (loc, perm[s0 + loc], V[vo:vo + n * r].reshape(n, r))
+        ro += r
+        vo += n * r
+    assert list(om) == sorted(ref) and len(om) == len(ref)
+    assert 5 in om and 7 not in om and "x" not in om
+    for c, (loc, glob, v) in ref.items():
+        op = om[c]
+        assert op is om[c]   # materialised once
+        assert np.array_equal(op.pivots_local, loc) and np.array_equal(op.pivots_global, glob)
+        assert np.array_equal(op.V, v)
+    with pytest.raises(KeyError):
+        om[3]
+    at, piv = om.pivot_arrays(30)
+    assert packaging._op_arrays(dict(om.items()), 30)[0].tolist() == at.tolist()
+    assert np.array_equal(packaging._op_arrays(dict(om.items()), 30)[1], piv)
+    # clusters outside the tree are left out, as by the generic walk
+    at8, piv8 = om.pivot_arrays(8)
+    g8 = packaging._op_arrays({k: v for k, v in om.items()}, 8)
+    assert np.array_equal(at8, g8[0]) and np.array_equal(piv8, g8[1])
+    # mutation: replace, delete, add; the flat table is withdrawn
+    new = gca.InterpolationOperator(99, np.array([0]), np.array([7]), np.zeros((1, 1)))
+    om[6] = new
+    del om[11]
+    om[50] = new
+    assert om[6] is new and 11 not in om and 50 in om
+    assert list(om) == [2, 5, 6, 40, 50] and len(om) == 5
+    assert om.pivot_arrays(60) is None
+    with pytest.raises(KeyError):
+        del om[11]
