@@ -537,6 +537,17 @@ __global__ void gather_entries_kernel(const double2 *__restrict__ src,
     if (i < n) dst[i] = src[idx[i]];
 }
 
+// host threads writing the skipped leaves of a symmetric download (memory
+// bound: a few threads saturate the copy; more would take cores from the
+// packaging threads); GCABEM_FILL_THREADS overrides
+unsigned fill_threads() {
+    static const unsigned n = [] {
+        const char *e = std::getenv("GCABEM_FILL_THREADS");
+        return e ? (unsigned)std::max(1, std::atoi(e)) : 8u;
+    }();
+    return n;
+}
+
 // SKIP leaf s of the host-filled list: its entries as the transpose of its
 // PRIMARY (already in `host`), written with streaming stores (the rows are
 // contiguous; no read-for-ownership of the target lines), then its singular
@@ -624,19 +635,49 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
         L->block_mtask_at.resize(B + 1);
         L->block_rtask_at.resize(B + 1);
     }
-    for (int64_t b = 0; b < B; ++b) {
-        const int64_t np = blk_nr[b0 + b] * blk_nc[b0 + b];
-        L->block_task_at[b] = ntasks;
-        L->block_pairs[b] = np;
-        const int64_t nt = (np + DISJOINT_TPB - 1) / DISJOINT_TPB;
-        ntasks += nt;
-        if (any_mirror) {
-            const int r = role_of(blk_leaf[b0 + b]);
-            L->block_mtask_at[b] = nmt;
-            L->block_rtask_at[b] = nrt;
-            if (r == ROLE_PRIMARY || r == ROLE_SELF) nmt += nt;
-            if (r == ROLE_NORMAL) nrt += nt;
-        }
+    {
+        // task offsets of the blocks (all / mirrored / plain): exclusive
+        // prefix sums, per block chunk on the pool, then the chunk offsets
+        constexpr int NP = 16;
+        int64_t tot[NP + 1][3] = {};
+        auto pass = [&](bool write) {
+            par_for(NP, 1, [&](int64_t t0, int64_t t1, int) {
+                for (int64_t t = t0; t < t1; ++t) {
+                    // first pass: chunk sums from 0 (tot[t] is another
+                    // chunk's output then); second pass: from the offsets
+                    int64_t a = write ? tot[t][0] : 0, m = write ? tot[t][1] : 0,
+                            n = write ? tot[t][2] : 0;
+                    for (int64_t b = t * B / NP; b < (t + 1) * B / NP; ++b) {
+                        const int64_t np = blk_nr[b0 + b] * blk_nc[b0 + b];
+                        const int64_t nt = (np + DISJOINT_TPB - 1) / DISJOINT_TPB;
+                        const int r = any_mirror ? role_of(blk_leaf[b0 + b]) : ROLE_NORMAL;
+                        if (write) {
+                            L->block_task_at[b] = a;
+                            L->block_pairs[b] = np;
+                            if (any_mirror) {
+                                L->block_mtask_at[b] = m;
+                                L->block_rtask_at[b] = n;
+                            }
+                        }
+                        a += nt;
+                        if (r == ROLE_PRIMARY || r == ROLE_SELF) m += nt;
+                        if (r == ROLE_NORMAL) n += nt;
+                    }
+                    if (!write) {
+                        tot[t + 1][0] = a;
+                        tot[t + 1][1] = m;
+                        tot[t + 1][2] = n;
+                    }
+                }
+            });
+        };
+        pass(false);  // chunk totals at tot[t + 1]
+        for (int t = 0; t < NP; ++t)
+            for (int c = 0; c < 3; ++c) tot[t + 1][c] += tot[t][c];
+        pass(true);   // offsets from tot[t]
+        ntasks = tot[NP][0];
+        nmt = any_mirror ? tot[NP][1] : 0;
+        nrt = any_mirror ? tot[NP][2] : 0;
     }
     L->block_task_at[B] = ntasks;
     if (any_mirror) {
@@ -863,36 +904,52 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
         // evaluation counts for the roofline: pairs of PRIMARY/SELF(upper)
         // blocks minus their vertex-sharing pairs (one mirrored evaluation
         // each), NORMAL pairs minus theirs
-        int64_t mp = 0, sp = 0, np_ = 0, up = 0;
-        for (int64_t b = 0; b < B; ++b) {
-            const int64_t g = b0 + b, lf = blk_leaf[g], nr = blk_nr[g], nc = blk_nc[g];
-            const int r = role_of(lf);
-            if (r == ROLE_PRIMARY) mp += nr * nc;
-            else if (r == ROLE_SKIP) sp += nr * nc;
-            else if (r == ROLE_NORMAL) np_ += nr * nc;
-            else {  // SELF: leaf entries (r0 + i, c0 + j) with r0 + i < c0 + j
-                const int64_t dr = blk_r0[g] - blk_c0[g];
-                for (int64_t i = 0; i < nr; ++i)
-                    up += std::max<int64_t>(0, nc - std::max<int64_t>(0, i + dr + 1));
+        // per-thread partial sums (integers: the order does not matter)
+        constexpr int NP = 16;
+        int64_t part[NP][6] = {};
+        par_for(NP, 1, [&](int64_t t0, int64_t t1, int) {
+            for (int64_t t = t0; t < t1; ++t) {
+                int64_t *q = part[t];  // mp, sp, np, up, sh_m, sh_n
+                for (int64_t b = t * B / NP; b < (t + 1) * B / NP; ++b) {
+                    const int64_t g = b0 + b, lf = blk_leaf[g], nr = blk_nr[g], nc = blk_nc[g];
+                    const int r = role_of(lf);
+                    if (r == ROLE_PRIMARY) q[0] += nr * nc;
+                    else if (r == ROLE_SKIP) q[1] += nr * nc;
+                    else if (r == ROLE_NORMAL) q[2] += nr * nc;
+                    else {  // SELF: leaf entries (r0 + i, c0 + j) with r0 + i < c0 + j
+                        const int64_t dr = blk_r0[g] - blk_c0[g];
+                        for (int64_t i = 0; i < nr; ++i)
+                            q[3] += std::max<int64_t>(0, nc - std::max<int64_t>(0, i + dr + 1));
+                    }
+                }
+                for (int64_t k = t * nitems / NP; k < (t + 1) * nitems / NP; ++k) {
+                    const int64_t lf = item_leaf[k];
+                    if (lf < leaf_lo || lf >= leaf_hi) continue;
+                    const int r = role_of(lf);
+                    if (r == ROLE_PRIMARY) ++q[4];
+                    else if (r == ROLE_NORMAL) ++q[5];
+                    else if (r == ROLE_SELF) {
+                        const int64_t ncol = leaf_shape[2 * lf + 1];
+                        const int64_t i = item_offset[k] / ncol, j = item_offset[k] % ncol;
+                        if (i < j) ++q[4];
+                    }
+                }
             }
-        }
-        int64_t sh_m = 0, sh_n = 0;
-        for (int64_t k = 0; k < nitems; ++k) {
-            const int64_t lf = item_leaf[k];
-            if (lf < leaf_lo || lf >= leaf_hi) continue;
-            const int r = role_of(lf);
-            if (r == ROLE_PRIMARY) ++sh_m;
-            else if (r == ROLE_NORMAL) ++sh_n;
-            else if (r == ROLE_SELF) {
-                const int64_t ncol = leaf_shape[2 * lf + 1];
-                const int64_t i = item_offset[k] / ncol, j = item_offset[k] % ncol;
-                if (i < j) ++sh_m;
-            }
+        });
+        int64_t mp = 0, sp = 0, np_ = 0, up = 0, sh_m = 0, sh_n = 0;
+        for (const auto &q : part) {
+            mp += q[0];
+            sp += q[1];
+            np_ += q[2];
+            up += q[3];
+            sh_m += q[4];
+            sh_n += q[5];
         }
         L->mirror_info[0] = mp + up - sh_m;
         L->mirror_info[1] = np_ - sh_n;
         L->mirror_info[2] = mp + up;
         L->mirror_info[3] = sp;
+        tr.mark("eval-counts");
     }
     if (any_mirror) {
         // host-filled SKIP leaves (symmetric download): runs of consecutive
@@ -1516,7 +1573,7 @@ int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, 
                 const int64_t s0 = fill[k].first, n = fill[k].second - fill[k].first;
                 par_for(n, 32, [&](int64_t a, int64_t b, int) {
                     for (int64_t h = a; h < b; ++h) host_fill_leaf(L, s0 + h, h1, patch);
-                }, 16u);
+                }, fill_threads());
                 tr.mark("filled");
             }
         });

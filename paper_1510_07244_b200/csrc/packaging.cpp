@@ -9,6 +9,7 @@
 // std::thread workers with a count / prefix-sum / fill pass so item order is
 // independent of the thread count.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -147,50 +148,84 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
     P.cols_at.resize(nleaves);
     P.flagged.resize(nleaves);
     P.leaf_base[0] = 0;
-    for (int64_t k = 0; k < nleaves; ++k) {
-        const int64_t r = leaves[3 * k], c = leaves[3 * k + 1], dense = leaves[3 * k + 2];
-        if (r < 0 || r >= nrow || c < 0 || c >= ncol) {
-            delete pk;
-            return fail("leaf cluster index out of range");
-        }
-        int64_t nr, nc;
-        if (dense) {
-            nr = row_size[r];
-            nc = col_size[c];
-            P.rows_at[k] = row_start[r];
-            P.cols_at[k] = col_perm_at + col_start[c];
-        } else {
-            nr = row_op_at[r + 1] - row_op_at[r];
-            nc = col_op_at[c + 1] - col_op_at[c];
-            P.rows_at[k] = nt + row_op_at[r];
-            P.cols_at[k] = col_piv_at + col_op_at[c];
-            if (nr <= 0 || nc <= 0) {
-                delete pk;
-                return fail("admissible leaf without an interpolation operator");
+    std::atomic<int> leaf_err{0};  // 1: cluster index out of range, 2: no operator
+    parallel_for(nleaves, nthreads, [&](int64_t lo, int64_t hi) {
+        for (int64_t k = lo; k < hi; ++k) {
+            const int64_t r = leaves[3 * k], c = leaves[3 * k + 1], dense = leaves[3 * k + 2];
+            if (r < 0 || r >= nrow || c < 0 || c >= ncol) {
+                leaf_err = 1;
+                return;
             }
+            int64_t nr, nc;
+            if (dense) {
+                nr = row_size[r];
+                nc = col_size[c];
+                P.rows_at[k] = row_start[r];
+                P.cols_at[k] = col_perm_at + col_start[c];
+            } else {
+                nr = row_op_at[r + 1] - row_op_at[r];
+                nc = col_op_at[c + 1] - col_op_at[c];
+                P.rows_at[k] = nt + row_op_at[r];
+                P.cols_at[k] = col_piv_at + col_op_at[c];
+                if (nr <= 0 || nc <= 0) {
+                    leaf_err = 2;
+                    return;
+                }
+            }
+            P.leaf_shape[2 * k] = nr;
+            P.leaf_shape[2 * k + 1] = nc;
+            // box_distance(t, s) == 0.0  <=>  boxes touch on every axis (exact)
+            bool touch = true;
+            for (int a = 0; a < 3; ++a)
+                touch = touch && row_lo[3 * r + a] <= col_hi[3 * c + a] &&
+                        col_lo[3 * c + a] <= row_hi[3 * r + a];
+            P.flagged[k] = touch ? 1 : 0;
         }
-        P.leaf_shape[2 * k] = nr;
-        P.leaf_shape[2 * k + 1] = nc;
-        P.leaf_base[k + 1] = P.leaf_base[k] + nr * nc;
-        // box_distance(t, s) == 0.0  <=>  boxes touch on every axis (exact)
-        bool touch = true;
-        for (int a = 0; a < 3; ++a)
-            touch = touch && row_lo[3 * r + a] <= col_hi[3 * c + a] &&
-                    col_lo[3 * c + a] <= row_hi[3 * r + a];
-        P.flagged[k] = touch ? 1 : 0;
+    });
+    if (leaf_err) {
+        delete pk;
+        return fail(leaf_err == 1 ? "leaf cluster index out of range"
+                                  : "admissible leaf without an interpolation operator");
     }
+    for (int64_t k = 0; k < nleaves; ++k)
+        P.leaf_base[k + 1] = P.leaf_base[k] + P.leaf_shape[2 * k] * P.leaf_shape[2 * k + 1];
     P.payload_len = P.leaf_base[nleaves];
     mark("leaves");
-    // split + greedy lists
-    P.blk.reserve(5 * nleaves);
-    for (int64_t k = 0; k < nleaves; ++k) {
-        const int64_t nr = P.leaf_shape[2 * k], nc = P.leaf_shape[2 * k + 1];
-        if (nr * nc > 1 || nr * nc * BYTES_PER_PAIR <= maxsize) {
-            split(k, 0, nr, 0, nc, maxsize, P.blk);
+    // split (per leaf, on the pool: per-thread block lists joined in leaf
+    // order) + greedy lists (sequential: the byte budget runs across leaves)
+    {
+        const int nparts = nleaves >= 4096 ? std::max(1, nthreads) : 1;
+        std::vector<std::vector<int64_t>> parts(nparts);
+        std::atomic<bool> tiny{false};
+        const int64_t per = (nleaves + nparts - 1) / nparts;
+        auto run = [&](int64_t t) {
+            std::vector<int64_t> &out = parts[t];
+            const int64_t lo = t * per, hi = std::min(nleaves, lo + per);
+            out.reserve(5 * std::max<int64_t>(hi - lo, 0) + 16);
+            for (int64_t k = lo; k < hi; ++k) {
+                const int64_t nr = P.leaf_shape[2 * k], nc = P.leaf_shape[2 * k + 1];
+                if (nr * nc > 1 || nr * nc * BYTES_PER_PAIR <= maxsize)
+                    split(k, 0, nr, 0, nc, maxsize, out);
+                else
+                    tiny = true;
+            }
+        };
+        if (nparts == 1) {
+            run(0);
         } else {
+            std::vector<std::thread> th;
+            for (int t = 1; t < nparts; ++t) th.emplace_back(run, t);
+            run(0);
+            for (auto &x : th) x.join();
+        }
+        if (tiny) {
             delete pk;
             return fail("maxsize smaller than one pair record (32 B)");
         }
+        size_t total = 0;
+        for (auto &v : parts) total += v.size();
+        P.blk.reserve(total);
+        for (auto &v : parts) P.blk.insert(P.blk.end(), v.begin(), v.end());
     }
     const int64_t B = (int64_t)P.blk.size() / 5;
     P.blk_list.resize(B);
