@@ -543,7 +543,7 @@ __global__ void gather_entries_kernel(const double2 *__restrict__ src,
 unsigned fill_threads() {
     static const unsigned n = [] {
         const char *e = std::getenv("GCABEM_FILL_THREADS");
-        return e ? (unsigned)std::max(1, std::atoi(e)) : 8u;
+        return e ? (unsigned)std::max(1, std::atoi(e)) : std::min(8u, host_cpus());
     }();
     return n;
 }
