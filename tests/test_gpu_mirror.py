@@ -215,3 +215,29 @@ def test_symmetric_download_staged_public_api(gload, monkeypatch):
     assert np.array_equal(out[True][1], out[False][1])
     assert out[False][2] == out[False][0].nbytes + out[False][1].nbytes
     assert out[True][2] < out[False][2]
+
+
+def test_symmetric_download_shards_and_devices(gload, monkeypatch):
+    """Process shards (leaf sets: each leaf with its mirror, payload laid out
+    set-wise) and several devices of one process (leaf ranges): the
+    symmetric download gives the full copy's buffers bit for bit."""
+    monkeypatch.setenv("GCABEM_SYM_MIN_RUN", "32")
+    from paper_1510_07244_b200 import gca
+    m, t, bt = sphere_setup(5)
+    ops, _ = gca.build_interpolation_operators(m, bt, kernels.KernelSpec("helmholtz", "single",
+                                                                         4.0), gca.GcaParams())
+    be = scheduler.Backend("cuda", devices=(0, 0))
+    cases = [dict(shard=(r, 2), stages=s) for r in range(2) for s in (1, 3)]
+    cases.append(dict(backends=(be,)))
+    for kw in cases:
+        out = {}
+        for sym in (False, True):
+            scheduler.clear_package_cache()
+            st = scheduler.AssemblyStats()
+            S, D = scheduler.run_assembly_pair(
+                m, bt, "helmholtz", 4.0, ops, ops,
+                scheduler.SchedulerParams(symmetric_download=sym, **kw), (3, 5), st)
+            out[sym] = (np.array(S.buffer), np.array(D.buffer), st.d2h_bytes)
+        assert np.array_equal(out[True][0], out[False][0]), kw
+        assert np.array_equal(out[True][1], out[False][1]), kw
+        assert out[True][2] < out[False][2], kw
