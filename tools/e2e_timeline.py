@@ -17,6 +17,8 @@ pk = _pkg.make_packages(m.triangles, bt, ops, ops, 8 << 20)
 for rep in range(int(os.environ.get("REPS", "4"))):
     scheduler.clear_package_cache()
     st = scheduler.AssemblyStats()
+    import resource
+    r0 = resource.getrusage(resource.RUSAGE_SELF)
     t0 = time.perf_counter()
     out = scheduler.run_assembly_pair(m, bt, cfg["equation"], cfg["kappa"], ops, ops,
                                       scheduler.SchedulerParams(
@@ -24,6 +26,10 @@ for rep in range(int(os.environ.get("REPS", "4"))):
                                           symmetric_download=os.environ.get("SYM", "1") == "1"),
                                       cfg["orders"], st)
     dt = time.perf_counter() - t0
+    r1 = resource.getrusage(resource.RUSAGE_SELF)
+    cpu = (r1.ru_utime - r0.ru_utime) + (r1.ru_stime - r0.ru_stime)
+    print(f"   host CPU {cpu:.3f} s (user {r1.ru_utime - r0.ru_utime:.3f}, sys "
+          f"{r1.ru_stime - r0.ru_stime:.3f}) = {cpu / dt:.1f} cores busy on average")
     print(f"{cfg_name} total {dt * 1e3:.1f} ms  d2h {st.d2h_bytes / 1e9:.2f} GB  phases " +
           " ".join(f"{k}={v * 1e3:.1f}" for k, v in st.phase_s.items()))
     for k, t in enumerate(st.stage_times):
