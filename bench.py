@@ -693,7 +693,8 @@ def run_ours(args, cfg, dist, log):
     backend = scheduler.Backend("cuda", devices=tuple(devices))
     params = scheduler.SchedulerParams(backends=(backend,), shard=shard,
                                        mirror=not args.no_mirror,
-                                       symmetric_download=not args.no_sym_download)
+                                       symmetric_download=False if args.no_sym_download
+                                       else None)
     e2e_t, e2e_phases, d2h, payload_bytes = [], [], 0, 0
 
     def assemble_all(stats_list):
@@ -813,7 +814,7 @@ def run_ours(args, cfg, dist, log):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d_job),
                 "d2h_bytes_per_step": int(d2h_job), "seconds_per_step": e2e_dt,
                 "payload_bytes_per_step": int(payload_job),
-                "symmetric_download": not args.no_sym_download,
+                "symmetric_download": bool(d2h_job < payload_job),
                 "phases_s": [{k: round(v, 4) for k, v in ph.items()} for ph in e2e_phases]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -43,6 +43,15 @@ DEFAULT_MAXSIZE = 8 * 2 ** 20
 # payload growth between consecutive ranges of a staged assembly (measured at
 # C3: 1.5 with 6 ranges beats 2 with 5 by ~5% e2e)
 STAGE_GROWTH = float(os.environ.get("GCABEM_STAGE_GROWTH", "1.5"))
+SYM_AUTO_BYTES = int(os.environ.get("GCABEM_SYM_AUTO_BYTES", str(2 << 30)))
+
+
+def _symmetric(params, payload_len: int) -> bool:
+    if params.symmetric_download is None:
+        return payload_len * 16 >= SYM_AUTO_BYTES
+    return bool(params.symmetric_download)
+
+
 # host threads packaging leaf ranges (and building their device layouts) ahead
 # of the device
 PACK_WORKERS = int(os.environ.get("GCABEM_PACK_WORKERS", "2"))
@@ -114,8 +123,11 @@ class SchedulerParams:
     # symmetric download of a mirrored single layer: SKIP leaves (the
     # transposes of earlier PRIMARY leaves) are written on the host instead
     # of copied over PCIe (gcabem_plan_set_symmetric_download); the host
-    # buffer is bitwise the device payload either way
-    symmetric_download: bool = True
+    # buffer is bitwise the device payload either way. None = when the link
+    # bounds the call: a payload of at least SYM_AUTO_BYTES per operator (a
+    # smaller call is bound by its host packaging, which the host-side
+    # transposes would slow down: C2 53 -> 59 ms, C3 178 -> 163 ms)
+    symmetric_download: bool | None = None
 
     def backend_for(self, case: str) -> Backend:
         wanted = self.affinity.get(case)
@@ -805,7 +817,7 @@ def _assemble_staged(mesh, block_tree, spec, pair, row_ops, col_ops, params, ord
             tr = time.monotonic()
             wait += tr - tw
             p = AssemblyPlan(dm, spec, pk, orders, pair=pair, mirror=params.mirror,
-                             symmetric_download=params.symmetric_download)
+                             symmetric_download=_symmetric(params, sp.payload_len))
             plans.append(p)
             tp = time.monotonic()
             if os.environ.get("GCABEM_TRACE"):
@@ -896,7 +908,7 @@ def _assemble(mesh, block_tree, spec, pair, row_ops, col_ops, params, orders, st
         for dev, rng in zip(devices, ranges):
             plans.append(AssemblyPlan(device_mesh(mesh, dev), spec, pk, orders, rng, pair=pair,
                                       mirror=params.mirror,
-                                      symmetric_download=params.symmetric_download))
+                                      symmetric_download=_symmetric(params, pk.payload_len)))
         phase["plan_create"] = time.monotonic() - ta
         phase["plan_host_prep"] = sum(p.prep_s for p in plans)
         ta = time.monotonic()
