@@ -75,6 +75,7 @@ struct Pinned {
 // Staging buffers survive across calls (per device): pinned allocation of
 // hundreds of MB costs more than a whole L6 GCA build.
 constexpr int SLOTS = 4;  // batches in flight: device output + pinned staging each
+constexpr int64_t INPLACE_ROWS = 256;  // clusters up to this size run ACA in the slot
 
 struct Staging {
     Pinned host[SLOTS];
@@ -333,16 +334,27 @@ int gcabem_gca_build(gcabem_mesh_t mesh, int equation, double kappa, int64_t ncl
             if (first_at[tid] < 0.0) first_at[tid] = std::chrono::duration<double>(t0 - t_start).count();
             const double *A = static_cast<const double *>(st.host[slot_of[b]].p) +
                               out_at[b][pos - bstart[b]] * width;
-            Aown.assign(A, A + cl_size[c] * nsrc * width);
-            if (remaining[b].fetch_sub(1) == 1) {  // slot drained: back to the free list
-                std::lock_guard<std::mutex> lk(mu);
-                free_slots.push_back(slot_of[b]);
-                cv.notify_all();
-            }
             const int64_t nr = cl_size[c];
+            auto release = [&] {
+                if (remaining[b].fetch_sub(1) == 1) {  // slot drained: back to the free list
+                    std::lock_guard<std::mutex> lk(mu);
+                    free_slots.push_back(slot_of[b]);
+                    cv.notify_all();
+                }
+            };
+            // a small cluster works on its matrix in the slot (done in well
+            // under a millisecond; its copy would cost a fifth of its ACA); a
+            // large one copies it out first, so that its long ACA does not
+            // hold the slot
+            const bool inplace = nr <= INPLACE_ROWS;
+            if (!inplace) {
+                Aown.assign(A, A + nr * nsrc * width);
+                release();
+            }
             int amb = 0;
-            int rc = gca_operator(equation == 1, Aown.data(), nr, nsrc, epsilon, G->rows[c],
-                                  G->V[c], &amb);
+            int rc = gca_operator(equation == 1, inplace ? A : Aown.data(), nr, nsrc, epsilon,
+                                  G->rows[c], G->V[c], &amb);
+            if (inplace) release();
             if (rc == 0 && amb) {
                 // a decision inside the tie window: redo this cluster on
                 // entries evaluated in the reference's own arithmetic
