@@ -1460,7 +1460,9 @@ int gcabem_plan_execute_download2(gcabem_plan_t p, double *host, double *host2, 
     const bool sym = p->sym && p->mirrored && !L->hf_lo.empty();
     const int64_t npatch = sym ? (int64_t)L->patch_out.size() : 0;
     if (npatch > 0) {
-        GC_CUDA(p->patch_vals.alloc(npatch, p->stream));
+        // kept across executes (the previous execute's copies from it are
+        // done: join_filler waited for them)
+        if (p->patch_vals.n < (size_t)npatch) GC_CUDA(p->patch_vals.alloc(npatch, p->stream));
         if (p->patch_host_bytes < sizeof(double2) * npatch) {
             pinned_release(p->patch_host, p->patch_host_bytes);
             p->patch_host = (double2 *)pinned_acquire(sizeof(double2) * npatch,
