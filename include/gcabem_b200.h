@@ -225,6 +225,24 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
                           const int64_t *col_perm, const int64_t *col_op_at,
                           const int64_t *col_piv, int64_t maxsize, int nthreads,
                           gcabem_packages_t *out);
+/* The same, with the panel base array [row perm | row pivots | col perm |
+ * col pivots] (the col part only when the trees or operators differ) and the
+ * triangles BORROWED from the caller (alive until gcabem_packages_free): the
+ * leaf ranges of one staged assembly share them instead of copying them per
+ * range; gcabem_packages_fetch then skips the panels (pass NULL). Replaces
+ * nothing in the reference (its packaging is per-list Python,
+ * scheduler.py:153-232). */
+int gcabem_packages_build_on(int64_t nt, const int64_t *triangles, int64_t nleaves,
+                             const int64_t *leaves, int64_t nrow, const int64_t *row_start,
+                             const int64_t *row_size, const double *row_lo,
+                             const double *row_hi, const int64_t *row_perm,
+                             const int64_t *row_op_at, const int64_t *row_piv, int64_t ncol,
+                             const int64_t *col_start, const int64_t *col_size,
+                             const double *col_lo, const double *col_hi,
+                             const int64_t *col_perm, const int64_t *col_op_at,
+                             const int64_t *col_piv, int64_t maxsize, int nthreads,
+                             const int64_t *panel_base, int64_t npanel_base,
+                             gcabem_packages_t *out);
 /* sizes[9]: {L, payload_len, npanels, nblocks, nlists, nitems, 0, 0, 0} */
 int gcabem_packages_sizes(gcabem_packages_t pk, int64_t *sizes);
 /* Planar (field-major) outputs: blocks 5 x nblocks {leaf, r0, nr, c0, nc};

@@ -80,6 +80,8 @@ _SIGS = {
     "gcabem_potential": ([_vp, _int, _int, _dbl, _int, _vp, _vp, _i64, _vp, _vp], _int),
     "gcabem_packages_build": ([_i64, _vp, _i64, _vp, _i64] + [_vp] * 7 + [_i64] + [_vp] * 7
                               + [_i64, _int, ctypes.POINTER(_vp)], _int),
+    "gcabem_packages_build_on": ([_i64, _vp, _i64, _vp, _i64] + [_vp] * 7 + [_i64] + [_vp] * 7
+                                 + [_i64, _int, _vp, _i64, ctypes.POINTER(_vp)], _int),
     "gcabem_packages_sizes": ([_vp, _vp], _int),
     "gcabem_packages_fetch": ([_vp] * 11, _int),
     "gcabem_packages_free": ([_vp], _int),

@@ -27,7 +27,12 @@ namespace {
 
 struct Packages {
     int64_t L = 0, payload_len = 0, nlists = 0;
-    std::vector<int64_t> panels;        // [row perm | row pivots | col perm | col pivots]
+    // panel base array [row perm | row pivots | col perm | col pivots]: owned,
+    // or the caller's (gcabem_packages_build_on: shared by the leaf ranges of
+    // one assembly, kept alive by the caller until free)
+    std::vector<int64_t> panels_own;
+    const int64_t *panels = nullptr;
+    int64_t npanels = 0;
     std::vector<int64_t> leaf_shape;    // L x 2
     std::vector<int64_t> leaf_base;     // L + 1
     std::vector<int64_t> rows_at, cols_at;
@@ -38,7 +43,8 @@ struct Packages {
     // the caller's arrays at fetch time (no intermediate copy)
     std::vector<int64_t> fb;            // flagged blocks
     std::vector<int64_t> cnt;           // item prefix sums over fb (F + 1)
-    std::vector<int64_t> triangles;     // nt x 3 copy for the fill pass
+    std::vector<int64_t> tri_own;       // nt x 3 copy for the fill pass (or borrowed:)
+    const int64_t *tri = nullptr;
     int nthreads = 1;
     int64_t S = 0;
 };
@@ -111,6 +117,23 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
                           const int64_t *col_perm, const int64_t *col_op_at,
                           const int64_t *col_piv, int64_t maxsize, int nthreads,
                           gcabem_packages_t *out) {
+    return gcabem_packages_build_on(nt, triangles, nleaves, leaves, nrow, row_start, row_size,
+                                    row_lo, row_hi, row_perm, row_op_at, row_piv, ncol,
+                                    col_start, col_size, col_lo, col_hi, col_perm, col_op_at,
+                                    col_piv, maxsize, nthreads, nullptr, 0, out);
+}
+
+int gcabem_packages_build_on(int64_t nt, const int64_t *triangles, int64_t nleaves,
+                             const int64_t *leaves, int64_t nrow, const int64_t *row_start,
+                             const int64_t *row_size, const double *row_lo,
+                             const double *row_hi, const int64_t *row_perm,
+                             const int64_t *row_op_at, const int64_t *row_piv, int64_t ncol,
+                             const int64_t *col_start, const int64_t *col_size,
+                             const double *col_lo, const double *col_hi,
+                             const int64_t *col_perm, const int64_t *col_op_at,
+                             const int64_t *col_piv, int64_t maxsize, int nthreads,
+                             const int64_t *panel_base, int64_t npanel_base,
+                             gcabem_packages_t *out) {
     auto fail = [](const char *m) { return gcabem_internal_error(GCABEM_ERR_ARG, m); };
     static const bool trace = std::getenv("GCABEM_TRACE") != nullptr;
     auto t_start = std::chrono::steady_clock::now();
@@ -131,17 +154,33 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
     P.L = nleaves;
     // panel base array: row perm, row pivots, (col perm, col pivots)
     const int64_t nrp = row_op_at[nrow];
-    P.panels.reserve(2 * (nt + nrp));
-    P.panels.insert(P.panels.end(), row_perm, row_perm + nt);
-    P.panels.insert(P.panels.end(), row_piv, row_piv + nrp);
-    int64_t col_perm_at = 0, col_piv_at = nt;
-    if (!shared_tree || col_piv != row_piv) {
-        col_perm_at = (int64_t)P.panels.size();
-        const int64_t ncp = col_op_at[ncol];
-        P.panels.insert(P.panels.end(), col_perm, col_perm + nt);
-        col_piv_at = (int64_t)P.panels.size();
-        P.panels.insert(P.panels.end(), col_piv, col_piv + ncp);
+    int64_t col_perm_at = 0, col_piv_at = nt, nbase = nt + nrp;
+    const bool own_cols = !shared_tree || col_piv != row_piv;
+    if (own_cols) {
+        col_perm_at = nt + nrp;
+        col_piv_at = col_perm_at + nt;
+        nbase = col_piv_at + col_op_at[ncol];
     }
+    if (panel_base) {
+        if (npanel_base != nbase) {
+            delete pk;
+            return fail("panel base array does not match the trees and operators");
+        }
+        P.panels = panel_base;
+        P.tri = triangles;
+    } else {
+        P.panels_own.reserve(nbase);
+        P.panels_own.insert(P.panels_own.end(), row_perm, row_perm + nt);
+        P.panels_own.insert(P.panels_own.end(), row_piv, row_piv + nrp);
+        if (own_cols) {
+            P.panels_own.insert(P.panels_own.end(), col_perm, col_perm + nt);
+            P.panels_own.insert(P.panels_own.end(), col_piv, col_piv + col_op_at[ncol]);
+        }
+        P.panels = P.panels_own.data();
+        P.tri_own.assign(triangles, triangles + 3 * nt);
+        P.tri = P.tri_own.data();
+    }
+    P.npanels = nbase;
     P.leaf_shape.resize(2 * nleaves);
     P.leaf_base.resize(nleaves + 1);
     P.rows_at.resize(nleaves);
@@ -315,7 +354,6 @@ int gcabem_packages_build(int64_t nt, const int64_t *triangles, int64_t nleaves,
     P.S = cnt[F];
     P.fb = std::move(fb);
     P.cnt = std::move(cnt);
-    P.triangles.assign(triangles, triangles + 3 * nt);
     P.nthreads = nthreads;
     *out = pk;
     return GCABEM_OK;
@@ -326,7 +364,7 @@ int gcabem_packages_sizes(gcabem_packages_t pk, int64_t *sizes) {
     if (!pk || !sizes) return GCABEM_ERR_ARG;
     sizes[0] = pk->L;
     sizes[1] = pk->payload_len;
-    sizes[2] = (int64_t)pk->panels.size();
+    sizes[2] = pk->npanels;
     sizes[3] = (int64_t)pk->blk.size() / 5;
     sizes[4] = pk->nlists;
     sizes[5] = pk->S;
@@ -344,7 +382,7 @@ int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_s
     auto cp = [](void *dst, const void *src, size_t bytes) {
         if (dst && bytes) std::memcpy(dst, src, bytes);
     };
-    cp(panels, P.panels.data(), P.panels.size() * 8);
+    cp(panels, P.panels, P.npanels * 8);
     cp(leaf_shape, P.leaf_shape.data(), P.leaf_shape.size() * 8);
     cp(leaf_base, P.leaf_base.data(), P.leaf_base.size() * 8);
     cp(rows_at, P.rows_at.data(), P.rows_at.size() * 8);
@@ -360,7 +398,7 @@ int gcabem_packages_fetch(gcabem_packages_t pk, int64_t *panels, int64_t *leaf_s
     // corrective items of the flagged blocks in argwhere (row-major) order,
     // block after block; block f's items start at cnt[f]
     const int64_t F = (int64_t)P.fb.size();
-    const int64_t *T = P.triangles.data();
+    const int64_t *T = P.tri;
     int64_t *o_case = items, *o_tx = items + S, *o_ty = items + 2 * S, *o_leaf = items + 3 * S,
             *o_off = items + 4 * S, *o_blk = items + 5 * S;
     parallel_for(F, P.nthreads, [&](int64_t lo, int64_t hi) {

@@ -244,6 +244,22 @@ class PackageInputs:
     col: tuple
     row_ops: tuple  # at, pivots
     col_ops: tuple
+    _panel_base: np.ndarray | None = None
+
+    @property
+    def panel_base(self) -> np.ndarray:
+        """[row perm | row pivots (| col perm | col pivots)]: the panel base
+        array every leaf range's packages index (the col part only when the
+        trees or the operators differ, as gcabem_packages_build lays it out);
+        built once, shared by the ranges (gcabem_packages_build_on)."""
+        if self._panel_base is None:
+            # (an operator table without pivots holds one placeholder entry)
+            parts = [self.row[4], self.row_ops[1][:int(self.row_ops[0][-1])]]
+            shared = self.col[0] is self.row[0] and self.col[4] is self.row[4]
+            if not shared or self.col_ops[1] is not self.row_ops[1]:
+                parts += [self.col[4], self.col_ops[1][:int(self.col_ops[0][-1])]]
+            self._panel_base = np.ascontiguousarray(np.concatenate(parts), dtype=np.int64)
+        return self._panel_base
 
 
 def package_inputs(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops):
@@ -394,15 +410,16 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
     h = ctypes.c_void_p()
     p = nat.ptr
     tr = _Trace("make_packages")
-    nat.check(nat.lib().gcabem_packages_build(
+    pbase = x.panel_base   # shared by every range of these inputs (borrowed natively)
+    nat.check(nat.lib().gcabem_packages_build_on(
         T.shape[0], p(T), leaves.shape[0], p(leaves), rs.size, p(rs), p(rz), p(rlo), p(rhi),
         p(rperm), p(rat), p(rpiv), cs.size, p(cs), p(cz), p(clo), p(chi), p(cperm), p(cat),
-        p(cpiv), int(maxsize), int(nthreads), ctypes.byref(h)))
+        p(cpiv), int(maxsize), int(nthreads), p(pbase), pbase.size, ctypes.byref(h)))
     try:
         sz = np.zeros(9, dtype=np.int64)
         nat.check(nat.lib().gcabem_packages_sizes(h, p(sz)))
-        L, plen, npan, nblk, nlists, nit = (int(x) for x in sz[:6])
-        panels = np.empty(npan, np.int64)
+        L, plen, npan, nblk, nlists, nit = (int(v) for v in sz[:6])
+        panels = pbase
         shape = np.empty((L, 2), np.int64)
         base = np.empty(L + 1, np.int64)
         rows_at = np.empty(L, np.int64)
@@ -414,7 +431,7 @@ def make_packages(triangles: np.ndarray, block_tree: BlockTree, row_ops, col_ops
         perms = np.empty((nit, 6), np.uint8)
         tr.mark("build+alloc")
         nat.check(nat.lib().gcabem_packages_fetch(
-            h, p(panels), p(shape), p(base), p(rows_at), p(cols_at), p(flagged), p(blocks),
+            h, None, p(shape), p(base), p(rows_at), p(cols_at), p(flagged), p(blocks),
             p(blk_list), p(items), p(perms)))
         tr.mark("fetch")
     finally:
