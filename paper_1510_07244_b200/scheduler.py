@@ -702,11 +702,14 @@ class StagedPackages:
         for t in self._threads:
             t.start()
         try:
-            ids, shape, _ = leaf_layout(block_tree, row_ops, col_ops, inputs)
-            self.leaf_ids = ids[sel]
-            self.leaf_shape = shape[sel]
-            base = np.zeros(L + 1, np.int64)
-            np.cumsum(self.leaf_shape[:, 0] * self.leaf_shape[:, 1], out=base[1:])
+            ids, shape, full_base = leaf_layout(block_tree, row_ops, col_ops, inputs)
+            if leaf_set is None:   # the whole tree: the layout as it is
+                self.leaf_ids, self.leaf_shape, base = ids, shape, full_base
+            else:
+                self.leaf_ids = ids[sel]
+                self.leaf_shape = shape[sel]
+                base = np.zeros(L + 1, np.int64)
+                np.cumsum(self.leaf_shape[:, 0] * self.leaf_shape[:, 1], out=base[1:])
             self.leaf_base = base
             self.payload_len = int(base[-1])
             ranges = list(self.ranges)
