@@ -684,14 +684,21 @@ class StagedPackages:
 
         nw = max(1, PACK_WORKERS)
 
+        claim = iter(range(1, 1 << 62))   # next range to package (under the lock)
+        claim_lock = threading.Lock()
+
         def work(w):
-            # worker 0 packages range 0 at once; ranges 1, 2, ... go round-robin
-            # to the workers once the cuts are known
+            # worker 0 packages range 0 at once; ranges 1, 2, ... go in order
+            # to whichever worker is free, once the cuts are known
             try:
                 if w == 0:
                     one(0)
                 self._layout.wait()
-                for k in range(1 + w, len(self.ranges), nw):
+                while True:
+                    with claim_lock:
+                        k = next(claim)
+                    if k >= len(self.ranges):
+                        return
                     one(k)
             except BaseException as exc:  # re-raised by stage()
                 self._err = exc
