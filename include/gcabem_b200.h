@@ -179,7 +179,9 @@ int gcabem_plan_execute(gcabem_plan_t plan);
  * gcabem_plan_synchronize before reading `host`. */
 int gcabem_plan_execute_download(gcabem_plan_t plan, double *host, int nchunks);
 int gcabem_plan_execute_download2(gcabem_plan_t plan, double *host, double *host2, int nchunks);
-/* Symmetric download (mirrored plans whose first payload is a single layer:
+/* Symmetric download (replaces nothing in the reference: its payloads are host
+ * arrays from the start, make_payloads scheduler.py:411-422; this is how the
+ * device payload reaches that host image). Mirrored plans whose first payload is a single layer:
  * L/H single layer and the pair kinds): execute_download copies neither the
  * SKIP leaves of runs of at least 16384 entries nor their value: a host
  * thread of the plan writes each as the transpose of its PRIMARY leaf (the
