@@ -135,9 +135,13 @@ __device__ __forceinline__ void p1_unscale(double kappa, double acc[9][2]) {
 }
 
 template <int KIND>
+// entry e of the pair whose entries start at base9 = 9 x (payload index) goes
+// to local[pos[base9 + e]] (the scatter plan's sorted position: the
+// gather-sum then reads each nonzero's contributions contiguously), or to
+// local[base9 + e] without a plan (pos null: index batches)
 __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy, bool helm_rot,
                                           double phi0, const uint8_t *px, const uint8_t *py,
-                                          double2 *dst) {
+                                          double2 *local, const int32_t *pos, int64_t base9) {
     const double g = gx * gy;
     const double scale = (KIND == L_SLP || KIND == L_DLP) ? INV_4PI : 1.0;
     double sn = 0.0, cs = 1.0;
@@ -153,7 +157,8 @@ __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy
                 re = r;
             }
             if (KIND == L_SLP || KIND == L_DLP) im = 0.0;
-            dst[3 * px[a] + py[b]] = make_double2((re * scale) * g, im * g);
+            const int64_t e = base9 + 3 * px[a] + py[b];
+            local[pos ? (int64_t)pos[e] : e] = make_double2((re * scale) * g, im * g);
         }
 }
 
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(DISJOINT_TPB)
 p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                    const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                    const int32_t *__restrict__ panels, double2 *__restrict__ local,
-                   double kappa) {
+                   const int32_t *__restrict__ pos, double kappa) {
     const int2 task = tasks[blockIdx.x];
     const BlockDesc b = blocks[task.x];
     const int k = task.y + threadIdx.x;
@@ -172,7 +177,7 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     const int i = inb ? k / b.nc : 0;
     const int j = inb ? k - i * b.nc : 0;
     const int tx = panels[b.rows_at + i], ty = panels[b.cols_at + j];
-    double2 *dst = local + 9 * (b.base + (int64_t)i * b.ld + j);
+    const int64_t base9 = 9 * (b.base + (int64_t)i * b.ld + j);
     bool shared;
     {
         const int a0 = T[3 * tx], a1 = T[3 * tx + 1], a2 = T[3 * tx + 2];
@@ -206,7 +211,8 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
     if (!active) {
         // singular pairs are overwritten by the singular pass; keep them 0
         if (inb)
-            for (int e = 0; e < 9; ++e) dst[e] = make_double2(0.0, 0.0);
+            for (int e = 0; e < 9; ++e)
+                local[pos ? (int64_t)pos[base9 + e] : base9 + e] = make_double2(0.0, 0.0);
         return;
     }
     double acc[9][2];
@@ -230,7 +236,7 @@ p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__
         p1_disjoint_pair<N, KIND, 0>(dO, e1x, e2x, e1y, e2y, n, kappa, 0.0, acc);
     }
     const uint8_t id[3] = {0, 1, 2};
-    p1_finish<KIND>(acc, cx->gram, cy->gram, rot, phi0, id, id, dst);
+    p1_finish<KIND>(acc, cx->gram, cy->gram, rot, phi0, id, id, local, pos, base9);
 }
 
 // --- generic rule (singular items, index batches) ---------------------------
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(GENERIC_TPB)
 p1_generic_kernel(const double *__restrict__ V, const int32_t *__restrict__ T,
                   const Chart *__restrict__ charts, const SingItem *__restrict__ items, int64_t n,
                   const double *__restrict__ rule, int64_t q, double2 *__restrict__ local,
-                  double kappa) {
+                  const int32_t *__restrict__ pos, double kappa) {
     const int64_t idx = (int64_t)blockIdx.x * GENERIC_TPB + threadIdx.x;
     const bool valid = idx < n;
     double dO[3] = {0, 0, 0}, e1x[3] = {0, 0, 0}, e2x[3] = {0, 0, 0};
@@ -342,7 +348,7 @@ p1_generic_kernel(const double *__restrict__ V, const int32_t *__restrict__ T,
     } else {
         p1_generic_rule<KIND, 0>(valid, dO, e1x, e2x, e1y, e2y, ny, rule, q, kappa, 0.0, acc);
     }
-    if (valid) p1_finish<KIND>(acc, gx, gy, tier > 0, phi0, it.px, it.py, local + 9 * it.out);
+    if (valid) p1_finish<KIND>(acc, gx, gy, tier > 0, phi0, it.px, it.py, local, pos, 9 * it.out);
 }
 
 // --- scatter plan and gather-sum --------------------------------------------
@@ -383,61 +389,76 @@ __global__ void rowptr_kernel(const uint64_t *__restrict__ ukeys, int64_t nnz, i
     if (r < nnz) col[r] = (int32_t)(ukeys[r] % (uint64_t)nv);
 }
 
-__global__ void gather_sum_kernel(const int64_t *__restrict__ seg, const int32_t *__restrict__ src,
-                                  int64_t nnz, const double2 *__restrict__ local,
-                                  double2 *__restrict__ out) {
+// nonzero e = the sum of its contributions, stored contiguously in sorted
+// order (local[seg[e] .. seg[e + 1])), in that order: deterministic
+__global__ void gather_sum_kernel(const int64_t *__restrict__ seg, int64_t nnz,
+                                  const double2 *__restrict__ local, double2 *__restrict__ out) {
     const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (e >= nnz) return;
     double re = 0.0, im = 0.0;
     for (int64_t q = seg[e]; q < seg[e + 1]; ++q) {
-        const double2 v = local[src[q]];
+        const double2 v = local[q];
         re += v.x;
         im += v.y;
     }
     out[e] = make_double2(re, im);
 }
 
+// pos[src[q]] = q: the sorted position of each (pair, entry)
+__global__ void invert_perm_kernel(const int32_t *__restrict__ src, int64_t n,
+                                   int32_t *__restrict__ pos) {
+    const int64_t q = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (q < n) pos[src[q]] = (int32_t)q;
+}
+
+// local entries back in pair order (the download of the local matrices)
+__global__ void unsort_kernel(const double2 *__restrict__ local, const int32_t *__restrict__ pos,
+                              int64_t n, double2 *__restrict__ out) {
+    const int64_t k = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (k < n) out[k] = local[pos[k]];
+}
+
 template <int N>
 cudaError_t launch_p1_disjoint_n(int kind, const Chart *charts, const int32_t *T,
                                  const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
-                                 const int32_t *panels, double2 *local, double kappa,
-                                 cudaStream_t s) {
+                                 const int32_t *panels, double2 *local, const int32_t *pos,
+                                 double kappa, cudaStream_t s) {
     const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
     switch (kind) {
-        case L_SLP: p1_disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, kappa); break;
-        case L_DLP: p1_disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, kappa); break;
-        case H_SLP: p1_disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, kappa); break;
-        default:    p1_disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, kappa); break;
+        case L_SLP: p1_disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
+        case L_DLP: p1_disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
+        case H_SLP: p1_disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
+        default:    p1_disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_p1_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
                                const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
-                               const int32_t *panels, double2 *local, double kappa,
-                               cudaStream_t s) {
+                               const int32_t *panels, double2 *local, const int32_t *pos,
+                               double kappa, cudaStream_t s) {
     if (ntasks <= 0) return cudaSuccess;
     switch (order) {
-        case 1: return launch_p1_disjoint_n<1>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
-        case 2: return launch_p1_disjoint_n<2>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
-        case 3: return launch_p1_disjoint_n<3>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
-        case 4: return launch_p1_disjoint_n<4>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
-        case 5: return launch_p1_disjoint_n<5>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
-        case 6: return launch_p1_disjoint_n<6>(kind, charts, T, blocks, tasks, ntasks, panels, local, kappa, s);
+        case 1: return launch_p1_disjoint_n<1>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 2: return launch_p1_disjoint_n<2>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 3: return launch_p1_disjoint_n<3>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 4: return launch_p1_disjoint_n<4>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 5: return launch_p1_disjoint_n<5>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 6: return launch_p1_disjoint_n<6>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_p1_generic(int kind, const double *V, const int32_t *T, const Chart *charts,
                               const SingItem *items, int64_t n, const double *rule, int64_t q,
-                              double2 *local, double kappa, cudaStream_t s) {
+                              double2 *local, const int32_t *pos, double kappa, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const dim3 grid((unsigned)((n + GENERIC_TPB - 1) / GENERIC_TPB)), block(GENERIC_TPB);
     switch (kind) {
-        case L_SLP: p1_generic_kernel<L_SLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, kappa); break;
-        case L_DLP: p1_generic_kernel<L_DLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, kappa); break;
-        case H_SLP: p1_generic_kernel<H_SLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, kappa); break;
-        default:    p1_generic_kernel<H_DLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, kappa); break;
+        case L_SLP: p1_generic_kernel<L_SLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, pos, kappa); break;
+        case L_DLP: p1_generic_kernel<L_DLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, pos, kappa); break;
+        case H_SLP: p1_generic_kernel<H_SLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, pos, kappa); break;
+        default:    p1_generic_kernel<H_DLP><<<grid, block, 0, s>>>(V, T, charts, items, n, rule, q, local, pos, kappa); break;
     }
     return cudaGetLastError();
 }
@@ -465,7 +486,8 @@ struct gcabem_p1_s {
     int64_t sq[3] = {0, 0, 0};
     PoolBuf<double2> local;       // 9 per pair
     DevBuf<int64_t> row_ptr, seg; // CSR rows (nv + 1), contribution segments (nnz + 1)
-    DevBuf<int32_t> col, src;     // CSR columns (nnz), sorted contributions (9 P)
+    DevBuf<int32_t> col;          // CSR columns (nnz)
+    DevBuf<int32_t> pos;          // sorted position of each (pair, entry) (9 P)
     DevBuf<double2> values;       // nnz
     int64_t nv = 0, nnz = 0;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -527,7 +549,8 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     if (e == cudaSuccess) e = keys.alloc(std::max<int64_t>(E, 1), s);
     if (e == cudaSuccess) e = keys_out.alloc(std::max<int64_t>(E, 1), s);
     if (e == cudaSuccess) e = vals.alloc(std::max<int64_t>(E, 1), s);
-    if (e == cudaSuccess) e = p->src.alloc(std::max<int64_t>(E, 1));
+    PoolBuf<int32_t> src;   // sorted contributions: inverted into p->pos below
+    if (e == cudaSuccess) e = src.alloc(std::max<int64_t>(E, 1), s);
     if (e == cudaSuccess && L->ntasks > 0) {
         p1_keys_kernel<<<(unsigned)L->ntasks, DISJOINT_TPB, 0, s>>>(
             mesh->T.p, L->blocks.p, L->tasks.p, L->panels.p, mesh->nv, keys.p, vals.p);
@@ -535,7 +558,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
     }
     size_t tb = 0, tb2 = 0, tb3 = 0;
     if (e == cudaSuccess)
-        e = cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_out.p, vals.p, p->src.p,
+        e = cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys_out.p, vals.p, src.p,
                                             (int)E, 0, end_bit, s);
     if (e == cudaSuccess) e = ukeys.alloc(std::max<int64_t>(E, 1), s);
     if (e == cudaSuccess) e = counts.alloc(E + 1, s);
@@ -548,7 +571,7 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
         e = cub::DeviceScan::ExclusiveSum(nullptr, tb3, counts.p, p->seg.p, (int)E + 1, s);
     if (e == cudaSuccess) e = tmp.alloc(std::max(tb, std::max(tb2, tb3)), s);
     if (e == cudaSuccess && E > 0)
-        e = cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_out.p, vals.p, p->src.p,
+        e = cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys_out.p, vals.p, src.p,
                                             (int)E, 0, end_bit, s);
     if (e == cudaSuccess && E > 0)
         e = cub::DeviceRunLengthEncode::Encode(tmp.p, tb2, keys_out.p, ukeys.p, counts.p,
@@ -573,6 +596,11 @@ int gcabem_p1_create(gcabem_layout_t L, int equation, int layer, double kappa, i
                                                                    p->row_ptr.p, p->col.p);
         e = cudaGetLastError();
     }
+    if (e == cudaSuccess) e = p->pos.alloc(std::max<int64_t>(E, 1));
+    if (e == cudaSuccess && E > 0) {
+        invert_perm_kernel<<<(unsigned)((E + 255) / 256), 256, 0, s>>>(src.p, E, p->pos.p);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     tr.mark("csr");
     if (e != cudaSuccess) {
@@ -593,17 +621,18 @@ int gcabem_p1_execute(gcabem_p1_t p) {
     if (e == cudaSuccess) e = cudaEventRecord(p->ev[0], s);
     if (e == cudaSuccess)
         e = launch_p1_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p, L->tasks.p,
-                               L->ntasks, L->panels.p, p->local.p, p->kappa, s);
+                               L->ntasks, L->panels.p, p->local.p, p->pos.p, p->kappa, s);
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         const int64_t n = L->case_at[c + 1] - L->case_at[c];
         if (n > 0)
             e = launch_p1_generic(p->kind, m->V.p, m->T.p, m->charts.p, L->items.p + L->case_at[c],
-                                  n, p->srule[c].p, p->sq[c], p->local.p, p->kappa, s);
+                                  n, p->srule[c].p, p->sq[c], p->local.p, p->pos.p, p->kappa,
+                                  s);
     }
     if (e == cudaSuccess) e = cudaEventRecord(p->ev[1], s);
     if (e == cudaSuccess && p->nnz > 0) {
         gather_sum_kernel<<<(unsigned)((p->nnz + 255) / 256), 256, 0, s>>>(
-            p->seg.p, p->src.p, p->nnz, p->local.p, p->values.p);
+            p->seg.p, p->nnz, p->local.p, p->values.p);
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaEventRecord(p->ev[2], s);
@@ -640,9 +669,16 @@ int gcabem_p1_download(gcabem_p1_t p, int64_t *row_ptr, int32_t *col, double *va
         e = cudaMemcpyAsync(col, p->col.p, 4 * p->nnz, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && values && p->nnz)
         e = cudaMemcpyAsync(values, p->values.p, 16 * p->nnz, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && local && p->L->payload_len)
-        e = cudaMemcpyAsync(local, p->local.p, 16 * 9 * p->L->payload_len, cudaMemcpyDeviceToHost,
-                            s);
+    PoolBuf<double2> unsorted;   // the local matrices in pair order
+    const int64_t E = 9 * p->L->payload_len;
+    if (e == cudaSuccess && local && E) e = unsorted.alloc(E, s);
+    if (e == cudaSuccess && local && E) {
+        unsort_kernel<<<(unsigned)((E + 255) / 256), 256, 0, s>>>(p->local.p, p->pos.p, E,
+                                                                 unsorted.p);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && local && E)
+        e = cudaMemcpyAsync(local, unsorted.p, 16 * E, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess)
         return gcabem_internal_error(GCABEM_ERR_CUDA,
@@ -708,7 +744,7 @@ int gcabem_p1_batch(gcabem_mesh_t mesh, int equation, int layer, double kappa, i
     if (e == cudaSuccess) e = dout.alloc(9 * n);
     if (e == cudaSuccess)
         e = launch_p1_generic(kind_of(equation, layer), mesh->V.p, mesh->T.p, mesh->charts.p, di.p,
-                              n, dr.p, nq, dout.p, kappa, s);
+                              n, dr.p, nq, dout.p, nullptr, kappa, s);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(out, dout.p, 16 * 9 * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
