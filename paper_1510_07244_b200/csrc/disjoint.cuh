@@ -51,6 +51,10 @@ static cudaError_t upload_tables(int n, const double *g, const double *gw) {
 #define GCABEM_EXPANDED_MAX_RATIO 1024.0
 #endif
 constexpr double EXPANDED_MAX_RATIO = GCABEM_EXPANDED_MAX_RATIO;
+// fused pair kinds roll the outer y loop from this order on (see below)
+#ifndef GCABEM_ROLL_OUTER_N
+#define GCABEM_ROLL_OUTER_N 6
+#endif
 
 // accumulator slots a kind uses (in[] / acc[] of 6): {re, im} of the single
 // layer or of a single kind's operator, then the pair kinds' double layer,
@@ -136,7 +140,7 @@ __device__ __forceinline__ void disjoint_expanded(const double dO[3], const doub
             double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             // fused pair kinds at orders >= 6 roll the outer y loop (the fully
             // unrolled N^2 body spills their two layers of state)
-            constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;
+            constexpr int OUTER = (kind_pair(KIND) && N >= GCABEM_ROLL_OUTER_N) ? 1 : N;
 #pragma unroll OUTER
             for (int d = 0; d < N; ++d) {
                 const double m2b = fma(c_gauss[N][d], b2, a2);
@@ -186,7 +190,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
         const double xon = DL ? fma(xo0, n[0], fma(xo1, n[1], xo2 * n[2])) : 0.0;
         const double xonm = DM ? fma(xo0, nx[0], fma(xo1, nx[1], xo2 * nx[2])) : 0.0;
         double in[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        constexpr int OUTER = (kind_pair(KIND) && N >= 6) ? 1 : N;  // see disjoint_expanded
+        constexpr int OUTER = (kind_pair(KIND) && N >= GCABEM_ROLL_OUTER_N) ? 1 : N;  // see disjoint_expanded
 #pragma unroll OUTER
         for (int c = 0; c < N; ++c) {
             const double gc = c_gauss[N][c];
