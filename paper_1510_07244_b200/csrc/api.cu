@@ -530,6 +530,24 @@ void pinned_release(void *ptr, size_t bytes) {
     g_pin_free.emplace(bytes, ptr);
 }
 
+// task lists of a layout from their per-block prefixes (block b's tasks are
+// (b, 0), (b, DISJOINT_TPB), ...): all blocks, mirrored (PRIMARY / SELF)
+// blocks, plain (NORMAL) blocks; a block has mirrored or plain tasks or none
+__global__ void expand_tasks_kernel(const int32_t *__restrict__ at,
+                                    const int32_t *__restrict__ at_m,
+                                    const int32_t *__restrict__ at_r, int2 *__restrict__ tasks,
+                                    int2 *__restrict__ mtasks, int2 *__restrict__ rtasks) {
+    const int b = blockIdx.x;
+    for (int t = threadIdx.x; t < at[b + 1] - at[b]; t += blockDim.x)
+        tasks[at[b] + t] = make_int2(b, t * DISJOINT_TPB);
+    if (mtasks)
+        for (int t = threadIdx.x; t < at_m[b + 1] - at_m[b]; t += blockDim.x)
+            mtasks[at_m[b] + t] = make_int2(b, t * DISJOINT_TPB);
+    if (rtasks)
+        for (int t = threadIdx.x; t < at_r[b + 1] - at_r[b]; t += blockDim.x)
+            rtasks[at_r[b] + t] = make_int2(b, t * DISJOINT_TPB);
+}
+
 __global__ void gather_entries_kernel(const double2 *__restrict__ src,
                                       const int64_t *__restrict__ idx, int64_t n,
                                       double2 *__restrict__ dst) {
@@ -724,13 +742,12 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     const int64_t S = L->case_at[3];
     L->item_out.resize(S);
     tr.mark("counts");
-    // one pinned arena: [BlockDesc B | int2 ntasks | int2 nmt | int2 nrt | int32 npanels |
-    // SingItem S]
+    // one pinned arena: [BlockDesc B | int32 task prefixes 3 (B + 1) | int32 npanels |
+    // SingItem S]; the task lists themselves are expanded on the device
+    // (expand_tasks_kernel: 32-pair tasks would be 4x the bytes to write and upload)
     auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t off_t = align(sizeof(BlockDesc) * B),
-                 off_mt = off_t + align(sizeof(int2) * ntasks),
-                 off_rt = off_mt + align(sizeof(int2) * nmt),
-                 off_p = off_rt + align(sizeof(int2) * nrt),
+                 off_p = off_t + 3 * align(sizeof(int32_t) * (B + 1)),
                  off_s = off_p + align(sizeof(int32_t) * npanels),
                  total = off_s + align(sizeof(SingItem) * S);
     // from the pinned pool (no lock held while filling: layouts of several
@@ -747,9 +764,12 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     }
     char *arena = static_cast<char *>(arena_blk.p);
     BlockDesc *bd = reinterpret_cast<BlockDesc *>(arena);
-    int2 *tasks = reinterpret_cast<int2 *>(arena + off_t);
-    int2 *mtasks = reinterpret_cast<int2 *>(arena + off_mt);
-    int2 *rtasks = reinterpret_cast<int2 *>(arena + off_rt);
+    int32_t *at3 = reinterpret_cast<int32_t *>(arena + off_t);  // all / mirrored / plain
+    const size_t at_stride = align(sizeof(int32_t) * (B + 1)) / sizeof(int32_t);
+    if (ntasks >= (int64_t(1) << 31)) {
+        delete L;
+        return set_error(GCABEM_ERR_ARG, "too many disjoint tasks for one layout");
+    }
     int32_t *pan = reinterpret_cast<int32_t *>(arena + off_p);
     SingItem *si = reinterpret_cast<SingItem *>(arena + off_s);
     par_for(B, 1 << 14, [&](int64_t lo, int64_t hi, int) {
@@ -778,20 +798,14 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
                               (int32_t)mld, (int32_t)dr};
             L->block_leaf[b] = lf;
             L->block_base[b] = base;
-            int64_t t = L->block_task_at[b];
-            for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
-                tasks[t++] = make_int2((int)b, (int)k0);
-            if (any_mirror && (role == ROLE_PRIMARY || role == ROLE_SELF)) {
-                int64_t q = L->block_mtask_at[b];
-                for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
-                    mtasks[q++] = make_int2((int)b, (int)k0);
-            } else if (any_mirror && role == ROLE_NORMAL) {
-                int64_t q = L->block_rtask_at[b];
-                for (int64_t k0 = 0; k0 < nr * nc; k0 += DISJOINT_TPB)
-                    rtasks[q++] = make_int2((int)b, (int)k0);
-            }
+            at3[b] = (int32_t)L->block_task_at[b];
+            at3[at_stride + b] = any_mirror ? (int32_t)L->block_mtask_at[b] : 0;
+            at3[2 * at_stride + b] = any_mirror ? (int32_t)L->block_rtask_at[b] : 0;
         }
     });
+    at3[B] = (int32_t)ntasks;
+    at3[at_stride + B] = (int32_t)nmt;
+    at3[2 * at_stride + B] = (int32_t)nrt;
     par_for(npanels, 1 << 16, [&](int64_t lo, int64_t hi, int) {
         for (int64_t k = lo; k < hi; ++k) {
             if (panels[k] < 0 || panels[k] >= mesh->nt) bad = true;
@@ -1020,9 +1034,16 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     if (e == cudaSuccess) e = L->panels.alloc(npanels, s);
     if (e == cudaSuccess) e = L->items.alloc(S, s);
     if (e == cudaSuccess && B) e = cudaMemcpyAsync(L->blocks.p, bd, sizeof(BlockDesc) * B, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && ntasks) e = cudaMemcpyAsync(L->tasks.p, tasks, sizeof(int2) * ntasks, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && nmt) e = cudaMemcpyAsync(L->mtasks.p, mtasks, sizeof(int2) * nmt, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess && nrt) e = cudaMemcpyAsync(L->rtasks.p, rtasks, sizeof(int2) * nrt, cudaMemcpyHostToDevice, s);
+    PoolBuf<int32_t> d_at;   // the three task prefixes, for the expansion below
+    if (e == cudaSuccess && B) e = d_at.alloc(3 * at_stride, s);
+    if (e == cudaSuccess && B)
+        e = cudaMemcpyAsync(d_at.p, at3, sizeof(int32_t) * 3 * at_stride, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && B && ntasks) {
+        expand_tasks_kernel<<<(unsigned)B, 32, 0, s>>>(d_at.p, d_at.p + at_stride,
+                                                       d_at.p + 2 * at_stride, L->tasks.p,
+                                                       L->mtasks.p, L->rtasks.p);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess && npanels) e = cudaMemcpyAsync(L->panels.p, pan, sizeof(int32_t) * npanels, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && S) e = cudaMemcpyAsync(L->items.p, si, sizeof(SingItem) * S, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && L->vertex_mirror) {

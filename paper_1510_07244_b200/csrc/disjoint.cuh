@@ -212,7 +212,7 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
     }
 }
 
-// One thread = one panel pair of one WorkBlock; a CTA = DISJOINT_TPB
+// One thread = one panel pair of one WorkBlock; a task = DISJOINT_TPB
 // consecutive (row-major) pairs of one block. Rule constants are
 // compile-time offsets into constant memory (DFMA operands), so the inner
 // N^2 loop issues no loads. Pairs that share a vertex are written as 0: the
@@ -230,6 +230,17 @@ __device__ __forceinline__ void disjoint_direct(const double dO[3], const double
 // C2), H_PAIR 5 (96 registers, a few spilled bytes in the cold full-sincos
 // tier; 4 and 6 measured 1.6% and 3% slower at C3, re-checked with the v11
 // point kernels)
+// threads per CTA of the disjoint kernels: a task's DISJOINT_TPB pairs may run
+// as CTA_SPLIT CTAs (the resident-CTA counts below are per 128 threads and
+// scale with the CTA size); with one-warp tasks the split is 1
+#ifndef GCABEM_DISJOINT_CTA
+#define GCABEM_DISJOINT_CTA 32
+#endif
+constexpr int DISJOINT_CTA = GCABEM_DISJOINT_CTA;
+constexpr int CTA_SPLIT = DISJOINT_TPB / DISJOINT_CTA;
+constexpr int CTA_SCALE = 128 / DISJOINT_CTA;   // resident CTAs per "128-thread CTA" below
+static_assert(DISJOINT_TPB % DISJOINT_CTA == 0 && DISJOINT_CTA % 32 == 0, "whole warps");
+
 #ifndef GCABEM_HPAIR_MINB
 #define GCABEM_HPAIR_MINB 5
 #endif
@@ -256,17 +267,18 @@ constexpr int disjoint_minb_mir(int n, int kind) {
 }
 
 template <int N, int KIND, bool MIR>
-__global__ void __launch_bounds__(DISJOINT_TPB, MIR ? disjoint_minb_mir(N, KIND)
-                                                    : disjoint_minb(N, KIND))
+__global__ void __launch_bounds__(DISJOINT_CTA, (MIR ? disjoint_minb_mir(N, KIND)
+                                                     : disjoint_minb(N, KIND)) * CTA_SCALE)
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                 const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
                 const int32_t *__restrict__ panels, double2 *__restrict__ payload,
                 double2 *__restrict__ payload2, double kappa) {
-    const int2 task = tasks[blockIdx.x];
+    // CTA_SPLIT CTAs of DISJOINT_CTA threads per task of DISJOINT_TPB pairs
+    const int2 task = tasks[blockIdx.x / CTA_SPLIT];
     const BlockDesc b = blocks[task.x];
-    const int k = task.y + threadIdx.x;
+    const int k = task.y + (int)(blockIdx.x % CTA_SPLIT) * DISJOINT_CTA + threadIdx.x;
     // no early exit before the warp votes below: every lane of the CTA's
-    // four full warps reaches them
+    // full warp(s) reaches them
     bool inb = k < b.nr * b.nc;
     const int i = inb ? k / b.nc : 0;
     const int j = inb ? k - i * b.nc : 0;
@@ -387,7 +399,7 @@ static cudaError_t launch_disjoint_nm(int kind, const Chart *charts, const int32
                                       const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
                                       const int32_t *panels, double2 *payload, double2 *payload2,
                                       double kappa, cudaStream_t s) {
-    const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
+    const dim3 grid((unsigned)(ntasks * CTA_SPLIT)), block(DISJOINT_CTA);
     switch (kind) {
         case L_SLP: disjoint_kernel<N, L_SLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
         case L_DLP: disjoint_kernel<N, L_DLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
