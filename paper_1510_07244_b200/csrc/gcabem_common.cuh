@@ -73,7 +73,10 @@ constexpr int MAX_ORDER = 12;
 // blocks are rank x rank, any size) and CTAs start and retire at a fine grain
 // (C3 step 28.53 -> 28.11 ms, C2 9.02 -> 8.93 ms against 128-pair tasks)
 constexpr int DISJOINT_TPB = 32;
-constexpr int GENERIC_TPB = 128;
+#ifndef GCABEM_GENERIC_TPB
+#define GCABEM_GENERIC_TPB 128
+#endif
+constexpr int GENERIC_TPB = GCABEM_GENERIC_TPB;
 constexpr int GREEN_TPB = 128;
 #ifndef GCABEM_RULE_CHUNK
 #define GCABEM_RULE_CHUNK 256
