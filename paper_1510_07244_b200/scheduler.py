@@ -52,6 +52,9 @@ def _symmetric(params, payload_len: int) -> bool:
     return bool(params.symmetric_download)
 
 
+# range 0 = the first 1/STAGE_FIRST of the leaves (the device and the link
+# start as soon as it is packaged)
+STAGE_FIRST = int(os.environ.get("GCABEM_STAGE_FIRST", "64"))
 # host threads packaging leaf ranges (and building their device layouts) ahead
 # of the device
 PACK_WORKERS = int(os.environ.get("GCABEM_PACK_WORKERS", "2"))
@@ -658,7 +661,7 @@ class StagedPackages:
         # the rest is cut leaf-aligned into ranges growing geometrically
         # (payload weights 1, g, g^2, ... with g = STAGE_GROWTH), each packaged
         # while the (longer) D2H of all earlier ranges runs. Ranges index the set.
-        first = L if n == 1 else max(1, L // 64)
+        first = L if n == 1 else max(1, L // STAGE_FIRST)
         self.ranges = [(0, first)]
         # allocated once at the maximum stage count and never replaced: the
         # worker thread stores into them while the ranges are still being cut
