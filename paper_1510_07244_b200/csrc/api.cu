@@ -104,6 +104,11 @@ cudaError_t pool_init(int device) {
 int gcabem_internal_error(int code, const char *msg) { return set_error(code, msg); }
 
 
+namespace {
+// TaskDesc lists of a layout (defined below, next to the other layout kernels)
+cudaError_t build_task_descs(gcabem_layout_s *L, cudaStream_t s);
+}  // namespace
+
 struct gcabem_plan_s {
     gcabem_mesh_t mesh = nullptr;
     gcabem_layout_t L = nullptr;
@@ -448,6 +453,7 @@ int gcabem_layout_create(gcabem_mesh_t mesh, int64_t payload_len, int64_t nblock
     cudaError_t e = pool_init(mesh->device);
     if (e == cudaSuccess) e = L->blocks.upload(bd.data(), bd.size(), s);
     if (e == cudaSuccess) e = L->tasks.upload(tasks.data(), tasks.size(), s);
+    if (e == cudaSuccess) e = build_task_descs(L, s);
     if (e == cudaSuccess) e = L->panels.upload(pan.data(), pan.size(), s);
     if (e == cudaSuccess) e = L->items.upload(si.data(), si.size(), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host vectors die here
@@ -528,6 +534,41 @@ void pinned_release(void *ptr, size_t bytes) {
     if (!ptr) return;
     std::lock_guard<std::mutex> lk(g_pin_mutex);
     g_pin_free.emplace(bytes, ptr);
+}
+
+// TaskDesc records of a task list (block descriptor copied next to the task)
+__global__ void task_desc_kernel(const BlockDesc *__restrict__ blocks,
+                                 const int2 *__restrict__ tasks, int64_t n,
+                                 TaskDesc *__restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int2 tk = tasks[t];
+    TaskDesc d;
+    d.b = blocks[tk.x];
+    d.k0 = tk.y;
+    d.pad = 0;
+    out[t] = d;
+}
+
+// the layout's three TaskDesc lists from its blocks and int2 task lists
+cudaError_t build_task_descs(gcabem_layout_s *L, cudaStream_t s) {
+    struct List {
+        const int2 *src;
+        int64_t n;
+        PoolBuf<TaskDesc> *dst;
+    } lists[3] = {{L->tasks.p, L->ntasks, &L->tdesc},
+                  {L->mtasks.p, L->nmtasks, &L->mtdesc},
+                  {L->rtasks.p, L->nrtasks, &L->rtdesc}};
+    for (const List &l : lists) {
+        if (l.n <= 0 || !l.src) continue;
+        cudaError_t e = l.dst->alloc(l.n, s);
+        if (e != cudaSuccess) return e;
+        task_desc_kernel<<<(unsigned)((l.n + 255) / 256), 256, 0, s>>>(L->blocks.p, l.src, l.n,
+                                                                        l.dst->p);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // task lists of a layout from their per-block prefixes (block b's tasks are
@@ -1053,6 +1094,7 @@ int gcabem_layout_from_packages(gcabem_mesh_t mesh, int64_t leaf_lo, int64_t lea
     }
     if (e == cudaSuccess && !L->patch_out.empty())
         e = L->patch_dev.upload(L->patch_out.data(), L->patch_out.size(), s);
+    if (e == cudaSuccess) e = build_task_descs(L, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the arena is reused after this
     tr.mark("upload");
     if (e != cudaSuccess) {
@@ -1322,18 +1364,16 @@ int enqueue_disjoint(gcabem_plan_t p, int64_t b0, int64_t b1) {
     cudaStream_t s = p->stream;
     if (!p->mirrored) {
         const int64_t t0 = L->block_task_at[b0], t1 = L->block_task_at[b1];
-        GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p,
-                                L->tasks.p + t0, t1 - t0, L->panels.p, p->payload.p,
-                                p->payload2.p, p->kappa, s));
+        GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->tdesc.p + t0, t1 - t0,
+                                L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
         return GCABEM_OK;
     }
     const int64_t r0 = L->block_rtask_at[b0], r1 = L->block_rtask_at[b1];
     const int64_t q0 = L->block_mtask_at[b0], q1 = L->block_mtask_at[b1];
-    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p,
-                            L->rtasks.p + r0, r1 - r0, L->panels.p, p->payload.p, p->payload2.p,
-                            p->kappa, s));
-    GC_CUDA(launch_disjoint(p->kind + MIRRORED, p->order, m->charts.p, m->T.p, L->blocks.p,
-                            L->mtasks.p + q0, q1 - q0, L->panels.p, p->payload.p, p->payload2.p,
+    GC_CUDA(launch_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->rtdesc.p + r0, r1 - r0,
+                            L->panels.p, p->payload.p, p->payload2.p, p->kappa, s));
+    GC_CUDA(launch_disjoint(p->kind + MIRRORED, p->order, m->charts.p, m->T.p,
+                            L->mtdesc.p + q0, q1 - q0, L->panels.p, p->payload.p, p->payload2.p,
                             p->kappa, s));
     return GCABEM_OK;
 }

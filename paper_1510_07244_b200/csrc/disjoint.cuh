@@ -270,13 +270,12 @@ template <int N, int KIND, bool MIR>
 __global__ void __launch_bounds__(DISJOINT_CTA, (MIR ? disjoint_minb_mir(N, KIND)
                                                      : disjoint_minb(N, KIND)) * CTA_SCALE)
 disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
-                const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
-                const int32_t *__restrict__ panels, double2 *__restrict__ payload,
+                const TaskDesc *__restrict__ tasks, const int32_t *__restrict__ panels, double2 *__restrict__ payload,
                 double2 *__restrict__ payload2, double kappa) {
     // CTA_SPLIT CTAs of DISJOINT_CTA threads per task of DISJOINT_TPB pairs
-    const int2 task = tasks[blockIdx.x / CTA_SPLIT];
-    const BlockDesc b = blocks[task.x];
-    const int k = task.y + (int)(blockIdx.x % CTA_SPLIT) * DISJOINT_CTA + threadIdx.x;
+    const TaskDesc &td = tasks[blockIdx.x / CTA_SPLIT];
+    const BlockDesc b = td.b;
+    const int k = td.k0 + (int)(blockIdx.x % CTA_SPLIT) * DISJOINT_CTA + threadIdx.x;
     // no early exit before the warp votes below: every lane of the CTA's
     // full warp(s) reaches them
     bool inb = k < b.nr * b.nc;
@@ -396,17 +395,17 @@ disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
 
 template <int N, bool MIR>
 static cudaError_t launch_disjoint_nm(int kind, const Chart *charts, const int32_t *T,
-                                      const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                      const TaskDesc *tasks, int64_t ntasks,
                                       const int32_t *panels, double2 *payload, double2 *payload2,
                                       double kappa, cudaStream_t s) {
     const dim3 grid((unsigned)(ntasks * CTA_SPLIT)), block(DISJOINT_CTA);
     switch (kind) {
-        case L_SLP: disjoint_kernel<N, L_SLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case L_DLP: disjoint_kernel<N, L_DLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case H_SLP: disjoint_kernel<N, H_SLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case H_DLP: disjoint_kernel<N, H_DLP, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        case L_PAIR: disjoint_kernel<N, L_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
-        default:    disjoint_kernel<N, H_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, payload, payload2, kappa); break;
+        case L_SLP: disjoint_kernel<N, L_SLP, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
+        case L_DLP: disjoint_kernel<N, L_DLP, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
+        case H_SLP: disjoint_kernel<N, H_SLP, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
+        case H_DLP: disjoint_kernel<N, H_DLP, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
+        case L_PAIR: disjoint_kernel<N, L_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
+        default:    disjoint_kernel<N, H_PAIR, MIR><<<grid, block, 0, s>>>(charts, T, tasks, panels, payload, payload2, kappa); break;
     }
     return cudaGetLastError();
 }
@@ -414,17 +413,17 @@ static cudaError_t launch_disjoint_nm(int kind, const Chart *charts, const int32
 // kind >= MIRRORED: the mirrored kernel (orders <= MAX_MIRROR_ORDER)
 template <int N>
 static cudaError_t launch_disjoint_n(int kind, const Chart *charts, const int32_t *T,
-                                     const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                     const TaskDesc *tasks, int64_t ntasks,
                                      const int32_t *panels, double2 *payload, double2 *payload2,
                                      double kappa, cudaStream_t s) {
     if (kind >= MIRRORED) {
         if constexpr (N <= MAX_MIRROR_ORDER)
-            return launch_disjoint_nm<N, true>(kind - MIRRORED, charts, T, blocks, tasks, ntasks,
+            return launch_disjoint_nm<N, true>(kind - MIRRORED, charts, T, tasks, ntasks,
                                                panels, payload, payload2, kappa, s);
         else
             return cudaErrorInvalidValue;
     }
-    return launch_disjoint_nm<N, false>(kind, charts, T, blocks, tasks, ntasks, panels, payload,
+    return launch_disjoint_nm<N, false>(kind, charts, T, tasks, ntasks, panels, payload,
                                         payload2, kappa, s);
 }
 

@@ -8,14 +8,14 @@ cudaError_t upload_disjoint_rule_o5_8(int n, const double *g, const double *gw) 
 }
 
 cudaError_t launch_disjoint_o5_8(int kind, int order, const Chart *charts, const int32_t *T,
-                                const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                const TaskDesc *tasks, int64_t ntasks,
                                 const int32_t *panels, double2 *payload, double2 *payload2,
                                 double kappa, cudaStream_t s) {
     switch (order) {
-        case 5: return launch_disjoint_n<5>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 6: return launch_disjoint_n<6>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 7: return launch_disjoint_n<7>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 8: return launch_disjoint_n<8>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 5: return launch_disjoint_n<5>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 6: return launch_disjoint_n<6>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 7: return launch_disjoint_n<7>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 8: return launch_disjoint_n<8>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -8,14 +8,14 @@ cudaError_t upload_disjoint_rule_o9_12(int n, const double *g, const double *gw)
 }
 
 cudaError_t launch_disjoint_o9_12(int kind, int order, const Chart *charts, const int32_t *T,
-                                const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                const TaskDesc *tasks, int64_t ntasks,
                                 const int32_t *panels, double2 *payload, double2 *payload2,
                                 double kappa, cudaStream_t s) {
     switch (order) {
-        case 9: return launch_disjoint_n<9>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 10: return launch_disjoint_n<10>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 11: return launch_disjoint_n<11>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
-        case 12: return launch_disjoint_n<12>(kind, charts, T, blocks, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 9: return launch_disjoint_n<9>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 10: return launch_disjoint_n<10>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 11: return launch_disjoint_n<11>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
+        case 12: return launch_disjoint_n<12>(kind, charts, T, tasks, ntasks, panels, payload, payload2, kappa, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -48,6 +48,16 @@ struct BlockDesc {
 };
 static_assert(sizeof(BlockDesc) == 56, "BlockDesc layout");
 
+// one disjoint task: its block's descriptor and the task's first pair, so a
+// disjoint CTA's prologue loads one record instead of task -> block (one
+// dependent global load fewer before the panel indices and charts)
+struct __align__(16) TaskDesc {
+    BlockDesc b;
+    int32_t k0;   // first pair of the task (row-major in the block)
+    int32_t pad;
+};
+static_assert(sizeof(TaskDesc) == 64, "TaskDesc layout");
+
 struct SingItem {
     int64_t out;          // payload index (leaf base + WorkItem.offset)
     int32_t tri_x, tri_y;
@@ -99,9 +109,8 @@ constexpr int MAX_MIRROR_ORDER = 8;
 #endif
 constexpr int64_t SYM_MIN_RUN = GCABEM_SYM_MIN_RUN;
 cudaError_t launch_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
-                            const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
-                            const int32_t *panels, double2 *payload, double2 *payload2,
-                            double kappa, cudaStream_t s);
+                            const TaskDesc *tasks, int64_t ntasks, const int32_t *panels,
+                            double2 *payload, double2 *payload2, double kappa, cudaStream_t s);
 // Generic-rule pair integrals: singular lists (vertex/edge/identical) and the
 // index-based batch. Charts gathered with permutations from V/T.
 // same_chart: every item has tri_x == tri_y and perm_x == perm_y (identical case).

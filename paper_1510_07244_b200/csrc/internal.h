@@ -124,6 +124,9 @@ struct gcabem_layout_s {
     // blocks (mirrored kernel) and of ROLE_NORMAL blocks (plain kernel);
     // ROLE_SKIP blocks have none. Empty when no leaf has a mirror.
     gcabem::PoolBuf<int2> mtasks, rtasks;
+    // the same three task lists as TaskDesc records (block descriptor + first
+    // pair) for the disjoint kernels (task_desc_kernel, at layout creation)
+    gcabem::PoolBuf<gcabem::TaskDesc> tdesc, mtdesc, rtdesc;
     int64_t nmtasks = 0, nrtasks = 0;
     std::vector<int64_t> block_mtask_at, block_rtask_at;
     // {evaluations by the mirrored kernel, by the plain kernel (pairs sharing
