@@ -167,12 +167,12 @@ __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy
 template <int N, int KIND>
 __global__ void __launch_bounds__(DISJOINT_TPB)
 p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
-                   const BlockDesc *__restrict__ blocks, const int2 *__restrict__ tasks,
+                   const TaskDesc *__restrict__ tasks,
                    const int32_t *__restrict__ panels, double2 *__restrict__ local,
                    const int32_t *__restrict__ pos, double kappa) {
-    const int2 task = tasks[blockIdx.x];
-    const BlockDesc b = blocks[task.x];
-    const int k = task.y + threadIdx.x;
+    const TaskDesc &td = tasks[blockIdx.x];   // block descriptor + first pair
+    const BlockDesc b = td.b;
+    const int k = td.k0 + threadIdx.x;
     const bool inb = k < b.nr * b.nc;
     const int i = inb ? k / b.nc : 0;
     const int j = inb ? k - i * b.nc : 0;
@@ -420,31 +420,31 @@ __global__ void unsort_kernel(const double2 *__restrict__ local, const int32_t *
 
 template <int N>
 cudaError_t launch_p1_disjoint_n(int kind, const Chart *charts, const int32_t *T,
-                                 const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                                 const TaskDesc *tasks, int64_t ntasks,
                                  const int32_t *panels, double2 *local, const int32_t *pos,
                                  double kappa, cudaStream_t s) {
     const dim3 grid((unsigned)ntasks), block(DISJOINT_TPB);
     switch (kind) {
-        case L_SLP: p1_disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
-        case L_DLP: p1_disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
-        case H_SLP: p1_disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
-        default:    p1_disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, blocks, tasks, panels, local, pos, kappa); break;
+        case L_SLP: p1_disjoint_kernel<N, L_SLP><<<grid, block, 0, s>>>(charts, T, tasks, panels, local, pos, kappa); break;
+        case L_DLP: p1_disjoint_kernel<N, L_DLP><<<grid, block, 0, s>>>(charts, T, tasks, panels, local, pos, kappa); break;
+        case H_SLP: p1_disjoint_kernel<N, H_SLP><<<grid, block, 0, s>>>(charts, T, tasks, panels, local, pos, kappa); break;
+        default:    p1_disjoint_kernel<N, H_DLP><<<grid, block, 0, s>>>(charts, T, tasks, panels, local, pos, kappa); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_p1_disjoint(int kind, int order, const Chart *charts, const int32_t *T,
-                               const BlockDesc *blocks, const int2 *tasks, int64_t ntasks,
+                               const TaskDesc *tasks, int64_t ntasks,
                                const int32_t *panels, double2 *local, const int32_t *pos,
                                double kappa, cudaStream_t s) {
     if (ntasks <= 0) return cudaSuccess;
     switch (order) {
-        case 1: return launch_p1_disjoint_n<1>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
-        case 2: return launch_p1_disjoint_n<2>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
-        case 3: return launch_p1_disjoint_n<3>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
-        case 4: return launch_p1_disjoint_n<4>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
-        case 5: return launch_p1_disjoint_n<5>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
-        case 6: return launch_p1_disjoint_n<6>(kind, charts, T, blocks, tasks, ntasks, panels, local, pos, kappa, s);
+        case 1: return launch_p1_disjoint_n<1>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
+        case 2: return launch_p1_disjoint_n<2>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
+        case 3: return launch_p1_disjoint_n<3>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
+        case 4: return launch_p1_disjoint_n<4>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
+        case 5: return launch_p1_disjoint_n<5>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
+        case 6: return launch_p1_disjoint_n<6>(kind, charts, T, tasks, ntasks, panels, local, pos, kappa, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -620,7 +620,7 @@ int gcabem_p1_execute(gcabem_p1_t p) {
     cudaError_t e = cudaSetDevice(m->device);
     if (e == cudaSuccess) e = cudaEventRecord(p->ev[0], s);
     if (e == cudaSuccess)
-        e = launch_p1_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->blocks.p, L->tasks.p,
+        e = launch_p1_disjoint(p->kind, p->order, m->charts.p, m->T.p, L->tdesc.p,
                                L->ntasks, L->panels.p, p->local.p, p->pos.p, p->kappa, s);
     for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
         const int64_t n = L->case_at[c + 1] - L->case_at[c];
