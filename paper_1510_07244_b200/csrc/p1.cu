@@ -162,10 +162,13 @@ __device__ __forceinline__ void p1_finish(double acc[9][2], double gx, double gy
         }
 }
 
-// unconstrained registers (242, 2 CTAs/SM): measured faster on the B200 than
-// 3 CTAs/SM with the y loop rolled (34.2 vs 30.6 ms at C4) -- ILP wins here
+// unconstrained registers (242, 8 warps/SM): measured faster on the B200 than
+// 12 warps/SM with the y loop rolled (34.2 vs 30.6 ms at C4) -- ILP wins here
+#ifndef GCABEM_P1_MINB
+#define GCABEM_P1_MINB 1
+#endif
 template <int N, int KIND>
-__global__ void __launch_bounds__(DISJOINT_TPB)
+__global__ void __launch_bounds__(DISJOINT_TPB, GCABEM_P1_MINB)
 p1_disjoint_kernel(const Chart *__restrict__ charts, const int32_t *__restrict__ T,
                    const TaskDesc *__restrict__ tasks,
                    const int32_t *__restrict__ panels, double2 *__restrict__ local,
